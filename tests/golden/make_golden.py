@@ -1,0 +1,226 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+The outputs (*.npz, *.fvsrn, golden.json) are committed; nothing on the GPU
+box reads /root/reference.  The reference is imported read-only; no source is
+copied.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import fvsrn  # noqa: E402
+from fvsrn.imaging import Camera  # noqa: E402
+from fvsrn.model import (  # noqa: E402
+    ModelConfig, assemble_input, checkpoint_save, decode_volume, eval_color,
+    eval_density, model_init)
+from fvsrn.render import (  # noqa: E402
+    ModelSource, RenderSettings, _march_geometry, camera_rays, raymarch_forward,
+    render_image)
+from fvsrn.train import fibonacci_cameras  # noqa: E402
+from fvsrn.transfer import TF_PRESETS, tf_eval  # noqa: E402
+from fvsrn.fused import fused_eval, plan_for_model  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def model_hashes(m):
+    return {
+        "weights": [sha(w) for w in m.params.weights],
+        "biases": [sha(b) for b in m.params.biases],
+        "grids": [sha(g.values) for g in m.grids],
+        "b_matrix": sha(m.spatial_encoder.b_matrix),
+    }
+
+
+class Counting(ModelSource):
+    count = 0
+
+    def sample(self, p, d):
+        Counting.count += len(p)
+        return super().sample(p, d)
+
+
+def counted_render(model, tf, cam, settings, t=None, fused=True):
+    Counting.count = 0
+    src = Counting(model, tf, t=t, use_fused=fused)
+    img = render_image(src, cam, settings)
+    return img.data, Counting.count
+
+
+CONFIGS = {
+    # name -> ModelConfig kwargs (BASELINE.json configs + test shapes)
+    "cfg1": dict(layers=4, hidden=32, grid_resolution=16, grid_channels=16, seed=0),
+    "cfg2": dict(layers=4, hidden=32, grid_resolution=32, grid_channels=16, seed=0),
+    "cfg3": dict(layers=6, hidden=64, grid_resolution=64, grid_channels=16, fourier_m=30, seed=0),
+    "tiny": dict(layers=2, hidden=16, fourier_m=6, grid_resolution=4, grid_channels=4, seed=7),
+    "temporal": dict(layers=4, hidden=32, grid_resolution=8, grid_channels=16,
+                     keyframe_times=[1, 11, 21], seed=0),
+    "temporal_both": dict(layers=3, hidden=32, grid_resolution=6, grid_channels=8,
+                          keyframe_times=[1, 6, 11], time_mode="both", seed=3),
+    "color_dirf": dict(head="color", layers=3, hidden=32, grid_resolution=8, grid_channels=8,
+                       direction_mode="dirF", fourier_m=12, seed=5),
+    "color_pos": dict(head="color", layers=3, hidden=32, grid_resolution=8, grid_channels=16,
+                      seed=11),
+    "random_fourier": dict(layers=3, hidden=48, fourier_mode="random", fourier_m=20,
+                           fourier_sigma=2.0, grid_resolution=8, grid_channels=16, seed=4),
+    "relu_nogrid": dict(layers=3, hidden=32, activation="relu", grid_resolution=0, seed=9),
+    "snake_f12": dict(layers=3, hidden=32, activation="snake", grid_resolution=5,
+                      grid_channels=12, seed=13),
+}
+
+
+def main():
+    rng = np.random.default_rng(20211203)
+    meta = {"reference": "fvsrn " + fvsrn.__version__, "models": {}, "renders": {}}
+    arrays = {}
+
+    models = {k: model_init(ModelConfig(**v)) for k, v in CONFIGS.items()}
+    for k, m in models.items():
+        meta["models"][k] = {"config": CONFIGS[k], "hashes": model_hashes(m),
+                             "input_width": m.config.input_width}
+
+    # --- rays + geometry (render.py:72-106,189-200)
+    cams = {
+        "fib0": fibonacci_cameras(8, 37, 23)[0],
+        "fib5": fibonacci_cameras(8, 37, 23)[5],
+        "center": Camera(eye=(0.5, 0.5, 3.5), target=(0.5, 0.5, 0.5), up=(0, 1, 0),
+                         fov_y=np.pi / 5, width=33, height=33),
+        "inside": Camera(eye=(0.3, 0.6, 0.4), target=(0.9, 0.1, 0.8), up=(0, 0, 1),
+                         fov_y=1.2, width=20, height=16),
+    }
+    for name, cam in cams.items():
+        o, d = camera_rays(cam)
+        tmin, ds, n = _march_geometry(o, d, RenderSettings(stepsize=1 / 128))
+        arrays[f"rays_{name}_o"] = o
+        arrays[f"rays_{name}_d"] = d
+        arrays[f"rays_{name}_tmin"] = tmin
+        arrays[f"rays_{name}_ds"] = ds
+        arrays[f"rays_{name}_n"] = n
+        meta.setdefault("cameras", {})[name] = {
+            "eye": list(map(float, cam.eye)), "target": list(map(float, cam.target)),
+            "up": list(map(float, cam.up)), "fov_y": float(cam.fov_y),
+            "width": cam.width, "height": cam.height}
+
+    # --- per-sample evaluation (model.py:248-279, 368-382)
+    p = rng.uniform(0.0, 1.0, size=(4096, 3))
+    p[:8] = [[0, 0, 0], [1, 1, 1], [0, 1, 0], [1, 0, 1], [0.5, 0.5, 0.5],
+             [-0.1, 0.5, 1.2], [1.0, 0.999999, 1e-9], [0.25, 0.75, 0.125]]
+    dirs = rng.normal(size=(4096, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    arrays["eval_p"] = p
+    arrays["eval_d"] = dirs
+    for k, m in models.items():
+        t = 6.5 if m.is_temporal else None
+        x = assemble_input(m, p[:257], dirs[:257] if m.config.direction_mode != "pos" else None, t)
+        arrays[f"assemble_{k}"] = x
+        if m.config.head == "density":
+            if m.is_temporal:
+                for tt in (1.0, 6.5, 11.0, 16.25, 21.0, 0.0, 30.0):
+                    arrays[f"density_{k}_t{tt}"] = eval_density(m, p, t=tt)
+            else:
+                arrays[f"density_{k}"] = eval_density(m, p)
+        else:
+            dd = dirs if m.config.direction_mode != "pos" else None
+            arrays[f"color_{k}"] = eval_color(m, p, dd)
+    # fused operator (fused.py:281-301)
+    for k in ("cfg1", "color_pos", "random_fourier"):
+        m = models[k]
+        x = rng.uniform(-1, 1, size=(1000, m.config.input_width)).astype(np.float32)
+        arrays[f"fused_x_{k}"] = x
+        arrays[f"fused_y_{k}"] = fused_eval(plan_for_model(m), m, x)
+
+    # --- transfer functions (transfer.py:57-65)
+    dens = np.concatenate([np.linspace(-0.2, 1.2, 141), rng.uniform(0, 1, 200)]).astype(np.float32)
+    arrays["tf_density"] = dens
+    for name, tf in TF_PRESETS.items():
+        rgb, sig = tf_eval(tf, dens)
+        arrays[f"tf_{name}_rgb"] = rgb
+        arrays[f"tf_{name}_sigma"] = sig
+
+    # --- renders (render.py:314-332), counted evals
+    def add_render(tag, model, tf_name, cam, settings, t=None, fused=True):
+        tf = TF_PRESETS[tf_name] if tf_name else None
+        img, cnt = counted_render(model, tf, cam, settings, t, fused)
+        arrays[f"render_{tag}"] = img
+        meta["renders"][tag] = {
+            "count": int(cnt), "tf": tf_name, "t": t,
+            "stepsize": settings.stepsize, "max_steps": settings.max_steps,
+            "background": list(settings.background), "et": settings.early_term_alpha,
+            "camera": {"eye": list(map(float, cam.eye)), "target": list(map(float, cam.target)),
+                       "up": list(map(float, cam.up)), "fov_y": float(cam.fov_y),
+                       "width": cam.width, "height": cam.height}}
+        print("render", tag, cnt, flush=True)
+
+    s128 = RenderSettings(stepsize=1.0 / 128)
+    fib128 = fibonacci_cameras(8, 128, 128)
+    add_render("cfg1_v0_gray", models["cfg1"], "grayscale", fib128[0], s128)
+    add_render("cfg1_v3_gray", models["cfg1"], "grayscale", fib128[3], s128)
+    fib64 = fibonacci_cameras(8, 64, 64)
+    add_render("cfg1_v6_warm", models["cfg1"], "warm", fib64[6], s128)
+    add_render("cfg1_v1_peaks_bg", models["cfg1"], "two_peaks", fib64[1],
+               RenderSettings(stepsize=1.0 / 100, background=(0.2, 0.3, 0.4)))
+    add_render("cfg2_v2_gray", models["cfg2"], "grayscale", fib64[2], RenderSettings(stepsize=1 / 256))
+    add_render("tiny_center_gray", models["tiny"], "grayscale", cams["center"],
+               RenderSettings(stepsize=1 / 64))
+    add_render("temporal_t6.5", models["temporal"], "grayscale", fib64[4],
+               RenderSettings(stepsize=1 / 128), t=6.5)
+    add_render("temporal_both_t3", models["temporal_both"], "warm", fib64[0],
+               RenderSettings(stepsize=1 / 96), t=3.0)
+    add_render("color_dirf", models["color_dirf"], None, fib64[5], RenderSettings(stepsize=1 / 64))
+    add_render("color_pos_et", models["color_pos"], None, fib64[7],
+               RenderSettings(stepsize=1 / 128, early_term_alpha=0.5))
+    add_render("inside_gray", models["cfg1"], "grayscale", cams["inside"],
+               RenderSettings(stepsize=1 / 128))
+    add_render("cfg3_v0_gray_48", models["cfg3"], "grayscale", fibonacci_cameras(8, 48, 48)[0],
+               RenderSettings(stepsize=1 / 192), fused=False)  # CapacityError on fused
+
+    # --- raymarch_forward on explicit rays, max_steps cap (render.py:203-238)
+    o = np.column_stack([rng.uniform(0.2, 0.8, 64), rng.uniform(0.2, 0.8, 64), np.full(64, -0.5)])
+    d = np.column_stack([rng.uniform(-0.2, 0.2, 64), rng.uniform(-0.2, 0.2, 64), np.ones(64)])
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    arrays["rays_explicit_o"] = o
+    arrays["rays_explicit_d"] = d
+    px, _ = raymarch_forward(ModelSource(models["cfg1"], TF_PRESETS["warm"], use_fused=True), o, d,
+                             RenderSettings(stepsize=1 / 300, max_steps=200))
+    arrays["rays_explicit_px"] = px
+
+    # --- decode (model.py:385-398)
+    arrays["decode_tiny_9"] = decode_volume(models["tiny"], 9).values
+    arrays["decode_cfg1_17"] = decode_volume(models["cfg1"], 17).values
+    arrays["decode_temporal_12_t16.25"] = decode_volume(models["temporal"], 12, t=16.25).values
+
+    # --- checkpoints written by the reference (model.py:430-472)
+    checkpoint_save(models["tiny"], HERE / "tiny_f32.fvsrn", "f32", "f32")
+    checkpoint_save(models["tiny"], HERE / "tiny_f16_u8.fvsrn", "f16", "u8")
+    checkpoint_save(models["temporal_both"], HERE / "temporal_both_f32.fvsrn", "f32", "f32")
+    from fvsrn.model import checkpoint_load
+    for name in ("tiny_f32", "tiny_f16_u8", "temporal_both_f32"):
+        back = checkpoint_load(HERE / f"{name}.fvsrn")
+        t = 3.0 if back.is_temporal else None
+        arrays[f"ckpt_{name}_density"] = eval_density(back, p[:512], t=t)
+
+    np.savez_compressed(HERE / "golden.npz", **arrays)
+    with open(HERE / "golden.json", "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    print("wrote", HERE / "golden.npz", os.path.getsize(HERE / "golden.npz"), "bytes")
+
+
+if __name__ == "__main__":
+    main()
