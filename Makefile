@@ -1,0 +1,22 @@
+# Builds the C-ABI shared library in-tree (travels to the GPU box with gpurun).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+CSRC := paper_2112_01579_b200/csrc
+LIB  := paper_2112_01579_b200/libfvsrn_b200.so
+SRCS := $(CSRC)/fvsrn_kernels.cu $(CSRC)/fvsrn_capi.cu
+HDRS := $(CSRC)/fvsrn_device.cuh $(CSRC)/fvsrn_kernels.cuh include/fvsrn_b200.h
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Xptxas -v --expt-relaxed-constexpr -Iinclude
+
+all: $(LIB)
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcudart_static -ldl -lrt -lpthread 2> build/ptxas.log || (cat build/ptxas.log; false)
+	@grep -E "registers|spill" build/ptxas.log | head -40
+
+$(shell mkdir -p build)
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean

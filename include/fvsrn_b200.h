@@ -1,0 +1,147 @@
+/*
+ * fvsrn_b200.h -- C ABI of the B200-native fV-SRN direct-volume-rendering path.
+ *
+ * The reference (`fvsrn` 0.1.0, /root/reference/pkg/src/fvsrn) is pure Python;
+ * its seams for this path are Python protocols, not a C ABI.  Each entry point
+ * below replaces one of them (citations are reference file:line):
+ *
+ *   fvsrn_model_create      <- model upload implied by ModelSource.__init__       render.py:147-166
+ *                              (weights/B/grid(s) of FvsrnModel                   model.py:136-162)
+ *   fvsrn_render            <- render_image(ModelSource(...), camera, settings)   render.py:314-332
+ *   fvsrn_render_device     <- same, device framebuffer / screen-tile subset      (multi-GPU)
+ *   fvsrn_render_rays       <- raymarch_forward(source, origins, dirs, settings)  render.py:203-238
+ *   fvsrn_eval_density      <- eval_density(model, p, t)                          model.py:368-373
+ *   fvsrn_eval_color        <- eval_color(model, p, d, t)                         model.py:376-382
+ *   fvsrn_decode_density    <- decode_volume(model, resolution, t)                model.py:385-398
+ *   fvsrn_fused_eval        <- fused_eval(plan, model, x)                         fused.py:281-301
+ *
+ * Conventions: every function returns an fvsrn_status; on failure
+ * fvsrn_last_error() (thread-local) holds a message.  Host-pointer variants are
+ * synchronous and copy results back; *_device variants take device pointers and
+ * a cudaStream_t (passed as void*) and are stream-ordered.  No function keeps a
+ * reference to caller memory after returning.  A model handle is immutable
+ * after creation and may be used concurrently from several host threads
+ * (per-call stream-ordered scratch, no global mutable state).
+ *
+ * There is no CPU fallback: without an sm_100a device every compute call fails
+ * with FVSRN_ECUDA.
+ */
+#ifndef FVSRN_B200_H
+#define FVSRN_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FVSRN_API __attribute__((visibility("default")))
+#else
+#define FVSRN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FVSRN_OK = 0,
+  FVSRN_EINVAL = 1,     /* contract violation      -> ValueError   */
+  FVSRN_ECAPACITY = 2,  /* network too large        -> CapacityError */
+  FVSRN_ECUDA = 3,      /* CUDA / device failure    -> RuntimeError */
+  FVSRN_ENOMEM = 4
+} fvsrn_status;
+
+/* nn.py:15 ACTIVATION_KINDS order */
+enum { FVSRN_ACT_RELU = 0, FVSRN_ACT_SIGMOID = 1, FVSRN_ACT_SOFTPLUS = 2,
+       FVSRN_ACT_SNAKE = 3, FVSRN_ACT_SNAKE_ALT = 4 };
+enum { FVSRN_HEAD_DENSITY = 0, FVSRN_HEAD_COLOR = 1 };              /* model.py:73 */
+enum { FVSRN_DIR_POS = 0, FVSRN_DIR_P = 1, FVSRN_DIR_F = 2 };       /* model.py:46 */
+enum { FVSRN_TIME_NONE = 0, FVSRN_TIME_DIRECT = 1, FVSRN_TIME_FOURIER = 2,
+       FVSRN_TIME_BOTH = 3 };                                          /* model.py:47 */
+enum { FVSRN_FOURIER_OFF = 0, FVSRN_FOURIER_NERF = 1, FVSRN_FOURIER_RANDOM = 2 };
+enum { FVSRN_GRID_F32 = 0, FVSRN_GRID_U8 = 1 };                      /* model.py:430-472 */
+
+typedef struct fvsrn_model* fvsrn_model_t;
+
+/* Everything FvsrnModel holds (model.py:136-162), as plain arrays. */
+typedef struct {
+  int32_t layers, hidden, d_in, d_out;     /* d_in = ModelConfig.input_width  */
+  int32_t activation, head, direction_mode;
+  int32_t fourier_mode, fourier_m, fourier_d_in;
+  const float* b_matrix;                   /* (fourier_m, fourier_d_in) f32    */
+  int32_t time_mode, time_fourier_count;
+  const float* time_b;                     /* (time_fourier_count,) f32 or NULL */
+  int32_t has_time_range; double time_range[2];
+  int32_t grid_resolution, grid_channels;  /* 0 disables the latent grid       */
+  int32_t n_grids;                         /* 1 static, or #keyframes          */
+  const double* keyframe_times;            /* n_grids entries if temporal      */
+  int32_t temporal;                        /* keyframe model?                  */
+  int32_t grid_precision;                  /* FVSRN_GRID_F32 | FVSRN_GRID_U8   */
+  const float* const* grids;               /* n_grids x (R,R,R,F) f32 (F32)    */
+  const uint8_t* const* grid_codes;        /* n_grids x (R,R,R,F) u8   (U8)    */
+  const float* const* grid_mins;           /* n_grids x (F,) f32       (U8)    */
+  const float* const* grid_maxs;           /* n_grids x (F,) f32       (U8)    */
+  const float* const* weights;             /* layers x (out,in) f32 row-major  */
+  const float* const* biases;              /* layers x (out,)       f32        */
+} fvsrn_model_desc;
+
+/* TransferFunction (transfer.py:11-54); n <= 64 control points. */
+typedef struct { int32_t n; const float* xs; const float* rgbs; const float* sigmas; } fvsrn_tf;
+
+/* Camera (imaging.py:14-42).  has_basis != 0: the caller supplies the per-frame
+ * basis of render.py:78-86 (forward, right, up', tan(fov/2)*W/H, tan(fov/2))
+ * computed with the reference's own numpy ops, making per-pixel rays bit-exact. */
+typedef struct {
+  double eye[3], target[3], up[3]; double fov_y; int32_t width, height;
+  int32_t has_basis; double b_forward[3], b_right[3], b_up[3]; double half_w, half_h;
+} fvsrn_camera;
+
+/* RenderSettings (render.py:49-69). */
+typedef struct {
+  double stepsize; int32_t max_steps; double background[3];
+  double early_term_alpha; double eps_blend;
+} fvsrn_settings;
+
+/* Screen-tile shard: this call renders tiles t = rank + k*world (8x8 px tiles,
+ * row-major tile order).  compact != 0 writes slot-ordered output
+ * (n_local_tiles*64 RGBA px) instead of the row-major frame. */
+typedef struct { int32_t rank, world, compact; } fvsrn_shard;
+
+FVSRN_API const char* fvsrn_last_error(void);
+FVSRN_API const char* fvsrn_version(void);
+FVSRN_API int32_t fvsrn_device_count(void);
+
+FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
+FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);
+/* Padded widths (K0, hidden_pad, out_pad), smem bytes; for plan/introspection. */
+FVSRN_API int32_t fvsrn_model_info(fvsrn_model_t model, int32_t* k0_pad, int32_t* hidden_pad,
+                         int32_t* smem_bytes);
+
+/* Full frame into host RGBA f32 (H,W,4); eval_count may be NULL. */
+FVSRN_API int32_t fvsrn_render(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,
+                     const fvsrn_settings* settings, double t, float* out_rgba,
+                     uint64_t* eval_count);
+/* Device framebuffer, stream-ordered; shard may be NULL (whole frame).
+ * d_eval_count: device u64 accumulated atomically, may be NULL. */
+FVSRN_API int32_t fvsrn_render_device(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,
+                            const fvsrn_settings* settings, double t, const fvsrn_shard* shard,
+                            float* d_out, unsigned long long* d_eval_count, void* stream);
+/* Reassemble world compact shard buffers [world][max_local_tiles*64][4] into (H,W,4). */
+FVSRN_API int32_t fvsrn_tiles_to_frame_device(const float* d_gathered, int32_t width, int32_t height,
+                                    int32_t world, float* d_frame, void* stream);
+/* raymarch_forward over explicit f64 rays (host arrays). */
+FVSRN_API int32_t fvsrn_render_rays(fvsrn_model_t model, const fvsrn_tf* tf, const double* origins,
+                          const double* dirs, int64_t n, const fvsrn_settings* settings,
+                          double t, float* out_px, uint64_t* eval_count);
+FVSRN_API int32_t fvsrn_eval_density(fvsrn_model_t model, const double* p, int64_t n, double t,
+                           float* out);
+FVSRN_API int32_t fvsrn_eval_color(fvsrn_model_t model, const double* p, const double* d, int64_t n,
+                         double t, float* out4);
+FVSRN_API int32_t fvsrn_decode_density(fvsrn_model_t model, int32_t resolution, double t, float* out);
+FVSRN_API int32_t fvsrn_decode_density_device(fvsrn_model_t model, int32_t resolution, double t,
+                                    int64_t lattice_begin, int64_t lattice_count,
+                                    float* d_out, void* stream);
+FVSRN_API int32_t fvsrn_fused_eval(fvsrn_model_t model, const float* x, int64_t n, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVSRN_B200_H */

@@ -1,0 +1,23 @@
+"""B200-native fV-SRN direct volume rendering (arXiv 2112.01579).
+
+Drop-in for the DVR hot path of the reference package ``fvsrn`` 0.1.0: the same
+host API (ModelConfig / model_init / checkpoint_load, TransferFunction, Camera,
+RenderSettings, ModelSource, render_image, raymarch_forward, eval_density,
+decode_volume, fused_eval), with every evaluation running in hand-written
+sm_100a CUDA kernels behind the C ABI of ``include/fvsrn_b200.h``.
+"""
+
+__version__ = "0.1.0"
+
+from ._lib import CapacityError
+from .fused import FusedPlan, fused_eval, plan_build, plan_for_model, warmup
+from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
+                   grid_quantize)
+from .imaging import Camera, Image, metric_psnr, png_bytes, write_png
+from .model import (CheckpointError, FvsrnModel, ModelConfig, checkpoint_load, checkpoint_save,
+                    decode_volume, eval_color, eval_density, memory_footprint, model_init)
+from .nn import FourierEncoder, MlpParams, fourier_make, init_params, nerf_rows
+from .render import (ModelSource, RayState, RenderSettings, camera_rays, fibonacci_cameras,
+                     raymarch_forward, render_image, render_rays)
+from .transfer import TF_PRESETS, TransferFunction, tf_from_json, tf_load, tf_save
+from .volume import ScalarVolume

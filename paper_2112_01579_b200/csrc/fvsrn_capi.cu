@@ -1,0 +1,789 @@
+// fvsrn_capi.cu -- the C ABI (include/fvsrn_b200.h): model upload, weight/grid
+// packing, per-frame constants, kernel launches.  Host code only.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fvsrn_b200.h"
+#include "fvsrn_kernels.cuh"
+
+using namespace fvsrn;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(FVSRN_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct Pack {                     // fragment-ordered weights + padded biases
+  std::vector<uint2> frag;
+  std::vector<float> bias;
+  std::vector<int> w_off, b_off;
+  int kt0 = 0;
+};
+
+// W_dev[l] : (N_l x K_l) floats in device column order (zero padded)
+void build_pack(const std::vector<std::vector<float>>& wdev, const std::vector<int>& K,
+                const std::vector<int>& N, const std::vector<std::vector<float>>& bdev, Pack& pk) {
+  const int L = (int)wdev.size();
+  pk.w_off.assign(L + 1, 0);
+  pk.b_off.assign(L + 1, 0);
+  pk.frag.clear();
+  pk.bias.clear();
+  for (int l = 0; l < L; ++l) {
+    pk.w_off[l] = (int)pk.frag.size();
+    pk.b_off[l] = (int)pk.bias.size();
+    const int KT = K[l] / 16, NT = N[l] / 8;
+    const auto& W = wdev[l];
+    for (int kt = 0; kt < KT; ++kt)
+      for (int nt = 0; nt < NT; ++nt)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int g = lane >> 2, q = lane & 3;
+          const int n = nt * 8 + g, k0 = kt * 16 + 2 * q;
+          auto h = [&](int k) { return __half_as_ushort(__float2half_rn(W[(size_t)n * K[l] + k])); };
+          uint2 u;
+          u.x = (uint32_t)h(k0) | ((uint32_t)h(k0 + 1) << 16);
+          u.y = (uint32_t)h(k0 + 8) | ((uint32_t)h(k0 + 9) << 16);
+          pk.frag.push_back(u);
+        }
+    for (int n = 0; n < N[l]; ++n) pk.bias.push_back(bdev[l][n]);
+  }
+  pk.w_off[L] = (int)pk.frag.size();
+  pk.b_off[L] = (int)pk.bias.size();
+}
+
+struct DevPack {
+  uint2* frag = nullptr;
+  float* bias = nullptr;
+  NetDev net{};
+};
+
+}  // namespace
+
+struct fvsrn_model {
+  int device = 0;
+  int layers = 0, hidden = 0, hid_pad = 0, d_in = 0, d_out = 0, act = 0, head = 0;
+  int dir_mode = 0, fourier_mode = 0, m = 0, fd_in = 3, raw_w = 3;
+  int time_mode = 0, tfc = 0, T = 0;
+  std::vector<float> time_b;
+  bool has_time_range = false;
+  double time_range[2] = {0, 0};
+  bool temporal = false;
+  std::vector<double> kf_times;
+  int R = 0, F = 0, f_pad = 0;
+  std::vector<__half*> grids;       // fp16 (R,R,R,f_pad)
+  float* d_bmat = nullptr;
+  int four_off = 0, raw_off = 0, k0 = 0;
+  // sample pack (device column order, time folded) and x pack (reference order)
+  DevPack ps, px;
+  int k0x = 0;
+  std::vector<float> b0_static;     // layer-0 bias, padded N0
+  std::vector<float> w0_time;       // N0 x T time columns of W0
+  int n0 = 0;
+  int num_sms = 148;
+  ~fvsrn_model() {
+    cudaSetDevice(device);
+    for (auto* g : grids) cudaFree(g);
+    cudaFree(d_bmat);
+    cudaFree(ps.frag); cudaFree(ps.bias);
+    cudaFree(px.frag); cudaFree(px.bias);
+  }
+};
+
+namespace {
+
+int upload(const void* host, size_t bytes, void** dev) {
+  CUDA_TRY(cudaMalloc(dev, bytes));
+  CUDA_TRY(cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice));
+  return FVSRN_OK;
+}
+
+int make_devpack(const Pack& pk, int layers, int act, int head, int out_real, DevPack& dp) {
+  int rc = upload(pk.frag.data(), pk.frag.size() * sizeof(uint2), (void**)&dp.frag);
+  if (rc) return rc;
+  rc = upload(pk.bias.data(), pk.bias.size() * sizeof(float), (void**)&dp.bias);
+  if (rc) return rc;
+  NetDev& n = dp.net;
+  n.wfrag = dp.frag;
+  n.bias = dp.bias;
+  n.layers = layers;
+  n.kt0 = pk.kt0;
+  n.act = act;
+  n.head = head;
+  n.out_real = out_real;
+  for (int l = 0; l <= layers; ++l) { n.w_off[l] = pk.w_off[l]; n.b_off[l] = pk.b_off[l]; }
+  n.w_total = (int)pk.frag.size();
+  n.b_total = (int)pk.bias.size();
+  return FVSRN_OK;
+}
+
+std::vector<__half> to_half_padded(const float* src, int R, int F, int f_pad) {
+  const size_t nvox = (size_t)R * R * R;
+  std::vector<__half> h(nvox * f_pad, __float2half_rn(0.f));
+  for (size_t v = 0; v < nvox; ++v)
+    for (int c = 0; c < F; ++c) h[v * f_pad + c] = __float2half_rn(src[v * F + c]);
+  return h;
+}
+
+// time features for a per-frame scalar t (model.py:190-197, 236-245)
+std::vector<double> time_features(const fvsrn_model* m, double t) {
+  double t0, t1;
+  if (m->has_time_range) { t0 = m->time_range[0]; t1 = m->time_range[1]; }
+  else { t0 = m->kf_times.front(); t1 = m->kf_times.back(); }
+  double tn = (t1 == t0) ? 0.0 : (std::min(std::max(t, t0), t1) - t0) / (t1 - t0);
+  std::vector<double> f;
+  if (m->time_mode == FVSRN_TIME_DIRECT || m->time_mode == FVSRN_TIME_BOTH) f.push_back(tn);
+  if (m->time_mode == FVSRN_TIME_FOURIER || m->time_mode == FVSRN_TIME_BOTH) {
+    std::vector<double> s, c;
+    for (int j = 0; j < m->tfc; ++j) {
+      double ph = tn * (double)m->time_b[j];
+      s.push_back(std::sin(ph));
+      c.push_back(std::cos(ph));
+    }
+    f.insert(f.end(), s.begin(), s.end());
+    f.insert(f.end(), c.begin(), c.end());
+  }
+  return f;
+}
+
+// keyframe bracket (model.py:200-209 for a scalar t)
+void bracket(const std::vector<double>& times, double t, int& lo, int& hi, double& w) {
+  const int n = (int)times.size();
+  double tc = std::min(std::max(t, times.front()), times.back());
+  int h = (int)(std::lower_bound(times.begin(), times.end(), tc) - times.begin());
+  h = std::min(std::max(h, 0), n - 1);
+  int l = (h > 0 && times[h] != tc) ? h - 1 : h;
+  lo = l; hi = h;
+  w = (h > l) ? (tc - times[l]) / (times[h] - times[l]) : 0.0;
+}
+
+struct FrameScratch {
+  void* buf = nullptr;
+  const __half* grid = nullptr;
+  float* b0 = nullptr;
+  TFDev* tf = nullptr;
+  unsigned long long* counters = nullptr;   // [0] queue, [1] evals
+};
+
+// Per-call device scratch: effective layer-0 bias (time folded), TF table,
+// counters, and the time-blended latent grid.  Stream-ordered allocation.
+int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t s,
+                FrameScratch& fs) {
+  if (m->temporal && !std::isfinite(t)) return fail(FVSRN_EINVAL, "timestep must be finite");
+  std::vector<float> b0 = m->b0_static;
+  if (m->T > 0) {
+    std::vector<double> f = time_features(m, t);
+    for (int n = 0; n < m->n0; ++n) {
+      float acc = b0[n];
+      for (int j = 0; j < m->T; ++j) acc += m->w0_time[(size_t)n * m->T + j] * (float)f[j];
+      b0[n] = acc;
+    }
+  }
+  TFDev th{};
+  if (tf) {
+    if (tf->n < 2 || tf->n > kMaxTF) return fail(FVSRN_EINVAL, "transfer function needs 2..64 points");
+    th.n = tf->n;
+    for (int i = 0; i < tf->n; ++i) {
+      th.xs[i] = tf->xs[i];
+      for (int c = 0; c < 3; ++c) th.val[i][c] = tf->rgbs[3 * i + c];
+      th.val[i][3] = tf->sigmas[i];
+    }
+    for (int i = 0; i + 1 < tf->n; ++i)
+      for (int c = 0; c < 4; ++c) {
+        double y0 = (c < 3) ? tf->rgbs[3 * i + c] : tf->sigmas[i];
+        double y1 = (c < 3) ? tf->rgbs[3 * (i + 1) + c] : tf->sigmas[i + 1];
+        th.slope[i][c] = (float)((y1 - y0) / ((double)tf->xs[i + 1] - (double)tf->xs[i]));
+      }
+  }
+  size_t grid_bytes = 0;
+  int lo = 0, hi = 0;
+  double w = 0.0;
+  if (m->f_pad > 0 && m->temporal) {
+    bracket(m->kf_times, t, lo, hi, w);
+    if (hi != lo) grid_bytes = (size_t)m->R * m->R * m->R * m->f_pad * sizeof(__half);
+  }
+  const size_t off_tf = 0, off_b0 = (sizeof(TFDev) + 255) / 256 * 256;
+  const size_t off_ct = off_b0 + 1024, off_grid = off_ct + 256;
+  CUDA_TRY(cudaMallocAsync(&fs.buf, off_grid + grid_bytes, s));
+  char* base = (char*)fs.buf;
+  fs.tf = (TFDev*)(base + off_tf);
+  fs.b0 = (float*)(base + off_b0);
+  fs.counters = (unsigned long long*)(base + off_ct);
+  CUDA_TRY(cudaMemcpyAsync(fs.tf, &th, sizeof(TFDev), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(fs.b0, b0.data(), b0.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(fs.counters, 0, 2 * sizeof(unsigned long long), s));
+  fs.grid = m->f_pad > 0 ? m->grids[m->temporal ? lo : 0] : nullptr;
+  if (grid_bytes) {
+    __half* g = (__half*)(base + off_grid);
+    CUDA_TRY(launch_blend(m->grids[lo], m->grids[hi], (float)w,
+                          (long long)m->R * m->R * m->R * m->f_pad, g, s));
+    fs.grid = g;
+  }
+  return FVSRN_OK;
+}
+
+FeatDev feat_for(const fvsrn_model* m, const __half* grid) {
+  FeatDev fd{};
+  fd.grid_res = m->R;
+  fd.f_pad = m->f_pad;
+  fd.grid = grid;
+  fd.fourier_mode = m->fourier_mode;
+  fd.m = m->m;
+  fd.fd_in = m->fd_in;
+  fd.bmat = m->d_bmat;
+  fd.four_off = m->four_off;
+  fd.raw_off = m->raw_off;
+  fd.raw_w = m->raw_w;
+  fd.k0 = m->k0;
+  fd.dir_mode = m->dir_mode;
+  return fd;
+}
+
+int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
+           long long work_warps) {
+  const void* fn = kernel_for(kind, m->hid_pad);
+  if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+  if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
+  long long blocks = (long long)m->num_sms * occ;
+  const long long need = (work_warps + (kThreads / 32) - 1) / (kThreads / 32);
+  if (need < blocks) blocks = std::max(1ll, need);
+  CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(kThreads), args, smem, s));
+  return FVSRN_OK;
+}
+
+MarchDev march_for(const fvsrn_settings* st) {
+  MarchDev md{};
+  md.stepsize = st->stepsize;
+  md.max_steps = st->max_steps;
+  md.et_alpha = st->early_term_alpha;
+  md.eps_blend = st->eps_blend;
+  for (int c = 0; c < 3; ++c) md.bg[c] = (float)st->background[c];
+  return md;
+}
+
+int check_settings(const fvsrn_settings* st) {
+  if (!st) return fail(FVSRN_EINVAL, "settings required");
+  if (!(st->stepsize > 0)) return fail(FVSRN_EINVAL, "stepsize must be positive");
+  if (!(st->early_term_alpha >= 0.0 && st->early_term_alpha <= 1.0))
+    return fail(FVSRN_EINVAL, "early termination threshold must lie in [0,1]");
+  if (st->max_steps < 1) return fail(FVSRN_EINVAL, "max_steps must be >= 1");
+  return FVSRN_OK;
+}
+
+int check_source(const fvsrn_model* m, const fvsrn_tf* tf, double t) {
+  if (m->head == FVSRN_HEAD_DENSITY && !tf)
+    return fail(FVSRN_EINVAL, "density-head models need a transfer function to render");
+  if (m->head == FVSRN_HEAD_COLOR && tf)
+    return fail(FVSRN_EINVAL, "color-head models do not take a transfer function");
+  if (!m->temporal && !std::isnan(t)) return fail(FVSRN_EINVAL, "timestep supplied to a non-temporal model");
+  if (m->temporal && std::isnan(t)) return fail(FVSRN_EINVAL, "temporal model requires a timestep to render");
+  return FVSRN_OK;
+}
+
+CamDev cam_for(const fvsrn_camera* c) {
+  // Same op sequence as render.py:78-86 (used when the caller does not pass the
+  // numpy-computed basis; the Python shim always passes it, see render.py host mirror).
+  CamDev cd{};
+  double f[3], r[3], u[3];
+  for (int a = 0; a < 3; ++a) f[a] = c->target[a] - c->eye[a];
+  double nf = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  for (int a = 0; a < 3; ++a) f[a] /= nf;
+  r[0] = f[1] * c->up[2] - f[2] * c->up[1];
+  r[1] = f[2] * c->up[0] - f[0] * c->up[2];
+  r[2] = f[0] * c->up[1] - f[1] * c->up[0];
+  double nr = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  for (int a = 0; a < 3; ++a) r[a] /= nr;
+  u[0] = r[1] * f[2] - r[2] * f[1];
+  u[1] = r[2] * f[0] - r[0] * f[2];
+  u[2] = r[0] * f[1] - r[1] * f[0];
+  for (int a = 0; a < 3; ++a) { cd.eye[a] = c->eye[a]; cd.fwd[a] = f[a]; cd.right[a] = r[a]; cd.up[a] = u[a]; }
+  cd.half_h = std::tan(c->fov_y / 2.0);
+  cd.half_w = cd.half_h * c->width / c->height;
+  cd.W = c->width;
+  cd.H = c->height;
+  return cd;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char* fvsrn_last_error(void) { return g_err.c_str(); }
+const char* fvsrn_version(void) { return "fvsrn_b200 0.1.0 (sm_100a, mma.sync f16/f32)"; }
+
+int32_t fvsrn_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_model_t* out) {
+  if (!d || !out) return fail(FVSRN_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->layers < 1 || d->hidden < 1) return fail(FVSRN_EINVAL, "layers and hidden must be positive");
+  if (d->layers > kMaxLayers) return fail(FVSRN_ECAPACITY, "too many layers for the GPU path");
+  if (d->head != FVSRN_HEAD_DENSITY && d->head != FVSRN_HEAD_COLOR) return fail(FVSRN_EINVAL, "bad head");
+  if (d->activation < 0 || d->activation > 4) return fail(FVSRN_EINVAL, "bad activation");
+  const int d_out = d->head == FVSRN_HEAD_DENSITY ? 1 : 4;
+  if (d->d_out != d_out) return fail(FVSRN_EINVAL, "d_out does not match head");
+  auto* m = new fvsrn_model();
+  std::unique_ptr<fvsrn_model> guard(m);
+  m->device = device;
+  m->layers = d->layers;
+  m->hidden = d->hidden;
+  m->hid_pad = round_up(d->hidden, 16);
+  if (m->hid_pad > kMaxHidden)
+    return fail(FVSRN_ECAPACITY, "hidden width " + std::to_string(d->hidden) + " exceeds the GPU path limit 128");
+  m->d_in = d->d_in;
+  m->d_out = d_out;
+  m->act = d->activation;
+  m->head = d->head;
+  m->dir_mode = d->direction_mode;
+  m->raw_w = d->direction_mode != FVSRN_DIR_POS ? 6 : 3;
+  m->fourier_mode = d->fourier_m > 0 ? d->fourier_mode : FVSRN_FOURIER_OFF;
+  m->m = m->fourier_mode == FVSRN_FOURIER_OFF ? 0 : d->fourier_m;
+  m->fd_in = d->fourier_d_in;
+  m->time_mode = d->time_mode;
+  m->tfc = d->time_fourier_count;
+  m->T = (d->time_mode == FVSRN_TIME_NONE) ? 0
+       : (d->time_mode == FVSRN_TIME_DIRECT) ? 1
+       : (d->time_mode == FVSRN_TIME_FOURIER) ? 2 * d->time_fourier_count
+                                              : 1 + 2 * d->time_fourier_count;
+  if (m->time_mode == FVSRN_TIME_FOURIER || m->time_mode == FVSRN_TIME_BOTH) {
+    if (!d->time_b) return fail(FVSRN_EINVAL, "time Fourier matrix required");
+    m->time_b.assign(d->time_b, d->time_b + d->time_fourier_count);
+  }
+  m->has_time_range = d->has_time_range != 0;
+  m->time_range[0] = d->time_range[0];
+  m->time_range[1] = d->time_range[1];
+  m->temporal = d->temporal != 0;
+  if (m->temporal) {
+    if (d->n_grids < 1 || !d->keyframe_times) return fail(FVSRN_EINVAL, "temporal model needs keyframes");
+    m->kf_times.assign(d->keyframe_times, d->keyframe_times + d->n_grids);
+    for (size_t i = 1; i < m->kf_times.size(); ++i)
+      if (!(m->kf_times[i] > m->kf_times[i - 1]))
+        return fail(FVSRN_EINVAL, "keyframe times must be strictly increasing");
+  }
+  m->R = d->grid_resolution;
+  m->F = d->grid_resolution > 0 ? d->grid_channels : 0;
+  m->f_pad = round_up(m->F, 8);
+  if (m->R == 1 || (m->R > 0 && m->F < 1)) return fail(FVSRN_EINVAL, "need R >= 2 and F >= 1");
+  // ---- device feature layout: [z | (sin,cos) pairs | raw] padded to 16
+  m->four_off = m->f_pad;
+  m->raw_off = m->f_pad + 2 * m->m;
+  const int width = m->raw_off + m->raw_w;
+  m->k0 = round_up(width, 16);
+  const int ref_w = m->raw_w + 2 * m->m + m->T + m->F;
+  if (ref_w != d->d_in)
+    return fail(FVSRN_EINVAL, "input width " + std::to_string(d->d_in) + " does not match config (" +
+                                  std::to_string(ref_w) + ")");
+  if (m->k0 > 256 || round_up(d->d_in, 16) > 256) return fail(FVSRN_ECAPACITY, "input too wide for the GPU path");
+  if (m->fourier_mode == FVSRN_FOURIER_NERF || m->fourier_mode == FVSRN_FOURIER_RANDOM) {
+    if (!d->b_matrix) return fail(FVSRN_EINVAL, "Fourier matrix required");
+    if (m->fd_in != 3 && m->fd_in != 6) return fail(FVSRN_EINVAL, "Fourier input must be 3 or 6 wide");
+  }
+  if (m->fourier_mode == FVSRN_FOURIER_NERF) {
+    // the recurrence assumes B = nerf_rows(m, fd_in) (nn.py:47-57); verify it
+    for (int i = 0; i < m->m; ++i)
+      for (int a = 0; a < m->fd_in; ++a) {
+        float want = (a == i % m->fd_in) ? (float)(2.0 * M_PI * std::ldexp(1.0, i / m->fd_in)) : 0.f;
+        if (d->b_matrix[i * m->fd_in + a] != want)
+          return fail(FVSRN_EINVAL, "nerf Fourier matrix is not the stacked powers-of-two identity");
+      }
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  {
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(FVSRN_ECUDA, "sm_100a device required");
+    m->num_sms = prop.multiProcessorCount;
+  }
+  if (m->fourier_mode == FVSRN_FOURIER_RANDOM) {
+    int rc = upload(d->b_matrix, sizeof(float) * m->m * m->fd_in, (void**)&m->d_bmat);
+    if (rc) return rc;
+  }
+  // ---- grids (fp16, channel-padded); u8 grids are dequantised exactly as grid.py:170-172
+  if (m->R > 0) {
+    const int ng = m->temporal ? d->n_grids : 1;
+    const size_t nvals = (size_t)m->R * m->R * m->R * m->F;
+    for (int gi = 0; gi < ng; ++gi) {
+      std::vector<float> f32(nvals);
+      if (d->grid_precision == FVSRN_GRID_U8) {
+        const uint8_t* c = d->grid_codes[gi];
+        const float* mn = d->grid_mins[gi];
+        const float* mx = d->grid_maxs[gi];
+        for (size_t i = 0; i < nvals; ++i) {
+          const int ch = (int)(i % m->F);
+          f32[i] = mn[ch] + ((float)c[i] / 255.0f) * (mx[ch] - mn[ch]);
+        }
+      } else {
+        if (!d->grids || !d->grids[gi]) return fail(FVSRN_EINVAL, "grid values required");
+        std::memcpy(f32.data(), d->grids[gi], nvals * sizeof(float));
+      }
+      auto h = to_half_padded(f32.data(), m->R, m->F, m->f_pad);
+      __half* dg = nullptr;
+      int rc = upload(h.data(), h.size() * sizeof(__half), (void**)&dg);
+      if (rc) return rc;
+      m->grids.push_back(dg);
+    }
+  }
+  // ---- weights: sample pack (device column order, time columns folded out) ...
+  const int L = m->layers;
+  std::vector<int> N(L), Ks(L), Kx(L);
+  for (int l = 0; l < L; ++l) {
+    N[l] = (l == L - 1) ? 8 : m->hid_pad;
+    Ks[l] = (l == 0) ? m->k0 : m->hid_pad;
+    Kx[l] = (l == 0) ? round_up(d->d_in, 16) : m->hid_pad;
+  }
+  std::vector<std::vector<float>> ws(L), wx(L), bs(L);
+  for (int l = 0; l < L; ++l) {
+    const int out_l = (l == L - 1) ? d_out : m->hidden;
+    const int in_l = (l == 0) ? d->d_in : m->hidden;
+    const float* W = d->weights[l];
+    const float* B = d->biases[l];
+    if (!W || !B) return fail(FVSRN_EINVAL, "weights/biases required");
+    ws[l].assign((size_t)N[l] * Ks[l], 0.f);
+    wx[l].assign((size_t)N[l] * Kx[l], 0.f);
+    bs[l].assign(N[l], 0.f);
+    for (int o = 0; o < out_l; ++o) {
+      bs[l][o] = B[o];
+      for (int i = 0; i < in_l; ++i) {
+        const float w = W[(size_t)o * in_l + i];
+        wx[l][(size_t)o * Kx[l] + i] = w;
+        int dc = i;
+        if (l == 0) {
+          // reference column i -> device column (model.py:3-6 layout)
+          if (i < m->raw_w) dc = m->raw_off + i;
+          else if (i < m->raw_w + m->m) dc = m->four_off + 2 * (i - m->raw_w);
+          else if (i < m->raw_w + 2 * m->m) dc = m->four_off + 2 * (i - m->raw_w - m->m) + 1;
+          else if (i < m->raw_w + 2 * m->m + m->T) dc = -1;   // time: folded into bias
+          else dc = i - (m->raw_w + 2 * m->m + m->T);
+        }
+        if (dc >= 0) ws[l][(size_t)o * Ks[l] + dc] = w;
+      }
+    }
+  }
+  m->n0 = N[0];
+  m->b0_static = bs[0];
+  if (m->T > 0) {
+    m->w0_time.assign((size_t)N[0] * m->T, 0.f);
+    const int out0 = (L == 1) ? d_out : m->hidden;
+    for (int o = 0; o < out0; ++o)
+      for (int j = 0; j < m->T; ++j)
+        m->w0_time[(size_t)o * m->T + j] = d->weights[0][(size_t)o * d->d_in + m->raw_w + 2 * m->m + j];
+  }
+  Pack pks, pkx;
+  build_pack(ws, Ks, N, bs, pks);
+  pks.kt0 = m->k0 / 16;
+  build_pack(wx, Kx, N, bs, pkx);
+  pkx.kt0 = Kx[0] / 16;
+  m->k0x = Kx[0];
+  int rc = make_devpack(pks, L, m->act, m->head, d_out, m->ps);
+  if (rc) return rc;
+  rc = make_devpack(pkx, L, m->act, m->head, d_out, m->px);
+  if (rc) return rc;
+  *out = guard.release();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_model_destroy(fvsrn_model_t m) {
+  if (!m) return FVSRN_OK;
+  delete m;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_model_info(fvsrn_model_t m, int32_t* k0_pad, int32_t* hidden_pad, int32_t* smem) {
+  if (!m) return fail(FVSRN_EINVAL, "null model");
+  if (k0_pad) *k0_pad = m->k0;
+  if (hidden_pad) *hidden_pad = m->hid_pad;
+  if (smem) *smem = (int32_t)stage_smem_bytes(m->ps.net, true, m->k0);
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_render_device(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
+                            const fvsrn_settings* st, double t, const fvsrn_shard* shard,
+                            float* d_out, unsigned long long* d_eval_count, void* stream) {
+  if (!m || !c || !d_out) return fail(FVSRN_EINVAL, "null argument");
+  int rc = check_settings(st);
+  if (rc) return rc;
+  if ((rc = check_source(m, tf, t))) return rc;
+  if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+  CUDA_TRY(cudaSetDevice(m->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  FrameScratch fs;
+  if ((rc = frame_setup(m, t, tf, s, fs))) return rc;
+  CamDev cam = cam_for(c);
+  if (c->has_basis) {
+    for (int a = 0; a < 3; ++a) { cam.fwd[a] = c->b_forward[a]; cam.right[a] = c->b_right[a]; cam.up[a] = c->b_up[a]; }
+    cam.half_w = c->half_w;
+    cam.half_h = c->half_h;
+  }
+  ShardDev sh{};
+  sh.rank = shard ? shard->rank : 0;
+  sh.world = shard ? shard->world : 1;
+  sh.compact = shard ? shard->compact : 0;
+  if (sh.world < 1 || sh.rank < 0 || sh.rank >= sh.world) return fail(FVSRN_EINVAL, "bad shard");
+  sh.tiles_x = (c->width + kTile - 1) / kTile;
+  sh.n_tiles = sh.tiles_x * ((c->height + kTile - 1) / kTile);
+  const long long local_tiles = (sh.n_tiles - sh.rank + sh.world - 1) / sh.world;
+  long long n_slots = std::max(0ll, local_tiles) * 64;
+  if (sh.compact) {  // compact buffers are sized for max_local tiles; zero the tail
+    const long long max_local = (sh.n_tiles + sh.world - 1) / sh.world;
+    if (max_local > local_tiles)
+      CUDA_TRY(cudaMemsetAsync(d_out + local_tiles * 64 * 4, 0, (max_local - local_tiles) * 64 * 16, s));
+  }
+  NetDev net = m->ps.net;
+  FeatDev fd = feat_for(m, fs.grid);
+  MarchDev md = march_for(st);
+  const TFDev* tfp = fs.tf;
+  const float* b0 = fs.b0;
+  const double* ro = nullptr;
+  const double* rd = nullptr;
+  unsigned long long* queue = fs.counters;
+  unsigned long long* evc = d_eval_count ? d_eval_count : fs.counters + 1;
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc};
+  const size_t smem = stage_smem_bytes(net, true, m->k0);
+  if ((rc = launch(m, KernelKind::kDVR, smem, args, s, n_slots / 32 + 1))) return rc;
+  CUDA_TRY(cudaFreeAsync(fs.buf, s));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_tiles_to_frame_device(const float* d_gathered, int32_t width, int32_t height,
+                                    int32_t world, float* d_frame, void* stream) {
+  if (!d_gathered || !d_frame || world < 1) return fail(FVSRN_EINVAL, "bad argument");
+  CUDA_TRY(launch_tiles_to_frame(d_gathered, width, height, world, d_frame, (cudaStream_t)stream));
+  return FVSRN_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  ~StreamGuard() { if (s) cudaStreamDestroy(s); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
+                     const fvsrn_settings* st, double t, float* out, uint64_t* eval_count) {
+  if (!m || !c || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const size_t bytes = (size_t)c->width * c->height * 16;
+  float* d_out = nullptr;
+  unsigned long long* d_cnt = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d_out, bytes + 16, sg.s));
+  d_cnt = (unsigned long long*)((char*)d_out + bytes);
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 8, sg.s));
+  int rc = fvsrn_render_device(m, tf, c, st, t, nullptr, d_out, d_cnt, sg.s);
+  if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  unsigned long long cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(&cnt, d_cnt, 8, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(d_out, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (eval_count) *eval_count = cnt;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* origins,
+                          const double* dirs, int64_t n, const fvsrn_settings* st, double t,
+                          float* out_px, uint64_t* eval_count) {
+  if (!m || (n > 0 && (!origins || !dirs || !out_px))) return fail(FVSRN_EINVAL, "null argument");
+  int rc = check_settings(st);
+  if (rc) return rc;
+  if ((rc = check_source(m, tf, t))) return rc;
+  if (eval_count) *eval_count = 0;
+  if (n == 0) return FVSRN_OK;
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const size_t rb = (size_t)n * 3 * sizeof(double), ob = (size_t)n * 16;
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, 2 * rb + ob, sg.s));
+  double* d_o = (double*)buf;
+  double* d_d = (double*)(buf + rb);
+  float* d_out = (float*)(buf + 2 * rb);
+  CUDA_TRY(cudaMemcpyAsync(d_o, origins, rb, cudaMemcpyHostToDevice, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(d_d, dirs, rb, cudaMemcpyHostToDevice, sg.s));
+  FrameScratch fs;
+  if ((rc = frame_setup(m, t, tf, sg.s, fs))) return rc;
+  NetDev net = m->ps.net;
+  FeatDev fd = feat_for(m, fs.grid);
+  MarchDev md = march_for(st);
+  CamDev cam{};
+  ShardDev sh{};
+  sh.world = 1;
+  const TFDev* tfp = fs.tf;
+  const float* b0 = fs.b0;
+  const double* ro = d_o;
+  const double* rd = d_d;
+  long long n_slots = n;
+  unsigned long long* queue = fs.counters;
+  unsigned long long* evc = fs.counters + 1;
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc};
+  const size_t smem = stage_smem_bytes(net, true, m->k0);
+  if ((rc = launch(m, KernelKind::kDVR, smem, args, sg.s, n_slots / 32 + 1))) return rc;
+  unsigned long long cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(out_px, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(&cnt, evc, 8, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(fs.buf, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (eval_count) *eval_count = cnt;
+  return FVSRN_OK;
+}
+
+static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64_t n, double t,
+                       float* out, int want_head) {
+  if (!m || (n > 0 && (!p || !out))) return fail(FVSRN_EINVAL, "null argument");
+  if (m->head != want_head)
+    return fail(FVSRN_EINVAL, want_head == FVSRN_HEAD_DENSITY ? "eval_density requires a density-head model"
+                                                              : "eval_color requires a color-head model");
+  if (!m->temporal && !std::isnan(t)) return fail(FVSRN_EINVAL, "timestep supplied to a non-temporal model");
+  if (m->temporal && std::isnan(t)) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
+  if (m->dir_mode != FVSRN_DIR_POS && !dd) return fail(FVSRN_EINVAL, "direction mode requires view directions");
+  if (n == 0) return FVSRN_OK;
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int oc = want_head == FVSRN_HEAD_DENSITY ? 1 : 4;
+  const size_t pb = (size_t)n * 3 * sizeof(double), ob = (size_t)n * oc * sizeof(float);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, 2 * pb + ob, sg.s));
+  double* d_p = (double*)buf;
+  double* d_d = dd ? (double*)(buf + pb) : nullptr;
+  float* d_out = (float*)(buf + 2 * pb);
+  CUDA_TRY(cudaMemcpyAsync(d_p, p, pb, cudaMemcpyHostToDevice, sg.s));
+  if (dd) CUDA_TRY(cudaMemcpyAsync(d_d, dd, pb, cudaMemcpyHostToDevice, sg.s));
+  FrameScratch fs;
+  int rc = frame_setup(m, t, nullptr, sg.s, fs);
+  if (rc) return rc;
+  NetDev net = m->ps.net;
+  FeatDev fd = feat_for(m, fs.grid);
+  const float* b0 = fs.b0;
+  int mode = 1, res = 0;
+  double step = 0;
+  long long begin = 0, count = n;
+  const double* pp = d_p;
+  const double* pd = d_d;
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out};
+  const size_t smem = stage_smem_bytes(net, false, m->k0);
+  if ((rc = launch(m, KernelKind::kSample, smem, args, sg.s, n / 32 + 1))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(fs.buf, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_eval_density(fvsrn_model_t m, const double* p, int64_t n, double t, float* out) {
+  return eval_common(m, p, nullptr, n, t, out, FVSRN_HEAD_DENSITY);
+}
+
+int32_t fvsrn_eval_color(fvsrn_model_t m, const double* p, const double* d, int64_t n, double t,
+                         float* out4) {
+  return eval_common(m, p, d, n, t, out4, FVSRN_HEAD_COLOR);
+}
+
+int32_t fvsrn_decode_density_device(fvsrn_model_t m, int32_t res, double t, int64_t lattice_begin,
+                                    int64_t lattice_count, float* d_out, void* stream) {
+  if (!m || !d_out) return fail(FVSRN_EINVAL, "null argument");
+  if (m->head != FVSRN_HEAD_DENSITY) return fail(FVSRN_EINVAL, "decode_volume requires a density-head model");
+  if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
+  if (!m->temporal && !std::isnan(t)) return fail(FVSRN_EINVAL, "timestep supplied to a non-temporal model");
+  if (m->temporal && std::isnan(t)) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
+  CUDA_TRY(cudaSetDevice(m->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  FrameScratch fs;
+  int rc = frame_setup(m, t, nullptr, s, fs);
+  if (rc) return rc;
+  NetDev net = m->ps.net;
+  FeatDev fd = feat_for(m, fs.grid);
+  const float* b0 = fs.b0;
+  int mode = 0;
+  double step = 1.0 / (double)(res - 1);
+  long long begin = lattice_begin, count = lattice_count;
+  const double* pp = nullptr;
+  const double* pd = nullptr;
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out};
+  const size_t smem = stage_smem_bytes(net, false, m->k0);
+  if ((rc = launch(m, KernelKind::kSample, smem, args, s, count / 32 + 1))) return rc;
+  CUDA_TRY(cudaFreeAsync(fs.buf, s));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out) {
+  if (!m || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const long long count = (long long)res * res * res;
+  float* d_out = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d_out, count * sizeof(float), sg.s));
+  int rc = fvsrn_decode_density_device(m, res, t, 0, count, d_out, sg.s);
+  if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, count * sizeof(float), cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(d_out, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_fused_eval(fvsrn_model_t m, const float* x, int64_t n, float* out) {
+  if (!m || (n > 0 && (!x || !out))) return fail(FVSRN_EINVAL, "null argument");
+  if (n == 0) return FVSRN_OK;
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int oc = m->head == FVSRN_HEAD_DENSITY ? 1 : 4;
+  const size_t xb = (size_t)n * m->d_in * sizeof(float), ob = (size_t)n * oc * sizeof(float);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, xb + ob, sg.s));
+  float* d_x = (float*)buf;
+  float* d_out = (float*)(buf + xb);
+  CUDA_TRY(cudaMemcpyAsync(d_x, x, xb, cudaMemcpyHostToDevice, sg.s));
+  NetDev net = m->px.net;
+  int d_in = m->d_in, k0 = m->k0x;
+  long long count = n;
+  const float* xp = d_x;
+  void* args[] = {&net, &d_in, &k0, &xp, &count, &d_out};
+  const size_t smem = stage_smem_bytes(net, false, m->k0x);
+  int rc = launch(m, KernelKind::kFused, smem, args, sg.s, n / 32 + 1);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  return FVSRN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,356 @@
+// fvsrn_device.cuh -- device building blocks of the fused fV-SRN DVR path (sm_100a).
+//
+// One warp evaluates the network for 32 samples at a time:
+//   * each lane assembles ITS OWN sample's input row (latent grid trilinear with
+//     16-byte fp16 loads + f32 FHFMA accumulation, NeRF Fourier features via a
+//     double-angle recurrence, raw position) into a per-warp shared-memory stage;
+//   * ldmatrix turns the stage into m16n8k16 A fragments; the MLP runs on the
+//     tensor cores (mma.sync f16 x f16 -> f32) with weights staged once per CTA
+//     in shared memory in B-fragment order (one conflict-free LDS.64 per MMA);
+//   * the f32 accumulators of two adjacent n8 tiles ARE the A fragment of the
+//     next layer's k16 tile, so activations stay in registers between layers;
+//   * the head output goes back to the owning lane through a 32x4 smem slot.
+//
+// Reference semantics followed (fvsrn 0.1.0, /root/reference/pkg/src/fvsrn):
+//   input layout / encoders  model.py:248-279, nn.py:47-57
+//   grid cell + weights      grid.py:47-84
+//   MLP + activations        nn.py:18-29, 195-204;  heads model.py:338-357
+//   transfer function        transfer.py:57-65
+//   compositing + ET         render.py:109-117, 219-232
+// The device feature order is a fixed permutation of the reference's
+// (z | sin/cos pairs | p | d); the host packs W0's columns accordingly, and the
+// per-frame time features are folded into the layer-0 bias.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace fvsrn {
+
+constexpr int kWarp = 32;
+constexpr int kMaxLayers = 24;
+constexpr int kMaxTF = 64;
+constexpr int kMaxHidden = 128;
+constexpr int kMaxK0 = 128;        // padded input width limit (8 k16 tiles)
+constexpr int kTile = 8;           // screen tile edge (pixels)
+
+// ---------------------------------------------------------------- params
+struct NetDev {
+  const uint2* wfrag;     // B fragments, all layers, [l][kt][nt][lane]
+  const float* bias;      // padded biases, all layers (layer 0 overridden per call)
+  int layers, kt0, act, head, out_real;
+  int w_off[kMaxLayers + 1];   // uint2 offsets
+  int b_off[kMaxLayers + 1];   // float offsets
+  int w_total, b_total;        // sizes (for smem staging)
+};
+
+struct FeatDev {              // how a lane builds its input row (device column order)
+  int grid_res, f_pad;        // latent grid (R, padded channels); f_pad == 0: no grid
+  const __half* grid;         // (R,R,R,f_pad) fp16, already time-blended for the frame
+  int fourier_mode, m, fd_in; // 0 off, 1 nerf, 2 random; fd_in 3 or 6
+  const float* bmat;          // random mode B (m, fd_in) f32 (device)
+  int four_off, raw_off, raw_w, k0;  // column offsets (halfs)
+  int dir_mode;               // 0 pos, 1 dirP, 2 dirF
+};
+
+struct TFDev {
+  int n;
+  float xs[kMaxTF];
+  float val[kMaxTF][4];       // r g b sigma at control points
+  float slope[kMaxTF][4];     // per segment
+};
+
+struct MarchDev {
+  double stepsize, et_alpha, eps_blend;
+  float bg[3];
+  int max_steps;
+};
+
+// ---------------------------------------------------------------- small helpers
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
+  float r;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(r) : "h"(a), "h"(b), "f"(c));
+  return r;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* smem_row_ptr) {
+  uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(smem_row_ptr));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// nn.py:18-29 (hidden activations; last layer linear)
+__device__ __forceinline__ float act_apply(int act, float x) {
+  switch (act) {
+    case 0: return fmaxf(x, 0.f);
+    case 1: return __fdividef(1.f, 1.f + __expf(-x));
+    case 2: return x > 20.f ? x : __logf(1.f + __expf(x));
+    case 3: { float s = __sinf(x); return fmaf(s, s, x); }
+    default: { float s = __sinf(x); return fmaf(s, s, 0.5f * x); }
+  }
+}
+
+// ---------------------------------------------------------------- warp MLP
+// Evaluates the whole network for the 32 rows staged in `stage` (row stride `rs`
+// halfs) and writes head inputs (pre-head raw outputs, up to 4 per row) to
+// `outbuf[row*4 + c]`.  MT = number of m16 tiles held at once (2 -> all 32 rows).
+template <int HID, int MT>
+struct WarpMLP {
+  static constexpr int NT = HID / 8;
+  static constexpr int KT = HID / 16;
+
+  __device__ static void act_pack(int act, const float (&acc)[MT][NT][4], uint32_t (&h)[MT][KT][4]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const float* a0 = acc[mt][2 * kt];
+        const float* a1 = acc[mt][2 * kt + 1];
+        h[mt][kt][0] = pack_half2(act_apply(act, a0[0]), act_apply(act, a0[1]));
+        h[mt][kt][1] = pack_half2(act_apply(act, a0[2]), act_apply(act, a0[3]));
+        h[mt][kt][2] = pack_half2(act_apply(act, a1[0]), act_apply(act, a1[1]));
+        h[mt][kt][3] = pack_half2(act_apply(act, a1[2]), act_apply(act, a1[3]));
+      }
+  }
+
+  __device__ static void bias_init(float (&acc)[MT][NT][4], const float* b, int q) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float2 bb = *reinterpret_cast<const float2*>(b + nt * 8 + 2 * q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        acc[mt][nt][0] = bb.x; acc[mt][nt][1] = bb.y;
+        acc[mt][nt][2] = bb.x; acc[mt][nt][3] = bb.y;
+      }
+    }
+  }
+
+  // m_base: first m16 tile index handled (0, or 0/1 when MT == 1)
+  __device__ static void run(const __half* stage, int rs, const NetDev& net, const uint2* wf,
+                             const float* bs, float* outbuf, int lane, int m_base) {
+    const int g = lane >> 2, q = lane & 3;
+    const int arow = lane & 15, acol = (lane >> 4) * 8;
+    float out_acc[MT][4];
+
+    if (net.layers == 1) {
+      float2 bb = *reinterpret_cast<const float2*>(bs + net.b_off[0] + 2 * q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        out_acc[mt][0] = bb.x; out_acc[mt][1] = bb.y; out_acc[mt][2] = bb.x; out_acc[mt][3] = bb.y;
+      }
+      for (int kt = 0; kt < net.kt0; ++kt) {
+        uint2 b = wf[net.w_off[0] + kt * 32 + lane];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t a[4];
+          ldmatrix_x4(a, stage + ((m_base + mt) * 16 + arow) * rs + kt * 16 + acol);
+          mma16816(out_acc[mt], a, b);
+        }
+      }
+    } else {
+      float acc[MT][NT][4];
+      uint32_t h[MT][KT][4];
+      // ---- layer 0: A from the stage, K = 16*kt0
+      bias_init(acc, bs + net.b_off[0], q);
+      for (int kt = 0; kt < net.kt0; ++kt) {
+        uint32_t a[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          ldmatrix_x4(a[mt], stage + ((m_base + mt) * 16 + arow) * rs + kt * 16 + acol);
+        const uint2* wl = wf + net.w_off[0] + kt * NT * 32 + lane;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          uint2 b = wl[nt * 32];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma16816(acc[mt][nt], a[mt], b);
+        }
+      }
+      act_pack(net.act, acc, h);
+      // ---- hidden layers
+      for (int l = 1; l < net.layers - 1; ++l) {
+        bias_init(acc, bs + net.b_off[l], q);
+        const uint2* wl = wf + net.w_off[l] + lane;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            uint2 b = wl[(kt * NT + nt) * 32];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) mma16816(acc[mt][nt], h[mt][kt], b);
+          }
+        act_pack(net.act, acc, h);
+      }
+      // ---- last layer: N = 8 (one n tile), linear
+      const int L = net.layers - 1;
+      float2 bb = *reinterpret_cast<const float2*>(bs + net.b_off[L] + 2 * q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        out_acc[mt][0] = bb.x; out_acc[mt][1] = bb.y; out_acc[mt][2] = bb.x; out_acc[mt][3] = bb.y;
+      }
+      const uint2* wl = wf + net.w_off[L] + lane;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        uint2 b = wl[kt * 32];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) mma16816(out_acc[mt], h[mt][kt], b);
+      }
+    }
+    if (q < 2) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r0 = (m_base + mt) * 16 + g;
+        *reinterpret_cast<float2*>(outbuf + r0 * 4 + 2 * q) = make_float2(out_acc[mt][0], out_acc[mt][1]);
+        *reinterpret_cast<float2*>(outbuf + (r0 + 8) * 4 + 2 * q) = make_float2(out_acc[mt][2], out_acc[mt][3]);
+      }
+    }
+  }
+};
+
+template <int HID>
+struct MLPDispatch {
+  static constexpr int MT = HID <= 64 ? 2 : 1;
+  __device__ static void eval32(const __half* stage, int rs, const NetDev& net, const uint2* wf,
+                                const float* bs, float* outbuf, int lane) {
+#pragma unroll
+    for (int mb = 0; mb < 2; mb += MT) WarpMLP<HID, MT>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
+  }
+};
+
+// ---------------------------------------------------------------- features
+// Trilinear latent lookup (grid.py:47-84): clamp, c = p*(R-1), i0 = min(int c, R-2),
+// 8-corner weighted sum; fp16 storage, f32 accumulation (FHFMA), 16-byte loads.
+__device__ __forceinline__ void grid_features(const FeatDev& fd, float px, float py, float pz,
+                                              __half* row) {
+  const int R = fd.grid_res;
+  const float s = (float)(R - 1);
+  float cx = fminf(fmaxf(px, 0.f), 1.f) * s;
+  float cy = fminf(fmaxf(py, 0.f), 1.f) * s;
+  float cz = fminf(fmaxf(pz, 0.f), 1.f) * s;
+  int x0 = min((int)cx, R - 2), y0 = min((int)cy, R - 2), z0 = min((int)cz, R - 2);
+  float fx = cx - (float)x0, fy = cy - (float)y0, fz = cz - (float)z0;
+  float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+  uint16_t w[8];
+  {
+    float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                   fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = __half_as_ushort(__float2half_rn(wf[k]));
+  }
+  const int F = fd.f_pad;
+  const int sz = F, sy = R * F, sx = R * R * F;
+  const __half* base = fd.grid + ((size_t)(x0 * R + y0) * R + z0) * F;
+  const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+  for (int c8 = 0; c8 < F; c8 += 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const uint4*>(base + off[k] + c8));
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] = fhfma((uint16_t)(u[j] & 0xffff), w[k], acc[2 * j]);
+        acc[2 * j + 1] = fhfma((uint16_t)(u[j] >> 16), w[k], acc[2 * j + 1]);
+      }
+    }
+    uint4 o;
+    o.x = pack_half2(acc[0], acc[1]); o.y = pack_half2(acc[2], acc[3]);
+    o.z = pack_half2(acc[4], acc[5]); o.w = pack_half2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(row + c8) = o;
+  }
+}
+
+// Fourier features as (sin_i, cos_i) half2 pairs (nn.py:47-57, model.py:269-272).
+// NeRF rows are 2^j * f32(2*pi) on one axis: one accurate base sincos per axis,
+// then the double-angle recurrence (exact scaling by 2 of the f32 B entries).
+__device__ __forceinline__ void fourier_features(const FeatDev& fd, const float (&v)[6],
+                                                 __half* row) {
+  uint32_t* dst = reinterpret_cast<uint32_t*>(row + fd.four_off);
+  if (fd.fourier_mode == 1) {
+    const int d = fd.fd_in;   // 3 or 6
+    float sn[6], cs[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      float r = v[a] - rintf(v[a]);                     // exact; keeps MUFU in [-pi, pi]
+      __sincosf(r * 6.28318548202514648f, &sn[a], &cs[a]);
+    }
+    for (int base = 0; base < fd.m; base += d) {
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+        if (a < d && base + a < fd.m) dst[base + a] = pack_half2(sn[a], cs[a]);
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        float s2 = 2.f * sn[a] * cs[a];
+        float c2 = fmaf(cs[a], cs[a], -sn[a] * sn[a]);
+        sn[a] = s2; cs[a] = c2;
+      }
+    }
+  } else if (fd.fourier_mode == 2) {
+    for (int i = 0; i < fd.m; ++i) {
+      float ph = 0.f;
+      for (int a = 0; a < fd.fd_in; ++a) ph = fmaf(__ldg(fd.bmat + i * fd.fd_in + a), v[a], ph);
+      float s, c;
+      sincosf(ph, &s, &c);
+      dst[i] = pack_half2(s, c);
+    }
+  }
+}
+
+// Assemble this lane's input row: [z | sin/cos pairs | p (| d) | 0-pad].
+__device__ __forceinline__ void assemble_row(const FeatDev& fd, float px, float py, float pz,
+                                             float dx, float dy, float dz, __half* row) {
+  if (fd.f_pad > 0) grid_features(fd, px, py, pz, row);
+  float v[6] = {px, py, pz, dx, dy, dz};
+  if (fd.fourier_mode != 0) fourier_features(fd, v, row);
+  // raw block (raw_off is even): p then d (dir modes)
+  uint32_t* dst = reinterpret_cast<uint32_t*>(row + fd.raw_off);
+  if (fd.raw_w == 3) {
+    dst[0] = pack_half2(px, py);
+    dst[1] = pack_half2(pz, 0.f);
+  } else {
+    dst[0] = pack_half2(px, py);
+    dst[1] = pack_half2(pz, dx);
+    dst[2] = pack_half2(dy, dz);
+  }
+}
+
+// ---------------------------------------------------------------- TF + heads
+__device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float softplusf_(float x) { return x > 20.f ? x : log1pf(__expf(x)); }
+
+// transfer.py:57-65: clamp to [0,1], piecewise-linear interpolation.
+__device__ __forceinline__ void tf_eval(const TFDev& tf, float dens, float& r, float& g, float& b,
+                                        float& sig) {
+  float d = fminf(fmaxf(dens, 0.f), 1.f);
+  int seg = 0;
+  for (int i = 1; i < tf.n - 1; ++i) seg += (d >= tf.xs[i]) ? 1 : 0;
+  float dx = d - tf.xs[seg];
+  r = fmaf(tf.slope[seg][0], dx, tf.val[seg][0]);
+  g = fmaf(tf.slope[seg][1], dx, tf.val[seg][1]);
+  b = fmaf(tf.slope[seg][2], dx, tf.val[seg][2]);
+  sig = fmaf(tf.slope[seg][3], dx, tf.val[seg][3]);
+}
+
+}  // namespace fvsrn

@@ -1,0 +1,384 @@
+// fvsrn_kernels.cu -- sm_100a kernels of the fV-SRN DVR hot path.
+//
+//   dvr_kernel        fused ray march: ray setup (f64, bit-exact geometry) -> per step
+//                     {latent grid, Fourier, MLP on tensor cores, head, TF, compositing,
+//                     early termination}; persistent warps refill lanes from a
+//                     chunked global work queue so MMA tiles stay full.
+//                     render.py:189-238, 314-332
+//   decode_kernel     batched world-space density decode on the vertex lattice
+//                     model.py:385-398
+//   eval_kernel       per-sample density / colour at given positions  model.py:368-382
+//   fused_eval_kernel head(mlp(x)) from assembled inputs              fused.py:281-301
+//   blend_grid_kernel per-frame keyframe pre-blend (trilinear is linear) model.py:219-233
+//   tiles_to_frame    reassembles gathered screen-tile shards (multi-GPU)
+#include "fvsrn_kernels.cuh"
+
+namespace fvsrn {
+
+__device__ __forceinline__ void stage_setup(const NetDev& net, const float* b0, const TFDev* tf_in,
+                                            int rs, uint2*& wf_s, float*& b_s, TFDev*& tf_s,
+                                            __half*& stage, float*& ob) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* p = smem;
+  wf_s = reinterpret_cast<uint2*>(p);
+  p += ((size_t)net.w_total * sizeof(uint2) + 15) / 16 * 16;
+  b_s = reinterpret_cast<float*>(p);
+  p += ((size_t)net.b_total * sizeof(float) + 15) / 16 * 16;
+  tf_s = reinterpret_cast<TFDev*>(p);
+  if (tf_in) p += (sizeof(TFDev) + 15) / 16 * 16;
+  const int warp = threadIdx.x >> 5;
+  const size_t per_warp = (size_t)kWarp * rs * sizeof(__half) + kWarp * 4 * sizeof(float);
+  stage = reinterpret_cast<__half*>(p + warp * per_warp);
+  ob = reinterpret_cast<float*>(p + warp * per_warp + (size_t)kWarp * rs * sizeof(__half));
+
+  for (int i = threadIdx.x; i < net.w_total; i += blockDim.x) wf_s[i] = net.wfrag[i];
+  for (int i = threadIdx.x; i < net.b_total; i += blockDim.x) b_s[i] = net.bias[i];
+  if (b0) {
+    const int n0 = net.b_off[1] - net.b_off[0];
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) b_s[i] = b0[i];
+  }
+  if (tf_in) {
+    const int words = sizeof(TFDev) / 4;
+    const int* src = reinterpret_cast<const int*>(tf_in);
+    int* dst = reinterpret_cast<int*>(tf_s);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  // zero the whole per-warp stage (pad columns must be finite: 0 * NaN = NaN)
+  const int lane = threadIdx.x & 31;
+  uint32_t* st = reinterpret_cast<uint32_t*>(stage);
+  for (int i = lane; i < kWarp * rs / 2; i += kWarp) st[i] = 0u;
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- ray setup (f64)
+// Bit-exact restatement of camera_rays (render.py:72-94), ray_box_intersect
+// (render.py:97-106) and _march_geometry (render.py:189-200): every f64 op is an
+// explicit _rn intrinsic so nvcc cannot contract it into an FMA.
+struct RayGeom {
+  double o[3], d[3], tmin, ds;
+  int n;
+};
+
+__device__ __forceinline__ void camera_dir(const CamDev& cam, int px, int py, double (&d)[3]) {
+  double gx = __dmul_rn(__dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn((double)px, 0.5), (double)cam.W), 2.0), 1.0),
+                        cam.half_w);
+  double gy = __dmul_rn(__dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn((double)py, 0.5), (double)cam.H), 2.0)),
+                        cam.half_h);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    d[a] = __dadd_rn(__dadd_rn(cam.fwd[a], __dmul_rn(gx, cam.right[a])), __dmul_rn(gy, cam.up[a]));
+  double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                                    __dmul_rn(d[2], d[2])));
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = __ddiv_rn(d[a], nrm);
+}
+
+__device__ __forceinline__ bool march_geometry(const MarchDev& md, RayGeom& r) {
+  double tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double dd = fabs(r.d[a]) < 1e-12 ? 1e-12 : r.d[a];
+    double tlo = __ddiv_rn(__dsub_rn(0.0, r.o[a]), dd);
+    double thi = __ddiv_rn(__dsub_rn(1.0, r.o[a]), dd);
+    tmin = fmax(tmin, fmin(tlo, thi));
+    tmax = fmin(tmax, fmax(tlo, thi));
+  }
+  tmin = fmax(tmin, 0.0);
+  if (!(tmax > tmin)) return false;
+  double len = __dsub_rn(tmax, tmin);
+  double nf = ceil(__ddiv_rn(len, md.stepsize));
+  long long n = (long long)nf;
+  if (n > md.max_steps) n = md.max_steps;
+  if (n < 1) n = 1;
+  r.n = (int)n;
+  r.tmin = tmin;
+  r.ds = __ddiv_rn(len, (double)n);
+  return true;
+}
+
+// slot -> pixel of this shard (8x8 tiles, tile = rank + lt*world); -1 if outside the frame
+__device__ __forceinline__ int slot_pixel(const CamDev& cam, const ShardDev& sh, long long s) {
+  long long lt = s >> 6;
+  int e = (int)(s & 63);
+  long long tile = sh.rank + lt * sh.world;
+  if (tile >= sh.n_tiles) return -1;
+  int tx = (int)(tile % sh.tiles_x), ty = (int)(tile / sh.tiles_x);
+  int px = tx * kTile + (e & 7), py = ty * kTile + (e >> 3);
+  if (px >= cam.W || py >= cam.H) return -1;
+  return py * cam.W + px;
+}
+
+// ---------------------------------------------------------------- DVR
+template <int HID>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+           MarchDev md, CamDev cam, ShardDev sh, const double* __restrict__ rays_o,
+           const double* __restrict__ rays_d, long long n_slots, float* __restrict__ out,
+           unsigned long long* __restrict__ queue, unsigned long long* __restrict__ eval_count) {
+  const int rs = fd.k0 + 8;
+  uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
+  stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
+  const int lane = threadIdx.x & 31;
+  const bool density = net.head == 0;
+  const bool use_dir = fd.dir_mode != 0;
+  const float eps1 = (float)(1.0 - md.eps_blend);
+  const float et = (float)md.et_alpha;
+  __half* myrow = stage + lane * rs;
+
+  bool has = false;
+  int k = 0, n = 0;
+  long long oslot = 0;
+  double o0 = 0, o1 = 0, o2 = 0, d0 = 0, d1 = 0, d2 = 0, tmin = 0, ds = 0;
+  float dsf = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+  unsigned long long evals = 0;
+  long long chunk_base = 0;
+  int chunk_left = 0;
+  bool qdone = false;
+
+  while (true) {
+    // ---- refill free lanes from the warp's chunk of the global work queue
+    while (true) {
+      unsigned need = __ballot_sync(0xffffffffu, !has);
+      if (need == 0) break;
+      if (chunk_left == 0) {
+        if (qdone) break;
+        unsigned long long cb = 0;
+        if (lane == 0) cb = atomicAdd(queue, 32ull);
+        cb = __shfl_sync(0xffffffffu, cb, 0);
+        if ((long long)cb >= n_slots) { qdone = true; break; }
+        chunk_base = (long long)cb;
+        chunk_left = (int)min(32ll, n_slots - (long long)cb);
+      }
+      const int rank = __popc(need & lanemask_lt());
+      const int take = min(__popc(need), chunk_left);
+      if (!has && rank < take) {
+        const long long s = chunk_base + rank;
+        RayGeom r;
+        bool valid = true;
+        long long dst;
+        if (rays_o) {
+          dst = s;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) { r.o[a] = rays_o[3 * s + a]; r.d[a] = rays_d[3 * s + a]; }
+        } else {
+          const int pix = slot_pixel(cam, sh, s);
+          dst = sh.compact ? s : pix;
+          if (pix < 0) {
+            valid = false;
+            if (sh.compact) *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            const int W = cam.W;
+            camera_dir(cam, pix % W, pix / W, r.d);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) r.o[a] = cam.eye[a];
+          }
+        }
+        if (valid) {
+          if (march_geometry(md, r)) {
+            has = true;
+            k = 0; n = r.n; oslot = dst;
+            o0 = r.o[0]; o1 = r.o[1]; o2 = r.o[2];
+            d0 = r.d[0]; d1 = r.d[1]; d2 = r.d[2];
+            tmin = r.tmin; ds = r.ds; dsf = (float)r.ds;
+            C0 = C1 = C2 = A = 0.f;
+          } else {
+            *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
+          }
+        }
+      }
+      chunk_base += take;
+      chunk_left -= take;
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, has);
+    if (act == 0) break;
+    evals += __popc(act);
+
+    // ---- sample position (render.py:224-225, f64) and input row
+    if (has) {
+      const double tk = __dadd_rn(tmin, __dmul_rn((double)k + 0.5, ds));
+      const float px = (float)__dadd_rn(o0, __dmul_rn(tk, d0));
+      const float py = (float)__dadd_rn(o1, __dmul_rn(tk, d1));
+      const float pz = (float)__dadd_rn(o2, __dmul_rn(tk, d2));
+      assemble_row(fd, px, py, pz, use_dir ? (float)d0 : 0.f, use_dir ? (float)d1 : 0.f,
+                   use_dir ? (float)d2 : 0.f, myrow);
+    }
+    __syncwarp();
+    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    __syncwarp();
+
+    // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
+    if (has) {
+      const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
+      float r, g, b, sig;
+      if (density) {
+        tf_eval(*tf, sigmoidf_(o.x), r, g, b, sig);
+      } else {
+        r = sigmoidf_(o.x); g = sigmoidf_(o.y); b = sigmoidf_(o.z); sig = softplusf_(o.w);
+      }
+      float alpha = 1.f - __expf(-sig * dsf);
+      alpha = fmaxf(fminf(alpha, eps1), 0.f);
+      const float tr = (1.f - A) * alpha;
+      C0 = fmaf(tr, r, C0); C1 = fmaf(tr, g, C1); C2 = fmaf(tr, b, C2);
+      A += tr;
+      ++k;
+      if (k >= n || A > et) {
+        const float om = 1.f - A;
+        *reinterpret_cast<float4*>(out + 4 * oslot) =
+            make_float4(fmaf(om, md.bg[0], C0), fmaf(om, md.bg[1], C1), fmaf(om, md.bg[2], C2), A);
+        has = false;
+      }
+    }
+  }
+  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+}
+
+// ---------------------------------------------------------------- decode / eval
+// mode 0: lattice decode (model.py:385-398); mode 1: positions (+dirs) from memory
+template <int HID>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, int res, double step,
+              long long begin, long long count, const double* __restrict__ pos,
+              const double* __restrict__ dirs, float* __restrict__ out) {
+  const int rs = fd.k0 + 8;
+  uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
+  stage_setup(net, b0, nullptr, rs, wf_s, b_s, tf, stage, ob);
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  __half* myrow = stage + lane * rs;
+  const bool density = net.head == 0;
+  for (long long c = gwarp; c * 32 < count; c += nwarps) {
+    const long long i = c * 32 + lane;
+    const bool valid = i < count;
+    if (valid) {
+      float px, py, pz, dx = 0.f, dy = 0.f, dz = 0.f;
+      if (mode == 0) {
+        const long long idx = begin + i;
+        const long long r2 = (long long)res * res;
+        const int ix = (int)(idx / r2), iy = (int)((idx / res) % res), iz = (int)(idx % res);
+        // numpy linspace(0,1,res): i*step + 0.0, last sample exactly 1.0
+        px = ix == res - 1 ? 1.f : (float)((double)ix * step);
+        py = iy == res - 1 ? 1.f : (float)((double)iy * step);
+        pz = iz == res - 1 ? 1.f : (float)((double)iz * step);
+      } else {
+        px = (float)pos[3 * i]; py = (float)pos[3 * i + 1]; pz = (float)pos[3 * i + 2];
+        if (dirs) { dx = (float)dirs[3 * i]; dy = (float)dirs[3 * i + 1]; dz = (float)dirs[3 * i + 2]; }
+      }
+      assemble_row(fd, px, py, pz, dx, dy, dz, myrow);
+    }
+    __syncwarp();
+    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    __syncwarp();
+    if (valid) {
+      const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
+      if (density) {
+        out[i] = sigmoidf_(o.x);
+      } else {
+        *reinterpret_cast<float4*>(out + 4 * i) =
+            make_float4(sigmoidf_(o.x), sigmoidf_(o.y), sigmoidf_(o.z), softplusf_(o.w));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// head(mlp(x)) with x already assembled in the reference column order.
+template <int HID>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+fused_eval_kernel(NetDev net, int d_in, int k0, const float* __restrict__ x, long long count,
+                  float* __restrict__ out) {
+  const int rs = k0 + 8;
+  uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
+  stage_setup(net, nullptr, nullptr, rs, wf_s, b_s, tf, stage, ob);
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  __half* myrow = stage + lane * rs;
+  for (long long c = gwarp; c * 32 < count; c += nwarps) {
+    const long long i = c * 32 + lane;
+    const bool valid = i < count;
+    if (valid)
+      for (int j = 0; j < d_in; ++j) myrow[j] = __float2half_rn(x[i * d_in + j]);
+    __syncwarp();
+    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    __syncwarp();
+    if (valid) {
+      const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
+      if (net.head == 0) out[i] = sigmoidf_(o.x);
+      else *reinterpret_cast<float4*>(out + 4 * i) =
+          make_float4(sigmoidf_(o.x), sigmoidf_(o.y), sigmoidf_(o.z), softplusf_(o.w));
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void blend_grid_kernel(const __half* __restrict__ lo, const __half* __restrict__ hi,
+                                  float w, long long n, __half* __restrict__ dst) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float a = __half2float(lo[i]), b = __half2float(hi[i]);
+    dst[i] = __float2half_rn((1.f - w) * a + w * b);
+  }
+}
+
+__global__ void tiles_to_frame_kernel(const float4* __restrict__ gathered, int W, int H, int world,
+                                      long long per_rank, int tiles_x, int n_tiles,
+                                      float4* __restrict__ frame) {
+  const long long total = per_rank * world;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / per_rank);
+    const long long s = i % per_rank;
+    const long long tile = r + (s >> 6) * world;
+    if (tile >= n_tiles) continue;
+    const int e = (int)(s & 63);
+    const int px = (int)(tile % tiles_x) * kTile + (e & 7), py = (int)(tile / tiles_x) * kTile + (e >> 3);
+    if (px < W && py < H) frame[(long long)py * W + px] = gathered[i];
+  }
+}
+
+// ---------------------------------------------------------------- launch table
+#define FVSRN_FOR_HIDDEN(X) X(16) X(32) X(48) X(64) X(96) X(128)
+
+template <int HID>
+static const void* dvr_ptr() { return (const void*)dvr_kernel<HID>; }
+template <int HID>
+static const void* sample_ptr() { return (const void*)sample_kernel<HID>; }
+template <int HID>
+static const void* fused_ptr() { return (const void*)fused_eval_kernel<HID>; }
+
+const void* kernel_for(KernelKind kind, int hid) {
+  switch (hid) {
+#define CASE(H)                                            \
+  case H:                                                  \
+    if (kind == KernelKind::kDVR) return dvr_ptr<H>();     \
+    if (kind == KernelKind::kSample) return sample_ptr<H>(); \
+    return fused_ptr<H>();
+    FVSRN_FOR_HIDDEN(CASE)
+#undef CASE
+    default: return nullptr;
+  }
+}
+
+cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
+                         cudaStream_t s) {
+  int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+  blend_grid_kernel<<<blocks, 256, 0, s>>>(lo, hi, w, n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,
+                                  cudaStream_t s) {
+  const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * tiles_y;
+  const long long max_local = (n_tiles + world - 1) / world;
+  const long long per_rank = max_local * 64;
+  const long long total = per_rank * world;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 8192);
+  tiles_to_frame_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(gathered), W, H,
+                                               world, per_rank, tiles_x, n_tiles,
+                                               reinterpret_cast<float4*>(frame));
+  return cudaGetLastError();
+}
+
+}  // namespace fvsrn

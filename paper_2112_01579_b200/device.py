@@ -1,0 +1,259 @@
+"""Device-resident fV-SRN model: one ``fvsrn_model_t`` per (model, GPU).
+
+Upload happens once (weights packed into fp16 mma B-fragments, grids to fp16
+(R,R,R,F_pad), u8 checkpoints dequantised with the reference formula); every
+render / eval call after that only ships per-frame constants (camera basis,
+TF, time) -- the ownership contract of SURVEY 8(b).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _lib as L
+
+
+def camera_basis(cam):
+    """render.py:78-86 evaluated with numpy (bit-identical per-frame basis)."""
+    eye = np.asarray(cam.eye, dtype=np.float64)
+    fwd = np.asarray(cam.target, dtype=np.float64) - eye
+    fwd = fwd / np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(cam.up, dtype=np.float64))
+    right = right / np.linalg.norm(right)
+    up = np.cross(right, fwd)
+    half_h = np.tan(cam.fov_y / 2.0)
+    half_w = half_h * cam.width / cam.height
+    return fwd, right, up, float(half_w), float(half_h)
+
+
+def camera_desc(cam) -> L.CameraDesc:
+    d = L.CameraDesc()
+    d.eye[:] = [float(v) for v in cam.eye]
+    d.target[:] = [float(v) for v in cam.target]
+    d.up[:] = [float(v) for v in cam.up]
+    d.fov_y = float(cam.fov_y)
+    d.width, d.height = int(cam.width), int(cam.height)
+    fwd, right, up, hw, hh = camera_basis(cam)
+    d.has_basis = 1
+    d.b_forward[:] = fwd.tolist()
+    d.b_right[:] = right.tolist()
+    d.b_up[:] = up.tolist()
+    d.half_w, d.half_h = hw, hh
+    return d
+
+
+class _TF:
+    """Keeps the TF arrays alive while the descriptor is in use."""
+
+    def __init__(self, tf):
+        self.xs = np.ascontiguousarray(tf.xs, dtype=np.float32)
+        self.rgbs = np.ascontiguousarray(tf.rgbs, dtype=np.float32)
+        self.sigmas = np.ascontiguousarray(tf.sigmas, dtype=np.float32)
+        self.desc = L.TFDesc(len(self.xs), L.fptr(self.xs), L.fptr(self.rgbs), L.fptr(self.sigmas))
+
+
+def tf_desc(tf):
+    return None if tf is None else _TF(tf)
+
+
+def settings_desc(s) -> L.SettingsDesc:
+    d = L.SettingsDesc()
+    d.stepsize = float(s.stepsize)
+    d.max_steps = int(s.max_steps)
+    d.background[:] = [float(v) for v in s.background]
+    d.early_term_alpha = float(s.early_term_alpha)
+    d.eps_blend = float(s.eps_blend)
+    return d
+
+
+class DeviceModel:
+    """Owns one native model handle; immutable after creation, thread-safe to use."""
+
+    def __init__(self, model, device: int | None = None):
+        lib = L.lib()
+        cfg = model.config
+        self.device = L.current_device() if device is None else int(device)
+        self.head = cfg.head
+        self.temporal = cfg.is_temporal
+        self.d_in = cfg.input_width
+        self.direction_mode = cfg.direction_mode
+        keep = []   # arrays that must outlive the create call
+
+        def f32(a):
+            a = np.ascontiguousarray(a, dtype=np.float32)
+            keep.append(a)
+            return a
+
+        d = L.ModelDesc()
+        d.layers, d.hidden = cfg.layers, cfg.hidden
+        d.d_in, d.d_out = cfg.input_width, cfg.output_width
+        d.activation = L.ACT_CODES[model.params.activation]
+        d.head = L.HEAD_CODES[cfg.head]
+        d.direction_mode = L.DIR_CODES[cfg.direction_mode]
+        enc = model.spatial_encoder
+        d.fourier_mode = L.FOURIER_CODES[enc.mode if enc.m > 0 else "off"]
+        d.fourier_m = enc.m
+        d.fourier_d_in = enc.d_in
+        d.b_matrix = L.fptr(f32(enc.b_matrix)) if enc.m > 0 else None
+        d.time_mode = L.TIME_CODES[cfg.time_mode]
+        d.time_fourier_count = cfg.time_fourier_count
+        if model.time_encoder is not None:
+            d.time_b = L.fptr(f32(model.time_encoder.b_matrix[:, 0]))
+        if cfg.time_range is not None:
+            d.has_time_range = 1
+            d.time_range[:] = [float(cfg.time_range[0]), float(cfg.time_range[1])]
+        grids = model.grids
+        d.grid_resolution = cfg.grid_resolution if grids else 0
+        d.grid_channels = cfg.grid_channels
+        d.n_grids = len(grids)
+        d.temporal = 1 if self.temporal else 0
+        if self.temporal:
+            kt = np.ascontiguousarray(model.keyframes.times, dtype=np.float64)
+            keep.append(kt)
+            d.keyframe_times = L.dptr(kt)
+        if grids:
+            quant = getattr(model, "quantized", None)
+            if quant:
+                d.grid_precision = L.GRID_U8
+                codes = [np.ascontiguousarray(q.codes, dtype=np.uint8) for q in quant]
+                keep.extend(codes)
+                d.grid_codes = (C.POINTER(C.c_uint8) * len(codes))(
+                    *[c.ctypes.data_as(C.POINTER(C.c_uint8)) for c in codes])
+                d.grid_mins = (L._f * len(quant))(*[L.fptr(f32(q.mins)) for q in quant])
+                d.grid_maxs = (L._f * len(quant))(*[L.fptr(f32(q.maxs)) for q in quant])
+            else:
+                d.grid_precision = L.GRID_F32
+                d.grids = (L._f * len(grids))(*[L.fptr(f32(g.values)) for g in grids])
+        d.weights = (L._f * cfg.layers)(*[L.fptr(f32(w)) for w in model.params.weights])
+        d.biases = (L._f * cfg.layers)(*[L.fptr(f32(b)) for b in model.params.biases])
+        h = C.c_void_p()
+        L.check(lib.fvsrn_model_create(C.byref(d), self.device, C.byref(h)))
+        self._h = h
+        self._lib = lib
+        del keep
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._lib.fvsrn_model_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+    def info(self):
+        k0, hp, sm = C.c_int32(), C.c_int32(), C.c_int32()
+        L.check(self._lib.fvsrn_model_info(self._h, C.byref(k0), C.byref(hp), C.byref(sm)))
+        return {"k0_pad": k0.value, "hidden_pad": hp.value, "smem_bytes": sm.value}
+
+    # ---------------------------------------------------------------- calls
+    def eval_density(self, p, t=None) -> np.ndarray:
+        p = np.ascontiguousarray(np.atleast_2d(np.asarray(p, dtype=np.float64)))
+        if p.shape[1] != 3:
+            raise ValueError(f"positions must have 3 components, got {p.shape}")
+        out = np.empty(len(p), dtype=np.float32)
+        L.check(self._lib.fvsrn_eval_density(self._h, L.dptr(p), len(p), L.t_arg(t), L.fptr(out)))
+        return out
+
+    def eval_color(self, p, d=None, t=None) -> np.ndarray:
+        p = np.ascontiguousarray(np.atleast_2d(np.asarray(p, dtype=np.float64)))
+        dd = None
+        if self.direction_mode != "pos":
+            if d is None:
+                raise ValueError(f"direction mode {self.direction_mode!r} requires view directions")
+            dd = np.ascontiguousarray(np.atleast_2d(np.asarray(d, dtype=np.float64)))
+            if dd.shape != p.shape:
+                raise ValueError("directions must match positions in shape")
+        out = np.empty((len(p), 4), dtype=np.float32)
+        L.check(self._lib.fvsrn_eval_color(self._h, L.dptr(p), L.dptr(dd) if dd is not None else None,
+                                           len(p), L.t_arg(t), L.fptr(out)))
+        return out
+
+    def decode(self, res: int, t=None) -> np.ndarray:
+        out = np.empty(int(res) ** 3, dtype=np.float32)
+        L.check(self._lib.fvsrn_decode_density(self._h, int(res), L.t_arg(t), L.fptr(out)))
+        return out
+
+    def fused_eval(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.ndim != 2 or x.shape[1] != self.d_in:
+            raise ValueError(f"expected assembled inputs (N, {self.d_in}), got {x.shape}")
+        oc = 1 if self.head == "density" else 4
+        out = np.empty((len(x), oc), dtype=np.float32)
+        L.check(self._lib.fvsrn_fused_eval(self._h, L.fptr(x), len(x), L.fptr(out)))
+        return out[:, 0] if oc == 1 else out
+
+    def render(self, tf, cam, settings, t=None):
+        """(H,W,4) f32 frame + evaluated-sample count (host buffer, synchronous)."""
+        out = np.empty((cam.height, cam.width, 4), dtype=np.float32)
+        cnt = C.c_uint64(0)
+        tfd = tf_desc(tf)
+        L.check(self._lib.fvsrn_render(self._h, C.byref(tfd.desc) if tfd else None,
+                                       C.byref(camera_desc(cam)), C.byref(settings_desc(settings)),
+                                       L.t_arg(t), L.fptr(out), C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def render_rays(self, tf, origins, dirs, settings, t=None):
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.float64).reshape(-1, 3))
+        d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))
+        if o.shape != d.shape:
+            raise ValueError("origins and dirs must have the same shape")
+        out = np.empty((len(o), 4), dtype=np.float32)
+        cnt = C.c_uint64(0)
+        tfd = tf_desc(tf)
+        L.check(self._lib.fvsrn_render_rays(self._h, C.byref(tfd.desc) if tfd else None, L.dptr(o),
+                                            L.dptr(d), len(o), C.byref(settings_desc(settings)),
+                                            L.t_arg(t), L.fptr(out), C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def render_device(self, tf, cam, settings, t, out_ptr: int, count_ptr: int | None,
+                      stream_ptr: int, rank: int = 0, world: int = 1, compact: bool = False):
+        """Stream-ordered render into a device buffer (e.g. a torch tensor's data_ptr)."""
+        tfd = tf_desc(tf)
+        sh = L.ShardDesc(int(rank), int(world), 1 if compact else 0)
+        L.check(self._lib.fvsrn_render_device(
+            self._h, C.byref(tfd.desc) if tfd else None, C.byref(camera_desc(cam)),
+            C.byref(settings_desc(settings)), L.t_arg(t), C.byref(sh), C.c_void_p(out_ptr),
+            C.c_void_p(count_ptr) if count_ptr else None, C.c_void_p(stream_ptr)))
+
+    def decode_device(self, res: int, t, begin: int, count: int, out_ptr: int, stream_ptr: int):
+        L.check(self._lib.fvsrn_decode_density_device(self._h, int(res), L.t_arg(t), int(begin),
+                                                      int(count), C.c_void_p(out_ptr),
+                                                      C.c_void_p(stream_ptr)))
+
+
+_cache_lock = threading.Lock()
+
+
+def device_model(model, device: int | None = None) -> DeviceModel:
+    """Cached upload of ``model`` (invalidate with ``model.invalidate_device()``)."""
+    dev = L.current_device() if device is None else int(device)
+    with _cache_lock:
+        cache = model.__dict__.setdefault("_device", {})
+        dm = cache.get(dev)
+        if dm is None:
+            dm = cache[dev] = DeviceModel(model, dev)
+        return dm
+
+
+def tiles_to_frame_device(gathered_ptr: int, width: int, height: int, world: int, frame_ptr: int,
+                          stream_ptr: int) -> None:
+    L.check(L.lib().fvsrn_tiles_to_frame_device(C.c_void_p(gathered_ptr), int(width), int(height),
+                                                int(world), C.c_void_p(frame_ptr),
+                                                C.c_void_p(stream_ptr)))
+
+
+def shard_slots(width: int, height: int, world: int) -> tuple[int, int]:
+    """(n_tiles, max_local_tiles * 64): compact per-rank buffer length in pixels."""
+    n_tiles = math.ceil(width / 8) * math.ceil(height / 8)
+    return n_tiles, math.ceil(n_tiles / world) * 64

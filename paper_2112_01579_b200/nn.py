@@ -1,0 +1,116 @@
+"""Network parameter containers and seeded initialisation (host side).
+
+Mirrors the parameter API of the reference ``fvsrn.nn`` (nn.py:15-168) so a
+reference user can build models the same way; evaluation itself runs on the
+GPU (``paper_2112_01579_b200.model`` / ``render``).  Initialisation draws from
+``numpy.random.default_rng(seed)`` in the reference's order, so a given seed
+yields bit-identical weights (pinned by tests/test_host_api.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+ACTIVATION_KINDS = ("relu", "sigmoid", "softplus", "snake", "snake_alt")
+
+
+def nerf_rows(m: int, d_in: int) -> np.ndarray:
+    """(m, d_in) f32 frequency matrix: row i has 2*pi*2**(i // d_in) on axis i % d_in."""
+    out = np.zeros((m, d_in), dtype=np.float32)
+    i = np.arange(m)
+    out[i, i % d_in] = (2.0 * np.pi) * np.exp2((i // d_in).astype(np.float64))
+    return out
+
+
+@dataclass(frozen=True)
+class FourierEncoder:
+    """v -> [v | sin(Bv) | cos(Bv)] with a frozen B (nn.py:60-76)."""
+
+    mode: str
+    b_matrix: np.ndarray
+    d_in: int
+    sigma: float = 1.0
+    seed: int = 0
+
+    @property
+    def m(self) -> int:
+        return int(self.b_matrix.shape[0])
+
+    @property
+    def out_width(self) -> int:
+        return self.d_in + 2 * self.m
+
+
+def fourier_make(mode: str, m: int, d_in: int, sigma: float = 1.0, seed: int = 0) -> FourierEncoder:
+    """nn.py:79-93 semantics: "off" (or m == 0), "nerf" (m % d_in == 0), "random"."""
+    if m < 0:
+        raise ValueError("m must be non-negative")
+    if mode == "off" or m == 0:
+        return FourierEncoder("off", np.zeros((0, d_in), np.float32), d_in)
+    if mode == "nerf":
+        if m % d_in:
+            raise ValueError(f"nerf mode needs m divisible by d_in, got m={m}, d_in={d_in}")
+        return FourierEncoder("nerf", nerf_rows(m, d_in), d_in)
+    if mode == "random":
+        b = np.random.default_rng(seed).normal(0.0, 2.0 * np.pi * sigma, size=(m, d_in))
+        return FourierEncoder("random", b.astype(np.float32), d_in, sigma, seed)
+    raise ValueError(f"unknown fourier mode {mode!r}")
+
+
+@dataclass
+class MlpParams:
+    """(out, in) weight matrices + biases; hidden layers share one activation."""
+
+    weights: list
+    biases: list
+    activation: str = "snake_alt"
+
+    def __post_init__(self):
+        if not self.weights or len(self.weights) != len(self.biases):
+            raise ValueError("weights and biases must be non-empty and equal length")
+        prev = None
+        for i, (w, b) in enumerate(zip(self.weights, self.biases)):
+            if w.ndim != 2 or b.shape != (w.shape[0],):
+                raise ValueError(f"layer {i} has inconsistent shapes {w.shape} / {b.shape}")
+            if prev is not None and w.shape[1] != prev:
+                raise ValueError(f"layer {i} input width does not chain")
+            prev = w.shape[0]
+        if self.activation not in ACTIVATION_KINDS:
+            raise ValueError(f"unknown activation kind {self.activation!r}")
+
+    @property
+    def layer_count(self) -> int:
+        return len(self.weights)
+
+    @property
+    def d_in(self) -> int:
+        return int(self.weights[0].shape[1])
+
+    @property
+    def d_out(self) -> int:
+        return int(self.weights[-1].shape[0])
+
+    @property
+    def hidden_channels(self) -> int:
+        return int(self.weights[0].shape[0])
+
+    @property
+    def param_count(self) -> int:
+        return int(sum(w.size + b.size for w, b in zip(self.weights, self.biases)))
+
+
+def init_params(layer_count: int, hidden: int, d_in: int, d_out: int, seed: int = 0,
+                activation: str = "snake_alt", dtype=np.float32) -> MlpParams:
+    """Xavier-uniform weights (drawn layer by layer from one generator), zero biases."""
+    if layer_count < 1:
+        raise ValueError("need at least one layer")
+    dims = [d_in, *([hidden] * (layer_count - 1)), d_out]
+    gen = np.random.default_rng(seed)
+    ws, bs = [], []
+    for fan_in, fan_out in zip(dims[:-1], dims[1:]):
+        lim = np.sqrt(6.0 / (fan_in + fan_out))
+        ws.append(gen.uniform(-lim, lim, size=(fan_out, fan_in)).astype(dtype))
+        bs.append(np.zeros(fan_out, dtype=dtype))
+    return MlpParams(ws, bs, activation)

@@ -1,0 +1,120 @@
+"""Screen-tile sharding of one DVR frame across GPUs (one process per GPU).
+
+SURVEY 8(e): rays are independent, so a frame splits into 8x8-pixel tiles
+assigned round-robin (tile t -> rank t mod world; the projected cube sits in the
+frame centre, so contiguous slabs would be imbalanced).  The model, grid and TF
+are replicated (each rank uploads its own copy).  Every rank renders its tiles
+into a compact slot-ordered buffer with the fused kernel; one NCCL gather moves
+the buffers to rank 0, where a permutation kernel writes the row-major frame.
+Tiles are rendered by exactly the same per-ray code as the 1-GPU path, so the
+gathered frame is bit-identical to a single-GPU render (tested).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+TILE = 8
+
+
+def tile_grid(width: int, height: int):
+    tx = math.ceil(width / TILE)
+    return tx, tx * math.ceil(height / TILE)
+
+
+def shard_pixel_index(width: int, height: int, rank: int, world: int) -> np.ndarray:
+    """Row-major pixel index of each compact slot of ``rank`` (-1 = padding).
+
+    Host mirror of slot_pixel() in fvsrn_kernels.cu; length max_local_tiles*64.
+    """
+    tx, n_tiles = tile_grid(width, height)
+    max_local = math.ceil(n_tiles / world)
+    s = np.arange(max_local * TILE * TILE)
+    tile = rank + (s >> 6) * world
+    e = s & 63
+    px = (tile % tx) * TILE + (e & 7)
+    py = (tile // tx) * TILE + (e >> 3)
+    ok = (tile < n_tiles) & (px < width) & (py < height)
+    return np.where(ok, py * width + px, -1)
+
+
+def reassemble_host(gathered: np.ndarray, width: int, height: int) -> np.ndarray:
+    """Host version of tiles_to_frame (used by CPU multi-process tests)."""
+    world = gathered.shape[0]
+    frame = np.zeros((height * width, 4), dtype=gathered.dtype)
+    for r in range(world):
+        idx = shard_pixel_index(width, height, r, world)
+        ok = idx >= 0
+        frame[idx[ok]] = gathered[r][ok]
+    return frame.reshape(height, width, 4)
+
+
+class TileShardRenderer:
+    """Renders frames of one ModelSource across the ranks of a torch.distributed group.
+
+    Each rank binds its own GPU (``torch.cuda.current_device()``); call
+    ``render(camera, settings)`` on every rank: rank 0 returns the (H,W,4)
+    device tensor, other ranks return None.
+    """
+
+    def __init__(self, source, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.source = source
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.dm = source.device_model
+        self._bufs = {}
+        self.last_eval_count = 0
+
+    def _buffers(self, width, height):
+        key = (width, height)
+        if key not in self._bufs:
+            t = self.torch
+            _, per_rank = _shard_len(width, height, self.world)
+            local = t.empty((per_rank, 4), dtype=t.float32, device="cuda")
+            gathered = (t.empty((self.world, per_rank, 4), dtype=t.float32, device="cuda")
+                        if self.rank == 0 else None)
+            frame = (t.empty((height, width, 4), dtype=t.float32, device="cuda")
+                     if self.rank == 0 else None)
+            count = t.zeros(1, dtype=t.int64, device="cuda")
+            self._bufs[key] = (local, gathered, frame, count)
+        return self._bufs[key]
+
+    def render(self, camera, settings, count: bool = False):
+        from .device import tiles_to_frame_device
+
+        t = self.torch
+        local, gathered, frame, cnt = self._buffers(camera.width, camera.height)
+        stream = t.cuda.current_stream().cuda_stream
+        if count:
+            cnt.zero_()
+        self.dm.render_device(self.source.tf, camera, settings, self.source.t, local.data_ptr(),
+                              cnt.data_ptr() if count else None, stream, rank=self.rank,
+                              world=self.world, compact=True)
+        if self.world > 1:
+            if self.rank == 0:
+                self.dist.gather(local, gather_list=list(gathered.unbind(0)), dst=0,
+                                 group=self.group)
+            else:
+                self.dist.gather(local, gather_list=None, dst=0, group=self.group)
+        elif gathered is not None:
+            gathered[0].copy_(local)
+        if self.rank == 0:
+            tiles_to_frame_device(gathered.data_ptr(), camera.width, camera.height, self.world,
+                                  frame.data_ptr(), stream)
+        if count:
+            if self.world > 1:
+                self.dist.all_reduce(cnt, group=self.group)
+            self.last_eval_count = int(cnt.item())
+        return frame if self.rank == 0 else None
+
+
+def _shard_len(width, height, world):
+    _, n_tiles = tile_grid(width, height)
+    return n_tiles, math.ceil(n_tiles / world) * TILE * TILE

@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) vs reference goldens and the oracle.
+
+Tolerances (north star): per-sample density max-abs <= 1e-2 (fp16 operands vs
+the fp32 reference), rendered images PSNR >= 40 dB.  Ray geometry is
+bit-exact (the evaluated-sample count with early termination disabled equals
+the reference's sum of per-ray step counts exactly).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2112_01579_b200 as P
+from oracle import fvsrn_oracle as O
+from tests.golden_util import GOLDEN, arrays, meta
+
+pytestmark = pytest.mark.gpu
+
+DENS_TOL = 1e-2
+
+
+def _model(name):
+    return P.model_init(P.ModelConfig(**meta()["models"][name]["config"]))
+
+
+def _omodel(name):
+    return O.model_init(O.OConfig(**meta()["models"][name]["config"]))
+
+
+def _cam(c):
+    return P.Camera(eye=c["eye"], target=c["target"], up=c["up"], fov_y=c["fov_y"],
+                    width=c["width"], height=c["height"])
+
+
+DENSITY_MODELS = ["cfg1", "cfg2", "cfg3", "tiny", "random_fourier", "relu_nogrid", "snake_f12"]
+
+
+@pytest.mark.parametrize("name", DENSITY_MODELS)
+def test_eval_density_vs_reference(name):
+    got = P.eval_density(_model(name), arrays()["eval_p"])
+    want = arrays()[f"density_{name}"]
+    err = np.abs(got - want).max()
+    assert err <= DENS_TOL, f"{name}: max abs density error {err:.3e}"
+
+
+@pytest.mark.parametrize("tt", [1.0, 6.5, 11.0, 16.25, 21.0, 0.0, 30.0])
+def test_eval_density_temporal(tt):
+    got = P.eval_density(_model("temporal"), arrays()["eval_p"], t=tt)
+    assert np.abs(got - arrays()[f"density_temporal_t{tt}"]).max() <= DENS_TOL
+    got = P.eval_density(_model("temporal_both"), arrays()["eval_p"], t=tt)
+    assert np.abs(got - arrays()[f"density_temporal_both_t{tt}"]).max() <= DENS_TOL
+
+
+@pytest.mark.parametrize("name", ["color_dirf", "color_pos"])
+def test_eval_color_vs_reference(name):
+    m = _model(name)
+    d = arrays()["eval_d"] if m.config.direction_mode != "pos" else None
+    got = P.eval_color(m, arrays()["eval_p"], d)
+    want = arrays()[f"color_{name}"]
+    assert np.abs(got - want).max() <= DENS_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "color_pos", "random_fourier"])
+def test_fused_eval_operator(name):
+    m = _model(name)
+    got = P.fused_eval(P.plan_build(m.config.layers, m.config.hidden, m.config.input_width,
+                                    m.config.output_width, budget_bytes=1 << 30), m,
+                       arrays()[f"fused_x_{name}"])
+    assert np.abs(got - arrays()[f"fused_y_{name}"]).max() <= DENS_TOL
+
+
+def test_decode_vs_reference():
+    a = arrays()
+    v = P.decode_volume(_model("tiny"), 9).values
+    assert np.abs(v - a["decode_tiny_9"]).max() <= DENS_TOL
+    v = P.decode_volume(_model("cfg1"), 17).values
+    assert np.abs(v - a["decode_cfg1_17"]).max() <= DENS_TOL
+    v = P.decode_volume(_model("temporal"), 12, t=16.25).values
+    assert np.abs(v - a["decode_temporal_12_t16.25"]).max() <= DENS_TOL
+
+
+def test_decode_full_256_vs_oracle_slices():
+    # config 4: full 256^3 decode on the GPU; oracle on two lattice slabs
+    m, om = _model("cfg2"), _omodel("cfg2")
+    vol = P.decode_volume(m, 256).values
+    assert vol.shape == (256, 256, 256)
+    axis = np.linspace(0.0, 1.0, 256)
+    for ix in (0, 137, 255):
+        gy, gz = np.meshgrid(axis, axis, indexing="ij")
+        pts = np.stack([np.full(gy.size, axis[ix]), gy.ravel(), gz.ravel()], -1)
+        want = O.eval_density(om, pts).reshape(256, 256)
+        assert np.abs(vol[ix] - want).max() <= DENS_TOL
+
+
+RENDER_MODEL = {"cfg1_v0_gray": "cfg1", "cfg1_v3_gray": "cfg1", "cfg1_v6_warm": "cfg1",
+                "cfg1_v1_peaks_bg": "cfg1", "cfg2_v2_gray": "cfg2", "tiny_center_gray": "tiny",
+                "temporal_t6.5": "temporal", "temporal_both_t3": "temporal_both",
+                "color_dirf": "color_dirf", "color_pos_et": "color_pos", "inside_gray": "cfg1",
+                "cfg3_v0_gray_48": "cfg3"}
+
+
+@pytest.mark.parametrize("tag", sorted(RENDER_MODEL))
+def test_render_vs_reference(tag):
+    r = meta()["renders"][tag]
+    m = _model(RENDER_MODEL[tag])
+    tf = P.TF_PRESETS[r["tf"]] if r["tf"] else None
+    src = P.ModelSource(m, tf, t=r["t"], use_fused=True)
+    s = P.RenderSettings(stepsize=r["stepsize"], max_steps=r["max_steps"],
+                         background=tuple(r["background"]), early_term_alpha=r["et"])
+    img = P.render_image(src, _cam(r["camera"]), s)
+    psnr = P.metric_psnr(img, arrays()[f"render_{tag}"])
+    assert psnr >= 40.0, f"{tag}: PSNR {psnr:.2f} dB"
+    # evaluated-sample count: identical up to early-termination threshold crossings
+    assert abs(src.last_eval_count - r["count"]) <= max(4, r["count"] // 10000), \
+        (src.last_eval_count, r["count"])
+
+
+@pytest.mark.parametrize("cam", ["fib0", "fib5", "center", "inside"])
+def test_ray_geometry_bit_exact_count(cam):
+    # ET disabled -> the count is exactly sum_n of render.py:189-200 (bit-exact f64 geometry)
+    c = _cam(meta()["cameras"][cam])
+    src = P.ModelSource(_model("tiny"), P.TF_PRESETS["grayscale"])
+    P.render_image(src, c, P.RenderSettings(stepsize=1 / 128, early_term_alpha=1.0))
+    assert src.last_eval_count == int(arrays()[f"rays_{cam}_n"].sum())
+
+
+def test_camera_rays_host_bit_exact():
+    for cam in ("fib0", "fib5", "center", "inside"):
+        o, d = P.camera_rays(_cam(meta()["cameras"][cam]))
+        assert np.array_equal(o, arrays()[f"rays_{cam}_o"])
+        assert np.array_equal(d, arrays()[f"rays_{cam}_d"])
+
+
+def test_raymarch_forward_explicit_rays():
+    a = arrays()
+    src = P.ModelSource(_model("cfg1"), P.TF_PRESETS["warm"])
+    px, st = P.raymarch_forward(src, a["rays_explicit_o"], a["rays_explicit_d"],
+                                P.RenderSettings(stepsize=1 / 300, max_steps=200))
+    assert st is None
+    assert O.metric_psnr(px, a["rays_explicit_px"]) >= 40.0
+    px2, st2 = P.raymarch_forward(src, a["rays_explicit_o"], a["rays_explicit_d"],
+                                  P.RenderSettings(stepsize=1 / 300, max_steps=200),
+                                  want_states=True)
+    assert st2.alpha.shape == (64,) and np.all(st2.alpha < 1.0)
+
+
+def test_render_deterministic_and_background():
+    m = _model("cfg1")
+    src = P.ModelSource(m, P.TF_PRESETS["warm"])
+    cam = P.fibonacci_cameras(8, 96, 80)[2]
+    s = P.RenderSettings(stepsize=1 / 128, background=(0.2, 0.3, 0.4))
+    a = P.render_image(src, cam, s).data
+    b = P.render_image(src, cam, s).data
+    assert np.array_equal(a, b)
+    miss = a[..., 3] == 0
+    assert miss.any()
+    np.testing.assert_array_equal(a[miss][:, :3],
+                                  np.broadcast_to(np.float32([0.2, 0.3, 0.4]), (miss.sum(), 3)))
+
+
+def test_render_cfg2_1024_rows_vs_oracle():
+    # BASELINE config 2 at full size on the GPU; oracle on every 64th row
+    m, om = _model("cfg2"), _omodel("cfg2")
+    cam = P.fibonacci_cameras(8, 1024, 1024)[1]
+    src = P.ModelSource(m, P.TF_PRESETS["grayscale"])
+    img = P.render_image(src, cam, P.RenderSettings(stepsize=1 / 256)).data
+    rows = np.arange(0, 1024, 64)
+    ocam = O.OCamera(cam.eye, cam.target, cam.up, cam.fov_y, 1024, 1024)
+    ref = O.render_image(om, O.TF_PRESETS["grayscale"], ocam, 1 / 256, rows=rows)
+    assert O.metric_psnr(img[rows], ref[rows]) >= 40.0
+    assert 70e6 < src.last_eval_count < 110e6
+
+
+def test_shards_reassemble_bit_identical():
+    torch = pytest.importorskip("torch")
+    from paper_2112_01579_b200 import device as D
+
+    m = _model("cfg1")
+    src = P.ModelSource(m, P.TF_PRESETS["grayscale"])
+    cam = P.fibonacci_cameras(8, 123, 77)[4]
+    s = P.RenderSettings(stepsize=1 / 128)
+    full = P.render_image(src, cam, s).data
+    for world in (2, 3, 8):
+        _, per_rank = D.shard_slots(cam.width, cam.height, world)
+        gathered = torch.zeros((world, per_rank, 4), dtype=torch.float32, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        for r in range(world):
+            src.device_model.render_device(src.tf, cam, s, None, gathered[r].data_ptr(), None,
+                                           stream, rank=r, world=world, compact=True)
+        frame = torch.zeros((cam.height, cam.width, 4), dtype=torch.float32, device="cuda")
+        D.tiles_to_frame_device(gathered.data_ptr(), cam.width, cam.height, world,
+                                frame.data_ptr(), stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(frame.cpu().numpy(), full), world
+
+
+@pytest.mark.parametrize("name", ["tiny_f32", "tiny_f16_u8", "temporal_both_f32"])
+def test_reference_checkpoints(name):
+    m = P.checkpoint_load(GOLDEN / f"{name}.fvsrn")
+    t = 3.0 if m.is_temporal else None
+    got = P.eval_density(m, arrays()["eval_p"][:512], t=t)
+    assert np.abs(got - arrays()[f"ckpt_{name}_density"]).max() <= DENS_TOL
+
+
+def test_contract_errors():
+    m = _model("tiny")
+    with pytest.raises(ValueError):
+        P.ModelSource(m)                                  # density head needs a TF
+    with pytest.raises(ValueError):
+        P.ModelSource(m, P.TF_PRESETS["grayscale"], t=1.0)
+    with pytest.raises(ValueError):
+        P.eval_density(_model("color_pos"), np.zeros((4, 3)))
+    with pytest.raises(ValueError):
+        P.eval_density(_model("temporal"), np.zeros((4, 3)))   # missing t
+    with pytest.raises(TypeError):
+        P.render_image(object(), P.fibonacci_cameras(1, 8, 8)[0])
+
+
+def test_empty_and_single_ray():
+    src = P.ModelSource(_model("tiny"), P.TF_PRESETS["grayscale"])
+    px, _ = P.raymarch_forward(src, np.zeros((0, 3)), np.zeros((0, 3)), P.RenderSettings())
+    assert px.shape == (0, 4)
+    img = P.render_image(src, P.fibonacci_cameras(1, 1, 1)[0], P.RenderSettings())
+    assert img.data.shape == (1, 1, 4)
+    assert P.eval_density(_model("tiny"), np.zeros((0, 3))).shape == (0,)
