@@ -1,0 +1,443 @@
+"""Benchmark: fV-SRN network evals/s and ms/frame of 1024^2 DVR on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A step is one DVR frame of the configuration's workload (default config 2:
+fV-SRN 4x32, 32^3x16 latent grid, m=14, 1024^2, stepsize 1/256 = 1 voxel of a
+256^3 field, grayscale TF), cycling through the 8 fibonacci_cameras views.
+Weights are random-init (ModelConfig seed 0); there is no dataset.
+
+* value  -- evals/s with the model resident in HBM, device-timed with CUDA events
+            around each frame on the launching stream (L2 flushed before every
+            frame, outside the events), max over ranks.
+* e2e    -- the same metric through the public API call a user makes
+            (render_image -> fvsrn_render: per-frame constants host->device,
+            framebuffer device->host inside the timed region).
+* roofline -- tensor-core FLOPs of the unpadded MLP per eval (7,168 at 4x32)
+            x evals per frame / frame time, vs MEASURED_PEAKS.json bf16 burst.
+* cpu_baseline -- the CPU oracle port (numpy + numba, thread pool like
+            render.py:320-331) on a bounded row sample of the same frame.
+
+Under torchrun (N > 1) every rank renders its round-robin share of 8x8 screen
+tiles and one NCCL gather brings the tiles to rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_fvsrn_b200")
+
+METRIC = "fV-SRN network evals/sec and ms/frame at 1024² DVR (1/2/4/8 B200) vs CPU ref"
+
+CONFIGS = {
+    "cfg1": dict(model=dict(layers=4, hidden=32, grid_resolution=16, grid_channels=16, seed=0),
+                 res=256, stepsize=1 / 128, kind="dvr",
+                 desc="config 1: fV-SRN 4x32, 16^3x16 grid, m=14, DVR 256^2, stepsize 1/128"),
+    "cfg2": dict(model=dict(layers=4, hidden=32, grid_resolution=32, grid_channels=16, seed=0),
+                 res=1024, stepsize=1 / 256, kind="dvr",
+                 desc="config 2: fV-SRN 4x32, 32^3x16 grid, m=14, DVR 1024^2, stepsize 1/256 "
+                      "(1 voxel of a 256^3 field)"),
+    "cfg3": dict(model=dict(layers=6, hidden=64, grid_resolution=64, grid_channels=16,
+                            fourier_m=30, seed=0),
+                 res=1024, stepsize=1 / 768, kind="dvr",
+                 desc="config 3: fV-SRN 6x64, 64^3x16 grid, m=30, DVR 1024^2, stepsize 1/768 "
+                      "(1 voxel of a 512x336x768 Jet-shaped field)"),
+    "cfg4": dict(model=dict(layers=4, hidden=32, grid_resolution=32, grid_channels=16, seed=0),
+                 res=256, kind="decode",
+                 desc="config 4: batched world-space density decode of the 256^3 lattice "
+                      "(config-2 weights)"),
+    "cfg5": dict(model=dict(layers=4, hidden=32, grid_resolution=32, grid_channels=16,
+                            keyframe_times=[1, 11, 21], seed=0),
+                 res=4096, stepsize=1 / 256, kind="dvr", t=6.5,
+                 desc="config 5: time-varying fV-SRN (3 keyframes, R32 F16), t=6.5, DVR 4096^2, "
+                      "stepsize 1/256"),
+}
+
+
+def mlp_flops(cfg: dict) -> int:
+    """2 * sum(in_i * out_i) over the unpadded layer widths."""
+    from paper_2112_01579_b200 import ModelConfig
+
+    c = ModelConfig(**cfg)
+    dims = [c.input_width] + [c.hidden] * (c.layers - 1) + [c.output_width]
+    return 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int, period: float = 0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json bf16_tflops burst)"
+    return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
+
+
+def ncu_traffic(config: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(config, {})
+        return e.get("dram_bytes_per_launch"), e
+    return None, {}
+
+
+# ------------------------------------------------------------------ CPU (oracle port)
+def cpu_render_sample(cfg_name: str, view: int, row_stride: int, threads: int):
+    """Oracle port on every row_stride-th row of one view; returns (evals, seconds)."""
+    from oracle import fvsrn_oracle as O
+
+    cfg = CONFIGS[cfg_name]
+    O.set_threads(threads)
+    m = O.model_init(O.OConfig(**cfg["model"]))
+    cam = O.fibonacci_cameras(8, cfg["res"], cfg["res"])[view % 8]
+    rows = np.arange(0, cfg["res"], row_stride)
+    cnt = [0]
+    t0 = time.perf_counter()
+    O.render_image(m, O.TF_PRESETS["grayscale"], cam, cfg["stepsize"], t=cfg.get("t"),
+                   counter=cnt, rows=rows, threads=threads)
+    return cnt[0], time.perf_counter() - t0
+
+
+def cpu_decode_sample(cfg_name: str, fraction: int, threads: int):
+    from oracle import fvsrn_oracle as O
+
+    cfg = CONFIGS[cfg_name]
+    O.set_threads(threads)
+    m = O.model_init(O.OConfig(**cfg["model"]))
+    res = cfg["res"]
+    axis = np.linspace(0.0, 1.0, res)
+    xs = axis[::fraction]
+    gx, gy, gz = np.meshgrid(xs, axis, axis, indexing="ij")
+    pts = np.stack([gx, gy, gz], -1).reshape(-1, 3)
+    t0 = time.perf_counter()
+    for lo in range(0, len(pts), 1 << 16):
+        O.eval_density(m, pts[lo:lo + (1 << 16)])
+    return len(pts), time.perf_counter() - t0
+
+
+def cpu_baseline(cfg_name: str, threads: int):
+    cfg = CONFIGS[cfg_name]
+    if cfg["kind"] == "decode":
+        cpu_decode_sample(cfg_name, 64, threads)       # JIT warm-up
+        n, dt = cpu_decode_sample(cfg_name, 8, threads)
+        sample = f"{cfg_name}: lattice slabs x[::8] of the {cfg['res']}^3 decode ({n} evals)"
+    else:
+        stride = max(1, cfg["res"] // 256)
+        cpu_render_sample(cfg_name, 0, cfg["res"] // 8, threads)   # JIT warm-up
+        n, dt = cpu_render_sample(cfg_name, 0, stride, threads)
+        sample = (f"{cfg_name} view 0, every {stride}th row ({cfg['res'] // stride} of "
+                  f"{cfg['res']} rows, {n} evals), {threads} threads")
+    return {"value": n / dt, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": sample, "seconds": dt,
+            "note": "numpy+numba restatement of render.py/model.py (oracle/fvsrn_oracle.py); the "
+                    "reference itself measured 3.2 M evals/s on 8 cores of the build container"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU path on the host cores (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    cfg = CONFIGS[args.config]
+    stride = max(1, cfg["res"] // 64) if cfg["kind"] == "dvr" else 32
+    runner = ((lambda v: cpu_render_sample(args.config, v, stride, threads))
+              if cfg["kind"] == "dvr" else (lambda v: cpu_decode_sample(args.config, stride, threads)))
+    for i in range(args.warmup):
+        runner(i)
+    tot_n = tot_t = 0.0
+    per = []
+    for i in range(args.steps):
+        n, dt = runner(i)
+        tot_n += n
+        tot_t += dt
+        per.append(dt)
+    value = tot_n / tot_t
+    sample = (f"{args.config}: every {stride}th row of view (step mod 8), oracle port, "
+              f"{threads} threads" if cfg["kind"] == "dvr"
+              else f"{args.config}: lattice x[::{stride}] slab set, {threads} threads")
+    line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights, ModelConfig seed 0)",
+            "config": {"workload": cfg["desc"], "sample_rows_stride": stride},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2112_01579_b200 as P
+    from paper_2112_01579_b200.sharding import TileShardRenderer
+
+    cfg = CONFIGS[args.config]
+    model = P.model_init(P.ModelConfig(**cfg["model"]))
+    flops = mlp_flops(cfg["model"])
+    t_frame = cfg.get("t")
+    res = cfg["res"]
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    launches_per_step = 1
+
+    if cfg["kind"] == "dvr":
+        src = P.ModelSource(model, P.TF_PRESETS["grayscale"], t=t_frame, use_fused=True)
+        cams = P.fibonacci_cameras(8, res, res)
+        settings = P.RenderSettings(stepsize=cfg["stepsize"])
+        if world > 1:
+            renderer = TileShardRenderer(src)
+            launches_per_step = 1 + (1 if rank == 0 else 0)
+
+            def step(i, count_ptr=None):
+                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_frame,
+                                          renderer._buffers(res, res)[0].data_ptr(), count_ptr,
+                                          stream.cuda_stream, rank=rank, world=world, compact=True)
+                local_buf, gathered, frame, _ = renderer._buffers(res, res)
+                if rank == 0:
+                    dist.gather(local_buf, gather_list=list(gathered.unbind(0)), dst=0)
+                    from paper_2112_01579_b200.device import tiles_to_frame_device
+                    tiles_to_frame_device(gathered.data_ptr(), res, res, world, frame.data_ptr(),
+                                          stream.cuda_stream)
+                else:
+                    dist.gather(local_buf, gather_list=None, dst=0)
+        else:
+            frame = torch.empty((res, res, 4), dtype=torch.float32, device="cuda")
+
+            def step(i, count_ptr=None):
+                src.device_model.render_device(src.tf, cams[i % 8], settings, t_frame,
+                                               frame.data_ptr(), count_ptr, stream.cuda_stream)
+        if t_frame is not None:
+            launches_per_step += 1          # per-frame keyframe pre-blend
+    else:  # decode: lattice split in contiguous slabs across ranks
+        total = res ** 3
+        per = -(-total // world)
+        begin, count = rank * per, max(0, min(per, total - rank * per))
+        vol = torch.empty(max(count, 1), dtype=torch.float32, device="cuda")
+        dm = P.device.device_model(model)
+
+        def step(i, count_ptr=None):
+            dm.decode_device(res, t_frame, begin, count, vol.data_ptr(), stream.cuda_stream)
+
+    # ---- warm-up
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- evaluated-sample counts (same frames as the timed loop, counted once)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    evals_per_step = []
+    for i in range(args.steps):
+        if cfg["kind"] == "dvr":
+            cnt.zero_()
+            step(i, cnt.data_ptr())
+            torch.cuda.synchronize()
+            c = cnt.clone()
+            if world > 1:
+                dist.all_reduce(c)
+            evals_per_step.append(int(c.item()))
+        else:
+            evals_per_step.append(res ** 3)
+    total_evals = sum(evals_per_step)
+
+    # ---- timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()                      # evict the L2 (outside the events)
+            evs[i][0].record(stream)
+            step(i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = torch.tensor([sum(per_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
+    tot_ms = float(tot_ms.item())
+    value = total_evals / (tot_ms / 1e3)
+    ms_per_step = tot_ms / args.steps
+
+    # ---- end-to-end through the public API (host buffers, copies inside the timing)
+    e2e = None
+    if not args.no_e2e:
+        if cfg["kind"] == "dvr":
+            if world == 1:
+                for i in range(2):
+                    P.render_image(src, cams[i % 8], settings)
+                t0 = time.perf_counter()
+                n_e = 0
+                for i in range(args.steps):
+                    P.render_image(src, cams[i % 8], settings)
+                    n_e += src.last_eval_count
+                dt = time.perf_counter() - t0
+                h2d = 4356 + 4 * 32
+                d2h = res * res * 16 + 8
+            else:
+                host = torch.empty((res, res, 4), dtype=torch.float32, pin_memory=True)
+                dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                n_e = 0
+                for i in range(args.steps):
+                    out = renderer.render(cams[i % 8], settings, count=True)
+                    n_e += renderer.last_eval_count
+                    if rank == 0:
+                        host.copy_(out)
+                torch.cuda.synchronize()
+                dist.barrier()
+                dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                dt = float(dt.item())
+                h2d = 4356 + 4 * 32
+                d2h = res * res * 16 if rank == 0 else 0
+        else:
+            t0 = time.perf_counter()
+            for i in range(max(2, args.steps // 4)):
+                vol_h = P.decode_volume(model, res, t=t_frame)
+            dt = time.perf_counter() - t0
+            n_e = max(2, args.steps // 4) * res ** 3
+            h2d, d2h = 4 * 32, res ** 3 * 4
+        e2e = {"value": n_e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * dt / args.steps
+               if cfg["kind"] == "dvr" else 1e3 * dt / max(2, args.steps // 4),
+               "api": "render_image(ModelSource) -> fvsrn_render" if cfg["kind"] == "dvr"
+               else "decode_volume -> fvsrn_decode_density"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peaks()
+    achieved = total_evals * flops / (tot_ms / 1e3) / 1e12
+    traffic, ncu = ncu_traffic(args.config)
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16 MMA operands / f32 accumulate, f64 ray setup",
+        "data": "synthetic (random-init weights, ModelConfig seed 0; fibonacci_cameras(8) views)",
+        "config": {"workload": cfg["desc"], "views": 8 if cfg["kind"] == "dvr" else None,
+                   "evals_per_step_mean": total_evals / args.steps,
+                   "ms_per_frame_median": statistics.median(per_ms),
+                   "l2": "flushed before every frame (256 MiB memset, outside the events)",
+                   "parallelism": f"screen-tile dp{world}" if world > 1 else "1 GPU",
+                   "tf": "grayscale", "t": t_frame},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "flops_per_eval": flops, "peak_source": peak_src,
+                     "note": "dominant kernel dvr_kernel; MUFU/FMA pipes bind first at c=32 "
+                             "(see profiles/)", **({"ncu": ncu} if ncu else {})},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, os.cpu_count() or 1)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

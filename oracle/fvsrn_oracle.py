@@ -164,6 +164,15 @@ def _cell_coords(res, p):
     return i0, coords - i0
 
 
+import threading
+
+_TLS = threading.local()   # .serial=True inside render_image's thread pool (no nested pools)
+
+
+def _serial():
+    return getattr(_TLS, "serial", False)
+
+
 if _HAVE_NUMBA:
     @njit(cache=False, parallel=True, fastmath=False)
     def _gather_nb(values, i0, frac, out):
@@ -191,7 +200,7 @@ def grid_sample(values, p):
     frac = frac.astype(np.float32)
     out = np.empty((i0.shape[0], values.shape[3]), dtype=np.float32)
     if _HAVE_NUMBA and len(i0) >= 1:
-        _gather_nb(values, i0, frac, out)
+        (_gather_nb_serial if _serial() else _gather_nb)(values, i0, frac, out)
         return out
     x0, y0, z0 = i0[:, 0], i0[:, 1], i0[:, 2]
     fx, fy, fz = frac[:, 0:1], frac[:, 1:2], frac[:, 2:3]
@@ -293,8 +302,76 @@ def act_eval(kind, x):
     raise ValueError(kind)
 
 
+_ACT = {k: i for i, k in enumerate(ACTIVATIONS)}
+
+if _HAVE_NUMBA:
+    @njit(cache=False, parallel=True, fastmath=True)
+    def _mlp_nb(x, wflat, bflat, dims, act, out):
+        """Per-sample f32 MLP over 32-sample tiles (the blocked evaluator of
+        fused.py:142-240, restated); used for large batches (CPU timing)."""
+        n = x.shape[0]
+        nl = dims.shape[0] - 1
+        maxw = 0
+        for i in range(nl + 1):
+            maxw = max(maxw, dims[i])
+        ntile = (n + 31) // 32
+        for t in prange(ntile):
+            lo = t * 32
+            cnt = min(n, lo + 32) - lo
+            a = np.zeros((maxw, 32), dtype=np.float32)
+            b = np.zeros((maxw, 32), dtype=np.float32)
+            for s in range(cnt):
+                for j in range(dims[0]):
+                    a[j, s] = x[lo + s, j]
+            wo = 0
+            bo = 0
+            for li in range(nl):
+                din, dout = dims[li], dims[li + 1]
+                for r in range(dout):
+                    bias = bflat[bo + r]
+                    for s in range(32):
+                        b[r, s] = bias
+                    for k in range(din):
+                        wv = wflat[wo + r * din + k]
+                        for s in range(32):
+                            b[r, s] += wv * a[k, s]
+                    if li < nl - 1:
+                        for s in range(32):
+                            v = b[r, s]
+                            if act == 0:
+                                v = max(v, np.float32(0.0))
+                            elif act == 1:
+                                v = np.float32(1.0) / (np.float32(1.0) + np.exp(-v))
+                            elif act == 2:
+                                v = np.log1p(np.exp(v)) if v < 20.0 else v
+                            else:
+                                sv = np.sin(v)
+                                v = (v if act == 3 else np.float32(0.5) * v) + sv * sv
+                            b[r, s] = v
+                wo += din * dout
+                bo += dout
+                a, b = b, a
+            for s in range(cnt):
+                for j in range(dims[nl]):
+                    out[lo + s, j] = a[j, s]
+
+
+if _HAVE_NUMBA:
+    _gather_nb_serial = njit(cache=False, parallel=False, nogil=True)(_gather_nb.py_func)
+    _mlp_nb_serial = njit(cache=False, parallel=False, fastmath=True, nogil=True)(_mlp_nb.py_func)
+
+
 def mlp_eval(model: OModel, x):
     """nn.py:195-204: h = act(h @ W.T + b) per layer, last layer linear, f32."""
+    if _HAVE_NUMBA and len(x) >= 256:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        dims = np.array([model.weights[0].shape[1]] + [w.shape[0] for w in model.weights], np.int64)
+        wflat = np.concatenate([w.ravel() for w in model.weights]).astype(np.float32)
+        bflat = np.concatenate(model.biases).astype(np.float32)
+        out = np.empty((len(x), dims[-1]), np.float32)
+        (_mlp_nb_serial if _serial() else _mlp_nb)(x, wflat, bflat, dims,
+                                                   _ACT[model.config.activation], out)
+        return out
     h = np.asarray(x, dtype=np.float32)
     last = len(model.weights) - 1
     for i, (w, b) in enumerate(zip(model.weights, model.biases)):
@@ -509,20 +586,38 @@ def raymarch_forward(model, tf, o, d, stepsize, max_steps=4096, background=(0, 0
 
 
 def render_image(model, tf, cam: OCamera, stepsize, max_steps=4096, background=(0, 0, 0),
-                 et_alpha=0.999, t=None, counter=None, rows=None):
-    """render.py:314-332 -> (H,W,4) f32.  ``rows`` restricts to a row subset
-    (used by the bounded CPU-baseline sample; rows not rendered stay 0)."""
+                 et_alpha=0.999, t=None, counter=None, rows=None, threads=1):
+    """render.py:314-332 -> (H,W,4) f32; ``threads`` > 1 splits the rays into
+    threads*4 chunks on a thread pool exactly like render.py:320-331.  ``rows``
+    restricts to a row subset (the bounded CPU-baseline sample; other rows stay 0)."""
     o, d = camera_rays(cam)
     img = np.zeros((cam.height * cam.width, 4), np.float32)
     if rows is None:
         sel = np.arange(cam.height * cam.width)
     else:
         sel = (np.asarray(rows)[:, None] * cam.width + np.arange(cam.width)[None]).reshape(-1)
-    chunk = 1 << 16
-    for lo in range(0, len(sel), chunk):
-        s = sel[lo:lo + chunk]
-        img[s] = raymarch_forward(model, tf, o[s], d[s], stepsize, max_steps, background,
-                                  et_alpha, t=t, counter=counter)
+    if threads <= 1 or len(sel) < 4096:
+        chunks = [sel[lo:lo + (1 << 16)] for lo in range(0, len(sel), 1 << 16)]
+    else:
+        chunks = [c for c in np.array_split(sel, threads * 4) if len(c)]
+    counts = [[0] for _ in chunks]
+
+    def run(i):
+        _TLS.serial = threads > 1
+        c = chunks[i]
+        img[c] = raymarch_forward(model, tf, o[c], d[c], stepsize, max_steps, background,
+                                  et_alpha, t=t, counter=counts[i])
+
+    if threads <= 1:
+        for i in range(len(chunks)):
+            run(i)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(run, range(len(chunks))))
+    if counter is not None:
+        counter[0] += sum(c[0] for c in counts)
     return img.reshape(cam.height, cam.width, 4)
 
 

@@ -258,9 +258,16 @@ FeatDev feat_for(const fvsrn_model* m, const __half* grid) {
   return fd;
 }
 
+bool fast_path(const fvsrn_model* m, KernelKind kind) {
+  if (m->act != FVSRN_ACT_SNAKE_ALT) return false;
+  if (kind == KernelKind::kFused) return true;
+  return m->fourier_mode == FVSRN_FOURIER_NERF && m->fd_in == 3 && m->raw_w == 3 &&
+         m->m == (m->hid_pad - 4) / 2 && m->f_pad == 16 && m->R > 0;
+}
+
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
-  const void* fn = kernel_for(kind, m->hid_pad);
+  const void* fn = kernel_for(kind, m->hid_pad, fast_path(m, kind));
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -483,6 +490,23 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
           else dc = i - (m->raw_w + 2 * m->m + m->T);
         }
         if (dc >= 0) ws[l][(size_t)o * Ks[l] + dc] = w;
+      }
+    }
+  }
+  // snake family: kernels evaluate h = x - cos2x (snake_alt) / 2x - cos2x (snake) and
+  // act(x) = h/2 + 1/2, so fold the 1/2 into the next layer's weights and the
+  // +1/2 * rowsum(W) into its bias (device_row: see act_h in fvsrn_device.cuh).
+  if (m->act == FVSRN_ACT_SNAKE || m->act == FVSRN_ACT_SNAKE_ALT) {
+    for (int l = 1; l < L; ++l) {
+      const int in_l = m->hidden;
+      for (int o = 0; o < N[l]; ++o) {
+        double rs = 0.0;
+        for (int i = 0; i < in_l; ++i) rs += (double)ws[l][(size_t)o * Ks[l] + i];
+        bs[l][o] = (float)((double)bs[l][o] + 0.5 * rs);
+        for (int i = 0; i < Ks[l]; ++i) {
+          ws[l][(size_t)o * Ks[l] + i] *= 0.5f;
+          wx[l][(size_t)o * Kx[l] + i] *= 0.5f;
+        }
       }
     }
   }

@@ -98,14 +98,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// nn.py:18-29 (hidden activations; last layer linear)
-__device__ __forceinline__ float act_apply(int act, float x) {
-  switch (act) {
-    case 0: return fmaxf(x, 0.f);
-    case 1: return __fdividef(1.f, 1.f + __expf(-x));
-    case 2: return x > 20.f ? x : __logf(1.f + __expf(x));
-    case 3: { float s = __sinf(x); return fmaf(s, s, x); }
-    default: { float s = __sinf(x); return fmaf(s, s, 0.5f * x); }
+// Hidden activations (nn.py:18-29).  For the snake family the kernel evaluates
+// h = x - cos 2x (snake_alt) or h = 2x - cos 2x (snake): snake_alt(x) = h/2 + 1/2
+// and snake(x) = h/2 + 1/2, so the host folds the 1/2 into the NEXT layer's
+// weights and the +1/2 into its bias (exact in fp16).  One FMUL + MUFU.COS + FADD.
+constexpr int kActRuntime = -1;
+
+template <int ACT>
+__device__ __forceinline__ float act_h(float x) {
+  if constexpr (ACT == 0) {
+    return fmaxf(x, 0.f);
+  } else if constexpr (ACT == 1) {
+    return __fdividef(1.f, 1.f + __expf(-x));
+  } else if constexpr (ACT == 2) {
+    return x > 20.f ? x : __logf(1.f + __expf(x));
+  } else if constexpr (ACT == 3) {
+    return fmaf(2.f, x, -__cosf(2.f * x));
+  } else {
+    return x - __cosf(2.f * x);
   }
 }
 
@@ -113,23 +123,38 @@ __device__ __forceinline__ float act_apply(int act, float x) {
 // Evaluates the whole network for the 32 rows staged in `stage` (row stride `rs`
 // halfs) and writes head inputs (pre-head raw outputs, up to 4 per row) to
 // `outbuf[row*4 + c]`.  MT = number of m16 tiles held at once (2 -> all 32 rows).
-template <int HID, int MT>
+template <int HID, int MT, int ACT>
 struct WarpMLP {
   static constexpr int NT = HID / 8;
   static constexpr int KT = HID / 16;
 
-  __device__ static void act_pack(int act, const float (&acc)[MT][NT][4], uint32_t (&h)[MT][KT][4]) {
+  template <int A>
+  __device__ static void act_pack_t(const float (&acc)[MT][NT][4], uint32_t (&h)[MT][KT][4]) {
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
         const float* a0 = acc[mt][2 * kt];
         const float* a1 = acc[mt][2 * kt + 1];
-        h[mt][kt][0] = pack_half2(act_apply(act, a0[0]), act_apply(act, a0[1]));
-        h[mt][kt][1] = pack_half2(act_apply(act, a0[2]), act_apply(act, a0[3]));
-        h[mt][kt][2] = pack_half2(act_apply(act, a1[0]), act_apply(act, a1[1]));
-        h[mt][kt][3] = pack_half2(act_apply(act, a1[2]), act_apply(act, a1[3]));
+        h[mt][kt][0] = pack_half2(act_h<A>(a0[0]), act_h<A>(a0[1]));
+        h[mt][kt][1] = pack_half2(act_h<A>(a0[2]), act_h<A>(a0[3]));
+        h[mt][kt][2] = pack_half2(act_h<A>(a1[0]), act_h<A>(a1[1]));
+        h[mt][kt][3] = pack_half2(act_h<A>(a1[2]), act_h<A>(a1[3]));
       }
+  }
+
+  __device__ static void act_pack(int act, const float (&acc)[MT][NT][4], uint32_t (&h)[MT][KT][4]) {
+    if constexpr (ACT != kActRuntime) {
+      act_pack_t<ACT>(acc, h);
+    } else {
+      switch (act) {   // warp-uniform, once per layer
+        case 0: act_pack_t<0>(acc, h); break;
+        case 1: act_pack_t<1>(acc, h); break;
+        case 2: act_pack_t<2>(acc, h); break;
+        case 3: act_pack_t<3>(acc, h); break;
+        default: act_pack_t<4>(acc, h); break;
+      }
+    }
   }
 
   __device__ static void bias_init(float (&acc)[MT][NT][4], const float* b, int q) {
@@ -225,13 +250,13 @@ struct WarpMLP {
   }
 };
 
-template <int HID>
+template <int HID, int ACT>
 struct MLPDispatch {
   static constexpr int MT = HID <= 64 ? 2 : 1;
   __device__ static void eval32(const __half* stage, int rs, const NetDev& net, const uint2* wf,
                                 const float* bs, float* outbuf, int lane) {
 #pragma unroll
-    for (int mb = 0; mb < 2; mb += MT) WarpMLP<HID, MT>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
+    for (int mb = 0; mb < 2; mb += MT) WarpMLP<HID, MT, ACT>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
   }
 };
 
@@ -310,7 +335,9 @@ __device__ __forceinline__ void fourier_features(const FeatDev& fd, const float 
   } else if (fd.fourier_mode == 2) {
     for (int i = 0; i < fd.m; ++i) {
       float ph = 0.f;
-      for (int a = 0; a < fd.fd_in; ++a) ph = fmaf(__ldg(fd.bmat + i * fd.fd_in + a), v[a], ph);
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+        if (a < fd.fd_in) ph = fmaf(__ldg(fd.bmat + i * fd.fd_in + a), v[a], ph);
       float s, c;
       sincosf(ph, &s, &c);
       dst[i] = pack_half2(s, c);
@@ -333,6 +360,98 @@ __device__ __forceinline__ void assemble_row(const FeatDev& fd, float px, float 
     dst[0] = pack_half2(px, py);
     dst[1] = pack_half2(pz, dx);
     dst[2] = pack_half2(dy, dz);
+  }
+}
+
+// ---------------------------------------------------------------- specialised row
+// Fast path for the default fV-SRN input (pos mode, NeRF m = NM on 3 axes, F = 16):
+// the whole row [z16 | (sin,cos) x NM | p | 0] is built in registers and written
+// with 16-byte stores (conflict-free at the odd 16-byte row stride).
+template <int NM>
+struct FastRow {
+  static constexpr int kWidth = 16 + 2 * NM + 3;
+  static constexpr int kK0 = (kWidth + 15) / 16 * 16;
+  static constexpr int kWords = kK0 / 2;
+
+  __device__ static void build(const FeatDev& fd, float px, float py, float pz, __half* row) {
+    uint32_t w[kWords];
+#pragma unroll
+    for (int i = 0; i < kWords; ++i) w[i] = 0u;
+    // latent grid (grid.py:47-84), 16 channels = 2 x 16-byte corner chunks
+    {
+      const int R = fd.grid_res;
+      const float s = (float)(R - 1);
+      float cx = fminf(fmaxf(px, 0.f), 1.f) * s;
+      float cy = fminf(fmaxf(py, 0.f), 1.f) * s;
+      float cz = fminf(fmaxf(pz, 0.f), 1.f) * s;
+      int x0 = min((int)cx, R - 2), y0 = min((int)cy, R - 2), z0 = min((int)cz, R - 2);
+      float fx = cx - (float)x0, fy = cy - (float)y0, fz = cz - (float)z0;
+      float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+      const float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                           fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+      uint16_t wk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) wk[k] = __half_as_ushort(__float2half_rn(wf[k]));
+      const int sz = 16, sy = R * 16, sx = R * R * 16;
+      const uint4* base = reinterpret_cast<const uint4*>(fd.grid + ((size_t)(x0 * R + y0) * R + z0) * 16);
+      const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+#pragma unroll
+      for (int c8 = 0; c8 < 2; ++c8) {
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(base + (off[k] >> 3) + c8);
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[2 * j] = fhfma((uint16_t)(u[j] & 0xffff), wk[k], acc[2 * j]);
+            acc[2 * j + 1] = fhfma((uint16_t)(u[j] >> 16), wk[k], acc[2 * j + 1]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[4 * c8 + j] = pack_half2(acc[2 * j], acc[2 * j + 1]);
+      }
+    }
+    // NeRF Fourier pairs: base angle f32(2 pi) * (p - rint p), then doubling
+    {
+      const float pv[3] = {px, py, pz};
+      float sn[3], cs[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) __sincosf((pv[a] - rintf(pv[a])) * 6.28318548202514648f, &sn[a], &cs[a]);
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+        const int a = i % 3;
+        if (i > 0 && a == 0) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            float s2 = 2.f * sn[b] * cs[b];
+            float c2 = fmaf(cs[b], cs[b], -sn[b] * sn[b]);
+            sn[b] = s2; cs[b] = c2;
+          }
+        }
+        w[8 + i] = pack_half2(sn[a], cs[a]);
+      }
+    }
+    w[8 + NM] = pack_half2(px, py);
+    w[9 + NM] = pack_half2(pz, 0.f);
+    uint4* dst = reinterpret_cast<uint4*>(row);
+#pragma unroll
+    for (int j = 0; j < kWords / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+};
+
+// NM > 0: specialised row; NM == 0: generic runtime layout
+template <int NM>
+__device__ __forceinline__ void assemble_row_t(const FeatDev& fd, float px, float py, float pz,
+                                               float dx, float dy, float dz, __half* row) {
+  if constexpr (NM > 0) {
+    FastRow<NM>::build(fd, px, py, pz, row);
+  } else {
+    assemble_row(fd, px, py, pz, dx, dy, dz, row);
   }
 }
 

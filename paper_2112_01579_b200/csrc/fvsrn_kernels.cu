@@ -109,8 +109,8 @@ __device__ __forceinline__ int slot_pixel(const CamDev& cam, const ShardDev& sh,
 }
 
 // ---------------------------------------------------------------- DVR
-template <int HID>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+template <int HID, int ACT, int NM>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
 dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
            MarchDev md, CamDev cam, ShardDev sh, const double* __restrict__ rays_o,
            const double* __restrict__ rays_d, long long n_slots, float* __restrict__ out,
@@ -199,11 +199,11 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
       const float px = (float)__dadd_rn(o0, __dmul_rn(tk, d0));
       const float py = (float)__dadd_rn(o1, __dmul_rn(tk, d1));
       const float pz = (float)__dadd_rn(o2, __dmul_rn(tk, d2));
-      assemble_row(fd, px, py, pz, use_dir ? (float)d0 : 0.f, use_dir ? (float)d1 : 0.f,
-                   use_dir ? (float)d2 : 0.f, myrow);
+      assemble_row_t<NM>(fd, px, py, pz, use_dir ? (float)d0 : 0.f, use_dir ? (float)d1 : 0.f,
+                         use_dir ? (float)d2 : 0.f, myrow);
     }
     __syncwarp();
-    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
 
     // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
@@ -234,8 +234,8 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
 
 // ---------------------------------------------------------------- decode / eval
 // mode 0: lattice decode (model.py:385-398); mode 1: positions (+dirs) from memory
-template <int HID>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+template <int HID, int ACT, int NM>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
 sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, int res, double step,
               long long begin, long long count, const double* __restrict__ pos,
               const double* __restrict__ dirs, float* __restrict__ out) {
@@ -264,10 +264,10 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
         px = (float)pos[3 * i]; py = (float)pos[3 * i + 1]; pz = (float)pos[3 * i + 2];
         if (dirs) { dx = (float)dirs[3 * i]; dy = (float)dirs[3 * i + 1]; dz = (float)dirs[3 * i + 2]; }
       }
-      assemble_row(fd, px, py, pz, dx, dy, dz, myrow);
+      assemble_row_t<NM>(fd, px, py, pz, dx, dy, dz, myrow);
     }
     __syncwarp();
-    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
     if (valid) {
       const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
@@ -283,8 +283,8 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
 }
 
 // head(mlp(x)) with x already assembled in the reference column order.
-template <int HID>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? 2 : 1)
+template <int HID, int ACT>
+__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
 fused_eval_kernel(NetDev net, int d_in, int k0, const float* __restrict__ x, long long count,
                   float* __restrict__ out) {
   const int rs = k0 + 8;
@@ -300,7 +300,7 @@ fused_eval_kernel(NetDev net, int d_in, int k0, const float* __restrict__ x, lon
     if (valid)
       for (int j = 0; j < d_in; ++j) myrow[j] = __float2half_rn(x[i * d_in + j]);
     __syncwarp();
-    MLPDispatch<HID>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
     if (valid) {
       const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
@@ -340,20 +340,18 @@ __global__ void tiles_to_frame_kernel(const float4* __restrict__ gathered, int W
 // ---------------------------------------------------------------- launch table
 #define FVSRN_FOR_HIDDEN(X) X(16) X(32) X(48) X(64) X(96) X(128)
 
-template <int HID>
-static const void* dvr_ptr() { return (const void*)dvr_kernel<HID>; }
-template <int HID>
-static const void* sample_ptr() { return (const void*)sample_kernel<HID>; }
-template <int HID>
-static const void* fused_ptr() { return (const void*)fused_eval_kernel<HID>; }
-
-const void* kernel_for(KernelKind kind, int hid) {
+// fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode); else generic
+const void* kernel_for(KernelKind kind, int hid, bool fast) {
   switch (hid) {
-#define CASE(H)                                            \
-  case H:                                                  \
-    if (kind == KernelKind::kDVR) return dvr_ptr<H>();     \
-    if (kind == KernelKind::kSample) return sample_ptr<H>(); \
-    return fused_ptr<H>();
+#define CASE(H)                                                                              \
+  case H:                                                                                    \
+    if (kind == KernelKind::kDVR)                                                            \
+      return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2>                               \
+                  : (const void*)dvr_kernel<H, kActRuntime, 0>;                              \
+    if (kind == KernelKind::kSample)                                                         \
+      return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2>                            \
+                  : (const void*)sample_kernel<H, kActRuntime, 0>;                           \
+    return fast ? (const void*)fused_eval_kernel<H, 4> : (const void*)fused_eval_kernel<H, kActRuntime>;
     FVSRN_FOR_HIDDEN(CASE)
 #undef CASE
     default: return nullptr;

@@ -8,7 +8,8 @@
 
 namespace fvsrn {
 
-constexpr int kThreads = 256;  // 8 independent warps per CTA; weights shared in smem
+constexpr int kThreads = 128;  // 4 independent warps per CTA; weights shared in smem
+constexpr int kMinBlocks = 4;  // -> <= 128 registers/thread, 16 warps/SM
 
 struct CamDev {
   double eye[3], fwd[3], right[3], up[3];
@@ -24,7 +25,8 @@ struct ShardDev {
 enum class KernelKind { kDVR, kSample, kFused };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
-const void* kernel_for(KernelKind kind, int hid_pad);
+// fast: specialised default-input / snake_alt variant (see FastRow).
+const void* kernel_for(KernelKind kind, int hid_pad, bool fast);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,

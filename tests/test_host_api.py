@@ -1,0 +1,191 @@
+"""CPU tests of the host-side mirror of the reference API and of the C-ABI library
+(no compute calls: this container has no GPU)."""
+
+import ctypes
+import hashlib
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2112_01579_b200 as P
+from paper_2112_01579_b200 import _lib
+from tests.golden_util import GOLDEN, arrays, meta
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", sorted(meta()["models"]))
+def test_model_init_bit_exact_vs_reference(name):
+    m = P.model_init(P.ModelConfig(**meta()["models"][name]["config"]))
+    h = meta()["models"][name]["hashes"]
+    assert [_sha(w) for w in m.params.weights] == h["weights"]
+    assert [_sha(b) for b in m.params.biases] == h["biases"]
+    assert [_sha(g.values) for g in m.grids] == h["grids"]
+    assert _sha(m.spatial_encoder.b_matrix) == h["b_matrix"]
+    assert m.config.input_width == meta()["models"][name]["input_width"]
+
+
+def test_config_validation_matches_reference():
+    with pytest.raises(ValueError):
+        P.ModelConfig(head="rgb")
+    with pytest.raises(ValueError):
+        P.ModelConfig(direction_mode="dirP")          # needs the colour head
+    with pytest.raises(ValueError):
+        P.ModelConfig(time_mode="direct")             # needs keyframes
+    with pytest.raises(ValueError):
+        P.ModelConfig(keyframe_times=[1, 2], grid_resolution=0)
+    assert P.ModelConfig().input_width == 47
+    assert P.ModelConfig(layers=6, hidden=64, fourier_m=30).input_width == 79
+
+
+@pytest.mark.parametrize("name", ["tiny_f32", "tiny_f16_u8", "temporal_both_f32"])
+def test_checkpoint_load_reference_files(name, tmp_path):
+    m = P.checkpoint_load(GOLDEN / f"{name}.fvsrn")
+    cfg_name = "temporal_both" if "temporal" in name else "tiny"
+    ref = P.model_init(P.ModelConfig(**meta()["models"][cfg_name]["config"]))
+    if name.endswith("f32"):
+        for a, b in zip(m.params.weights, ref.params.weights):
+            assert np.array_equal(a, b)
+        for a, b in zip(m.grids, ref.grids):
+            assert np.array_equal(a.values, b.values)
+    else:
+        assert m.quantized is not None and len(m.quantized) == 1
+        q = P.grid_quantize(ref.grid)
+        assert np.array_equal(m.quantized[0].codes, q.codes)
+    # round trip through our writer
+    out = tmp_path / "rt.fvsrn"
+    P.checkpoint_save(m, out)
+    back = P.checkpoint_load(out)
+    for a, b in zip(back.params.weights, m.params.weights):
+        assert np.array_equal(a, b)
+
+
+def test_checkpoint_errors(tmp_path):
+    m = P.model_init(P.ModelConfig(layers=2, hidden=16, fourier_m=6, grid_resolution=4,
+                                   grid_channels=4, seed=7))
+    p = tmp_path / "x.fvsrn"
+    P.checkpoint_save(m, p)
+    raw = p.read_bytes()
+    (tmp_path / "bad.fvsrn").write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(P.CheckpointError):
+        P.checkpoint_load(tmp_path / "bad.fvsrn")
+    (tmp_path / "trunc.fvsrn").write_bytes(raw[:-64])
+    with pytest.raises(P.CheckpointError):
+        P.checkpoint_load(tmp_path / "trunc.fvsrn")
+
+
+def test_quantize_known_answers():
+    v = np.zeros((2, 2, 2, 1), np.float32)
+    v[0, 0, 0, 0], v[1, 1, 1, 0] = -1.0, 1.0
+    assert P.grid_quantize(P.LatentGrid(v)).codes[0, 1, 0, 0] == 128
+    g = P.LatentGrid(np.full((3, 3, 3, 2), 0.42, np.float32))
+    q = P.grid_quantize(g)
+    assert np.all(q.codes == 0)
+    assert np.array_equal(P.grid_dequantize(q).values, g.values)
+
+
+CAPACITY_FRONTIER = {32: 22, 48: 10, 64: 6, 96: 3, 128: 2}   # PAPER.md Table 1
+
+
+@pytest.mark.parametrize("c,l", CAPACITY_FRONTIER.items())
+def test_plan_build_table1_frontier(c, l):
+    plan = P.plan_build(l, c, c - 1, 1)
+    assert plan.resident_weight_bytes + plan.resident_scratch_bytes <= plan.budget_bytes
+    with pytest.raises(P.CapacityError):
+        P.plan_build(l + 1, c, c - 1, 1)
+
+
+def test_plan_build_worked_example():
+    plan = P.plan_build(4, 48, 47, 1)
+    assert (plan.m_w, plan.m_s, plan.w) == (18816, 3072, 9)
+    assert P.plan_build(4, 32, 47, 1).padded_widths == (48, 32, 32, 32, 16)
+
+
+def test_transfer_function_validation():
+    tf = P.TF_PRESETS["warm"]
+    assert tf.max_sigma == 10.0
+    with pytest.raises(ValueError):
+        P.TransferFunction.from_points([(0.0, (0, 0, 0), 0.0)])
+    with pytest.raises(ValueError):
+        P.TransferFunction.from_points([(0.0, (0, 0, 0), 0.0), (0.5, (1, 1, 1), 1.0)])
+    with pytest.raises(ValueError):
+        P.TransferFunction.from_points([(0.0, (0, 0, 0), -1.0), (1.0, (1, 1, 1), 1.0)])
+    back = P.tf_from_json([{"x": x, "rgb": list(r), "sigma": s}
+                           for x, r, s in zip(tf.xs, tf.rgbs, tf.sigmas)])
+    assert np.array_equal(back.xs, tf.xs)
+
+
+def test_camera_and_settings_validation():
+    with pytest.raises(ValueError):
+        P.Camera(eye=(0, 0, 0), target=(0, 0, 0), up=(0, 1, 0), fov_y=1.0, width=4, height=4)
+    with pytest.raises(ValueError):
+        P.Camera(eye=(0, 0, 1), target=(0, 0, 0), up=(0, 0, 1), fov_y=1.0, width=4, height=4)
+    with pytest.raises(ValueError):
+        P.RenderSettings(stepsize=0.0)
+    with pytest.raises(ValueError):
+        P.RenderSettings(early_term_alpha=1.5)
+    assert P.RenderSettings.for_voxels(256, 1.0).stepsize == 1.0 / 256
+
+
+@pytest.mark.parametrize("cam", ["fib0", "fib5", "center", "inside"])
+def test_camera_rays_bit_exact(cam):
+    c = meta()["cameras"][cam]
+    o, d = P.camera_rays(P.Camera(eye=c["eye"], target=c["target"], up=c["up"],
+                                  fov_y=c["fov_y"], width=c["width"], height=c["height"]))
+    assert np.array_equal(o, arrays()[f"rays_{cam}_o"])
+    assert np.array_equal(d, arrays()[f"rays_{cam}_d"])
+
+
+def test_fibonacci_cameras_match_reference_views():
+    r = meta()["renders"]["cfg1_v0_gray"]["camera"]
+    cam = P.fibonacci_cameras(8, 128, 128)[0]
+    assert np.array_equal(cam.eye, np.array(r["eye"]))
+    assert np.array_equal(cam.up, np.array(r["up"]))
+
+
+def test_psnr_known_answers():
+    x = np.zeros((2, 2, 4), np.float32)
+    assert P.metric_psnr(x, x) == 99.0
+    assert P.metric_psnr(x, x + 1) == pytest.approx(0.0)
+    with pytest.raises(ValueError):
+        P.metric_psnr(x, np.zeros((2, 3, 4)))
+
+
+# ------------------------------------------------------------------ C ABI library
+def _header_symbols():
+    text = (ROOT / "include" / "fvsrn_b200.h").read_text()
+    return sorted(set(re.findall(r"FVSRN_API\s+[\w\s\*]+?\b(fvsrn_\w+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _lib.lib()
+    syms = _header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTS), "ctypes table and header disagree"
+    assert b"sm_100a" in lib.fvsrn_version()
+
+
+def test_library_reports_errors_without_gpu():
+    lib = _lib.lib()
+    # a null descriptor is a contract violation, reported as ValueError
+    h = ctypes.c_void_p()
+    rc = lib.fvsrn_model_create(None, 0, ctypes.byref(h))
+    assert rc == _lib.FVSRN_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
