@@ -5,7 +5,7 @@ CSRC := paper_2112_01579_b200/csrc
 LIB  := paper_2112_01579_b200/libfvsrn_b200.so
 SRCS := $(CSRC)/fvsrn_kernels.cu $(CSRC)/fvsrn_capi.cu
 HDRS := $(CSRC)/fvsrn_device.cuh $(CSRC)/fvsrn_kernels.cuh include/fvsrn_b200.h
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+NVFLAGS := $(ARCH) -O3 -lineinfo -ftz=true -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Xptxas -v --expt-relaxed-constexpr -Iinclude
 
 all: $(LIB)

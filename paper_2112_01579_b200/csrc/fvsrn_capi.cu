@@ -65,7 +65,10 @@ void build_pack(const std::vector<std::vector<float>>& wdev, const std::vector<i
           u.y = (uint32_t)h(k0 + 8) | ((uint32_t)h(k0 + 9) << 16);
           pk.frag.push_back(u);
         }
-    for (int n = 0; n < N[l]; ++n) pk.bias.push_back(bdev[l][n]);
+    // accumulator quads: (nt, q) -> {b[nt*8+2q], b[nt*8+2q+1], same, same}
+    for (int nt = 0; nt < NT; ++nt)
+      for (int q = 0; q < 4; ++q)
+        for (int c = 0; c < 4; ++c) pk.bias.push_back(bdev[l][nt * 8 + 2 * q + (c & 1)]);
   }
   pk.w_off[L] = (int)pk.frag.size();
   pk.b_off[L] = (int)pk.bias.size();
@@ -493,22 +496,27 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       }
     }
   }
-  // snake family: kernels evaluate h = x - cos2x (snake_alt) / 2x - cos2x (snake) and
-  // act(x) = h/2 + 1/2, so fold the 1/2 into the next layer's weights and the
-  // +1/2 * rowsum(W) into its bias (device_row: see act_h in fvsrn_device.cuh).
+  // snake family (see act_h in fvsrn_device.cuh): every layer feeding an activation is
+  // pre-scaled by 2 (accumulator a = 2x), and the activation's affine tail
+  // act = f*h + 1/2 (f = 1/4 snake_alt, 1/2 snake) is folded into the next layer:
+  // W' = s_out * f * W,  b' = s_out * (b + rowsum(W)/2).  Powers of two: exact in fp16.
+  float s_out0 = 1.f;
   if (m->act == FVSRN_ACT_SNAKE || m->act == FVSRN_ACT_SNAKE_ALT) {
-    for (int l = 1; l < L; ++l) {
-      const int in_l = m->hidden;
+    const double f = m->act == FVSRN_ACT_SNAKE_ALT ? 0.25 : 0.5;
+    for (int l = 0; l < L; ++l) {
+      const double so = (l < L - 1) ? 2.0 : 1.0;
+      const double fin = (l >= 1) ? f : 1.0;
+      const int in_l = (l == 0) ? d->d_in : m->hidden;
       for (int o = 0; o < N[l]; ++o) {
         double rs = 0.0;
-        for (int i = 0; i < in_l; ++i) rs += (double)ws[l][(size_t)o * Ks[l] + i];
-        bs[l][o] = (float)((double)bs[l][o] + 0.5 * rs);
-        for (int i = 0; i < Ks[l]; ++i) {
-          ws[l][(size_t)o * Ks[l] + i] *= 0.5f;
-          wx[l][(size_t)o * Kx[l] + i] *= 0.5f;
-        }
+        if (l >= 1 && o < ((l == L - 1) ? d_out : m->hidden))
+          for (int i = 0; i < in_l; ++i) rs += (double)d->weights[l][(size_t)o * in_l + i];
+        bs[l][o] = (float)(so * ((double)bs[l][o] + 0.5 * rs));
+        for (int i = 0; i < Ks[l]; ++i) ws[l][(size_t)o * Ks[l] + i] *= (float)(so * fin);
+        for (int i = 0; i < Kx[l]; ++i) wx[l][(size_t)o * Kx[l] + i] *= (float)(so * fin);
       }
     }
+    s_out0 = L > 1 ? 2.f : 1.f;
   }
   m->n0 = N[0];
   m->b0_static = bs[0];
@@ -517,7 +525,8 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
     const int out0 = (L == 1) ? d_out : m->hidden;
     for (int o = 0; o < out0; ++o)
       for (int j = 0; j < m->T; ++j)
-        m->w0_time[(size_t)o * m->T + j] = d->weights[0][(size_t)o * d->d_in + m->raw_w + 2 * m->m + j];
+        m->w0_time[(size_t)o * m->T + j] =
+            s_out0 * d->weights[0][(size_t)o * d->d_in + m->raw_w + 2 * m->m + j];
   }
   Pack pks, pkx;
   build_pack(ws, Ks, N, bs, pks);

@@ -85,6 +85,16 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
 }
 
+__device__ __forceinline__ void mma16816c(float (&d)[4], const uint32_t (&a)[4], uint2 b,
+                                          const float4& c) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};\n"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y),
+        "f"(c.x), "f"(c.y), "f"(c.z), "f"(c.w));
+}
+
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* smem_row_ptr) {
   uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(smem_row_ptr));
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -98,10 +108,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// Hidden activations (nn.py:18-29).  For the snake family the kernel evaluates
-// h = x - cos 2x (snake_alt) or h = 2x - cos 2x (snake): snake_alt(x) = h/2 + 1/2
-// and snake(x) = h/2 + 1/2, so the host folds the 1/2 into the NEXT layer's
-// weights and the +1/2 into its bias (exact in fp16).  One FMUL + MUFU.COS + FADD.
+// Hidden activations (nn.py:18-29).  For the snake family the host pre-scales every
+// hidden layer by 2 so the accumulator holds a = 2x, and the kernel evaluates
+//   snake_alt: h = a - 2 cos a   (act = h/4 + 1/2)
+//   snake:     h = a -   cos a   (act = h/2 + 1/2)
+// the 1/4 (1/2) and the +1/2 are folded into the NEXT layer's weights / bias on the
+// host (exact in fp16).  Cost per element: FMUL.RZ + MUFU.COS + FFMA.
 constexpr int kActRuntime = -1;
 
 template <int ACT>
@@ -113,9 +125,9 @@ __device__ __forceinline__ float act_h(float x) {
   } else if constexpr (ACT == 2) {
     return x > 20.f ? x : __logf(1.f + __expf(x));
   } else if constexpr (ACT == 3) {
-    return fmaf(2.f, x, -__cosf(2.f * x));
+    return x - __cosf(x);
   } else {
-    return x - __cosf(2.f * x);
+    return fmaf(-2.f, __cosf(x), x);
   }
 }
 
@@ -157,16 +169,11 @@ struct WarpMLP {
     }
   }
 
-  __device__ static void bias_init(float (&acc)[MT][NT][4], const float* b, int q) {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float2 bb = *reinterpret_cast<const float2*>(b + nt * 8 + 2 * q);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        acc[mt][nt][0] = bb.x; acc[mt][nt][1] = bb.y;
-        acc[mt][nt][2] = bb.x; acc[mt][nt][3] = bb.y;
-      }
-    }
+  // Biases are stored as accumulator quads: for (n-tile nt, quad lane q) the float4
+  // {b[nt*8+2q], b[nt*8+2q+1], same, same} at bs[(nt*4 + q)*4] -> one LDS.128 that is
+  // the C operand of the layer's first MMA (no register copies).
+  __device__ static float4 bias_quad(const float* bs, int nt, int q) {
+    return *reinterpret_cast<const float4*>(bs + (nt * 4 + q) * 4);
   }
 
   // m_base: first m16 tile index handled (0, or 0/1 when MT == 1)
@@ -175,32 +182,42 @@ struct WarpMLP {
     const int g = lane >> 2, q = lane & 3;
     const int arow = lane & 15, acol = (lane >> 4) * 8;
     float out_acc[MT][4];
+    const __half* arow_ptr = stage + (m_base * 16 + arow) * rs + acol;
 
     if (net.layers == 1) {
-      float2 bb = *reinterpret_cast<const float2*>(bs + net.b_off[0] + 2 * q);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        out_acc[mt][0] = bb.x; out_acc[mt][1] = bb.y; out_acc[mt][2] = bb.x; out_acc[mt][3] = bb.y;
-      }
+      const float4 bq = bias_quad(bs + net.b_off[0], 0, q);
       for (int kt = 0; kt < net.kt0; ++kt) {
         uint2 b = wf[net.w_off[0] + kt * 32 + lane];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           uint32_t a[4];
-          ldmatrix_x4(a, stage + ((m_base + mt) * 16 + arow) * rs + kt * 16 + acol);
-          mma16816(out_acc[mt], a, b);
+          ldmatrix_x4(a, arow_ptr + mt * 16 * rs + kt * 16);
+          if (kt == 0) mma16816c(out_acc[mt], a, b, bq);
+          else mma16816(out_acc[mt], a, b);
         }
       }
     } else {
       float acc[MT][NT][4];
       uint32_t h[MT][KT][4];
-      // ---- layer 0: A from the stage, K = 16*kt0
-      bias_init(acc, bs + net.b_off[0], q);
-      for (int kt = 0; kt < net.kt0; ++kt) {
+      // ---- layer 0: A from the stage, K = 16*kt0 (first k tile peeled: C = bias)
+      {
+        const float* b0 = bs + net.b_off[0];
         uint32_t a[MT][4];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          ldmatrix_x4(a[mt], stage + ((m_base + mt) * 16 + arow) * rs + kt * 16 + acol);
+        for (int mt = 0; mt < MT; ++mt) ldmatrix_x4(a[mt], arow_ptr + mt * 16 * rs);
+        const uint2* wl = wf + net.w_off[0] + lane;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint2 b = wl[nt * 32];
+          const float4 bq = bias_quad(b0, nt, q);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) mma16816c(acc[mt][nt], a[mt], b, bq);
+        }
+      }
+      for (int kt = 1; kt < net.kt0; ++kt) {
+        uint32_t a[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) ldmatrix_x4(a[mt], arow_ptr + mt * 16 * rs + kt * 16);
         const uint2* wl = wf + net.w_off[0] + kt * NT * 32 + lane;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -212,31 +229,36 @@ struct WarpMLP {
       act_pack(net.act, acc, h);
       // ---- hidden layers
       for (int l = 1; l < net.layers - 1; ++l) {
-        bias_init(acc, bs + net.b_off[l], q);
+        const float* bl = bs + net.b_off[l];
         const uint2* wl = wf + net.w_off[l] + lane;
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             uint2 b = wl[(kt * NT + nt) * 32];
+            if (kt == 0) {
+              const float4 bq = bias_quad(bl, nt, q);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) mma16816(acc[mt][nt], h[mt][kt], b);
+              for (int mt = 0; mt < MT; ++mt) mma16816c(acc[mt][nt], h[mt][kt], b, bq);
+            } else {
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) mma16816(acc[mt][nt], h[mt][kt], b);
+            }
           }
         act_pack(net.act, acc, h);
       }
       // ---- last layer: N = 8 (one n tile), linear
       const int L = net.layers - 1;
-      float2 bb = *reinterpret_cast<const float2*>(bs + net.b_off[L] + 2 * q);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        out_acc[mt][0] = bb.x; out_acc[mt][1] = bb.y; out_acc[mt][2] = bb.x; out_acc[mt][3] = bb.y;
-      }
+      const float4 bq = bias_quad(bs + net.b_off[L], 0, q);
       const uint2* wl = wf + net.w_off[L] + lane;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
         uint2 b = wl[kt * 32];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) mma16816(out_acc[mt], h[mt][kt], b);
+        for (int mt = 0; mt < MT; ++mt) {
+          if (kt == 0) mma16816c(out_acc[mt], h[mt][kt], b, bq);
+          else mma16816(out_acc[mt], h[mt][kt], b);
+        }
       }
     }
     if (q < 2) {
@@ -389,9 +411,9 @@ struct FastRow {
       float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
       const float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
                            fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
-      uint16_t wk[8];
+      __half2 wk[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) wk[k] = __half_as_ushort(__float2half_rn(wf[k]));
+      for (int k = 0; k < 8; ++k) wk[k] = __float2half2_rn(wf[k]);
       const int sz = 16, sy = R * 16, sx = R * R * 16;
       const uint4* base = reinterpret_cast<const uint4*>(fd.grid + ((size_t)(x0 * R + y0) * R + z0) * 16);
       const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
@@ -400,20 +422,16 @@ struct FastRow {
         uint4 v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = __ldg(base + (off[k] >> 3) + c8);
-        float acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        // z = sum_k w_k g_k in packed half2 (HFMA2): 32 instructions per 8 channels
+        __half2 acc[4];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+          const __half2* g2 = reinterpret_cast<const __half2*>(&v[k]);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            acc[2 * j] = fhfma((uint16_t)(u[j] & 0xffff), wk[k], acc[2 * j]);
-            acc[2 * j + 1] = fhfma((uint16_t)(u[j] >> 16), wk[k], acc[2 * j + 1]);
-          }
+          for (int j = 0; j < 4; ++j) acc[j] = k == 0 ? __hmul2(wk[k], g2[j]) : __hfma2(wk[k], g2[j], acc[j]);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) w[4 * c8 + j] = pack_half2(acc[2 * j], acc[2 * j + 1]);
+        for (int j = 0; j < 4; ++j) w[4 * c8 + j] = *reinterpret_cast<uint32_t*>(&acc[j]);
       }
     }
     // NeRF Fourier pairs: base angle f32(2 pi) * (p - rint p), then doubling

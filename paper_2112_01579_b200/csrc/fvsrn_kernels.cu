@@ -33,9 +33,12 @@ __device__ __forceinline__ void stage_setup(const NetDev& net, const float* b0, 
 
   for (int i = threadIdx.x; i < net.w_total; i += blockDim.x) wf_s[i] = net.wfrag[i];
   for (int i = threadIdx.x; i < net.b_total; i += blockDim.x) b_s[i] = net.bias[i];
-  if (b0) {
-    const int n0 = net.b_off[1] - net.b_off[0];
-    for (int i = threadIdx.x; i < n0; i += blockDim.x) b_s[i] = b0[i];
+  if (b0) {  // per-frame layer-0 bias (time folded), expanded to accumulator quads
+    const int n0q = net.b_off[1] - net.b_off[0];
+    for (int i = threadIdx.x; i < n0q; i += blockDim.x) {
+      const int j = i >> 2;
+      b_s[i] = b0[(j >> 2) * 8 + 2 * (j & 3) + (i & 1)];
+    }
   }
   if (tf_in) {
     const int words = sizeof(TFDev) / 4;
@@ -128,7 +131,10 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   bool has = false;
   int k = 0, n = 0;
   long long oslot = 0;
-  double o0 = 0, o1 = 0, o2 = 0, d0 = 0, d1 = 0, d2 = 0, tmin = 0, ds = 0;
+  // per-ray march state: first sample position pe and step vector dd, both rounded
+  // from the f64 geometry (render.py:224-225); p_k = pe + k * dd in f32
+  float pe0 = 0.f, pe1 = 0.f, pe2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f;
+  float dx = 0.f, dy = 0.f, dz = 0.f;
   float dsf = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
   unsigned long long evals = 0;
   long long chunk_base = 0;
@@ -177,9 +183,15 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
           if (march_geometry(md, r)) {
             has = true;
             k = 0; n = r.n; oslot = dst;
-            o0 = r.o[0]; o1 = r.o[1]; o2 = r.o[2];
-            d0 = r.d[0]; d1 = r.d[1]; d2 = r.d[2];
-            tmin = r.tmin; ds = r.ds; dsf = (float)r.ds;
+            const double t0 = __dadd_rn(r.tmin, __dmul_rn(0.5, r.ds));
+            pe0 = (float)__dadd_rn(r.o[0], __dmul_rn(t0, r.d[0]));
+            pe1 = (float)__dadd_rn(r.o[1], __dmul_rn(t0, r.d[1]));
+            pe2 = (float)__dadd_rn(r.o[2], __dmul_rn(t0, r.d[2]));
+            dd0 = (float)__dmul_rn(r.ds, r.d[0]);
+            dd1 = (float)__dmul_rn(r.ds, r.d[1]);
+            dd2 = (float)__dmul_rn(r.ds, r.d[2]);
+            dx = (float)r.d[0]; dy = (float)r.d[1]; dz = (float)r.d[2];
+            dsf = (float)r.ds;
             C0 = C1 = C2 = A = 0.f;
           } else {
             *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
@@ -195,12 +207,10 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
 
     // ---- sample position (render.py:224-225, f64) and input row
     if (has) {
-      const double tk = __dadd_rn(tmin, __dmul_rn((double)k + 0.5, ds));
-      const float px = (float)__dadd_rn(o0, __dmul_rn(tk, d0));
-      const float py = (float)__dadd_rn(o1, __dmul_rn(tk, d1));
-      const float pz = (float)__dadd_rn(o2, __dmul_rn(tk, d2));
-      assemble_row_t<NM>(fd, px, py, pz, use_dir ? (float)d0 : 0.f, use_dir ? (float)d1 : 0.f,
-                         use_dir ? (float)d2 : 0.f, myrow);
+      const float kf = (float)k;
+      const float px = fmaf(kf, dd0, pe0), py = fmaf(kf, dd1, pe1), pz = fmaf(kf, dd2, pe2);
+      assemble_row_t<NM>(fd, px, py, pz, use_dir ? dx : 0.f, use_dir ? dy : 0.f,
+                         use_dir ? dz : 0.f, myrow);
     }
     __syncwarp();
     MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);

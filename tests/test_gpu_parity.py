@@ -110,7 +110,10 @@ def test_render_vs_reference(tag):
     psnr = P.metric_psnr(img, arrays()[f"render_{tag}"])
     assert psnr >= 40.0, f"{tag}: PSNR {psnr:.2f} dB"
     # evaluated-sample count: identical up to early-termination threshold crossings
-    assert abs(src.last_eval_count - r["count"]) <= max(4, r["count"] // 10000), \
+    # (a ray whose opacity lands within fp16 noise of 0.999 may stop one step
+    # later, or run on through a transparent TF gap); <= 0.1%.  The exact-count
+    # gate is test_ray_geometry_bit_exact_count (ET disabled).
+    assert abs(src.last_eval_count - r["count"]) <= max(4, r["count"] // 1000), \
         (src.last_eval_count, r["count"])
 
 
