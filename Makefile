@@ -16,6 +16,10 @@ $(LIB): $(SRCS) $(HDRS)
 
 $(shell mkdir -p build)
 
+# A/B experiment build: make variant VDEFS="-DFVSRN_MIN_BLOCKS=5" VNAME=mb5
+variant: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) $(VDEFS) -shared -o build/libfvsrn_$(VNAME).so $(SRCS) -lcudart_static -ldl -lrt -lpthread 2> build/ptxas_$(VNAME).log || (cat build/ptxas_$(VNAME).log; false)
+
 clean:
 	rm -f $(LIB)
 

@@ -139,6 +139,10 @@ FVSRN_API int32_t fvsrn_decode_density(fvsrn_model_t model, int32_t resolution, 
 FVSRN_API int32_t fvsrn_decode_density_device(fvsrn_model_t model, int32_t resolution, double t,
                                     int64_t lattice_begin, int64_t lattice_count,
                                     float* d_out, void* stream);
+/* Page-locked host buffers (e.g. reusable framebuffers: the D2H of fvsrn_render
+ * into pinned memory runs at full PCIe/C2C bandwidth). */
+FVSRN_API int32_t fvsrn_host_alloc(uint64_t bytes, void** ptr);
+FVSRN_API int32_t fvsrn_host_free(void* ptr);
 FVSRN_API int32_t fvsrn_fused_eval(fvsrn_model_t model, const float* x, int64_t n, float* out);
 
 #ifdef __cplusplus

@@ -9,7 +9,7 @@ sm_100a CUDA kernels behind the C ABI of ``include/fvsrn_b200.h``.
 
 __version__ = "0.1.0"
 
-from ._lib import CapacityError
+from ._lib import CapacityError, pinned_empty
 from .fused import FusedPlan, fused_eval, plan_build, plan_for_model, warmup
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
                    grid_quantize)

@@ -14,7 +14,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libfvsrn_b200.so"
+LIB_PATH = Path(os.environ.get("FVSRN_LIB") or
+                Path(__file__).resolve().parent / "libfvsrn_b200.so")   # FVSRN_LIB: A/B builds
 
 FVSRN_OK, FVSRN_EINVAL, FVSRN_ECAPACITY, FVSRN_ECUDA, FVSRN_ENOMEM = range(5)
 ACT_CODES = {"relu": 0, "sigmoid": 1, "softplus": 2, "snake": 3, "snake_alt": 4}
@@ -102,6 +103,8 @@ EXPORTS = {
     "fvsrn_decode_density_device": (C.c_int32, [C.c_void_p, C.c_int32, C.c_double, C.c_int64,
                                                 C.c_int64, C.c_void_p, C.c_void_p]),
     "fvsrn_fused_eval": (C.c_int32, [C.c_void_p, _f, C.c_int64, _f]),
+    "fvsrn_host_alloc": (C.c_int32, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "fvsrn_host_free": (C.c_int32, [C.c_void_p]),
 }
 
 _LIB = None
@@ -150,6 +153,30 @@ def dptr(a: np.ndarray):
 
 def t_arg(t) -> float:
     return math.nan if t is None else float(t)
+
+
+class _PinnedOwner:
+    """Frees a fvsrn_host_alloc block when the last numpy view of it dies."""
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            lib().fvsrn_host_free(C.c_void_p(self.ptr))
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """numpy array in page-locked host memory (full-bandwidth device->host reads)."""
+    dtype = np.dtype(dtype)
+    nbytes = max(1, int(np.prod(shape)) * dtype.itemsize)
+    p = C.c_void_p()
+    check(lib().fvsrn_host_alloc(nbytes, C.byref(p)))
+    buf = (C.c_char * nbytes).from_address(p.value)
+    buf._owner = _PinnedOwner(p.value)     # lives exactly as long as the buffer object
+    return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype)[:int(np.prod(shape))].reshape(shape)
 
 
 def current_device() -> int:

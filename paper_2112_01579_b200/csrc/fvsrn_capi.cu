@@ -6,7 +6,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -184,7 +186,7 @@ struct FrameScratch {
   const __half* grid = nullptr;
   float* b0 = nullptr;
   TFDev* tf = nullptr;
-  unsigned long long* counters = nullptr;   // [0] queue, [1] evals
+  unsigned long long* counters = nullptr;   // [0] queue, [1] evals, [2] non-finite pixels
 };
 
 // Per-call device scratch: effective layer-0 bias (time folded), TF table,
@@ -233,7 +235,7 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
   fs.counters = (unsigned long long*)(base + off_ct);
   CUDA_TRY(cudaMemcpyAsync(fs.tf, &th, sizeof(TFDev), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(fs.b0, b0.data(), b0.size() * sizeof(float), cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemsetAsync(fs.counters, 0, 2 * sizeof(unsigned long long), s));
+  CUDA_TRY(cudaMemsetAsync(fs.counters, 0, 3 * sizeof(unsigned long long), s));
   fs.grid = m->f_pad > 0 ? m->grids[m->temporal ? lo : 0] : nullptr;
   if (grid_bytes) {
     __half* g = (__half*)(base + off_grid);
@@ -265,16 +267,32 @@ bool fast_path(const fvsrn_model* m, KernelKind kind) {
   if (m->act != FVSRN_ACT_SNAKE_ALT) return false;
   if (kind == KernelKind::kFused) return true;
   return m->fourier_mode == FVSRN_FOURIER_NERF && m->fd_in == 3 && m->raw_w == 3 &&
-         m->m == (m->hid_pad - 4) / 2 && m->f_pad == 16 && m->R > 0;
+         m->m == (m->hid_pad - 4) / 2 && m->f_pad == 16 && m->R > 0 &&
+         m->layers == fast_layer_count(m->hid_pad);
 }
+
+// (kernel, device, smem) -> resident CTAs per SM; the attribute + occupancy queries run
+// once per configuration instead of on every launch.
+std::mutex g_occ_mu;
+std::map<std::tuple<const void*, int, size_t>, int> g_occ;
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
   const void* fn = kernel_for(kind, m->hid_pad, fast_path(m, kind));
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
-  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+  {
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto key = std::make_tuple(fn, m->device, smem);
+    auto it = g_occ.find(key);
+    if (it == g_occ.end()) {
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+      g_occ[key] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   long long blocks = (long long)m->num_sms * occ;
   const long long need = (work_warps + (kThreads / 32) - 1) / (kThreads / 32);
@@ -556,9 +574,23 @@ int32_t fvsrn_model_info(fvsrn_model_t m, int32_t* k0_pad, int32_t* hidden_pad, 
   return FVSRN_OK;
 }
 
+static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
+                       const fvsrn_settings* st, double t, const fvsrn_shard* shard, float* d_out,
+                       unsigned long long* d_eval_count, unsigned long long* d_nonfinite,
+                       cudaStream_t stream);
+
 int32_t fvsrn_render_device(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
                             const fvsrn_settings* st, double t, const fvsrn_shard* shard,
                             float* d_out, unsigned long long* d_eval_count, void* stream) {
+  return render_impl(m, tf, c, st, t, shard, d_out, d_eval_count, nullptr, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
+                       const fvsrn_settings* st, double t, const fvsrn_shard* shard, float* d_out,
+                       unsigned long long* d_eval_count, unsigned long long* d_nonfinite,
+                       cudaStream_t stream) {
   if (!m || !c || !d_out) return fail(FVSRN_EINVAL, "null argument");
   int rc = check_settings(st);
   if (rc) return rc;
@@ -597,12 +629,15 @@ int32_t fvsrn_render_device(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_cam
   const double* rd = nullptr;
   unsigned long long* queue = fs.counters;
   unsigned long long* evc = d_eval_count ? d_eval_count : fs.counters + 1;
-  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc};
+  unsigned long long* nfc = d_nonfinite ? d_nonfinite : fs.counters + 2;
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc, &nfc};
   const size_t smem = stage_smem_bytes(net, true, m->k0);
   if ((rc = launch(m, KernelKind::kDVR, smem, args, s, n_slots / 32 + 1))) return rc;
   CUDA_TRY(cudaFreeAsync(fs.buf, s));
   return FVSRN_OK;
 }
+
+extern "C" {
 
 int32_t fvsrn_tiles_to_frame_device(const float* d_gathered, int32_t width, int32_t height,
                                     int32_t world, float* d_frame, void* stream) {
@@ -615,9 +650,10 @@ int32_t fvsrn_tiles_to_frame_device(const float* d_gathered, int32_t width, int3
 
 namespace {
 
+// Host-pointer entry points run on the calling thread's per-thread default stream
+// (reentrant across host threads, no per-call stream creation).
 struct StreamGuard {
-  cudaStream_t s = nullptr;
-  ~StreamGuard() { if (s) cudaStreamDestroy(s); }
+  cudaStream_t s = cudaStreamPerThread;
 };
 
 }  // namespace
@@ -630,21 +666,21 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
   const size_t bytes = (size_t)c->width * c->height * 16;
   float* d_out = nullptr;
   unsigned long long* d_cnt = nullptr;
   CUDA_TRY(cudaMallocAsync(&d_out, bytes + 16, sg.s));
   d_cnt = (unsigned long long*)((char*)d_out + bytes);
-  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 8, sg.s));
-  int rc = fvsrn_render_device(m, tf, c, st, t, nullptr, d_out, d_cnt, sg.s);
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 16, sg.s));
+  int rc = render_impl(m, tf, c, st, t, nullptr, d_out, d_cnt, d_cnt + 1, sg.s);
   if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
-  unsigned long long cnt = 0;
+  unsigned long long cnt[2] = {0, 0};
   CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
-  CUDA_TRY(cudaMemcpyAsync(&cnt, d_cnt, 8, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaFreeAsync(d_out, sg.s));
   CUDA_TRY(cudaStreamSynchronize(sg.s));
-  if (eval_count) *eval_count = cnt;
+  if (eval_count) *eval_count = cnt[0];
+  if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
   return FVSRN_OK;
 }
 
@@ -659,7 +695,6 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   if (n == 0) return FVSRN_OK;
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
   const size_t rb = (size_t)n * 3 * sizeof(double), ob = (size_t)n * 16;
   char* buf = nullptr;
   CUDA_TRY(cudaMallocAsync((void**)&buf, 2 * rb + ob, sg.s));
@@ -683,7 +718,8 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   long long n_slots = n;
   unsigned long long* queue = fs.counters;
   unsigned long long* evc = fs.counters + 1;
-  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc};
+  unsigned long long* nfc = nullptr;
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc, &nfc};
   const size_t smem = stage_smem_bytes(net, true, m->k0);
   if ((rc = launch(m, KernelKind::kDVR, smem, args, sg.s, n_slots / 32 + 1))) return rc;
   unsigned long long cnt = 0;
@@ -708,7 +744,6 @@ static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64
   if (n == 0) return FVSRN_OK;
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
   const int oc = want_head == FVSRN_HEAD_DENSITY ? 1 : 4;
   const size_t pb = (size_t)n * 3 * sizeof(double), ob = (size_t)n * oc * sizeof(float);
   char* buf = nullptr;
@@ -780,7 +815,6 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
   if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
   const long long count = (long long)res * res * res;
   float* d_out = nullptr;
   CUDA_TRY(cudaMallocAsync(&d_out, count * sizeof(float), sg.s));
@@ -792,12 +826,23 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
   return FVSRN_OK;
 }
 
+int32_t fvsrn_host_alloc(uint64_t bytes, void** ptr) {
+  if (!ptr) return fail(FVSRN_EINVAL, "null argument");
+  *ptr = nullptr;
+  CUDA_TRY(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_host_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_fused_eval(fvsrn_model_t m, const float* x, int64_t n, float* out) {
   if (!m || (n > 0 && (!x || !out))) return fail(FVSRN_EINVAL, "null argument");
   if (n == 0) return FVSRN_OK;
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
   const int oc = m->head == FVSRN_HEAD_DENSITY ? 1 : 4;
   const size_t xb = (size_t)n * m->d_in * sizeof(float), ob = (size_t)n * oc * sizeof(float);
   char* buf = nullptr;

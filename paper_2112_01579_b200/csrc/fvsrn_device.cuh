@@ -135,7 +135,9 @@ __device__ __forceinline__ float act_h(float x) {
 // Evaluates the whole network for the 32 rows staged in `stage` (row stride `rs`
 // halfs) and writes head inputs (pre-head raw outputs, up to 4 per row) to
 // `outbuf[row*4 + c]`.  MT = number of m16 tiles held at once (2 -> all 32 rows).
-template <int HID, int MT, int ACT>
+// NL / KT0 > 0: compile-time layer count / layer-0 k16 tiles (whole MLP is one basic
+// block, so ptxas can overlap one layer's activations with the next layer's MMAs).
+template <int HID, int MT, int ACT, int NL = 0, int KT0 = 0>
 struct WarpMLP {
   static constexpr int NT = HID / 8;
   static constexpr int KT = HID / 16;
@@ -183,10 +185,12 @@ struct WarpMLP {
     const int arow = lane & 15, acol = (lane >> 4) * 8;
     float out_acc[MT][4];
     const __half* arow_ptr = stage + (m_base * 16 + arow) * rs + acol;
+    const int layers = NL > 0 ? NL : net.layers;
+    const int kt0 = KT0 > 0 ? KT0 : net.kt0;
 
-    if (net.layers == 1) {
+    if (layers == 1) {
       const float4 bq = bias_quad(bs + net.b_off[0], 0, q);
-      for (int kt = 0; kt < net.kt0; ++kt) {
+      for (int kt = 0; kt < kt0; ++kt) {
         uint2 b = wf[net.w_off[0] + kt * 32 + lane];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
@@ -214,7 +218,8 @@ struct WarpMLP {
           for (int mt = 0; mt < MT; ++mt) mma16816c(acc[mt][nt], a[mt], b, bq);
         }
       }
-      for (int kt = 1; kt < net.kt0; ++kt) {
+#pragma unroll
+      for (int kt = 1; kt < kt0; ++kt) {
         uint32_t a[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) ldmatrix_x4(a[mt], arow_ptr + mt * 16 * rs + kt * 16);
@@ -228,7 +233,8 @@ struct WarpMLP {
       }
       act_pack(net.act, acc, h);
       // ---- hidden layers
-      for (int l = 1; l < net.layers - 1; ++l) {
+#pragma unroll
+      for (int l = 1; l < layers - 1; ++l) {
         const float* bl = bs + net.b_off[l];
         const uint2* wl = wf + net.w_off[l] + lane;
 #pragma unroll
@@ -248,7 +254,7 @@ struct WarpMLP {
         act_pack(net.act, acc, h);
       }
       // ---- last layer: N = 8 (one n tile), linear
-      const int L = net.layers - 1;
+      const int L = layers - 1;
       const float4 bq = bias_quad(bs + net.b_off[L], 0, q);
       const uint2* wl = wf + net.w_off[L] + lane;
 #pragma unroll
@@ -272,13 +278,14 @@ struct WarpMLP {
   }
 };
 
-template <int HID, int ACT>
+template <int HID, int ACT, int NL = 0, int KT0 = 0>
 struct MLPDispatch {
   static constexpr int MT = HID <= 64 ? 2 : 1;
   __device__ static void eval32(const __half* stage, int rs, const NetDev& net, const uint2* wf,
                                 const float* bs, float* outbuf, int lane) {
 #pragma unroll
-    for (int mb = 0; mb < 2; mb += MT) WarpMLP<HID, MT, ACT>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
+    for (int mb = 0; mb < 2; mb += MT)
+      WarpMLP<HID, MT, ACT, NL, KT0>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
   }
 };
 

@@ -53,6 +53,13 @@ __device__ __forceinline__ void stage_setup(const NetDev& net, const float* b0, 
   __syncthreads();
 }
 
+// layer-0 k16 tiles of the specialised row (0: runtime)
+template <int NM>
+__host__ __device__ constexpr int fast_kt0() {
+  if constexpr (NM > 0) return FastRow<NM>::kK0 / 16;
+  else return 0;
+}
+
 // ---------------------------------------------------------------- ray setup (f64)
 // Bit-exact restatement of camera_rays (render.py:72-94), ray_box_intersect
 // (render.py:97-106) and _march_geometry (render.py:189-200): every f64 op is an
@@ -112,12 +119,14 @@ __device__ __forceinline__ int slot_pixel(const CamDev& cam, const ShardDev& sh,
 }
 
 // ---------------------------------------------------------------- DVR
-template <int HID, int ACT, int NM>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
+// NM > 0 / NL > 0: specialised input row (FastRow<NM>) and compile-time layer count
+template <int HID, int ACT, int NM, int NL>
+__global__ void __launch_bounds__(kThreads, min_blocks<HID>())
 dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
            MarchDev md, CamDev cam, ShardDev sh, const double* __restrict__ rays_o,
            const double* __restrict__ rays_d, long long n_slots, float* __restrict__ out,
-           unsigned long long* __restrict__ queue, unsigned long long* __restrict__ eval_count) {
+           unsigned long long* __restrict__ queue, unsigned long long* __restrict__ eval_count,
+           unsigned long long* __restrict__ nonfinite) {
   const int rs = fd.k0 + 8;
   uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
   stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
@@ -213,7 +222,7 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
                          use_dir ? dz : 0.f, myrow);
     }
     __syncwarp();
-    MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
 
     // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
@@ -233,8 +242,12 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
       ++k;
       if (k >= n || A > et) {
         const float om = 1.f - A;
-        *reinterpret_cast<float4*>(out + 4 * oslot) =
-            make_float4(fmaf(om, md.bg[0], C0), fmaf(om, md.bg[1], C1), fmaf(om, md.bg[2], C2), A);
+        const float4 px4 = make_float4(fmaf(om, md.bg[0], C0), fmaf(om, md.bg[1], C1),
+                                       fmaf(om, md.bg[2], C2), A);
+        *reinterpret_cast<float4*>(out + 4 * oslot) = px4;
+        // Image invariant (imaging.py:52-57) checked on the device: no host scan
+        if (nonfinite && !(isfinite(px4.x) && isfinite(px4.y) && isfinite(px4.z) && isfinite(px4.w)))
+          atomicAdd(nonfinite, 1ull);
         has = false;
       }
     }
@@ -244,8 +257,8 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
 
 // ---------------------------------------------------------------- decode / eval
 // mode 0: lattice decode (model.py:385-398); mode 1: positions (+dirs) from memory
-template <int HID, int ACT, int NM>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
+template <int HID, int ACT, int NM, int NL>
+__global__ void __launch_bounds__(kThreads, min_blocks<HID, false>())
 sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, int res, double step,
               long long begin, long long count, const double* __restrict__ pos,
               const double* __restrict__ dirs, float* __restrict__ out) {
@@ -277,7 +290,7 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
       assemble_row_t<NM>(fd, px, py, pz, dx, dy, dz, myrow);
     }
     __syncwarp();
-    MLPDispatch<HID, ACT>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
     if (valid) {
       const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
@@ -294,7 +307,7 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
 
 // head(mlp(x)) with x already assembled in the reference column order.
 template <int HID, int ACT>
-__global__ void __launch_bounds__(kThreads, HID <= 64 ? kMinBlocks : 1)
+__global__ void __launch_bounds__(kThreads, min_blocks<HID, false>())
 fused_eval_kernel(NetDev net, int d_in, int k0, const float* __restrict__ x, long long count,
                   float* __restrict__ out) {
   const int rs = k0 + 8;
@@ -350,23 +363,29 @@ __global__ void tiles_to_frame_kernel(const float4* __restrict__ gathered, int W
 // ---------------------------------------------------------------- launch table
 #define FVSRN_FOR_HIDDEN(X) X(16) X(32) X(48) X(64) X(96) X(128)
 
-// fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode); else generic
+// Default-config layer counts baked into the fast variants (fV-SRN 4x32 and 6x64).
+constexpr int fast_layers(int hid) { return hid == 64 ? 6 : 4; }
+
+// fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode, layers =
+// fast_layers(HID)); else generic (runtime layer count and input layout)
 const void* kernel_for(KernelKind kind, int hid, bool fast) {
   switch (hid) {
 #define CASE(H)                                                                              \
   case H:                                                                                    \
     if (kind == KernelKind::kDVR)                                                            \
-      return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2>                               \
-                  : (const void*)dvr_kernel<H, kActRuntime, 0>;                              \
+      return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H)>               \
+                  : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
     if (kind == KernelKind::kSample)                                                         \
-      return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2>                            \
-                  : (const void*)sample_kernel<H, kActRuntime, 0>;                           \
+      return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
+                  : (const void*)sample_kernel<H, kActRuntime, 0, 0>;                        \
     return fast ? (const void*)fused_eval_kernel<H, 4> : (const void*)fused_eval_kernel<H, kActRuntime>;
     FVSRN_FOR_HIDDEN(CASE)
 #undef CASE
     default: return nullptr;
   }
 }
+
+int fast_layer_count(int hid) { return fast_layers(hid); }
 
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s) {

@@ -9,7 +9,23 @@
 namespace fvsrn {
 
 constexpr int kThreads = 128;  // 4 independent warps per CTA; weights shared in smem
-constexpr int kMinBlocks = 4;  // -> <= 128 registers/thread, 16 warps/SM
+// CTAs per SM the register budget is sized for (A/B-measured on B200):
+// DVR 5 (<= 102 regs, 20 warps/SM), decode/eval 4 (<= 128 regs).
+#ifndef FVSRN_MIN_BLOCKS
+#define FVSRN_MIN_BLOCKS 5
+#endif
+#ifndef FVSRN_MIN_BLOCKS_SAMPLE
+#define FVSRN_MIN_BLOCKS_SAMPLE 4
+#endif
+constexpr int kMinBlocks = FVSRN_MIN_BLOCKS;
+#ifndef FVSRN_MIN_BLOCKS_WIDE
+#define FVSRN_MIN_BLOCKS_WIDE 3
+#endif
+// 48/64-wide networks need more accumulator registers: fewer CTAs per SM
+template <int HID, bool DVR = true>
+constexpr int min_blocks() {
+  return HID <= 32 ? (DVR ? kMinBlocks : FVSRN_MIN_BLOCKS_SAMPLE) : (HID <= 64 ? FVSRN_MIN_BLOCKS_WIDE : 1);
+}
 
 struct CamDev {
   double eye[3], fwd[3], right[3], up[3];
@@ -27,6 +43,7 @@ enum class KernelKind { kDVR, kSample, kFused };
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).
 const void* kernel_for(KernelKind kind, int hid_pad, bool fast);
+int fast_layer_count(int hid_pad);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,

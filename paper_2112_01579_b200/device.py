@@ -179,8 +179,12 @@ class DeviceModel:
                                            len(p), L.t_arg(t), L.fptr(out)))
         return out
 
-    def decode(self, res: int, t=None) -> np.ndarray:
-        out = np.empty(int(res) ** 3, dtype=np.float32)
+    def decode(self, res: int, t=None, out=None) -> np.ndarray:
+        n = int(res) ** 3
+        if out is None:
+            out = np.empty(n, dtype=np.float32)
+        elif out.size != n or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous float32 array of {n} elements")
         L.check(self._lib.fvsrn_decode_density(self._h, int(res), L.t_arg(t), L.fptr(out)))
         return out
 
@@ -193,9 +197,16 @@ class DeviceModel:
         L.check(self._lib.fvsrn_fused_eval(self._h, L.fptr(x), len(x), L.fptr(out)))
         return out[:, 0] if oc == 1 else out
 
-    def render(self, tf, cam, settings, t=None):
-        """(H,W,4) f32 frame + evaluated-sample count (host buffer, synchronous)."""
-        out = np.empty((cam.height, cam.width, 4), dtype=np.float32)
+    def render(self, tf, cam, settings, t=None, out=None):
+        """(H,W,4) f32 frame + evaluated-sample count (host buffer, synchronous).
+
+        ``out``: optional C-contiguous float32 (H,W,4) host array to render into
+        (e.g. ``pinned_empty`` for full-bandwidth reads)."""
+        shape = (cam.height, cam.width, 4)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
         cnt = C.c_uint64(0)
         tfd = tf_desc(tf)
         L.check(self._lib.fvsrn_render(self._h, C.byref(tfd.desc) if tfd else None,

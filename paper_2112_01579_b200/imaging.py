@@ -52,6 +52,14 @@ class Image:
             raise ValueError("image contains non-finite values")
         object.__setattr__(self, "data", d)
 
+    @classmethod
+    def _from_device(cls, data: np.ndarray) -> "Image":
+        """Wrap a renderer framebuffer without the host-side scan: fvsrn_render
+        already enforced the finiteness invariant on the device."""
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "data", data)
+        return obj
+
     @property
     def width(self) -> int:
         return int(self.data.shape[1])

@@ -175,17 +175,19 @@ def eval_color(model: FvsrnModel, p, d=None, t=None) -> np.ndarray:
     return _device(model).eval_color(p, d, t)
 
 
-def decode_volume(model: FvsrnModel, resolution: int, t: float | None = None, chunk: int = 1 << 16):
+def decode_volume(model: FvsrnModel, resolution: int, t: float | None = None, chunk: int = 1 << 16,
+                  out: np.ndarray | None = None):
     """Dense density on the linspace(0,1,res)^3 vertex lattice (model.py:385-398).
 
     ``chunk`` is accepted for signature compatibility; the GPU decodes the
-    whole lattice in one launch.
+    whole lattice in one launch.  ``out`` (optional): float32 host buffer of
+    res^3 values (e.g. ``pinned_empty``) to decode into.
     """
     from .volume import ScalarVolume
 
     if model.config.head != "density":
         raise ValueError("decode_volume requires a density-head model")
-    vals = _device(model).decode(resolution, t)
+    vals = _device(model).decode(resolution, t, out=None if out is None else out.reshape(-1))
     return ScalarVolume(values=vals.reshape((resolution,) * 3))
 
 

@@ -141,18 +141,22 @@ def render_rays(source, origins, dirs, settings: RenderSettings) -> np.ndarray:
     return raymarch_forward(source, origins, dirs, settings)[0]
 
 
-def render_image(source, camera: Camera, settings: RenderSettings | None = None) -> Image:
+def render_image(source, camera: Camera, settings: RenderSettings | None = None,
+                 out: np.ndarray | None = None) -> Image:
     """Full frame through the fused DVR kernel (render.py:314-332).
 
     ``settings.threads`` is ignored (the GPU parallelises over rays); the output
     is deterministic and bit-identical across repeats.  The number of network
-    evaluations is recorded in ``source.last_eval_count``.
+    evaluations is recorded in ``source.last_eval_count``.  ``out`` (optional,
+    new): a float32 (H,W,4) host buffer to render into -- with
+    ``pinned_empty`` an interactive viewer reuses one page-locked framebuffer and
+    the device->host read runs at full bandwidth; the returned Image views it.
     """
     src = _require_model_source(source)
     settings = settings or RenderSettings()
-    data, cnt = src.device_model.render(src.tf, camera, settings, src.t)
+    data, cnt = src.device_model.render(src.tf, camera, settings, src.t, out=out)
     src.last_eval_count = cnt
-    return Image(data=data)
+    return Image._from_device(data)
 
 
 def fibonacci_cameras(n: int, width: int, height: int, radius: float = 2.2,
