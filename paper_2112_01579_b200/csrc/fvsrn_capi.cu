@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -21,6 +22,11 @@ using namespace fvsrn;
 namespace {
 
 thread_local std::string g_err;
+// LPT tile ordering on/off (FVSRN_LPT=0 disables; A/B measurements)
+const bool g_lpt_enabled = [] {
+  const char* e = std::getenv("FVSRN_LPT");
+  return !(e && e[0] == '0');
+}();
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -56,17 +62,27 @@ void build_pack(const std::vector<std::vector<float>>& wdev, const std::vector<i
     pk.b_off[l] = (int)pk.bias.size();
     const int KT = K[l] / 16, NT = N[l] / 8;
     const auto& W = wdev[l];
-    for (int kt = 0; kt < KT; ++kt)
-      for (int nt = 0; nt < NT; ++nt)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int g = lane >> 2, q = lane & 3;
-          const int n = nt * 8 + g, k0 = kt * 16 + 2 * q;
-          auto h = [&](int k) { return __half_as_ushort(__float2half_rn(W[(size_t)n * K[l] + k])); };
-          uint2 u;
-          u.x = (uint32_t)h(k0) | ((uint32_t)h(k0 + 1) << 16);
-          u.y = (uint32_t)h(k0 + 8) | ((uint32_t)h(k0 + 9) << 16);
-          pk.frag.push_back(u);
-        }
+    auto frag = [&](int kt, int nt, int lane) {
+      const int g = lane >> 2, q = lane & 3;
+      const int n = nt * 8 + g, k0 = kt * 16 + 2 * q;
+      auto h = [&](int k) { return __half_as_ushort(__float2half_rn(W[(size_t)n * K[l] + k])); };
+      uint2 u;
+      u.x = (uint32_t)h(k0) | ((uint32_t)h(k0 + 1) << 16);
+      u.y = (uint32_t)h(k0 + 8) | ((uint32_t)h(k0 + 9) << 16);
+      return u;
+    };
+    if (FVSRN_BPAIRS && NT >= 2) {  // hidden-width layer: [kt][n-tile pair][lane] -> LDS.128
+      for (int kt = 0; kt < KT; ++kt)
+        for (int p = 0; p < NT / 2; ++p)
+          for (int lane = 0; lane < 32; ++lane) {
+            pk.frag.push_back(frag(kt, 2 * p, lane));
+            pk.frag.push_back(frag(kt, 2 * p + 1, lane));
+          }
+    } else {        // [kt][nt][lane] x uint2 (always for the one-tile output layer)
+      for (int kt = 0; kt < KT; ++kt)
+        for (int nt = 0; nt < NT; ++nt)
+          for (int lane = 0; lane < 32; ++lane) pk.frag.push_back(frag(kt, nt, lane));
+    }
     // accumulator quads: (nt, q) -> {b[nt*8+2q], b[nt*8+2q+1], same, same}
     for (int nt = 0; nt < NT; ++nt)
       for (int q = 0; q < 4; ++q)
@@ -623,6 +639,18 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
   NetDev net = m->ps.net;
   FeatDev fd = feat_for(m, fs.grid);
   MarchDev md = march_for(st);
+  // LPT schedule: longest tiles first (removes the persistent kernel's long-ray tail)
+  void* lpt = nullptr;
+  if (local_tiles >= 2 * m->num_sms && g_lpt_enabled) {
+    const int nl = (int)local_tiles;
+    const size_t sb = tile_order_scratch_bytes(nl);
+    CUDA_TRY(cudaMallocAsync(&lpt, 16 * (size_t)nl + sb + 256, s));
+    unsigned* cost = (unsigned*)lpt;
+    unsigned* order = cost + 2 * (size_t)nl;
+    void* scratch = (char*)lpt + 16 * (size_t)nl;
+    CUDA_TRY(launch_tile_order(cam, md, sh, nl, cost, order, scratch, sb, s));
+    sh.order = order;
+  }
   const TFDev* tfp = fs.tf;
   const float* b0 = fs.b0;
   const double* ro = nullptr;
@@ -634,6 +662,7 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
   const size_t smem = stage_smem_bytes(net, true, m->k0);
   if ((rc = launch(m, KernelKind::kDVR, smem, args, s, n_slots / 32 + 1))) return rc;
   CUDA_TRY(cudaFreeAsync(fs.buf, s));
+  if (lpt) CUDA_TRY(cudaFreeAsync(lpt, s));
   return FVSRN_OK;
 }
 

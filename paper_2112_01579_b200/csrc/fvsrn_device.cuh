@@ -116,6 +116,42 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // host (exact in fp16).  Cost per element: FMUL.RZ + MUFU.COS + FFMA.
 constexpr int kActRuntime = -1;
 
+// B-fragment storage: 1 = pairs of n8 tiles per LDS.128, 0 = one LDS.64 per tile
+#ifndef FVSRN_BPAIRS
+#define FVSRN_BPAIRS 0
+#endif
+// two-point TF coefficients held in registers in the DVR kernel
+#ifndef FVSRN_TF_REGS
+#define FVSRN_TF_REGS 0
+#endif
+
+// Every FVSRN_POLY_EVERY-th snake activation evaluates cos on the FMA pipe instead of
+// MUFU (balances the XU/MIO and FMA pipes; 0 = all MUFU).  cos(a) = cos(2 pi r) with
+// r = a/(2 pi) - rint(.) in [-1/2, 1/2]: degree-4 minimax in r^2, |err| < 4.3e-5.
+#ifndef FVSRN_POLY_EVERY
+#define FVSRN_POLY_EVERY 0
+#endif
+__device__ __forceinline__ float cos_poly(float a) {
+  const float t = a * 0.15915494309189535f;
+  const float k = (t + 12582912.f) - 12582912.f;     // round to nearest (|t| < 2^22)
+  const float r = t - k;
+  const float u = r * r;
+  float p = fmaf(45.62269592285156f, u, -82.3971176147461f);
+  p = fmaf(p, u, 64.67363739013672f);
+  p = fmaf(p, u, -19.731164932250977f);
+  return fmaf(p, u, 0.9999644756317139f);
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_h(float x);
+
+template <int ACT, bool POLY>
+__device__ __forceinline__ float act_h2(float x) {
+  if constexpr (POLY && ACT == 4) return fmaf(-2.f, cos_poly(x), x);
+  else if constexpr (POLY && ACT == 3) return x - cos_poly(x);
+  else return act_h<ACT>(x);
+}
+
 template <int ACT>
 __device__ __forceinline__ float act_h(float x) {
   if constexpr (ACT == 0) {
@@ -150,10 +186,15 @@ struct WarpMLP {
       for (int kt = 0; kt < KT; ++kt) {
         const float* a0 = acc[mt][2 * kt];
         const float* a1 = acc[mt][2 * kt + 1];
-        h[mt][kt][0] = pack_half2(act_h<A>(a0[0]), act_h<A>(a0[1]));
-        h[mt][kt][1] = pack_half2(act_h<A>(a0[2]), act_h<A>(a0[3]));
-        h[mt][kt][2] = pack_half2(act_h<A>(a1[0]), act_h<A>(a1[1]));
-        h[mt][kt][3] = pack_half2(act_h<A>(a1[2]), act_h<A>(a1[3]));
+        constexpr int P = FVSRN_POLY_EVERY;
+        const int e = (mt * KT + kt) * 8;   // element index within this thread's tile set
+#define FVSRN_ACT(i, x) (P > 0 && ((e + (i)) % (P > 0 ? P : 1)) == (P > 0 ? P - 1 : 0) \
+                             ? act_h2<A, true>(x) : act_h2<A, false>(x))
+        h[mt][kt][0] = pack_half2(FVSRN_ACT(0, a0[0]), FVSRN_ACT(1, a0[1]));
+        h[mt][kt][1] = pack_half2(FVSRN_ACT(2, a0[2]), FVSRN_ACT(3, a0[3]));
+        h[mt][kt][2] = pack_half2(FVSRN_ACT(4, a1[0]), FVSRN_ACT(5, a1[1]));
+        h[mt][kt][3] = pack_half2(FVSRN_ACT(6, a1[2]), FVSRN_ACT(7, a1[3]));
+#undef FVSRN_ACT
       }
   }
 
@@ -169,6 +210,18 @@ struct WarpMLP {
         default: act_pack_t<4>(acc, h); break;
       }
     }
+  }
+
+  // B fragments of a hidden-width layer, stored in pairs: one LDS.128 per lane holds the
+  // fragments of n8 tiles (2p, 2p+1) of k16 tile kt -> [kt][p][lane] x uint4.
+  // (The compiler merges the two uint2 halves of one uint4 into a single load.)
+  __device__ static uint2 bfrag(const uint2* wl, int kt, int nt, int lane) {
+#if FVSRN_BPAIRS
+    const uint4 v = *reinterpret_cast<const uint4*>(wl + ((kt * (NT / 2) + (nt >> 1)) * 32 + lane) * 2);
+    return (nt & 1) ? make_uint2(v.z, v.w) : make_uint2(v.x, v.y);
+#else
+    return wl[(kt * NT + nt) * 32 + lane];
+#endif
   }
 
   // Biases are stored as accumulator quads: for (n-tile nt, quad lane q) the float4
@@ -209,10 +262,9 @@ struct WarpMLP {
         uint32_t a[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) ldmatrix_x4(a[mt], arow_ptr + mt * 16 * rs);
-        const uint2* wl = wf + net.w_off[0] + lane;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const uint2 b = wl[nt * 32];
+          const uint2 b = bfrag(wf + net.w_off[0], 0, nt, lane);
           const float4 bq = bias_quad(b0, nt, q);
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) mma16816c(acc[mt][nt], a[mt], b, bq);
@@ -223,10 +275,9 @@ struct WarpMLP {
         uint32_t a[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) ldmatrix_x4(a[mt], arow_ptr + mt * 16 * rs + kt * 16);
-        const uint2* wl = wf + net.w_off[0] + kt * NT * 32 + lane;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          uint2 b = wl[nt * 32];
+          const uint2 b = bfrag(wf + net.w_off[0], kt, nt, lane);
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) mma16816(acc[mt][nt], a[mt], b);
         }
@@ -236,12 +287,11 @@ struct WarpMLP {
 #pragma unroll
       for (int l = 1; l < layers - 1; ++l) {
         const float* bl = bs + net.b_off[l];
-        const uint2* wl = wf + net.w_off[l] + lane;
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            uint2 b = wl[(kt * NT + nt) * 32];
+            const uint2 b = bfrag(wf + net.w_off[l], kt, nt, lane);
             if (kt == 0) {
               const float4 bq = bias_quad(bl, nt, q);
 #pragma unroll

@@ -11,6 +11,8 @@
 //   fused_eval_kernel head(mlp(x)) from assembled inputs              fused.py:281-301
 //   blend_grid_kernel per-frame keyframe pre-blend (trilinear is linear) model.py:219-233
 //   tiles_to_frame    reassembles gathered screen-tile shards (multi-GPU)
+#include <cub/cub.cuh>
+
 #include "fvsrn_kernels.cuh"
 
 namespace fvsrn {
@@ -136,6 +138,14 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   const float eps1 = (float)(1.0 - md.eps_blend);
   const float et = (float)md.et_alpha;
   __half* myrow = stage + lane * rs;
+  // two-point TFs (the presets' grayscale) live in registers: no per-sample smem lookups
+  const bool tf_two = FVSRN_TF_REGS && density && tf->n == 2;
+  float tf0[4], tfk[4], tfx0 = 0.f;
+  if (tf_two) {
+    tfx0 = tf->xs[0];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { tf0[c] = tf->val[0][c]; tfk[c] = tf->slope[0][c]; }
+  }
 
   bool has = false;
   int k = 0, n = 0;
@@ -167,7 +177,9 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
       const int rank = __popc(need & lanemask_lt());
       const int take = min(__popc(need), chunk_left);
       if (!has && rank < take) {
-        const long long s = chunk_base + rank;
+        const long long qs = chunk_base + rank;
+        // queue position -> canonical slot (LPT order permutes whole tiles)
+        const long long s = (!rays_o && sh.order) ? ((long long)sh.order[qs >> 6] << 6) | (qs & 63) : qs;
         RayGeom r;
         bool valid = true;
         long long dst;
@@ -229,7 +241,11 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
     if (has) {
       const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
       float r, g, b, sig;
-      if (density) {
+      if (tf_two) {
+        const float dx = fminf(fmaxf(sigmoidf_(o.x), 0.f), 1.f) - tfx0;
+        r = fmaf(tfk[0], dx, tf0[0]); g = fmaf(tfk[1], dx, tf0[1]);
+        b = fmaf(tfk[2], dx, tf0[2]); sig = fmaf(tfk[3], dx, tf0[3]);
+      } else if (density) {
         tf_eval(*tf, sigmoidf_(o.x), r, g, b, sig);
       } else {
         r = sigmoidf_(o.x); g = sigmoidf_(o.y); b = sigmoidf_(o.z); sig = softplusf_(o.w);
@@ -253,6 +269,51 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
     }
   }
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+}
+
+// ---------------------------------------------------------------- LPT schedule
+__global__ void tile_cost_kernel(CamDev cam, MarchDev md, ShardDev sh, long long n_slots,
+                                 unsigned* __restrict__ cost, unsigned* __restrict__ iota) {
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
+       s += (long long)gridDim.x * blockDim.x) {
+    unsigned n = 0;
+    const int pix = slot_pixel(cam, sh, s);
+    if (pix >= 0) {
+      RayGeom r;
+      camera_dir(cam, pix % cam.W, pix / cam.W, r.d);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) r.o[a] = cam.eye[a];
+      if (march_geometry(md, r)) n = (unsigned)r.n + 4;   // + refill/setup overhead
+    }
+    // a warp covers 32 consecutive slots of one 64-slot tile
+    unsigned sum = __reduce_add_sync(0xffffffffu, n);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(cost + (s >> 6), sum);
+      if ((s & 63) == 0) iota[s >> 6] = (unsigned)(s >> 6);
+    }
+  }
+}
+
+size_t tile_order_scratch_bytes(int n_local) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const unsigned*)nullptr,
+                                            (unsigned*)nullptr, (const unsigned*)nullptr,
+                                            (unsigned*)nullptr, n_local);
+  return bytes;
+}
+
+cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
+                              int n_local, unsigned* cost, unsigned* order, void* scratch,
+                              size_t scratch_bytes, cudaStream_t s) {
+  // cost[0:n] keys, cost[n:2n] sorted keys, order[0:n] values, order[n:2n] iota
+  cudaError_t e = cudaMemsetAsync(cost, 0, sizeof(unsigned) * n_local, s);
+  if (e != cudaSuccess) return e;
+  const long long n_slots = (long long)n_local * 64;
+  const int blocks = (int)std::min<long long>((n_slots + 255) / 256, 148 * 16);
+  tile_cost_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, n_slots, cost, order + n_local);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairsDescending(scratch, scratch_bytes, cost, cost + n_local,
+                                                   order + n_local, order, n_local, 0, 32, s);
 }
 
 // ---------------------------------------------------------------- decode / eval

@@ -36,6 +36,7 @@ struct CamDev {
 struct ShardDev {
   int rank, world, compact;
   int tiles_x, n_tiles;
+  const unsigned* order;   // work-queue order of local tiles (longest first), or nullptr
 };
 
 enum class KernelKind { kDVR, kSample, kFused };
@@ -44,6 +45,12 @@ enum class KernelKind { kDVR, kSample, kFused };
 // fast: specialised default-input / snake_alt variant (see FastRow).
 const void* kernel_for(KernelKind kind, int hid_pad, bool fast);
 int fast_layer_count(int hid_pad);
+// LPT schedule: exact per-tile step counts (same f64 geometry as the renderer), then
+// local tiles sorted by descending cost.  `order` receives n_local tile indices.
+cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
+                              int n_local, unsigned* cost, unsigned* order, void* scratch,
+                              size_t scratch_bytes, cudaStream_t s);
+size_t tile_order_scratch_bytes(int n_local);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,
