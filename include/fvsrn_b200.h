@@ -145,6 +145,25 @@ FVSRN_API int32_t fvsrn_host_alloc(uint64_t bytes, void** ptr);
 FVSRN_API int32_t fvsrn_host_free(void* ptr);
 FVSRN_API int32_t fvsrn_fused_eval(fvsrn_model_t model, const float* x, int64_t n, float* out);
 
+/* Ground-truth DVR of a dense scalar volume: VolumeSource(volume, tf)
+ * (render.py:132-141, volume.py:213-255) -- same ray setup, TF, compositing and ET as
+ * fvsrn_render, the network replaced by the reference's trilinear volume lookup.
+ * values: (nx, ny, nz) f32 in [0,1], C order (ScalarVolume.values). */
+typedef struct fvsrn_volume* fvsrn_volume_t;
+FVSRN_API int32_t fvsrn_volume_create(const float* values, int32_t nx, int32_t ny, int32_t nz,
+                                      int32_t device, fvsrn_volume_t* out);
+FVSRN_API int32_t fvsrn_volume_destroy(fvsrn_volume_t volume);
+FVSRN_API int32_t fvsrn_volume_render(fvsrn_volume_t volume, const fvsrn_tf* tf,
+                                      const fvsrn_camera* cam, const fvsrn_settings* settings,
+                                      float* out_rgba, uint64_t* sample_count);
+FVSRN_API int32_t fvsrn_volume_render_device(fvsrn_volume_t volume, const fvsrn_tf* tf,
+                                             const fvsrn_camera* cam, const fvsrn_settings* settings,
+                                             const fvsrn_shard* shard, float* d_out, void* stream);
+FVSRN_API int32_t fvsrn_volume_render_rays(fvsrn_volume_t volume, const fvsrn_tf* tf,
+                                           const double* origins, const double* dirs, int64_t n,
+                                           const fvsrn_settings* settings, float* out_px,
+                                           uint64_t* sample_count);
+
 #ifdef __cplusplus
 }
 #endif

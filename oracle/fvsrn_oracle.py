@@ -554,9 +554,37 @@ def model_sample(model: OModel, tf: OTF | None, p, d, t):
     return out[:, :3], out[:, 3]
 
 
+def sample_volume(values, p):
+    """volume.py:213-255 (_trilinear): clip, per-axis (dims-1) scale, i0 = max(min(int,
+    dims-2), 0), f32 fractions, lerp x then y then z (f32)."""
+    p = np.atleast_2d(np.asarray(p, np.float64))
+    dims = np.asarray(values.shape[:3])
+    coords = np.clip(p, 0.0, 1.0) * (dims - 1)
+    i0 = np.maximum(np.minimum(coords.astype(np.int64), dims - 2), 0)
+    f = (coords - i0).astype(values.dtype)
+    x0, y0, z0 = i0[:, 0], i0[:, 1], i0[:, 2]
+    fx, fy, fz = f[:, 0], f[:, 1], f[:, 2]
+    v = values
+    c00 = v[x0, y0, z0] * (1 - fx) + v[x0 + 1, y0, z0] * fx
+    c10 = v[x0, y0 + 1, z0] * (1 - fx) + v[x0 + 1, y0 + 1, z0] * fx
+    c01 = v[x0, y0, z0 + 1] * (1 - fx) + v[x0 + 1, y0, z0 + 1] * fx
+    c11 = v[x0, y0 + 1, z0 + 1] * (1 - fx) + v[x0 + 1, y0 + 1, z0 + 1] * fx
+    c0 = c00 * (1 - fy) + c10 * fy
+    c1 = c01 * (1 - fy) + c11 * fy
+    return c0 * (1 - fz) + c1 * fz
+
+
+@dataclass
+class OVolume:
+    """A ground-truth source: VolumeSource(volume, tf) of render.py:132-141."""
+
+    values: np.ndarray
+
+
 def raymarch_forward(model, tf, o, d, stepsize, max_steps=4096, background=(0, 0, 0),
                      et_alpha=0.999, eps_blend=EPS_BLEND, t=None, counter=None):
-    """render.py:203-238 wavefront march; counter[0] += evaluated samples."""
+    """render.py:203-238 wavefront march; counter[0] += evaluated samples.
+    ``model`` may be an OModel or an OVolume (ground-truth VolumeSource)."""
     o = np.asarray(o, np.float64)
     d = np.asarray(d, np.float64)
     n = len(o)
@@ -572,7 +600,10 @@ def raymarch_forward(model, tf, o, d, stepsize, max_steps=4096, background=(0, 0
         idx = np.nonzero(active)[0]
         tk = tmin[idx] + (k + 0.5) * ds[idx]
         p = o[idx] + tk[:, None] * d[idx]
-        rgb, sig = model_sample(model, tf, p, d[idx], t)
+        if isinstance(model, OVolume):
+            rgb, sig = tf_eval(tf, sample_volume(model.values, p))
+        else:
+            rgb, sig = model_sample(model, tf, p, d[idx], t)
         if counter is not None:
             counter[0] += len(idx)
         c[idx], a[idx] = composite_step(c[idx], a[idx], rgb.astype(np.float64),

@@ -17,7 +17,7 @@ from .imaging import Camera, Image, metric_psnr, png_bytes, write_png
 from .model import (CheckpointError, FvsrnModel, ModelConfig, checkpoint_load, checkpoint_save,
                     decode_volume, eval_color, eval_density, memory_footprint, model_init)
 from .nn import FourierEncoder, MlpParams, fourier_make, init_params, nerf_rows
-from .render import (ModelSource, RayState, RenderSettings, camera_rays, fibonacci_cameras,
-                     raymarch_forward, render_image, render_rays)
+from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays,
+                     fibonacci_cameras, raymarch_forward, render_image, render_rays)
 from .transfer import TF_PRESETS, TransferFunction, tf_from_json, tf_load, tf_save
 from .volume import ScalarVolume

@@ -103,6 +103,16 @@ EXPORTS = {
     "fvsrn_decode_density_device": (C.c_int32, [C.c_void_p, C.c_int32, C.c_double, C.c_int64,
                                                 C.c_int64, C.c_void_p, C.c_void_p]),
     "fvsrn_fused_eval": (C.c_int32, [C.c_void_p, _f, C.c_int64, _f]),
+    "fvsrn_volume_create": (C.c_int32, [_f, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                        C.POINTER(C.c_void_p)]),
+    "fvsrn_volume_destroy": (C.c_int32, [C.c_void_p]),
+    "fvsrn_volume_render": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),
+                                        C.POINTER(SettingsDesc), _f, C.POINTER(C.c_uint64)]),
+    "fvsrn_volume_render_device": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),
+                                               C.POINTER(SettingsDesc), C.POINTER(ShardDesc),
+                                               C.c_void_p, C.c_void_p]),
+    "fvsrn_volume_render_rays": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), _d, _d, C.c_int64,
+                                             C.POINTER(SettingsDesc), _f, C.POINTER(C.c_uint64)]),
     "fvsrn_host_alloc": (C.c_int32, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "fvsrn_host_free": (C.c_int32, [C.c_void_p]),
 }

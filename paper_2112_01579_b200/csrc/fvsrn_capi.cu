@@ -16,6 +16,7 @@
 
 #include "../../include/fvsrn_b200.h"
 #include "fvsrn_kernels.cuh"
+#include "fvsrn_volume.cuh"
 
 using namespace fvsrn;
 
@@ -197,6 +198,26 @@ void bracket(const std::vector<double>& times, double t, int& lo, int& hi, doubl
   w = (h > l) ? (tc - times[l]) / (times[h] - times[l]) : 0.0;
 }
 
+// TransferFunction -> device table: control values + per-segment slopes (f64 -> f32),
+// i.e. np.interp's fp[i] + (x - xp[i]) * slope_i (transfer.py:57-65).
+int build_tf(const fvsrn_tf* tf, TFDev& th) {
+  if (tf->n < 2 || tf->n > kMaxTF) return fail(FVSRN_EINVAL, "transfer function needs 2..64 points");
+  th = TFDev{};
+  th.n = tf->n;
+  for (int i = 0; i < tf->n; ++i) {
+    th.xs[i] = tf->xs[i];
+    for (int c = 0; c < 3; ++c) th.val[i][c] = tf->rgbs[3 * i + c];
+    th.val[i][3] = tf->sigmas[i];
+  }
+  for (int i = 0; i + 1 < tf->n; ++i)
+    for (int c = 0; c < 4; ++c) {
+      double y0 = (c < 3) ? tf->rgbs[3 * i + c] : tf->sigmas[i];
+      double y1 = (c < 3) ? tf->rgbs[3 * (i + 1) + c] : tf->sigmas[i + 1];
+      th.slope[i][c] = (float)((y1 - y0) / ((double)tf->xs[i + 1] - (double)tf->xs[i]));
+    }
+  return FVSRN_OK;
+}
+
 struct FrameScratch {
   void* buf = nullptr;
   const __half* grid = nullptr;
@@ -221,19 +242,8 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
   }
   TFDev th{};
   if (tf) {
-    if (tf->n < 2 || tf->n > kMaxTF) return fail(FVSRN_EINVAL, "transfer function needs 2..64 points");
-    th.n = tf->n;
-    for (int i = 0; i < tf->n; ++i) {
-      th.xs[i] = tf->xs[i];
-      for (int c = 0; c < 3; ++c) th.val[i][c] = tf->rgbs[3 * i + c];
-      th.val[i][3] = tf->sigmas[i];
-    }
-    for (int i = 0; i + 1 < tf->n; ++i)
-      for (int c = 0; c < 4; ++c) {
-        double y0 = (c < 3) ? tf->rgbs[3 * i + c] : tf->sigmas[i];
-        double y1 = (c < 3) ? tf->rgbs[3 * (i + 1) + c] : tf->sigmas[i + 1];
-        th.slope[i][c] = (float)((y1 - y0) / ((double)tf->xs[i + 1] - (double)tf->xs[i]));
-      }
+    int rc = build_tf(tf, th);
+    if (rc) return rc;
   }
   size_t grid_bytes = 0;
   int lo = 0, hi = 0;
@@ -890,6 +900,169 @@ int32_t fvsrn_fused_eval(fvsrn_model_t m, const float* x, int64_t n, float* out)
   CUDA_TRY(cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaFreeAsync(buf, sg.s));
   CUDA_TRY(cudaStreamSynchronize(sg.s));
+  return FVSRN_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================ volumes
+struct fvsrn_volume {
+  int device = 0, X = 0, Y = 0, Z = 0, num_sms = 148;
+  float* d_values = nullptr;
+  ~fvsrn_volume() {
+    cudaSetDevice(device);
+    cudaFree(d_values);
+  }
+};
+
+namespace {
+
+int volume_render_impl(fvsrn_volume_t v, const fvsrn_tf* tf, const fvsrn_camera* c,
+                       const double* d_o, const double* d_d, long long n_rays,
+                       const fvsrn_settings* st, const fvsrn_shard* shard, float* d_out,
+                       unsigned long long* d_counters /* [samples, nonfinite] or null */,
+                       cudaStream_t s) {
+  int rc = check_settings(st);
+  if (rc) return rc;
+  if (!tf) return fail(FVSRN_EINVAL, "VolumeSource needs a transfer function");
+  TFDev th;
+  if ((rc = build_tf(tf, th))) return rc;
+  CUDA_TRY(cudaSetDevice(v->device));
+  char* scratch = nullptr;
+  const size_t off_ct = (sizeof(TFDev) + 255) / 256 * 256;
+  CUDA_TRY(cudaMallocAsync((void**)&scratch, off_ct + 64, s));
+  TFDev* d_tf = (TFDev*)scratch;
+  unsigned long long* ct = (unsigned long long*)(scratch + off_ct);
+  CUDA_TRY(cudaMemcpyAsync(d_tf, &th, sizeof(TFDev), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(ct, 0, 32, s));
+  MarchDev md = march_for(st);
+  CamDev cam{};
+  ShardDev sh{};
+  sh.world = 1;
+  long long n_slots = n_rays;
+  void* lpt = nullptr;
+  if (!d_o) {
+    if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+    cam = cam_for(c);
+    if (c->has_basis) {
+      for (int a = 0; a < 3; ++a) { cam.fwd[a] = c->b_forward[a]; cam.right[a] = c->b_right[a]; cam.up[a] = c->b_up[a]; }
+      cam.half_w = c->half_w;
+      cam.half_h = c->half_h;
+    }
+    sh.rank = shard ? shard->rank : 0;
+    sh.world = shard ? shard->world : 1;
+    sh.compact = shard ? shard->compact : 0;
+    if (sh.world < 1 || sh.rank < 0 || sh.rank >= sh.world) return fail(FVSRN_EINVAL, "bad shard");
+    sh.tiles_x = (c->width + kTile - 1) / kTile;
+    sh.n_tiles = sh.tiles_x * ((c->height + kTile - 1) / kTile);
+    const long long local_tiles = std::max(0ll, (long long)(sh.n_tiles - sh.rank + sh.world - 1) / sh.world);
+    n_slots = local_tiles * 64;
+    if (sh.compact) {
+      const long long max_local = (sh.n_tiles + sh.world - 1) / sh.world;
+      if (max_local > local_tiles)
+        CUDA_TRY(cudaMemsetAsync(d_out + local_tiles * 64 * 4, 0, (max_local - local_tiles) * 64 * 16, s));
+    }
+    if (local_tiles >= 2 * v->num_sms && g_lpt_enabled) {
+      const int nl = (int)local_tiles;
+      const size_t sb = tile_order_scratch_bytes(nl);
+      CUDA_TRY(cudaMallocAsync(&lpt, 16 * (size_t)nl + sb + 256, s));
+      unsigned* cost = (unsigned*)lpt;
+      unsigned* order = cost + 2 * (size_t)nl;
+      CUDA_TRY(launch_tile_order(cam, md, sh, nl, cost, order, (char*)lpt + 16 * (size_t)nl, sb, s));
+      sh.order = order;
+    }
+  }
+  VolDev vd{v->d_values, v->X, v->Y, v->Z};
+  if (n_slots > 0)
+    CUDA_TRY(launch_volume_dvr(vd, d_tf, md, cam, sh, d_o, d_d, n_slots, d_out, ct, v->num_sms, s));
+  if (d_counters) CUDA_TRY(cudaMemcpyAsync(d_counters, ct + 1, 16, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaFreeAsync(scratch, s));
+  if (lpt) CUDA_TRY(cudaFreeAsync(lpt, s));
+  return FVSRN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fvsrn_volume_create(const float* values, int32_t nx, int32_t ny, int32_t nz, int32_t device,
+                            fvsrn_volume_t* out) {
+  if (!values || !out) return fail(FVSRN_EINVAL, "null argument");
+  *out = nullptr;
+  if (nx < 2 || ny < 2 || nz < 2) return fail(FVSRN_EINVAL, "volume dims must be >= 2 for trilinear sampling");
+  auto v = std::make_unique<fvsrn_volume>();
+  v->device = device;
+  v->X = nx; v->Y = ny; v->Z = nz;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  v->num_sms = prop.multiProcessorCount;
+  int rc = upload(values, sizeof(float) * (size_t)nx * ny * nz, (void**)&v->d_values);
+  if (rc) return rc;
+  *out = v.release();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_volume_destroy(fvsrn_volume_t v) {
+  delete v;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_volume_render(fvsrn_volume_t v, const fvsrn_tf* tf, const fvsrn_camera* c,
+                            const fvsrn_settings* st, float* out, uint64_t* sample_count) {
+  if (!v || !c || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+  CUDA_TRY(cudaSetDevice(v->device));
+  StreamGuard sg;
+  const size_t bytes = (size_t)c->width * c->height * 16;
+  float* d_out = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d_out, bytes + 16, sg.s));
+  unsigned long long* d_cnt = (unsigned long long*)((char*)d_out + bytes);
+  int rc = volume_render_impl(v, tf, c, nullptr, nullptr, 0, st, nullptr, d_out, d_cnt, sg.s);
+  if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  unsigned long long cnt[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(d_out, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (sample_count) *sample_count = cnt[0];
+  if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_volume_render_device(fvsrn_volume_t v, const fvsrn_tf* tf, const fvsrn_camera* c,
+                                   const fvsrn_settings* st, const fvsrn_shard* shard, float* d_out,
+                                   void* stream) {
+  if (!v || !c || !d_out) return fail(FVSRN_EINVAL, "null argument");
+  return volume_render_impl(v, tf, c, nullptr, nullptr, 0, st, shard, d_out, nullptr,
+                            (cudaStream_t)stream);
+}
+
+int32_t fvsrn_volume_render_rays(fvsrn_volume_t v, const fvsrn_tf* tf, const double* origins,
+                                 const double* dirs, int64_t n, const fvsrn_settings* st,
+                                 float* out_px, uint64_t* sample_count) {
+  if (!v || (n > 0 && (!origins || !dirs || !out_px))) return fail(FVSRN_EINVAL, "null argument");
+  if (sample_count) *sample_count = 0;
+  if (n == 0) return check_settings(st);
+  CUDA_TRY(cudaSetDevice(v->device));
+  StreamGuard sg;
+  const size_t rb = (size_t)n * 3 * sizeof(double), ob = (size_t)n * 16;
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, 2 * rb + ob + 16, sg.s));
+  double* d_o = (double*)buf;
+  double* d_d = (double*)(buf + rb);
+  float* d_out = (float*)(buf + 2 * rb);
+  unsigned long long* d_cnt = (unsigned long long*)(buf + 2 * rb + ob);
+  CUDA_TRY(cudaMemcpyAsync(d_o, origins, rb, cudaMemcpyHostToDevice, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(d_d, dirs, rb, cudaMemcpyHostToDevice, sg.s));
+  int rc = volume_render_impl(v, tf, nullptr, d_o, d_d, n, st, nullptr, d_out, d_cnt, sg.s);
+  if (rc) { cudaFreeAsync(buf, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  unsigned long long cnt[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(out_px, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (sample_count) *sample_count = cnt[0];
   return FVSRN_OK;
 }
 

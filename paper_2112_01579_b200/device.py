@@ -243,6 +243,66 @@ class DeviceModel:
                                                       C.c_void_p(stream_ptr)))
 
 
+class DeviceVolume:
+    """A ScalarVolume resident on one GPU (f32, reference layout) for ground-truth DVR."""
+
+    def __init__(self, volume, device: int | None = None):
+        lib = L.lib()
+        self.device = L.current_device() if device is None else int(device)
+        v = np.ascontiguousarray(volume.values, dtype=np.float32)
+        if v.ndim != 3:
+            raise ValueError(f"volume must be 3D, got {v.shape}")
+        h = C.c_void_p()
+        L.check(lib.fvsrn_volume_create(L.fptr(v), v.shape[0], v.shape[1], v.shape[2],
+                                        self.device, C.byref(h)))
+        self._h, self._lib, self.shape = h, lib, v.shape
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._lib.fvsrn_volume_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+    def render(self, tf, cam, settings, out=None):
+        shape = (cam.height, cam.width, 4)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+        cnt = C.c_uint64(0)
+        tfd = tf_desc(tf)
+        L.check(self._lib.fvsrn_volume_render(self._h, C.byref(tfd.desc), C.byref(camera_desc(cam)),
+                                              C.byref(settings_desc(settings)), L.fptr(out),
+                                              C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def render_rays(self, tf, origins, dirs, settings):
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.float64).reshape(-1, 3))
+        d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))
+        if o.shape != d.shape:
+            raise ValueError("origins and dirs must have the same shape")
+        out = np.empty((len(o), 4), dtype=np.float32)
+        cnt = C.c_uint64(0)
+        tfd = tf_desc(tf)
+        L.check(self._lib.fvsrn_volume_render_rays(self._h, C.byref(tfd.desc), L.dptr(o), L.dptr(d),
+                                                   len(o), C.byref(settings_desc(settings)),
+                                                   L.fptr(out), C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def render_device(self, tf, cam, settings, out_ptr: int, stream_ptr: int, rank: int = 0,
+                      world: int = 1, compact: bool = False):
+        tfd = tf_desc(tf)
+        sh = L.ShardDesc(int(rank), int(world), 1 if compact else 0)
+        L.check(self._lib.fvsrn_volume_render_device(
+            self._h, C.byref(tfd.desc), C.byref(camera_desc(cam)), C.byref(settings_desc(settings)),
+            C.byref(sh), C.c_void_p(out_ptr), C.c_void_p(stream_ptr)))
+
+
 _cache_lock = threading.Lock()
 
 

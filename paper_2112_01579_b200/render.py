@@ -14,7 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .device import device_model
+from .device import DeviceVolume, device_model
 from .imaging import Camera, Image
 
 EPS_BLEND = 1e-5
@@ -91,6 +91,24 @@ class ModelSource:
         return out[:, :3], out[:, 3]
 
 
+class VolumeSource:
+    """Ground-truth source: trilinear density through a transfer function
+    (render.py:132-141).  The volume is uploaded once (f32, reference layout) and
+    frames render with fvsrn_volume_render: same ray setup, TF, compositing and early
+    termination as ModelSource, densities bit-identical to sample_volume."""
+
+    def __init__(self, volume, tf, device: int | None = None):
+        self.volume = volume
+        self.tf = tf
+        self.device_volume = DeviceVolume(volume, device)
+        self.last_eval_count = 0
+
+    def sample(self, p, d):
+        raise NotImplementedError("the B200 VolumeSource renders whole frames / ray batches "
+                                  "(render_image, raymarch_forward); per-sample host calls are "
+                                  "not part of the GPU path")
+
+
 def camera_rays(camera: Camera):
     """Per-pixel (origins, unit dirs), row-major from the top-left (render.py:72-94).
 
@@ -110,9 +128,9 @@ def camera_rays(camera: Camera):
     return np.broadcast_to(camera.eye, dirs.shape).copy(), dirs
 
 
-def _require_model_source(source) -> ModelSource:
-    if not isinstance(source, ModelSource):
-        raise TypeError("the B200 renderer draws ModelSource instances (fV-SRN models); "
+def _require_model_source(source):
+    if not isinstance(source, (ModelSource, VolumeSource)):
+        raise TypeError("the B200 renderer draws ModelSource or VolumeSource instances; "
                         f"got {type(source).__name__}")
     return source
 
@@ -127,7 +145,10 @@ def raymarch_forward(source, origins, dirs, settings: RenderSettings, want_state
     if want_states:
         settings = RenderSettings(settings.stepsize, settings.max_steps, settings.background,
                                   1.0, settings.eps_blend)
-    px, cnt = src.device_model.render_rays(src.tf, origins, dirs, settings, src.t)
+    if isinstance(src, VolumeSource):
+        px, cnt = src.device_volume.render_rays(src.tf, origins, dirs, settings)
+    else:
+        px, cnt = src.device_model.render_rays(src.tf, origins, dirs, settings, src.t)
     src.last_eval_count = cnt
     states = None
     if want_states:
@@ -154,7 +175,10 @@ def render_image(source, camera: Camera, settings: RenderSettings | None = None,
     """
     src = _require_model_source(source)
     settings = settings or RenderSettings()
-    data, cnt = src.device_model.render(src.tf, camera, settings, src.t, out=out)
+    if isinstance(src, VolumeSource):
+        data, cnt = src.device_volume.render(src.tf, camera, settings, out=out)
+    else:
+        data, cnt = src.device_model.render(src.tf, camera, settings, src.t, out=out)
     src.last_eval_count = cnt
     return Image._from_device(data)
 

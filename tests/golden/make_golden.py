@@ -34,6 +34,8 @@ from fvsrn.render import (  # noqa: E402
 from fvsrn.train import fibonacci_cameras  # noqa: E402
 from fvsrn.transfer import TF_PRESETS, tf_eval  # noqa: E402
 from fvsrn.fused import fused_eval, plan_for_model  # noqa: E402
+from fvsrn.render import VolumeSource  # noqa: E402
+from fvsrn.volume import ScalarVolume, synth_field  # noqa: E402
 
 
 def sha(a) -> str:
@@ -190,6 +192,32 @@ def main():
                RenderSettings(stepsize=1 / 128))
     add_render("cfg3_v0_gray_48", models["cfg3"], "grayscale", fibonacci_cameras(8, 48, 48)[0],
                RenderSettings(stepsize=1 / 192), fused=False)  # CapacityError on fused
+
+    # --- ground-truth DVR through VolumeSource (render.py:132-141, volume.py:213-255)
+    vols = {
+        "sphere32": synth_field("sphere", 32),
+        "gauss48": synth_field("gaussians", 48, {"n_components": 8}, seed=42),
+        "random975": ScalarVolume(values=np.random.default_rng(1234).uniform(0, 1, size=(9, 7, 5))
+                                  .astype(np.float32)),
+    }
+    for k, v in vols.items():
+        arrays[f"volume_{k}"] = v.values
+    vol_renders = [("sphere32", "grayscale", fib64[0], 1 / 32, (0, 0, 0)),
+                   ("gauss48", "warm", fib64[3], 1 / 48, (0.1, 0.2, 0.3)),
+                   ("random975", "two_peaks", fib64[5], 1 / 40, (0, 0, 0))]
+    for vname, tfname, cam, step, bg in vol_renders:
+        Counting.count = 0
+        st = RenderSettings(stepsize=step, background=bg)
+        img = render_image(VolumeSource(vols[vname], TF_PRESETS[tfname]), cam, st)
+        tag = f"vol_{vname}_{tfname}"
+        arrays[f"render_{tag}"] = img.data
+        meta["renders"][tag] = {
+            "count": None, "tf": tfname, "t": None, "volume": vname,
+            "stepsize": st.stepsize, "max_steps": st.max_steps,
+            "background": list(st.background), "et": st.early_term_alpha,
+            "camera": {"eye": list(map(float, cam.eye)), "target": list(map(float, cam.target)),
+                       "up": list(map(float, cam.up)), "fov_y": float(cam.fov_y),
+                       "width": cam.width, "height": cam.height}}
 
     # --- raymarch_forward on explicit rays, max_steps cap (render.py:203-238)
     o = np.column_stack([rng.uniform(0.2, 0.8, 64), rng.uniform(0.2, 0.8, 64), np.full(64, -0.5)])

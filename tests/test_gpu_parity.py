@@ -225,3 +225,44 @@ def test_empty_and_single_ray():
     img = P.render_image(src, P.fibonacci_cameras(1, 1, 1)[0], P.RenderSettings())
     assert img.data.shape == (1, 1, 4)
     assert P.eval_density(_model("tiny"), np.zeros((0, 3))).shape == (0,)
+
+
+# ------------------------------------------------------------------ VolumeSource
+@pytest.mark.parametrize("tag", ["vol_sphere32_grayscale", "vol_gauss48_warm",
+                                 "vol_random975_two_peaks"])
+def test_volume_source_vs_reference(tag):
+    r = meta()["renders"][tag]
+    vol = P.ScalarVolume(arrays()[f"volume_{r['volume']}"])
+    src = P.VolumeSource(vol, P.TF_PRESETS[r["tf"]])
+    s = P.RenderSettings(stepsize=r["stepsize"], max_steps=r["max_steps"],
+                         background=tuple(r["background"]), early_term_alpha=r["et"])
+    img = P.render_image(src, _cam(r["camera"]), s)
+    assert P.metric_psnr(img, arrays()[f"render_{tag}"]) >= 60.0
+
+
+def test_volume_source_empty_and_beer_lambert():
+    # tests/test_render.py:208-226 of the reference, on the GPU path
+    empty = P.ScalarVolume(np.zeros((8, 8, 8), np.float32))
+    cam = P.Camera(eye=(0.5, 0.5, 3.5), target=(0.5, 0.5, 0.5), up=(0, 1, 0), fov_y=np.pi / 5,
+                   width=9, height=9)
+    img = P.render_image(P.VolumeSource(empty, P.TF_PRESETS["grayscale"]), cam,
+                         P.RenderSettings(stepsize=0.05, background=(0.2, 0.3, 0.4)))
+    np.testing.assert_allclose(img.data[:, :, :3], np.broadcast_to([0.2, 0.3, 0.4], (9, 9, 3)),
+                               atol=1e-6)
+    ones = P.ScalarVolume(np.ones((4, 4, 4), np.float32))
+    tf = P.TransferFunction.from_points([(0.0, (1, 1, 1), 8.0), (1.0, (1, 1, 1), 8.0)])
+    px, _ = P.raymarch_forward(P.VolumeSource(ones, tf), np.array([[0.5, 0.5, -1.0]]),
+                               np.array([[0.0, 0.0, 1.0]]), P.RenderSettings(stepsize=1.0 / 1000))
+    assert px[0, 3] == pytest.approx(1 - np.exp(-8.0), rel=0.01)
+
+
+def test_model_vs_dense_decode_on_gpu():
+    # tests/test_render.py:236-243: render the model and its 64^3 decode, PSNR > 40 dB
+    m = _model("tiny")
+    s = P.RenderSettings.for_voxels(64, 1.0)
+    cam = P.Camera(eye=(0.5, 0.5, 2.5), target=(0.5, 0.5, 0.5), up=(0, 1, 0), fov_y=np.pi / 5,
+                   width=48, height=48)
+    img_model = P.render_image(P.ModelSource(m, P.TF_PRESETS["grayscale"]), cam, s)
+    img_dec = P.render_image(P.VolumeSource(P.decode_volume(m, 64), P.TF_PRESETS["grayscale"]),
+                             cam, s)
+    assert P.metric_psnr(img_model, img_dec) > 40.0

@@ -120,3 +120,13 @@ def test_psnr_known_answers():
     assert O.metric_psnr(x, x) == 99.0
     assert O.metric_psnr(x, x + 1.0) == pytest.approx(0.0)
     assert O.metric_psnr(x, x + 0.1) == pytest.approx(20.0)
+
+
+@pytest.mark.parametrize("tag", ["vol_sphere32_grayscale", "vol_gauss48_warm",
+                                 "vol_random975_two_peaks"])
+def test_volume_source_render_matches_reference(tag):
+    r = meta()["renders"][tag]
+    vol = O.OVolume(arrays()[f"volume_{r['volume']}"])
+    img = O.render_image(vol, O.TF_PRESETS[r["tf"]], _cam(r["camera"]), r["stepsize"],
+                         r["max_steps"], tuple(r["background"]), r["et"])
+    assert O.metric_psnr(img, arrays()[f"render_{tag}"]) > 90.0
