@@ -333,6 +333,8 @@ MarchDev march_for(const fvsrn_settings* st) {
   md.max_steps = st->max_steps;
   md.et_alpha = st->early_term_alpha;
   md.eps_blend = st->eps_blend;
+  md.eps1_f = (float)(1.0 - st->eps_blend);
+  md.et_f = (float)st->early_term_alpha;
   for (int c = 0; c < 3; ++c) md.bg[c] = (float)st->background[c];
   return md;
 }

@@ -63,7 +63,20 @@ struct MarchDev {
   double stepsize, et_alpha, eps_blend;
   float bg[3];
   int max_steps;
+  float eps1_f, et_f;         // f32(1 - eps_blend), f32(et_alpha): loop invariants from the host
 };
+
+// floor(c) for 0 <= c < 2^23 on the FMA/ALU pipes (no F2I/I2F on the XU pipe):
+// c + 2^23 rounded toward -inf holds floor(c) in its low mantissa bits.
+__device__ __forceinline__ float floor_pos(float c, int& i) {
+  const float m = __fadd_rd(c, 8388608.f);
+  i = __float_as_int(m) - 0x4B000000;
+  return m - 8388608.f;
+}
+// round-to-nearest-even for |v| < 2^22 on the FMA pipe (no FRND on the XU pipe)
+__device__ __forceinline__ float rint_fma(float v) {
+  return __fsub_rn(__fadd_rn(v, 12582912.f), 12582912.f);
+}
 
 // ---------------------------------------------------------------- small helpers
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
@@ -460,11 +473,16 @@ struct FastRow {
     {
       const int R = fd.grid_res;
       const float s = (float)(R - 1);
+      const float rm2 = (float)(R - 2);
       float cx = fminf(fmaxf(px, 0.f), 1.f) * s;
       float cy = fminf(fmaxf(py, 0.f), 1.f) * s;
       float cz = fminf(fmaxf(pz, 0.f), 1.f) * s;
-      int x0 = min((int)cx, R - 2), y0 = min((int)cy, R - 2), z0 = min((int)cz, R - 2);
-      float fx = cx - (float)x0, fy = cy - (float)y0, fz = cz - (float)z0;
+      int x0, y0, z0;   // i0 = min(int c, R-2) (grid.py:47-53), c >= 0 so trunc == floor
+      float x0f = floor_pos(cx, x0), y0f = floor_pos(cy, y0), z0f = floor_pos(cz, z0);
+      if (x0 > R - 2) { x0 = R - 2; x0f = rm2; }
+      if (y0 > R - 2) { y0 = R - 2; y0f = rm2; }
+      if (z0 > R - 2) { z0 = R - 2; z0f = rm2; }
+      float fx = cx - x0f, fy = cy - y0f, fz = cz - z0f;
       float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
       const float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
                            fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
@@ -496,7 +514,7 @@ struct FastRow {
       const float pv[3] = {px, py, pz};
       float sn[3], cs[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) __sincosf((pv[a] - rintf(pv[a])) * 6.28318548202514648f, &sn[a], &cs[a]);
+      for (int a = 0; a < 3; ++a) __sincosf((pv[a] - rint_fma(pv[a])) * 6.28318548202514648f, &sn[a], &cs[a]);
 #pragma unroll
       for (int i = 0; i < NM; ++i) {
         const int a = i % 3;
@@ -531,7 +549,20 @@ __device__ __forceinline__ void assemble_row_t(const FeatDev& fd, float px, floa
 }
 
 // ---------------------------------------------------------------- TF + heads
-__device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+// sigmoid as 1/2 + tanh(x/2)/2: one MUFU.TANH instead of EX2 + RCP (|err| < 2.5e-4,
+// A/B switch FVSRN_SIGMOID_TANH=0 restores the two-MUFU form).
+#ifndef FVSRN_SIGMOID_TANH
+#define FVSRN_SIGMOID_TANH 1
+#endif
+__device__ __forceinline__ float sigmoidf_(float x) {
+#if FVSRN_SIGMOID_TANH
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return fmaf(0.5f, t, 0.5f);
+#else
+  return __fdividef(1.f, 1.f + __expf(-x));
+#endif
+}
 __device__ __forceinline__ float softplusf_(float x) { return x > 20.f ? x : log1pf(__expf(x)); }
 
 // transfer.py:57-65: clamp to [0,1], piecewise-linear interpolation.

@@ -78,8 +78,8 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   const int lane = threadIdx.x & 31;
   const bool density = net.head == 0;
   const bool use_dir = fd.dir_mode != 0;
-  const float eps1 = (float)(1.0 - md.eps_blend);
-  const float et = (float)md.et_alpha;
+  const float eps1 = md.eps1_f;
+  const float et = md.et_f;
   __half* myrow = stage + lane * rs;
   // two-point TFs (the presets' grayscale) live in registers: no per-sample smem lookups
   const bool tf_two = FVSRN_TF_REGS && density && tf->n == 2;
