@@ -108,6 +108,11 @@ typedef struct { int32_t rank, world, compact; } fvsrn_shard;
 FVSRN_API const char* fvsrn_last_error(void);
 FVSRN_API const char* fvsrn_version(void);
 FVSRN_API int32_t fvsrn_device_count(void);
+/* DVR kernel selection for the default fV-SRN shapes (no reference counterpart: a
+ * measurement / A-B switch; the environment variable FVSRN_DVR sets the initial value).
+ * 0 auto (measured faster per width), 1 tcgen05/TMEM, 2 warp-specialised mma.sync,
+ * 3 single-role mma.sync.  Returns the previous mode, or FVSRN_EINVAL. */
+FVSRN_API int32_t fvsrn_set_dvr_kernel(int32_t mode);
 
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
 FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);

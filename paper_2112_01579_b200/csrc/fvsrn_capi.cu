@@ -1,3 +1,4 @@
+#include <atomic>
 // fvsrn_capi.cu -- the C ABI (include/fvsrn_b200.h): model upload, weight/grid
 // packing, per-frame constants, kernel launches.  Host code only.
 #include <cuda_fp16.h>
@@ -16,6 +17,7 @@
 
 #include "../../include/fvsrn_b200.h"
 #include "fvsrn_kernels.cuh"
+#include "fvsrn_tc.cuh"
 #include "fvsrn_volume.cuh"
 
 using namespace fvsrn;
@@ -28,6 +30,21 @@ const bool g_lpt_enabled = [] {
   const char* e = std::getenv("FVSRN_LPT");
   return !(e && e[0] == '0');
 }();
+
+// DVR kernel for the default fV-SRN shapes: FVSRN_DVR=tc (tcgen05/TMEM), ws
+// (warp-specialised mma.sync) or warp (single-role mma.sync); unset = the measured
+// faster one per width (auto: tcgen05 for 64-wide, mma.sync for 32-wide).
+// Other shapes always run the mma.sync dvr_kernel.
+enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3 };
+std::atomic<int> g_dvr_mode_i{[] {
+  const char* e = std::getenv("FVSRN_DVR");
+  if (e && std::string(e) == "tc") return (int)DvrMode::kTC;
+  if (e && std::string(e) == "ws") return (int)DvrMode::kWS;
+  if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
+  return (int)DvrMode::kAuto;
+}()};
+inline DvrMode dvr_mode() { return (DvrMode)g_dvr_mode_i.load(std::memory_order_relaxed); }
+bool use_tc(const fvsrn_model* m);
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -117,6 +134,10 @@ struct fvsrn_model {
   int four_off = 0, raw_off = 0, k0 = 0;
   // sample pack (device column order, time folded) and x pack (reference order)
   DevPack ps, px;
+  // tcgen05 pack (canonical K-major fp16 tiles + f32 biases), default shapes only
+  uint4* d_wtc = nullptr;
+  float* d_btc = nullptr;
+  bool tc_ok = false;
   int k0x = 0;
   std::vector<float> b0_static;     // layer-0 bias, padded N0
   std::vector<float> w0_time;       // N0 x T time columns of W0
@@ -128,6 +149,7 @@ struct fvsrn_model {
     cudaFree(d_bmat);
     cudaFree(ps.frag); cudaFree(ps.bias);
     cudaFree(px.frag); cudaFree(px.bias);
+    cudaFree(d_wtc); cudaFree(d_btc);
   }
 };
 
@@ -304,7 +326,10 @@ std::map<std::tuple<const void*, int, size_t>, int> g_occ;
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
-  const void* fn = kernel_for(kind, m->hid_pad, fast_path(m, kind));
+  const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad)
+                                               : kernel_for(kind, m->hid_pad, fast_path(m, kind));
+  const int threads = kind == KernelKind::kDVRWS ? kWsThreads
+                      : kind == KernelKind::kDVRTC ? kTcThreads : kThreads;
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
   int occ = 0;
   {
@@ -313,18 +338,70 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
     auto it = g_occ.find(key);
     if (it == g_occ.end()) {
       CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+      if (kind == KernelKind::kDVRTC) {
+        // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; the real
+        // limits are registers (launch bounds), shared memory and TMEM columns (each
+        // CTA allocates <= 64 of 512), so size the persistent grid from those.
+        cudaFuncAttributes fa;
+        CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+        int smem_sm = 0, regs_sm = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device));
+        CUDA_TRY(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, m->device));
+        const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + 1024);
+        const int by_regs = regs_sm / std::max(1, fa.numRegs * threads);
+        occ = std::max(1, std::min(std::min(by_smem, by_regs), 8));
+      }
       g_occ[key] = occ;
+      if (std::getenv("FVSRN_DEBUG_OCC"))
+        std::fprintf(stderr, "fvsrn: kernel kind %d hid %d threads %d smem %zu -> %d CTAs/SM\n", (int)kind,
+                     m->hid_pad, threads, smem, occ);
     } else {
       occ = it->second;
     }
   }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   long long blocks = (long long)m->num_sms * occ;
-  const long long need = (work_warps + (kThreads / 32) - 1) / (kThreads / 32);
+  const long long need = (work_warps + (threads / 32) - 1) / (threads / 32);
   if (need < blocks) blocks = std::max(1ll, need);
-  CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(kThreads), args, smem, s));
+  CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, s));
   return FVSRN_OK;
+}
+
+bool use_tc(const fvsrn_model* m) {
+  if (!m->tc_ok || !fast_path(m, KernelKind::kDVR)) return false;
+  if (dvr_mode() == DvrMode::kTC) return true;
+  return dvr_mode() == DvrMode::kAuto && m->hid_pad == 64;
+}
+
+// Stream-ordered per-frame ray records: a, b (+ d for direction-input models).
+int alloc_recs(const fvsrn_model* m, long long n_slots, cudaStream_t s, RayRecs& rr, void*& buf) {
+  const size_t n = (size_t)std::max(1ll, n_slots);
+  const int parts = m->dir_mode != 0 ? 3 : 2;
+  CUDA_TRY(cudaMallocAsync(&buf, n * sizeof(float4) * parts, s));
+  float4* f = (float4*)buf;
+  rr.a = f;
+  rr.b = f + n;
+  rr.d = parts == 3 ? f + 2 * n : nullptr;
+  return FVSRN_OK;
+}
+
+// The fused DVR launch: tcgen05 kernel for the default shapes (FVSRN_DVR=tc), else the
+// warp-specialised or single-role mma.sync kernel.  Same arguments for all three.
+int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp, const float*& b0,
+               MarchDev& md, CamDev& cam, ShardDev& sh, int& explicit_rays, RayRecs& rr,
+               long long& n_slots, float*& d_out, unsigned long long*& queue,
+               unsigned long long*& evc, unsigned long long*& nfc, cudaStream_t s) {
+  if (n_slots <= 0) return FVSRN_OK;
+  if (use_tc(m)) {
+    TcNetDev tn{m->d_wtc, m->d_btc, m->head};
+    void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+    return launch(m, KernelKind::kDVRTC, tc_smem_bytes(m->hid_pad), args, s, n_slots / 32 + 1);
+  }
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+  if (dvr_mode() == DvrMode::kWS)
+    return launch(m, KernelKind::kDVRWS, ws_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
+  return launch(m, KernelKind::kDVR, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
 }
 
 MarchDev march_for(const fvsrn_settings* st) {
@@ -388,6 +465,11 @@ CamDev cam_for(const fvsrn_camera* c) {
 extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
+
+int32_t fvsrn_set_dvr_kernel(int32_t mode) {
+  if (mode < 0 || mode > 3) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..3");
+  return g_dvr_mode_i.exchange(mode);
+}
 const char* fvsrn_version(void) { return "fvsrn_b200 0.1.0 (sm_100a, mma.sync f16/f32)"; }
 
 int32_t fvsrn_device_count(void) {
@@ -574,6 +656,29 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
         m->w0_time[(size_t)o * m->T + j] =
             s_out0 * d->weights[0][(size_t)o * d->d_in + m->raw_w + 2 * m->m + j];
   }
+  // tcgen05 pack for the default shapes (see TcNetDev in fvsrn_tc.cuh)
+  if ((m->hid_pad == 32 || m->hid_pad == 64) && L == tc_layers(m->hid_pad) && m->f_pad == 16 &&
+      m->R > 0 && m->act == FVSRN_ACT_SNAKE_ALT && m->fourier_mode == FVSRN_FOURIER_NERF &&
+      m->fd_in == 3 && m->raw_w == 3 && m->m == (m->hid_pad - 4) / 2) {
+    const int H = m->hid_pad;
+    std::vector<__half> wt;
+    std::vector<float> bt;
+    for (int l = 0; l < L; ++l) {
+      const int Nt = (l == L - 1) ? 16 : H, K = Ks[l];
+      std::vector<__half> tile((size_t)Nt * K, __float2half_rn(0.f));
+      for (int n = 0; n < Nt && n < N[l]; ++n)
+        for (int k = 0; k < K; ++k)
+          tile[(size_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] =
+              __float2half_rn(ws[l][(size_t)n * K + k]);
+      wt.insert(wt.end(), tile.begin(), tile.end());
+      for (int n = 0; n < Nt; ++n) bt.push_back(n < N[l] ? bs[l][n] : 0.f);
+    }
+    int rc = upload(wt.data(), wt.size() * sizeof(__half), (void**)&m->d_wtc);
+    if (rc) return rc;
+    rc = upload(bt.data(), bt.size() * sizeof(float), (void**)&m->d_btc);
+    if (rc) return rc;
+    m->tc_ok = true;
+  }
   Pack pks, pkx;
   build_pack(ws, Ks, N, bs, pks);
   pks.kt0 = m->k0 / 16;
@@ -651,29 +756,40 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
   NetDev net = m->ps.net;
   FeatDev fd = feat_for(m, fs.grid);
   MarchDev md = march_for(st);
-  // LPT schedule: longest tiles first (removes the persistent kernel's long-ray tail)
+  // per-slot ray records (f64 setup once per ray, outside the march loop) and the LPT
+  // schedule: longest tiles first (removes the persistent kernel's long-ray tail)
+  RayRecs rr{};
+  void* recs = nullptr;
+  if ((rc = alloc_recs(m, n_slots, s, rr, recs))) return rc;
   void* lpt = nullptr;
-  if (local_tiles >= 2 * m->num_sms && g_lpt_enabled) {
+  const bool use_lpt = local_tiles >= 2 * m->num_sms && g_lpt_enabled;
+  unsigned* cost = nullptr;
+  unsigned* order = nullptr;
+  size_t sb = 0;
+  if (use_lpt) {
     const int nl = (int)local_tiles;
-    const size_t sb = tile_order_scratch_bytes(nl);
+    sb = tile_order_scratch_bytes(nl);
     CUDA_TRY(cudaMallocAsync(&lpt, 16 * (size_t)nl + sb + 256, s));
-    unsigned* cost = (unsigned*)lpt;
-    unsigned* order = cost + 2 * (size_t)nl;
-    void* scratch = (char*)lpt + 16 * (size_t)nl;
-    CUDA_TRY(launch_tile_order(cam, md, sh, nl, cost, order, scratch, sb, s));
+    cost = (unsigned*)lpt;
+    order = cost + 2 * (size_t)nl;
+    CUDA_TRY(cudaMemsetAsync(cost, 0, sizeof(unsigned) * nl, s));
+  }
+  CUDA_TRY(launch_ray_setup(cam, md, sh, nullptr, nullptr, n_slots, rr, d_out, cost,
+                            order ? order + local_tiles : nullptr, s));
+  if (use_lpt) {
+    CUDA_TRY(launch_tile_sort((int)local_tiles, cost, order, (char*)lpt + 16 * (size_t)local_tiles, sb, s));
     sh.order = order;
   }
   const TFDev* tfp = fs.tf;
   const float* b0 = fs.b0;
-  const double* ro = nullptr;
-  const double* rd = nullptr;
+  int explicit_rays = 0;
   unsigned long long* queue = fs.counters;
   unsigned long long* evc = d_eval_count ? d_eval_count : fs.counters + 1;
   unsigned long long* nfc = d_nonfinite ? d_nonfinite : fs.counters + 2;
-  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc, &nfc};
-  const size_t smem = stage_smem_bytes(net, true, m->k0);
-  if ((rc = launch(m, KernelKind::kDVR, smem, args, s, n_slots / 32 + 1))) return rc;
+  if ((rc = launch_dvr(m, net, fd, tfp, b0, md, cam, sh, explicit_rays, rr, n_slots, d_out, queue, evc, nfc, s)))
+    return rc;
   CUDA_TRY(cudaFreeAsync(fs.buf, s));
+  CUDA_TRY(cudaFreeAsync(recs, s));
   if (lpt) CUDA_TRY(cudaFreeAsync(lpt, s));
   return FVSRN_OK;
 }
@@ -754,15 +870,18 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   sh.world = 1;
   const TFDev* tfp = fs.tf;
   const float* b0 = fs.b0;
-  const double* ro = d_o;
-  const double* rd = d_d;
   long long n_slots = n;
+  RayRecs rr{};
+  void* recs = nullptr;
+  if ((rc = alloc_recs(m, n_slots, sg.s, rr, recs))) return rc;
+  CUDA_TRY(launch_ray_setup(cam, md, sh, d_o, d_d, n_slots, rr, d_out, nullptr, nullptr, sg.s));
+  int explicit_rays = 1;
   unsigned long long* queue = fs.counters;
   unsigned long long* evc = fs.counters + 1;
   unsigned long long* nfc = nullptr;
-  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &ro, &rd, &n_slots, &d_out, &queue, &evc, &nfc};
-  const size_t smem = stage_smem_bytes(net, true, m->k0);
-  if ((rc = launch(m, KernelKind::kDVR, smem, args, sg.s, n_slots / 32 + 1))) return rc;
+  if ((rc = launch_dvr(m, net, fd, tfp, b0, md, cam, sh, explicit_rays, rr, n_slots, d_out, queue, evc, nfc, sg.s)))
+    return rc;
+  CUDA_TRY(cudaFreeAsync(recs, sg.s));
   unsigned long long cnt = 0;
   CUDA_TRY(cudaMemcpyAsync(out_px, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaMemcpyAsync(&cnt, evc, 8, cudaMemcpyDeviceToHost, sg.s));

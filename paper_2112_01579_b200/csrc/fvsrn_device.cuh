@@ -465,6 +465,9 @@ struct FastRow {
   static constexpr int kK0 = (kWidth + 15) / 16 * 16;
   static constexpr int kWords = kK0 / 2;
 
+  // CS: distance (in 16-byte chunks) between consecutive 8-column chunks of the row:
+  // 1 = row-major stage, 8 = UMMA K-major canonical layout (128 B per core matrix).
+  template <int CS = 1>
   __device__ static void build(const FeatDev& fd, float px, float py, float pz, __half* row) {
     uint32_t w[kWords];
 #pragma unroll
@@ -533,7 +536,7 @@ struct FastRow {
     w[9 + NM] = pack_half2(pz, 0.f);
     uint4* dst = reinterpret_cast<uint4*>(row);
 #pragma unroll
-    for (int j = 0; j < kWords / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    for (int j = 0; j < kWords / 4; ++j) dst[j * CS] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 };
 
@@ -542,7 +545,7 @@ template <int NM>
 __device__ __forceinline__ void assemble_row_t(const FeatDev& fd, float px, float py, float pz,
                                                float dx, float dy, float dz, __half* row) {
   if constexpr (NM > 0) {
-    FastRow<NM>::build(fd, px, py, pz, row);
+    FastRow<NM>::template build<1>(fd, px, py, pz, row);
   } else {
     assemble_row(fd, px, py, pz, dx, dy, dz, row);
   }

@@ -15,6 +15,7 @@
 
 #include "fvsrn_kernels.cuh"
 #include "fvsrn_geometry.cuh"
+#include "fvsrn_march.cuh"
 
 namespace fvsrn {
 
@@ -64,152 +65,244 @@ __host__ __device__ constexpr int fast_kt0() {
 }
 
 // ---------------------------------------------------------------- DVR
-// NM > 0 / NL > 0: specialised input row (FastRow<NM>) and compile-time layer count
+// NM > 0 / NL > 0: specialised input row (FastRow<NM>) and compile-time layer count.
+// Persistent warps, 32 rays per warp; free lanes refill from a chunked global queue of
+// precomputed ray records (ray_setup_kernel), so the MMA tiles stay full.
 template <int HID, int ACT, int NM, int NL>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID>())
 dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
-           MarchDev md, CamDev cam, ShardDev sh, const double* __restrict__ rays_o,
-           const double* __restrict__ rays_d, long long n_slots, float* __restrict__ out,
-           unsigned long long* __restrict__ queue, unsigned long long* __restrict__ eval_count,
-           unsigned long long* __restrict__ nonfinite) {
+           MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+           float* __restrict__ out, unsigned long long* __restrict__ queue,
+           unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
   const int rs = fd.k0 + 8;
   uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
   stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
   const int lane = threadIdx.x & 31;
   const bool density = net.head == 0;
   const bool use_dir = fd.dir_mode != 0;
-  const float eps1 = md.eps1_f;
-  const float et = md.et_f;
   __half* myrow = stage + lane * rs;
-  // two-point TFs (the presets' grayscale) live in registers: no per-sample smem lookups
-  const bool tf_two = FVSRN_TF_REGS && density && tf->n == 2;
-  float tf0[4], tfk[4], tfx0 = 0.f;
-  if (tf_two) {
-    tfx0 = tf->xs[0];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) { tf0[c] = tf->val[0][c]; tfk[c] = tf->slope[0][c]; }
-  }
-
-  bool has = false;
-  int k = 0, n = 0;
-  long long oslot = 0;
-  // per-ray march state: first sample position pe and step vector dd, both rounded
-  // from the f64 geometry (render.py:224-225); p_k = pe + k * dd in f32
-  float pe0 = 0.f, pe1 = 0.f, pe2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f;
-  float dx = 0.f, dy = 0.f, dz = 0.f;
-  float dsf = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+  RayLane r;
+  r.has = false;
+  LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
-  long long chunk_base = 0;
-  int chunk_left = 0;
-  bool qdone = false;
 
   while (true) {
-    // ---- refill free lanes from the warp's chunk of the global work queue
-    while (true) {
-      unsigned need = __ballot_sync(0xffffffffu, !has);
-      if (need == 0) break;
-      if (chunk_left == 0) {
-        if (qdone) break;
-        unsigned long long cb = 0;
-        if (lane == 0) cb = atomicAdd(queue, 32ull);
-        cb = __shfl_sync(0xffffffffu, cb, 0);
-        if ((long long)cb >= n_slots) { qdone = true; break; }
-        chunk_base = (long long)cb;
-        chunk_left = (int)min(32ll, n_slots - (long long)cb);
-      }
-      const int rank = __popc(need & lanemask_lt());
-      const int take = min(__popc(need), chunk_left);
-      if (!has && rank < take) {
-        const long long qs = chunk_base + rank;
-        // queue position -> canonical slot (LPT order permutes whole tiles)
-        const long long s = (!rays_o && sh.order) ? ((long long)sh.order[qs >> 6] << 6) | (qs & 63) : qs;
-        RayGeom r;
-        bool valid = true;
-        long long dst;
-        if (rays_o) {
-          dst = s;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) { r.o[a] = rays_o[3 * s + a]; r.d[a] = rays_d[3 * s + a]; }
-        } else {
-          const int pix = slot_pixel(cam, sh, s);
-          dst = sh.compact ? s : pix;
-          if (pix < 0) {
-            valid = false;
-            if (sh.compact) *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else {
-            const int W = cam.W;
-            camera_dir(cam, pix % W, pix / W, r.d);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) r.o[a] = cam.eye[a];
-          }
-        }
-        if (valid) {
-          if (march_geometry(md, r)) {
-            has = true;
-            k = 0; n = r.n; oslot = dst;
-            const double t0 = __dadd_rn(r.tmin, __dmul_rn(0.5, r.ds));
-            pe0 = (float)__dadd_rn(r.o[0], __dmul_rn(t0, r.d[0]));
-            pe1 = (float)__dadd_rn(r.o[1], __dmul_rn(t0, r.d[1]));
-            pe2 = (float)__dadd_rn(r.o[2], __dmul_rn(t0, r.d[2]));
-            dd0 = (float)__dmul_rn(r.ds, r.d[0]);
-            dd1 = (float)__dmul_rn(r.ds, r.d[1]);
-            dd2 = (float)__dmul_rn(r.ds, r.d[2]);
-            dx = (float)r.d[0]; dy = (float)r.d[1]; dz = (float)r.d[2];
-            dsf = (float)r.ds;
-            C0 = C1 = C2 = A = 0.f;
-          } else {
-            *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
-          }
-        }
-      }
-      chunk_base += take;
-      chunk_left -= take;
-    }
-    const unsigned act = __ballot_sync(0xffffffffu, has);
+    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    const unsigned act = __ballot_sync(0xffffffffu, r.has);
     if (act == 0) break;
     evals += __popc(act);
-
-    // ---- sample position (render.py:224-225, f64) and input row
-    if (has) {
-      const float kf = (float)k;
-      const float px = fmaf(kf, dd0, pe0), py = fmaf(kf, dd1, pe1), pz = fmaf(kf, dd2, pe2);
-      assemble_row_t<NM>(fd, px, py, pz, use_dir ? dx : 0.f, use_dir ? dy : 0.f,
-                         use_dir ? dz : 0.f, myrow);
+    // ---- sample position p_k = pe + k * dd (render.py:224-225) and input row
+    if (r.has) {
+      const float kf = (float)r.k;
+      assemble_row_t<NM>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
+                         use_dir ? r.dx : 0.f, use_dir ? r.dy : 0.f, use_dir ? r.dz : 0.f, myrow);
     }
     __syncwarp();
     MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
-
     // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
-    if (has) {
-      const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
-      float r, g, b, sig;
-      if (tf_two) {
-        const float dx = fminf(fmaxf(sigmoidf_(o.x), 0.f), 1.f) - tfx0;
-        r = fmaf(tfk[0], dx, tf0[0]); g = fmaf(tfk[1], dx, tf0[1]);
-        b = fmaf(tfk[2], dx, tf0[2]); sig = fmaf(tfk[3], dx, tf0[3]);
-      } else if (density) {
-        tf_eval(*tf, sigmoidf_(o.x), r, g, b, sig);
+    if (r.has)
+      composite_step(r, *reinterpret_cast<const float4*>(ob + 4 * lane), density, *tf, md, out, nonfinite);
+  }
+  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+}
+
+// ---------------------------------------------------------------- ray setup
+// One thread per slot, canonical slot order: camera ray (render.py:72-94) or explicit ray,
+// slab test and march geometry (render.py:97-106, 189-200) in f64 with explicit _rn ops,
+// then the f32 first-sample position and step vector (render.py:224-225).  Rays that do
+// not march get their final pixel here (background, or zero for padding slots of compact
+// shards).  Optionally accumulates the per-64-slot-tile step count for the LPT order.
+__global__ void ray_setup_kernel(CamDev cam, MarchDev md, ShardDev sh, const double* __restrict__ rays_o,
+                                 const double* __restrict__ rays_d, long long n_slots, RayRecs rr,
+                                 float* __restrict__ out, unsigned* __restrict__ tile_cost,
+                                 unsigned* __restrict__ iota) {
+  for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
+       s += (long long)gridDim.x * blockDim.x) {
+    RayGeom g;
+    bool valid = true;
+    long long dst;
+    if (rays_o) {
+      dst = s;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { g.o[a] = rays_o[3 * s + a]; g.d[a] = rays_d[3 * s + a]; }
+    } else {
+      const int pix = slot_pixel(cam, sh, s);
+      dst = sh.compact ? s : pix;
+      if (pix < 0) {
+        valid = false;
+        if (sh.compact) *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        r = sigmoidf_(o.x); g = sigmoidf_(o.y); b = sigmoidf_(o.z); sig = softplusf_(o.w);
-      }
-      float alpha = 1.f - __expf(-sig * dsf);
-      alpha = fmaxf(fminf(alpha, eps1), 0.f);
-      const float tr = (1.f - A) * alpha;
-      C0 = fmaf(tr, r, C0); C1 = fmaf(tr, g, C1); C2 = fmaf(tr, b, C2);
-      A += tr;
-      ++k;
-      if (k >= n || A > et) {
-        const float om = 1.f - A;
-        const float4 px4 = make_float4(fmaf(om, md.bg[0], C0), fmaf(om, md.bg[1], C1),
-                                       fmaf(om, md.bg[2], C2), A);
-        *reinterpret_cast<float4*>(out + 4 * oslot) = px4;
-        // Image invariant (imaging.py:52-57) checked on the device: no host scan
-        if (nonfinite && !(isfinite(px4.x) && isfinite(px4.y) && isfinite(px4.z) && isfinite(px4.w)))
-          atomicAdd(nonfinite, 1ull);
-        has = false;
+        camera_dir(cam, pix % cam.W, pix / cam.W, g.d);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g.o[a] = cam.eye[a];
       }
     }
+    int n = 0;
+    float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
+    if (valid) {
+      if (march_geometry(md, g)) {
+        n = g.n;
+        const double t0 = __dadd_rn(g.tmin, __dmul_rn(0.5, g.ds));
+        ra.x = (float)__dadd_rn(g.o[0], __dmul_rn(t0, g.d[0]));
+        ra.y = (float)__dadd_rn(g.o[1], __dmul_rn(t0, g.d[1]));
+        ra.z = (float)__dadd_rn(g.o[2], __dmul_rn(t0, g.d[2]));
+        rb = make_float4((float)__dmul_rn(g.ds, g.d[0]), (float)__dmul_rn(g.ds, g.d[1]),
+                         (float)__dmul_rn(g.ds, g.d[2]), (float)g.ds);
+        if (rr.d) rr.d[s] = make_float4((float)g.d[0], (float)g.d[1], (float)g.d[2], 0.f);
+      } else {
+        *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
+      }
+    }
+    ra.w = __int_as_float(n);
+    rr.a[s] = ra;
+    rr.b[s] = rb;
+    if (tile_cost) {
+      // a warp covers 32 consecutive slots of one 64-slot tile (+4: refill/setup overhead)
+      const unsigned sum = __reduce_add_sync(0xffffffffu, n > 0 ? (unsigned)n + 4u : 0u);
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(tile_cost + (s >> 6), sum);
+        if ((s & 63) == 0) iota[s >> 6] = (unsigned)(s >> 6);
+      }
+    }
+  }
+}
+
+cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
+                             const double* rays_o, const double* rays_d, long long n_slots,
+                             const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
+                             cudaStream_t s) {
+  if (n_slots <= 0) return cudaSuccess;
+  // blocks of 256 keep the tile-cost warp reduction inside one 64-slot tile
+  const int blocks = (int)std::min<long long>((n_slots + 255) / 256, 148 * 32);
+  ray_setup_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, rays_o, rays_d, n_slots, rr, out, tile_cost, iota);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, void* scratch,
+                             size_t scratch_bytes, cudaStream_t s) {
+  // cost[0:n] keys, cost[n:2n] sorted keys, order[n:2n] iota -> order[0:n]
+  return cub::DeviceRadixSort::SortPairsDescending(scratch, scratch_bytes, cost, cost + n_local,
+                                                   order + n_local, order, n_local, 0, 32, s);
+}
+
+// ---------------------------------------------------------------- warp-specialised DVR
+// The per-sample pipeline has two halves with disjoint pipe profiles: the producer half
+// (ray refill, latent-grid gather + trilinear, Fourier features, head/TF/compositing/ET)
+// runs on the FMA/ALU/LSU pipes; the consumer half (the MLP: HMMA + one MUFU.COS per
+// hidden activation) saturates the XU pipe.  Run in the same warp they alternate in
+// bursts and stall each other (ncu: mio/math throttle).  Here each CTA holds 4
+// producer warps (0-3) and 4 consumer warps (4-7); producer w and consumer w+4 form a
+// pair on the same SM sub-partition.  The producer owns 64 rays (two groups of 32, one
+// per lane each) and ping-pongs two row buffers: while the consumer runs the MLP over
+// group g's rows, the producer composites group g^1's previous outputs and builds its
+// next rows.  One named barrier per pair is the rendezvous (both sides bar.sync, so a
+// phase can never be over-counted); a per-buffer control word says run / skip / exit.
+template <int HID, int ACT, int NM, int NL>
+__global__ void __launch_bounds__(kWsThreads, ws_min_blocks<HID>())
+dvr_ws_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+              MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+              float* __restrict__ out, unsigned long long* __restrict__ queue,
+              unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  const int rs = fd.k0 + 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* p = smem;
+  uint2* wf_s = reinterpret_cast<uint2*>(p);
+  p += ((size_t)net.w_total * sizeof(uint2) + 15) / 16 * 16;
+  float* b_s = reinterpret_cast<float*>(p);
+  p += ((size_t)net.b_total * sizeof(float) + 15) / 16 * 16;
+  TFDev* tf = reinterpret_cast<TFDev*>(p);
+  p += (sizeof(TFDev) + 15) / 16 * 16;
+  int* ctrl_all = reinterpret_cast<int*>(p);
+  p += 16 * sizeof(int);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp & (kWsPairs - 1);
+  const size_t buf_bytes = (size_t)kWarp * rs * sizeof(__half) + kWarp * 4 * sizeof(float);
+  unsigned char* pb = p + (size_t)pair * 2 * buf_bytes;
+  __half* st[2] = {reinterpret_cast<__half*>(pb), reinterpret_cast<__half*>(pb + buf_bytes)};
+  float* ob[2] = {reinterpret_cast<float*>(pb + (size_t)kWarp * rs * sizeof(__half)),
+                  reinterpret_cast<float*>(pb + buf_bytes + (size_t)kWarp * rs * sizeof(__half))};
+  volatile int* ctrl = ctrl_all + 2 * pair;
+
+  for (int i = threadIdx.x; i < net.w_total; i += blockDim.x) wf_s[i] = net.wfrag[i];
+  for (int i = threadIdx.x; i < net.b_total; i += blockDim.x) b_s[i] = net.bias[i];
+  if (b0) {
+    const int n0q = net.b_off[1] - net.b_off[0];
+    for (int i = threadIdx.x; i < n0q; i += blockDim.x) {
+      const int j = i >> 2;
+      b_s[i] = b0[(j >> 2) * 8 + 2 * (j & 3) + (i & 1)];
+    }
+  }
+  {
+    const int words = sizeof(TFDev) / 4;
+    const int* src = reinterpret_cast<const int*>(tf_g);
+    int* dst = reinterpret_cast<int*>(tf);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  if (warp < kWsPairs) {   // producer zeroes its pair's buffers (pad columns stay finite)
+    uint32_t* z = reinterpret_cast<uint32_t*>(pb);
+    for (int i = lane; i < (int)(2 * buf_bytes / 4); i += kWarp) z[i] = 0u;
+  }
+  __syncthreads();
+  const unsigned bar = 1 + pair;
+
+  if (warp >= kWsPairs) {
+    // ---------------- consumer: the MLP over whichever buffer the producer filled
+    for (int b = 0;; b ^= 1) {
+      named_bar_sync(bar, 2 * kWarp);
+      const int c = ctrl[b];
+      if (c < 0) break;
+      if (c > 0) MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(st[b], rs, net, wf_s, b_s, ob[b], lane);
+    }
+    return;
+  }
+
+  // ---------------- producer
+  const bool density = net.head == 0;
+  const bool use_dir = fd.dir_mode != 0;
+  RayLane g[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) g[i].has = false;
+  LaneQueue q{0, 0, false};
+  unsigned long long evals = 0;
+  bool act[2] = {false, false};
+
+  auto consume = [&](RayLane& r, const float* obuf) {
+    if (r.has) composite_step(r, *reinterpret_cast<const float4*>(obuf + 4 * lane), density, *tf, md, out, nonfinite);
+  };
+  // refill group i and write its next input rows; returns whether any lane is active
+  auto produce = [&](RayLane& r, __half* stage) -> bool {
+    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    const unsigned a = __ballot_sync(0xffffffffu, r.has);
+    evals += __popc(a);
+    if (r.has) {
+      const float kf = (float)r.k;
+      const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
+      assemble_row_t<NM>(fd, px, py, pz, use_dir ? r.dx : 0.f, use_dir ? r.dy : 0.f,
+                         use_dir ? r.dz : 0.f, stage + lane * rs);
+    }
+    __syncwarp();
+    return a != 0;
+  };
+
+  act[0] = produce(g[0], st[0]);
+  if (lane == 0) ctrl[0] = act[0] ? 1 : 0;
+  named_bar_sync(bar, 2 * kWarp);
+  act[1] = produce(g[1], st[1]);
+  if (lane == 0) ctrl[1] = act[1] ? 1 : 0;
+  named_bar_sync(bar, 2 * kWarp);
+  while (true) {
+    bool done = false;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (!done) {
+        if (act[b]) consume(g[b], ob[b]);
+        act[b] = produce(g[b], st[b]);
+        done = !act[0] && !act[1];   // queue drained, nothing in flight in either buffer
+        if (lane == 0) ctrl[b] = done ? -1 : (act[b] ? 1 : 0);
+        named_bar_sync(bar, 2 * kWarp);
+      }
+    }
+    if (done) break;
   }
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
@@ -379,6 +472,9 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
     if (kind == KernelKind::kDVR)                                                            \
       return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H)>               \
                   : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
+    if (kind == KernelKind::kDVRWS)                                                          \
+      return fast ? (const void*)dvr_ws_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
+                  : (const void*)dvr_ws_kernel<H, kActRuntime, 0, 0>;                        \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
                   : (const void*)sample_kernel<H, kActRuntime, 0, 0>;                        \

@@ -27,6 +27,17 @@ constexpr int min_blocks() {
   return HID <= 32 ? (DVR ? kMinBlocks : FVSRN_MIN_BLOCKS_SAMPLE) : (HID <= 64 ? FVSRN_MIN_BLOCKS_WIDE : 1);
 }
 
+// warp-specialised DVR: 4 producer + 4 consumer warps per CTA
+constexpr int kWsThreads = 256;
+constexpr int kWsPairs = 4;
+#ifndef FVSRN_WS_MIN_BLOCKS
+#define FVSRN_WS_MIN_BLOCKS 2
+#endif
+template <int HID>
+constexpr int ws_min_blocks() {
+  return HID <= 32 ? FVSRN_WS_MIN_BLOCKS : 1;
+}
+
 struct CamDev {
   double eye[3], fwd[3], right[3], up[3];
   double half_w, half_h;
@@ -39,7 +50,18 @@ struct ShardDev {
   const unsigned* order;   // work-queue order of local tiles (longest first), or nullptr
 };
 
-enum class KernelKind { kDVR, kSample, kFused };
+// Per-slot ray records written once per frame by ray_setup_kernel (the f64 ray setup of
+// render.py:72-106, 189-200 and the first-sample position / step vector of :224-225,
+// rounded to f32), so the march loops never run f64 code:
+//   a[s] = (pe.x, pe.y, pe.z, n as int bits)   n = 0: no march (pixel already written)
+//   b[s] = (dd.x, dd.y, dd.z, ds)              d[s] = (dir.x, dir.y, dir.z, 0), dir modes only
+struct RayRecs {
+  float4* a;
+  float4* b;
+  float4* d;
+};
+
+enum class KernelKind { kDVR, kDVRWS, kDVRTC, kSample, kFused };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).
@@ -51,6 +73,14 @@ cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const Shard
                               int n_local, unsigned* cost, unsigned* order, void* scratch,
                               size_t scratch_bytes, cudaStream_t s);
 size_t tile_order_scratch_bytes(int n_local);
+// Ray records for n_slots slots (camera rays of this shard, or explicit rays when
+// rays_o != nullptr); tile_cost/iota (may be null) receive the LPT keys / values.
+cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
+                             const double* rays_o, const double* rays_d, long long n_slots,
+                             const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
+                             cudaStream_t s);
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, void* scratch,
+                             size_t scratch_bytes, cudaStream_t s);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,
@@ -61,6 +91,14 @@ inline size_t stage_smem_bytes(const NetDev& net, bool with_tf, int k0) {
   if (with_tf) b += (sizeof(TFDev) + 15) / 16 * 16;
   const int rs = k0 + 8;
   b += (size_t)(kThreads / kWarp) * ((size_t)kWarp * rs * 2 + kWarp * 4 * 4);
+  return b;
+}
+
+inline size_t ws_smem_bytes(const NetDev& net, int k0) {
+  size_t b = ((size_t)net.w_total * 8 + 15) / 16 * 16 + ((size_t)net.b_total * 4 + 15) / 16 * 16;
+  b += (sizeof(TFDev) + 15) / 16 * 16 + 16 * sizeof(int);
+  const int rs = k0 + 8;
+  b += (size_t)kWsPairs * 2 * ((size_t)kWarp * rs * 2 + kWarp * 4 * 4);
   return b;
 }
 

@@ -1,0 +1,60 @@
+// fvsrn_tc.cuh -- shapes and shared-memory map of the tcgen05 DVR kernel (fvsrn_tc.cu).
+#pragma once
+#include "fvsrn_kernels.cuh"
+
+namespace fvsrn {
+
+constexpr int kTcThreads = 128;   // 4 warps = 128 rays = one M=128 UMMA tile
+
+// CTAs per SM the register budget is sized for (128 regs for 32-wide, 168 for 64-wide)
+#ifndef FVSRN_TC_MIN_BLOCKS
+#define FVSRN_TC_MIN_BLOCKS 4
+#endif
+#ifndef FVSRN_TC_MIN_BLOCKS_WIDE
+#define FVSRN_TC_MIN_BLOCKS_WIDE 3
+#endif
+template <int HID>
+constexpr int tc_min_blocks() {
+  return HID <= 32 ? FVSRN_TC_MIN_BLOCKS : FVSRN_TC_MIN_BLOCKS_WIDE;
+}
+
+// Weights of all layers, fp16, each layer an (N x K) K-major tile in the UMMA canonical
+// no-swizzle layout: element (n, k) at half index
+//   (n/8)*(K/8)*64 + (k/8)*64 + (n%8)*8 + (k%8)
+// with N = HID (hidden layers) or 16 (output layer, rows >= d_out zero) and K = K0
+// (layer 0) or HID.  Biases: f32, HID per layer, 16 for the output layer.
+struct TcNetDev {
+  const uint4* w;
+  const float* b;
+  int head;
+};
+
+__host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int HID, int NM, int NL>
+struct TcShape {
+  static constexpr int kK0 = tc_round(16 + 2 * NM + 3, 16);   // FastRow<NM>::kK0
+  static constexpr int kKA = kK0 > HID ? kK0 : HID;          // A tile width (halfs)
+  static constexpr int kNLast = 16;
+  static constexpr int kTCols = HID <= 32 ? 32 : (HID <= 64 ? 64 : 128);
+  static constexpr uint32_t kSboA = (uint32_t)(kKA / 8) * 128u;
+  static constexpr int w_off(int l) { return l == 0 ? 0 : HID * kK0 + (l - 1) * HID * HID; }
+  static constexpr int kWTotal = HID * kK0 + (NL - 2) * HID * HID + kNLast * HID;   // halfs
+  static constexpr int b_off(int l) { return l * HID; }
+  static constexpr int kBTotal = (NL - 1) * HID + kNLast;
+  // shared memory map (bytes)
+  static constexpr int kWOff = 0;
+  static constexpr int kBOff = tc_round(kWOff + kWTotal * 2, 16);
+  static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
+  static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
+  static constexpr int kMbarOff = kAOff + kTcThreads * kKA * 2;
+  static constexpr int kSmem = kMbarOff + 16;
+};
+
+// tcgen05 DVR kernel for the default fV-SRN shapes (hid 32: 4 layers, m=14; hid 64:
+// 6 layers, m=30), or nullptr.  Same argument list as dvr_kernel with TcNetDev first.
+const void* tc_kernel_for(int hid);
+size_t tc_smem_bytes(int hid);
+inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
+
+}  // namespace fvsrn

@@ -328,3 +328,16 @@ def shard_slots(width: int, height: int, world: int) -> tuple[int, int]:
     """(n_tiles, max_local_tiles * 64): compact per-rank buffer length in pixels."""
     n_tiles = math.ceil(width / 8) * math.ceil(height / 8)
     return n_tiles, math.ceil(n_tiles / world) * 64
+
+
+DVR_KERNELS = {"auto": 0, "tc": 1, "ws": 2, "warp": 3}
+
+
+def set_dvr_kernel(name: str) -> str:
+    """Select the DVR kernel for the default fV-SRN shapes ("auto", "tc" = tcgen05/TMEM,
+    "ws" = warp-specialised mma.sync, "warp" = single-role mma.sync); returns the previous
+    selection.  A measurement switch: every choice renders the same image within fp16
+    noise (tests/test_gpu_parity.py::test_dvr_kernel_variants)."""
+    prev = L.lib().fvsrn_set_dvr_kernel(DVR_KERNELS[name])
+    L.check(0 if prev >= 0 else prev)
+    return {v: k for k, v in DVR_KERNELS.items()}[prev]
