@@ -43,6 +43,11 @@ std::atomic<int> g_dvr_mode_i{[] {
   if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
   return (int)DvrMode::kAuto;
 }()};
+// tcgen05 kernel: two 128-ray tiles per CTA in ping-pong (FVSRN_TC_TILES=1: one tile)
+const bool g_tc_two_tiles = [] {
+  const char* e = std::getenv("FVSRN_TC_TILES");
+  return !(e && e[0] == '1');
+}();
 inline DvrMode dvr_mode() { return (DvrMode)g_dvr_mode_i.load(std::memory_order_relaxed); }
 bool use_tc(const fvsrn_model* m);
 
@@ -326,7 +331,7 @@ std::map<std::tuple<const void*, int, size_t>, int> g_occ;
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
-  const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad)
+  const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
                                                : kernel_for(kind, m->hid_pad, fast_path(m, kind));
   const int threads = kind == KernelKind::kDVRWS ? kWsThreads
                       : kind == KernelKind::kDVRTC ? kTcThreads : kThreads;
@@ -396,7 +401,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
     void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    return launch(m, KernelKind::kDVRTC, tc_smem_bytes(m->hid_pad), args, s, n_slots / 32 + 1);
+    return launch(m, KernelKind::kDVRTC, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
+                  g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1);
   }
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
   if (dvr_mode() == DvrMode::kWS)

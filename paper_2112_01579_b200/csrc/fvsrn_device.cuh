@@ -155,6 +155,21 @@ __device__ __forceinline__ float cos_poly(float a) {
   return fmaf(p, u, 0.9999644756317139f);
 }
 
+// snake_alt h = x - 2 cos x entirely on the FMA pipe (9 FP32 ops, no MUFU):
+// k = rint(x/2pi) by the 1.5*2^23 trick, r = x/2pi - k in [-1/2, 1/2] (one FFMA),
+// -2 cos(2 pi r) as a degree-4 minimax polynomial in r^2 (|err| < 9e-5), h = x + p.
+__device__ __forceinline__ float snake_alt_h_fma(float x) {
+  const float kb = fmaf(x, 0.15915494309189535f, 12582912.f);
+  const float k = kb - 12582912.f;
+  const float r = fmaf(x, 0.15915494309189535f, -k);
+  const float u = r * r;
+  float p = fmaf(-91.24539184570312f, u, 164.7942352294922f);
+  p = fmaf(p, u, -129.34727478027344f);
+  p = fmaf(p, u, 39.46232986450195f);
+  p = fmaf(p, u, -1.999928951263428f);
+  return x + p;
+}
+
 template <int ACT>
 __device__ __forceinline__ float act_h(float x);
 
@@ -470,6 +485,14 @@ struct FastRow {
   template <int CS = 1>
   __device__ static void build(const FeatDev& fd, float px, float py, float pz, __half* row) {
     uint32_t w[kWords];
+    words(fd, px, py, pz, w);
+    uint4* dst = reinterpret_cast<uint4*>(row);
+#pragma unroll
+    for (int j = 0; j < kWords / 4; ++j) dst[j * CS] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+
+  // the row as kWords packed fp16 pairs (column 2i in the low half of w[i])
+  __device__ static void words(const FeatDev& fd, float px, float py, float pz, uint32_t (&w)[kWords]) {
 #pragma unroll
     for (int i = 0; i < kWords; ++i) w[i] = 0u;
     // latent grid (grid.py:47-84), 16 channels = 2 x 16-byte corner chunks
@@ -534,9 +557,6 @@ struct FastRow {
     }
     w[8 + NM] = pack_half2(px, py);
     w[9 + NM] = pack_half2(pz, 0.f);
-    uint4* dst = reinterpret_cast<uint4*>(row);
-#pragma unroll
-    for (int j = 0; j < kWords / 4; ++j) dst[j * CS] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 };
 

@@ -50,6 +50,104 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
   else tmem_st_x64(taddr, v);
 }
 
+// Activation of element e of a row: every FVSRN_TC_POLY-th element evaluates its cosine
+// on the FMA pipe instead of the XU (MUFU) pipe.  The tcgen05 kernels are XU-bound in
+// their activation phases with issue slots to spare, so moving ~1/3 of the cosines
+// balances the two (0 disables).
+#ifndef FVSRN_TC_POLY
+#define FVSRN_TC_POLY 0
+#endif
+#ifndef FVSRN_TC_SPLIT
+#define FVSRN_TC_SPLIT 0
+#endif
+// hidden-layer A operands in TMEM (tcgen05.st of the packed activations, MMA reads A
+// from TMEM) instead of the shared-memory A tile: removes 2 x 128 B of shared-memory
+// traffic per sample and layer
+#ifndef FVSRN_TC_TMEM_A
+#define FVSRN_TC_TMEM_A 1
+#endif
+// layer-0 input rows in TMEM too (no shared-memory A tile at all): 1 on, 0 off,
+// 2 = 32-wide only (measured: faster at 32-wide, slower at 64-wide)
+#ifndef FVSRN_TC_TMEM_A0
+#define FVSRN_TC_TMEM_A0 2
+#endif
+// snake_alt activations of one accumulator row -> fp16 chunks of the A tile row
+// (chunk c = columns 8c..8c+7 at +128 B per chunk in the canonical layout)
+template <int HID>
+__device__ __forceinline__ void act_row(const uint32_t (&acc)[HID], __half* row) {
+  constexpr int P = FVSRN_TC_POLY;
+#pragma unroll
+  for (int c = 0; c < HID / 8; ++c) {
+    uint32_t w4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float h[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int e = 8 * c + 2 * j + i;       // compile-time after unrolling
+        const float x = __uint_as_float(acc[e]);
+        h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
+      }
+      w4[j] = pack_half2(h[0], h[1]);
+    }
+    *reinterpret_cast<uint4*>(row + c * 64) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
+// snake_alt activations of one accumulator row -> packed fp16 pairs (TMEM A operand)
+template <int HID>
+__device__ __forceinline__ void act_words(const uint32_t (&acc)[HID], uint32_t (&w)[HID / 2]) {
+  constexpr int P = FVSRN_TC_POLY;
+#pragma unroll
+  for (int j = 0; j < HID / 2; ++j) {
+    float h[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = 2 * j + i;
+      const float x = __uint_as_float(acc[e]);
+      h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
+    }
+    w[j] = pack_half2(h[0], h[1]);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_st_x16(taddr, r);
+  else if constexpr (N == 32) tmem_st_x32(taddr, r);
+  else tmem_st_x64(taddr, r);
+}
+
+// store N words (N = sum of powers of two from {32, 16, 8, 4}) at consecutive columns
+template <int N, int OFF = 0, int M>
+__device__ __forceinline__ void tmem_st_any(uint32_t taddr, const uint32_t (&r)[M]) {
+  if constexpr (N >= 32) {
+    uint32_t v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = r[OFF + i];
+    tmem_st_x32(taddr + OFF, v);
+    tmem_st_any<N - 32, OFF + 32>(taddr, r);
+  } else if constexpr (N >= 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = r[OFF + i];
+    tmem_st_x16(taddr + OFF, v);
+    tmem_st_any<N - 16, OFF + 16>(taddr, r);
+  } else if constexpr (N >= 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = r[OFF + i];
+    tmem_st_x8(taddr + OFF, v);
+    tmem_st_any<N - 8, OFF + 8>(taddr, r);
+  } else if constexpr (N >= 4) {
+    uint32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = r[OFF + i];
+    tmem_st_x4(taddr + OFF, v);
+    tmem_st_any<N - 4, OFF + 4>(taddr, r);
+  }
+}
+
 }  // namespace
 
 template <int HID, int NM, int NL>
@@ -81,7 +179,12 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     uint4* az = reinterpret_cast<uint4*>(a_s);   // pad columns must stay finite
     for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
   }
-  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), S::kTCols);
+  constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
+  // TMEM columns: D [0, kTCols), A [kTCols, kTCols + max(K0, HID)/2)
+  constexpr uint32_t kAcols = kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
+  constexpr uint32_t kNeed = S::kTCols + kAcols;
+  constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
+  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
   if (tid == 0) mbar_init(smem_u32(mbar), 1);
   tc_fence_before();
   __syncthreads();
@@ -104,13 +207,24 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
     tmem_bias<HID>(t_row, b_s + S::b_off(0));
-    if (r.has) {
+    if constexpr (kA0) {
+      // tcgen05.st is .sync.aligned: every lane stores (rays-less lanes a zero row)
+      uint32_t w[FastRow<NM>::kWords];
+      if (r.has) {
+        const float kf = (float)r.k;
+        FastRow<NM>::words(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2), w);
+      } else {
+#pragma unroll
+        for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
+      }
+      tmem_st_any<FastRow<NM>::kWords>(t_row + S::kTCols, w);
+    } else if (r.has) {
       const float kf = (float)r.k;
       FastRow<NM>::template build<8>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1),
                                      fmaf(kf, r.dd2, r.pe2), myrow);
     }
     tmem_wait_st();
-    fence_proxy_async_smem();
+    if constexpr (!kA0) fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
 #pragma unroll
@@ -123,29 +237,47 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
         const uint32_t id = idesc_f16(128, N);
 #pragma unroll
-        for (int kk = 0; kk < K / 16; ++kk)
-          umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA), smem_desc(wb + kk * 256u, 128u, sbo_b),
-                   id, 1u);
+        for (int kk = 0; kk < K / 16; ++kk) {
+          if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
+            umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+          else
+            umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
+                     smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+        }
         umma_commit(mb);
       }
       mbar_wait(mb, phase);
       phase ^= 1u;
       tc_fence_after();
       if (l < NL - 1) {
-        uint32_t acc[HID];
-        tmem_ld<HID>(t_row, acc);
-        tmem_wait_ld();
-        if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-        else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-        // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns
-#pragma unroll
-        for (int c = 0; c < HID / 8; ++c) {
-          uint32_t w4[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            w4[j] = pack_half2(act_h<4>(__uint_as_float(acc[8 * c + 2 * j])),
-                               act_h<4>(__uint_as_float(acc[8 * c + 2 * j + 1])));
-          *reinterpret_cast<uint4*>(myrow + c * 64) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
+        // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
+        if constexpr (FVSRN_TC_TMEM_A) {
+          uint32_t acc[HID];
+          tmem_ld<HID>(t_row, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          uint32_t w[HID / 2];
+          act_words<HID>(acc, w);
+          tmem_st<HID / 2>(t_row + S::kTCols, w);
+        } else if constexpr (FVSRN_TC_SPLIT && HID == 64) {
+          uint32_t acc[32];
+          tmem_ld<32>(t_row, acc);
+          tmem_wait_ld();
+          act_row<32>(acc, myrow);
+          tmem_ld<32>(t_row + 32, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_row<32>(acc, myrow + 4 * 64);
+        } else {
+          uint32_t acc[HID];
+          tmem_ld<HID>(t_row, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_row<HID>(acc, myrow);
         }
         tmem_wait_st();
         fence_proxy_async_smem();
@@ -165,21 +297,158 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, S::kTCols);
+  if (warp == 0) tmem_dealloc(tmem, kAlloc);
 }
 
-const void* tc_kernel_for(int hid) {
+// Two-tile ping-pong variant: every thread owns two rays (tile 0 row t, tile 1 row t),
+// with one A tile, one TMEM accumulator region and one mbarrier per tile.  While the
+// tensor core runs layer l+1 of one tile, the CTA evaluates the activations (XU pipe)
+// or composites / refills / builds the next rows (FMA/LSU pipes) of the other tile, so
+// the MMA round trip and the CTA barriers overlap useful work.
+template <int HID, int NM, int NL>
+__global__ void __launch_bounds__(kTcThreads, tc2_min_blocks<HID>())
+dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+               MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+               float* __restrict__ out, unsigned long long* __restrict__ queue,
+               unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  using S = TcShape<HID, NM, NL>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __half* w_s = reinterpret_cast<__half*>(smem + S::kWOff);
+  float* b_s = reinterpret_cast<float*>(smem + S::kBOff);
+  TFDev* tf = reinterpret_cast<TFDev*>(smem + S::kTFOff);
+  __half* a_s0 = reinterpret_cast<__half*>(smem + S::kAOff);
+  __half* a_s1 = reinterpret_cast<__half*>(smem + S::kAOff + S::kATile);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::kAOff + 2 * S::kATile);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kAOff + 2 * S::kATile + 16);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {
+    const uint4* src = net.w;
+    uint4* dst = reinterpret_cast<uint4*>(w_s);
+    for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
+    for (int i = tid; i < S::kBTotal; i += kTcThreads)
+      b_s[i] = (b0 && i < HID) ? b0[i] : net.b[i];
+    const int words = sizeof(TFDev) / 4;
+    const int* ts = reinterpret_cast<const int*>(tf_g);
+    int* td = reinterpret_cast<int*>(tf);
+    for (int i = tid; i < words; i += kTcThreads) td[i] = ts[i];
+    uint4* az = reinterpret_cast<uint4*>(a_s0);   // pad columns must stay finite
+    for (int i = tid; i < 2 * kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 2 * S::kTCols);
+  if (tid == 0) { mbar_init(smem_u32(mbar), 1); mbar_init(smem_u32(mbar + 1), 1); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t w_base = smem_u32(w_s);
+  const uint32_t a_base[2] = {smem_u32(a_s0), smem_u32(a_s1)};
+  const uint32_t mb[2] = {smem_u32(mbar), smem_u32(mbar + 1)};
+  const uint32_t t_d[2] = {tmem, tmem + (uint32_t)S::kTCols};               // accumulator columns
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;                     // this warp's lanes
+  const int row_off = (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
+  __half* myrow[2] = {a_s0 + row_off, a_s1 + row_off};
+  const bool density = net.head == 0;
+
+  RayLane r[2];
+  r[0].has = false;
+  r[1].has = false;
+  LaneQueue q{0, 0, false};
+  unsigned long long evals = 0;
+  uint32_t phase[2] = {0u, 0u};
+  bool live[2];
+
+  auto issue = [&](int l, int t) {
+    if (tid == 0) {
+      tc_fence_after();
+      const int K = l == 0 ? S::kK0 : HID;
+      const int N = l == NL - 1 ? S::kNLast : HID;
+      const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
+      const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
+      const uint32_t id = idesc_f16(128, N);
+#pragma unroll
+      for (int kk = 0; kk < K / 16; ++kk)
+        umma_f16(t_d[t], smem_desc(a_base[t] + kk * 256u, 128u, S::kSboA),
+                 smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+      umma_commit(mb[t]);
+    }
+  };
+  // refill tile t, pre-load its layer-0 bias, write its rows; returns (CTA-wide) whether
+  // the tile has any ray, after the fences + barrier that make the rows MMA-visible
+  auto start = [&](int t) -> bool {
+    ws_refill(r[t], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    evals += __popc(__ballot_sync(0xffffffffu, r[t].has));
+    tmem_bias<HID>(t_d[t] + lane_off, b_s + S::b_off(0));
+    if (r[t].has) {
+      const float kf = (float)r[t].k;
+      FastRow<NM>::template build<8>(fd, fmaf(kf, r[t].dd0, r[t].pe0), fmaf(kf, r[t].dd1, r[t].pe1),
+                                     fmaf(kf, r[t].dd2, r[t].pe2), myrow[t]);
+    }
+    tmem_wait_st();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    return __syncthreads_or(r[t].has) != 0;
+  };
+
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    live[t] = start(t);
+    if (live[t]) issue(0, t);
+  }
+  while (live[0] || live[1]) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (!live[t]) continue;
+        mbar_wait(mb[t], phase[t]);
+        phase[t] ^= 1u;
+        tc_fence_after();
+        const uint32_t t_row = t_d[t] + lane_off;
+        if (l < NL - 1) {
+          uint32_t acc[HID];
+          tmem_ld<HID>(t_row, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_row<HID>(acc, myrow[t]);
+          tmem_wait_st();
+          fence_proxy_async_smem();
+          tc_fence_before();
+          __syncthreads();
+          issue(l + 1, t);
+        } else {
+          uint32_t o[4];
+          tmem_ld_x4(t_row, o);
+          tmem_wait_ld();
+          if (r[t].has)
+            composite_step(r[t], make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
+                                             __uint_as_float(o[2]), __uint_as_float(o[3])),
+                           density, *tf, md, out, nonfinite);
+          live[t] = start(t);
+          if (live[t]) issue(0, t);
+        }
+      }
+    }
+  }
+  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 2 * S::kTCols);
+}
+
+const void* tc_kernel_for(int hid, bool two_tiles) {
   switch (hid) {
-    case 32: return (const void*)dvr_tc_kernel<32, 14, 4>;
-    case 64: return (const void*)dvr_tc_kernel<64, 30, 6>;
+    case 32: return two_tiles ? (const void*)dvr_tc2_kernel<32, 14, 4> : (const void*)dvr_tc_kernel<32, 14, 4>;
+    case 64: return two_tiles ? (const void*)dvr_tc2_kernel<64, 30, 6> : (const void*)dvr_tc_kernel<64, 30, 6>;
     default: return nullptr;
   }
 }
 
-size_t tc_smem_bytes(int hid) {
+size_t tc_smem_bytes(int hid, bool two_tiles) {
   switch (hid) {
-    case 32: return TcShape<32, 14, 4>::kSmem;
-    case 64: return TcShape<64, 30, 6>::kSmem;
+    case 32: return two_tiles ? TcShape<32, 14, 4>::kSmem2 : TcShape<32, 14, 4>::kSmem;
+    case 64: return two_tiles ? TcShape<64, 30, 6>::kSmem2 : TcShape<64, 30, 6>::kSmem;
     default: return 0;
   }
 }

@@ -17,6 +17,17 @@ template <int HID>
 constexpr int tc_min_blocks() {
   return HID <= 32 ? FVSRN_TC_MIN_BLOCKS : FVSRN_TC_MIN_BLOCKS_WIDE;
 }
+// two-tile variant (two rays per thread)
+#ifndef FVSRN_TC2_MIN_BLOCKS
+#define FVSRN_TC2_MIN_BLOCKS 3
+#endif
+#ifndef FVSRN_TC2_MIN_BLOCKS_WIDE
+#define FVSRN_TC2_MIN_BLOCKS_WIDE 2
+#endif
+template <int HID>
+constexpr int tc2_min_blocks() {
+  return HID <= 32 ? FVSRN_TC2_MIN_BLOCKS : FVSRN_TC2_MIN_BLOCKS_WIDE;
+}
 
 // Weights of all layers, fp16, each layer an (N x K) K-major tile in the UMMA canonical
 // no-swizzle layout: element (n, k) at half index
@@ -47,14 +58,17 @@ struct TcShape {
   static constexpr int kBOff = tc_round(kWOff + kWTotal * 2, 16);
   static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
   static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
-  static constexpr int kMbarOff = kAOff + kTcThreads * kKA * 2;
+  static constexpr int kATile = kTcThreads * kKA * 2;
+  static constexpr int kMbarOff = kAOff + kATile;
   static constexpr int kSmem = kMbarOff + 16;
+  static constexpr int kSmem2 = kAOff + 2 * kATile + 32;   // two-tile variant
 };
 
 // tcgen05 DVR kernel for the default fV-SRN shapes (hid 32: 4 layers, m=14; hid 64:
 // 6 layers, m=30), or nullptr.  Same argument list as dvr_kernel with TcNetDev first.
-const void* tc_kernel_for(int hid);
-size_t tc_smem_bytes(int hid);
+// two_tiles: the ping-pong variant (256 rays per CTA).
+const void* tc_kernel_for(int hid, bool two_tiles);
+size_t tc_smem_bytes(int hid, bool two_tiles);
 inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
 
 }  // namespace fvsrn

@@ -9,7 +9,7 @@ for ent in "$@"; do
     for p in "${parts[@]}"; do
       case "$p" in default) ;; *=*) envs+=("$p") ;; *) L=$p ;; esac
     done
-    env "${envs[@]}" FVSRN_LIB=$L python bench.py --config $c --no-cpu-baseline --no-e2e --steps 16 2>&1 | tail -1 | \
+    timeout 120 env "${envs[@]}" FVSRN_LIB=$L python bench.py --config $c --no-cpu-baseline --no-e2e --steps 16 2>&1 | tail -1 | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$ent', '$c', round(d['ms_per_step'],3), 'ms', round(d['value']/1e9,2), 'Gev/s', d['clocks'].get('sm_mhz'))" || echo "$ent $c FAILED"
   done
 done
