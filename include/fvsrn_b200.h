@@ -113,6 +113,10 @@ FVSRN_API int32_t fvsrn_device_count(void);
  * 0 auto (measured faster per width), 1 tcgen05/TMEM, 2 warp-specialised mma.sync,
  * 3 single-role mma.sync.  Returns the previous mode, or FVSRN_EINVAL. */
 FVSRN_API int32_t fvsrn_set_dvr_kernel(int32_t mode);
+/* Latent-grid sampler for 16-channel grids (measurement switch; env FVSRN_GRID sets the
+ * initial value): 0 auto, 1 texture units (RGBA16F 3D textures, hardware trilinear),
+ * 2 LDG.128 + HFMA2 trilinear.  Returns the previous mode, or FVSRN_EINVAL. */
+FVSRN_API int32_t fvsrn_set_grid_sampler(int32_t mode);
 
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
 FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);

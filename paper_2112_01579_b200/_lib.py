@@ -81,6 +81,7 @@ EXPORTS = {
     # name: (restype, argtypes)
     "fvsrn_last_error": (C.c_char_p, []),
     "fvsrn_set_dvr_kernel": (C.c_int32, [C.c_int32]),
+    "fvsrn_set_grid_sampler": (C.c_int32, [C.c_int32]),
     "fvsrn_version": (C.c_char_p, []),
     "fvsrn_device_count": (C.c_int32, []),
     "fvsrn_model_create": (C.c_int32, [C.POINTER(ModelDesc), C.c_int32, C.POINTER(C.c_void_p)]),

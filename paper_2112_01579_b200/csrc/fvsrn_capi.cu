@@ -1,3 +1,4 @@
+#include <array>
 #include <atomic>
 // fvsrn_capi.cu -- the C ABI (include/fvsrn_b200.h): model upload, weight/grid
 // packing, per-frame constants, kernel launches.  Host code only.
@@ -35,6 +36,10 @@ const bool g_lpt_enabled = [] {
 // (warp-specialised mma.sync) or warp (single-role mma.sync); unset = the measured
 // faster one per width (auto: tcgen05 for 64-wide, mma.sync for 32-wide).
 // Other shapes always run the mma.sync dvr_kernel.
+#ifndef FVSRN_TEX_DEFAULT
+#define FVSRN_TEX_DEFAULT 1
+#endif
+constexpr bool kTexDefault = FVSRN_TEX_DEFAULT != 0;
 enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3 };
 std::atomic<int> g_dvr_mode_i{[] {
   const char* e = std::getenv("FVSRN_DVR");
@@ -43,11 +48,20 @@ std::atomic<int> g_dvr_mode_i{[] {
   if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
   return (int)DvrMode::kAuto;
 }()};
-// tcgen05 kernel: two 128-ray tiles per CTA in ping-pong (FVSRN_TC_TILES=1: one tile)
+// tcgen05 kernel: one 128-ray tile per CTA (default, measured faster), or two tiles in
+// ping-pong (FVSRN_TC_TILES=2)
 const bool g_tc_two_tiles = [] {
   const char* e = std::getenv("FVSRN_TC_TILES");
-  return !(e && e[0] == '1');
+  return e && e[0] == '2';
 }();
+// latent-grid sampler for F = 16 grids: 0 auto, 1 texture units, 2 LDG + HFMA2
+std::atomic<int> g_grid_mode{[] {
+  const char* e = std::getenv("FVSRN_GRID");
+  if (e && std::string(e) == "tex") return 1;
+  if (e && std::string(e) == "ldg") return 2;
+  return 0;
+}()};
+bool use_tex(const fvsrn_model* m);
 inline DvrMode dvr_mode() { return (DvrMode)g_dvr_mode_i.load(std::memory_order_relaxed); }
 bool use_tc(const fvsrn_model* m);
 
@@ -143,6 +157,9 @@ struct fvsrn_model {
   uint4* d_wtc = nullptr;
   float* d_btc = nullptr;
   bool tc_ok = false;
+  // texture path (F padded to 16): per grid 4 RGBA16F 3D arrays + texture objects
+  std::vector<cudaArray_t> tex_arrays;
+  std::vector<std::array<cudaTextureObject_t, 4>> tex;
   int k0x = 0;
   std::vector<float> b0_static;     // layer-0 bias, padded N0
   std::vector<float> w0_time;       // N0 x T time columns of W0
@@ -155,6 +172,9 @@ struct fvsrn_model {
     cudaFree(ps.frag); cudaFree(ps.bias);
     cudaFree(px.frag); cudaFree(px.bias);
     cudaFree(d_wtc); cudaFree(d_btc);
+    for (auto& t4 : tex)
+      for (auto t : t4) cudaDestroyTextureObject(t);
+    for (auto a : tex_arrays) cudaFreeArray(a);
   }
 };
 
@@ -182,6 +202,40 @@ int make_devpack(const Pack& pk, int layers, int act, int head, int out_real, De
   for (int l = 0; l <= layers; ++l) { n.w_off[l] = pk.w_off[l]; n.b_off[l] = pk.b_off[l]; }
   n.w_total = (int)pk.frag.size();
   n.b_total = (int)pk.bias.size();
+  return FVSRN_OK;
+}
+
+// 4 RGBA16F 3D arrays (channels 4j..4j+3) of one fp16 (R,R,R,16) grid + texture objects
+// (linear filtering, clamp addressing, unnormalised coordinates).  Array width = grid z.
+int make_grid_textures(fvsrn_model* m, const std::vector<__half>& h) {
+  const int R = m->R;
+  const size_t nvox = (size_t)R * R * R;
+  std::array<cudaTextureObject_t, 4> t4{};
+  std::vector<__half> plane(nvox * 4);
+  for (int j = 0; j < 4; ++j) {
+    for (size_t v = 0; v < nvox; ++v)
+      for (int c = 0; c < 4; ++c) plane[v * 4 + c] = h[v * 16 + 4 * j + c];
+    cudaChannelFormatDesc cd = cudaCreateChannelDescHalf4();
+    cudaArray_t arr = nullptr;
+    CUDA_TRY(cudaMalloc3DArray(&arr, &cd, make_cudaExtent(R, R, R)));
+    m->tex_arrays.push_back(arr);
+    cudaMemcpy3DParms cp{};
+    cp.srcPtr = make_cudaPitchedPtr(plane.data(), (size_t)R * 4 * sizeof(__half), R, R);
+    cp.dstArray = arr;
+    cp.extent = make_cudaExtent(R, R, R);
+    cp.kind = cudaMemcpyHostToDevice;
+    CUDA_TRY(cudaMemcpy3D(&cp));
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeArray;
+    rd.res.array.array = arr;
+    cudaTextureDesc td{};
+    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModeLinear;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    CUDA_TRY(cudaCreateTextureObject(&t4[j], &rd, &td, nullptr));
+  }
+  m->tex.push_back(t4);
   return FVSRN_OK;
 }
 
@@ -248,10 +302,20 @@ int build_tf(const fvsrn_tf* tf, TFDev& th) {
 struct FrameScratch {
   void* buf = nullptr;
   const __half* grid = nullptr;
+  bool tex_on = false;
+  float tex_w = 0.f;
+  const cudaTextureObject_t* tex_lo = nullptr;
+  const cudaTextureObject_t* tex_hi = nullptr;
   float* b0 = nullptr;
   TFDev* tf = nullptr;
   unsigned long long* counters = nullptr;   // [0] queue, [1] evals, [2] non-finite pixels
 };
+
+bool use_tex(const fvsrn_model* m) {
+  if (m->tex.empty()) return false;
+  const int g = g_grid_mode.load(std::memory_order_relaxed);
+  return g == 1 || (g == 0 && kTexDefault);
+}
 
 // Per-call device scratch: effective layer-0 bias (time folded), TF table,
 // counters, and the time-blended latent grid.  Stream-ordered allocation.
@@ -275,9 +339,15 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
   size_t grid_bytes = 0;
   int lo = 0, hi = 0;
   double w = 0.0;
+  fs.tex_on = use_tex(m);
   if (m->f_pad > 0 && m->temporal) {
     bracket(m->kf_times, t, lo, hi, w);
-    if (hi != lo) grid_bytes = (size_t)m->R * m->R * m->R * m->f_pad * sizeof(__half);
+    if (hi != lo && !fs.tex_on) grid_bytes = (size_t)m->R * m->R * m->R * m->f_pad * sizeof(__half);
+  }
+  if (fs.tex_on) {   // keyframe blend happens in the kernel (two texture sets)
+    fs.tex_lo = m->tex[m->temporal ? lo : 0].data();
+    fs.tex_hi = m->tex[m->temporal ? hi : 0].data();
+    fs.tex_w = (m->temporal && hi != lo) ? (float)w : 0.f;
   }
   const size_t off_tf = 0, off_b0 = (sizeof(TFDev) + 255) / 256 * 256;
   const size_t off_ct = off_b0 + 1024, off_grid = off_ct + 256;
@@ -299,8 +369,12 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
   return FVSRN_OK;
 }
 
-FeatDev feat_for(const fvsrn_model* m, const __half* grid) {
+FeatDev feat_for(const fvsrn_model* m, const FrameScratch& fs) {
   FeatDev fd{};
+  const __half* grid = fs.grid;
+  fd.tex_on = fs.tex_on ? 1 : 0;
+  fd.tex_w = fs.tex_w;
+  for (int j = 0; j < 4 && fs.tex_on; ++j) { fd.tex_lo[j] = fs.tex_lo[j]; fd.tex_hi[j] = fs.tex_hi[j]; }
   fd.grid_res = m->R;
   fd.f_pad = m->f_pad;
   fd.grid = grid;
@@ -472,6 +546,11 @@ extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
 
+int32_t fvsrn_set_grid_sampler(int32_t mode) {
+  if (mode < 0 || mode > 2) return fail(FVSRN_EINVAL, "grid sampler mode must be 0..2");
+  return g_grid_mode.exchange(mode);
+}
+
 int32_t fvsrn_set_dvr_kernel(int32_t mode) {
   if (mode < 0 || mode > 3) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..3");
   return g_dvr_mode_i.exchange(mode);
@@ -592,6 +671,7 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       int rc = upload(h.data(), h.size() * sizeof(__half), (void**)&dg);
       if (rc) return rc;
       m->grids.push_back(dg);
+      if (m->f_pad == 16 && (rc = make_grid_textures(m, h))) return rc;
     }
   }
   // ---- weights: sample pack (device column order, time columns folded out) ...
@@ -760,7 +840,7 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
       CUDA_TRY(cudaMemsetAsync(d_out + local_tiles * 64 * 4, 0, (max_local - local_tiles) * 64 * 16, s));
   }
   NetDev net = m->ps.net;
-  FeatDev fd = feat_for(m, fs.grid);
+  FeatDev fd = feat_for(m, fs);
   MarchDev md = march_for(st);
   // per-slot ray records (f64 setup once per ray, outside the march loop) and the LPT
   // schedule: longest tiles first (removes the persistent kernel's long-ray tail)
@@ -869,7 +949,7 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   FrameScratch fs;
   if ((rc = frame_setup(m, t, tf, sg.s, fs))) return rc;
   NetDev net = m->ps.net;
-  FeatDev fd = feat_for(m, fs.grid);
+  FeatDev fd = feat_for(m, fs);
   MarchDev md = march_for(st);
   CamDev cam{};
   ShardDev sh{};
@@ -923,7 +1003,7 @@ static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64
   int rc = frame_setup(m, t, nullptr, sg.s, fs);
   if (rc) return rc;
   NetDev net = m->ps.net;
-  FeatDev fd = feat_for(m, fs.grid);
+  FeatDev fd = feat_for(m, fs);
   const float* b0 = fs.b0;
   int mode = 1, res = 0;
   double step = 0;
@@ -962,7 +1042,7 @@ int32_t fvsrn_decode_density_device(fvsrn_model_t m, int32_t res, double t, int6
   int rc = frame_setup(m, t, nullptr, s, fs);
   if (rc) return rc;
   NetDev net = m->ps.net;
-  FeatDev fd = feat_for(m, fs.grid);
+  FeatDev fd = feat_for(m, fs);
   const float* b0 = fs.b0;
   int mode = 0;
   double step = 1.0 / (double)(res - 1);

@@ -50,6 +50,11 @@ struct FeatDev {              // how a lane builds its input row (device column 
   const float* bmat;          // random mode B (m, fd_in) f32 (device)
   int four_off, raw_off, raw_w, k0;  // column offsets (halfs)
   int dir_mode;               // 0 pos, 1 dirP, 2 dirF
+  // texture path (FastRow, F = 16): 4 RGBA16F 3D textures per grid, trilinear filtering
+  // in the texture units; temporal models blend the bracketing keyframes (weight tex_w)
+  int tex_on;
+  float tex_w;
+  unsigned long long tex_lo[4], tex_hi[4];
 };
 
 struct TFDev {
@@ -495,8 +500,27 @@ struct FastRow {
   __device__ static void words(const FeatDev& fd, float px, float py, float pz, uint32_t (&w)[kWords]) {
 #pragma unroll
     for (int i = 0; i < kWords; ++i) w[i] = 0u;
-    // latent grid (grid.py:47-84), 16 channels = 2 x 16-byte corner chunks
-    {
+    // latent grid (grid.py:47-84), 16 channels
+    if (fd.tex_on) {
+      // texture units: unnormalised coordinates, texel centres at i + 1/2, clamp
+      // addressing (== the reference's clamp of p and of i0 <= R-2); array width is the
+      // grid's z axis (fastest in memory), depth its x axis
+      const float s = (float)(fd.grid_res - 1);
+      const float tz = fmaf(fminf(fmaxf(px, 0.f), 1.f), s, 0.5f);
+      const float ty = fmaf(fminf(fmaxf(py, 0.f), 1.f), s, 0.5f);
+      const float tx = fmaf(fminf(fmaxf(pz, 0.f), 1.f), s, 0.5f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 v = tex3D<float4>(fd.tex_lo[j], tx, ty, tz);
+        if (fd.tex_w != 0.f) {
+          const float4 u = tex3D<float4>(fd.tex_hi[j], tx, ty, tz);
+          v.x = fmaf(fd.tex_w, u.x - v.x, v.x); v.y = fmaf(fd.tex_w, u.y - v.y, v.y);
+          v.z = fmaf(fd.tex_w, u.z - v.z, v.z); v.w = fmaf(fd.tex_w, u.w - v.w, v.w);
+        }
+        w[2 * j] = pack_half2(v.x, v.y);
+        w[2 * j + 1] = pack_half2(v.z, v.w);
+      }
+    } else {
       const int R = fd.grid_res;
       const float s = (float)(R - 1);
       const float rm2 = (float)(R - 2);

@@ -341,3 +341,15 @@ def set_dvr_kernel(name: str) -> str:
     prev = L.lib().fvsrn_set_dvr_kernel(DVR_KERNELS[name])
     L.check(0 if prev >= 0 else prev)
     return {v: k for k, v in DVR_KERNELS.items()}[prev]
+
+
+GRID_SAMPLERS = {"auto": 0, "tex": 1, "ldg": 2}
+
+
+def set_grid_sampler(name: str) -> str:
+    """Latent-grid sampler for 16-channel grids: "tex" (texture units, hardware trilinear
+    with 8-bit fractional weights), "ldg" (LDG.128 + HFMA2 trilinear) or "auto"; returns
+    the previous selection."""
+    prev = L.lib().fvsrn_set_grid_sampler(GRID_SAMPLERS[name])
+    L.check(0 if prev >= 0 else prev)
+    return {v: k for k, v in GRID_SAMPLERS.items()}[prev]

@@ -268,14 +268,18 @@ def test_model_vs_dense_decode_on_gpu():
     assert P.metric_psnr(img_model, img_dec) > 40.0
 
 
+@pytest.mark.parametrize("sampler", ["tex", "ldg"])
 @pytest.mark.parametrize("kernel", ["tc", "ws", "warp"])
-@pytest.mark.parametrize("tag", ["cfg1_v1_peaks_bg", "cfg2_v2_gray", "cfg3_v0_gray_48", "inside_gray"])
-def test_dvr_kernel_variants(kernel, tag):
-    """Every DVR kernel (tcgen05/TMEM, warp-specialised and single-role mma.sync) renders
-    the reference image (PSNR >= 40 dB) with the reference's evaluated-sample count."""
+@pytest.mark.parametrize("tag", ["cfg1_v1_peaks_bg", "cfg2_v2_gray", "cfg3_v0_gray_48", "inside_gray",
+                                 "temporal_t6.5"])
+def test_dvr_kernel_variants(kernel, tag, sampler):
+    """Every DVR kernel (tcgen05/TMEM, warp-specialised and single-role mma.sync) with
+    either latent-grid sampler (texture units / LDG + HFMA2) renders the reference image
+    (PSNR >= 40 dB) with the reference's evaluated-sample count."""
     from paper_2112_01579_b200 import device as D
 
     prev = D.set_dvr_kernel(kernel)
+    prev_s = D.set_grid_sampler(sampler)
     try:
         r = meta()["renders"][tag]
         src = P.ModelSource(_model(RENDER_MODEL[tag]), P.TF_PRESETS[r["tf"]], t=r["t"])
@@ -291,6 +295,27 @@ def test_dvr_kernel_variants(kernel, tag):
         assert src2.last_eval_count == int(arrays()["rays_fib0_n"].sum())
     finally:
         D.set_dvr_kernel(prev)
+        D.set_grid_sampler(prev_s)
+
+
+@pytest.mark.parametrize("sampler", ["tex", "ldg"])
+def test_grid_sampler_density_and_decode(sampler):
+    """Per-sample densities (static and temporal) and the lattice decode through each
+    latent-grid sampler stay within the north-star tolerance of the reference."""
+    from paper_2112_01579_b200 import device as D
+
+    prev = D.set_grid_sampler(sampler)
+    try:
+        for name in ("cfg1", "cfg2", "cfg3"):
+            got = P.eval_density(_model(name), arrays()["eval_p"])
+            assert np.abs(got - arrays()[f"density_{name}"]).max() <= DENS_TOL, name
+        for tt in (1.0, 6.5, 16.25, 30.0):
+            got = P.eval_density(_model("temporal"), arrays()["eval_p"], t=tt)
+            assert np.abs(got - arrays()[f"density_temporal_t{tt}"]).max() <= DENS_TOL, tt
+        v = P.decode_volume(_model("cfg1"), 17).values
+        assert np.abs(v - arrays()["decode_cfg1_17"]).max() <= DENS_TOL
+    finally:
+        D.set_grid_sampler(prev)
 
 
 @pytest.mark.parametrize("kernel", ["tc", "warp"])
