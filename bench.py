@@ -272,7 +272,6 @@ def main():
     res = cfg["res"]
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-    launches_per_step = 1
 
     if cfg["kind"] == "dvr":
         src = P.ModelSource(model, P.TF_PRESETS["grayscale"], t=t_frame, use_fused=True)
@@ -280,7 +279,6 @@ def main():
         settings = P.RenderSettings(stepsize=cfg["stepsize"])
         if world > 1:
             renderer = TileShardRenderer(src)
-            launches_per_step = 1 + (1 if rank == 0 else 0)
 
             def step(i, count_ptr=None):
                 renderer.dm.render_device(src.tf, cams[i % 8], settings, t_frame,
@@ -300,8 +298,6 @@ def main():
             def step(i, count_ptr=None):
                 src.device_model.render_device(src.tf, cams[i % 8], settings, t_frame,
                                                frame.data_ptr(), count_ptr, stream.cuda_stream)
-        if t_frame is not None:
-            launches_per_step += 1          # per-frame keyframe pre-blend
     else:  # decode: lattice split in contiguous slabs across ranks
         total = res ** 3
         per = -(-total // world)
@@ -334,11 +330,14 @@ def main():
     total_evals = sum(evals_per_step)
 
     # ---- timed region
+    from paper_2112_01579_b200 import device as DEV
+
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    DEV.kernel_timer(True)      # CUDA events around the dominant kernel, launch counts
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
             flush.zero_()                      # evict the L2 (outside the events)
@@ -348,6 +347,8 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    dom_ms, dom_launches, lib_launches = DEV.kernel_timer_read()
+    DEV.kernel_timer(False)
     per_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = torch.tensor([sum(per_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -365,12 +366,13 @@ def main():
                 fb = P.pinned_empty((res, res, 4))
                 for i in range(2):
                     P.render_image(src, cams[i % 8], settings, out=fb)
-                t0 = time.perf_counter()
-                n_e = 0
-                for i in range(args.steps):
-                    P.render_image(src, cams[i % 8], settings, out=fb)
-                    n_e += src.last_eval_count
-                dt = time.perf_counter() - t0
+                with ClockSampler(local) as e2e_clocks:
+                    t0 = time.perf_counter()
+                    n_e = 0
+                    for i in range(args.steps):
+                        P.render_image(src, cams[i % 8], settings, out=fb)
+                        n_e += src.last_eval_count
+                    dt = time.perf_counter() - t0
                 h2d = 4356 + 4 * 32
                 d2h = res * res * 16 + 8
             else:
@@ -401,9 +403,11 @@ def main():
             n_e = max(2, args.steps // 4) * res ** 3
             h2d, d2h = 4 * 32, res ** 3 * 4
         e2e = {"value": n_e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+               **({"clocks": e2e_clocks.summary()} if cfg["kind"] == "dvr" and world == 1 else {}),
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * dt / args.steps
                if cfg["kind"] == "dvr" else 1e3 * dt / max(2, args.steps // 4),
-               "api": "render_image(ModelSource, out=pinned framebuffer) -> fvsrn_render"
+               "api": "render_image(ModelSource, out=pinned framebuffer) -> fvsrn_render "
+                      "(mapped page-locked framebuffer: the kernel stores pixels over PCIe)"
                if cfg["kind"] == "dvr" else "decode_volume(out=pinned) -> fvsrn_decode_density"}
 
     if rank != 0:
@@ -412,8 +416,19 @@ def main():
         return
 
     peak, peak_src = measured_peaks()
-    achieved = total_evals * flops / (tot_ms / 1e3) / 1e12
+    # rank 0's dominant-kernel time (the march / decode kernel alone, CUDA events on its
+    # stream); its algorithmic FLOPs are rank 0's share of the evaluations
+    rank0_evals = total_evals / world
+    achieved = rank0_evals * flops / (dom_ms / 1e3) / 1e12
     traffic, ncu = ncu_traffic(args.config)
+    mc = cfg["model"]
+    mufu_per_eval = (mc["layers"] - 1) * mc["hidden"] + 6 + 2
+    sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+    xu_peak = 16 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6
+    xu_achieved = rank0_evals * mufu_per_eval / (dom_ms / 1e3)
+    kernel_name = {"cfg3": "dvr_tc_kernel<64,30,6> (tcgen05/TMEM)",
+                   "cfg4": "sample_kernel<32,4,14,4> (mma.sync)"}.get(
+        args.config, "dvr_kernel<32,4,14,4> (mma.sync)")
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -429,9 +444,14 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "flops_per_eval": flops, "peak_source": peak_src,
-                     "note": "dominant kernel dvr_kernel; MUFU/FMA pipes bind first at c=32 "
-                             "(see profiles/)", **({"ncu": ncu} if ncu else {})},
-        "gpu_launches": launches_per_step * args.steps,
+                     "kernel": kernel_name, "kernel_ms_per_launch": dom_ms / max(1, dom_launches),
+                     "kernel_share_of_step": dom_ms / tot_ms if world == 1 else None,
+                     "xu_pipe": {"mufu_per_eval": mufu_per_eval, "achieved_Gops": xu_achieved / 1e9,
+                                 "peak_Gops": xu_peak / 1e9, "frac": xu_achieved / xu_peak,
+                                 "note": "MUFU (16/clk/SM) is the binding pipe: one cos per "
+                                         "hidden activation; see DESIGN.md section 4"},
+                     **({"ncu": ncu} if ncu else {})},
+        "gpu_launches": lib_launches,
         "clocks": clocks.summary(),
     }
     if e2e is not None:

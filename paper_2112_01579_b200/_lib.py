@@ -82,6 +82,9 @@ EXPORTS = {
     "fvsrn_last_error": (C.c_char_p, []),
     "fvsrn_set_dvr_kernel": (C.c_int32, [C.c_int32]),
     "fvsrn_set_grid_sampler": (C.c_int32, [C.c_int32]),
+    "fvsrn_kernel_timer": (C.c_int32, [C.c_int32]),
+    "fvsrn_kernel_timer_read": (C.c_int32, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int64)]),
     "fvsrn_version": (C.c_char_p, []),
     "fvsrn_device_count": (C.c_int32, []),
     "fvsrn_model_create": (C.c_int32, [C.POINTER(ModelDesc), C.c_int32, C.POINTER(C.c_void_p)]),

@@ -62,8 +62,36 @@ std::atomic<int> g_grid_mode{[] {
   return 0;
 }()};
 bool use_tex(const fvsrn_model* m);
+// render straight into mapped page-locked framebuffers (FVSRN_ZERO_COPY=0: copy instead)
+const bool g_zero_copy = [] {
+  const char* e = std::getenv("FVSRN_ZERO_COPY");
+  return !(e && e[0] == '0');
+}();
+// device alias of a mapped page-locked host buffer (fvsrn_host_alloc), else nullptr
+float* mapped_device_ptr(void* host) {
+  if (!g_zero_copy) return nullptr;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+      pa.devicePointer)
+    return (float*)pa.devicePointer;
+  cudaGetLastError();
+  return nullptr;
+}
 inline DvrMode dvr_mode() { return (DvrMode)g_dvr_mode_i.load(std::memory_order_relaxed); }
 bool use_tc(const fvsrn_model* m);
+
+// Per-thread kernel timer (fvsrn_kernel_timer): CUDA events around every launch of the
+// dominant kernel (the march / decode kernel) and a count of all library launches.
+struct KernelTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t used = 0;
+  long long launches = 0;
+};
+thread_local KernelTimer g_kt;
+void count_launch() {
+  if (g_kt.on) ++g_kt.launches;
+}
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -364,6 +392,7 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
     __half* g = (__half*)(base + off_grid);
     CUDA_TRY(launch_blend(m->grids[lo], m->grids[hi], (float)w,
                           (long long)m->R * m->R * m->R * m->f_pad, g, s));
+    count_launch();
     fs.grid = g;
   }
   return FVSRN_OK;
@@ -443,7 +472,20 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   long long blocks = (long long)m->num_sms * occ;
   const long long need = (work_warps + (threads / 32) - 1) / (threads / 32);
   if (need < blocks) blocks = std::max(1ll, need);
+  std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+  if (g_kt.on && kind != KernelKind::kFused) {
+    if (g_kt.used == g_kt.ev.size()) {
+      std::pair<cudaEvent_t, cudaEvent_t> p;
+      CUDA_TRY(cudaEventCreate(&p.first));
+      CUDA_TRY(cudaEventCreate(&p.second));
+      g_kt.ev.push_back(p);
+    }
+    ev = &g_kt.ev[g_kt.used++];
+    CUDA_TRY(cudaEventRecord(ev->first, s));
+  }
   CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, s));
+  count_launch();
+  if (ev) CUDA_TRY(cudaEventRecord(ev->second, s));
   return FVSRN_OK;
 }
 
@@ -546,6 +588,29 @@ extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
 
+int32_t fvsrn_kernel_timer(int32_t enable) {
+  g_kt.on = enable != 0;
+  g_kt.used = 0;
+  g_kt.launches = 0;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_kernel_timer_read(double* dominant_ms, int64_t* dominant_launches, int64_t* total_launches) {
+  double ms = 0.0;
+  for (size_t i = 0; i < g_kt.used; ++i) {
+    CUDA_TRY(cudaEventSynchronize(g_kt.ev[i].second));
+    float e = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&e, g_kt.ev[i].first, g_kt.ev[i].second));
+    ms += e;
+  }
+  if (dominant_ms) *dominant_ms = ms;
+  if (dominant_launches) *dominant_launches = (int64_t)g_kt.used;
+  if (total_launches) *total_launches = g_kt.launches;
+  g_kt.used = 0;
+  g_kt.launches = 0;
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_set_grid_sampler(int32_t mode) {
   if (mode < 0 || mode > 2) return fail(FVSRN_EINVAL, "grid sampler mode must be 0..2");
   return g_grid_mode.exchange(mode);
@@ -643,6 +708,12 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) return fail(FVSRN_ECUDA, "sm_100a device required");
     m->num_sms = prop.multiProcessorCount;
+    // per-frame scratch (ray records, framebuffers) comes from the stream-ordered pool;
+    // keep freed blocks cached instead of unmapping them at every synchronisation
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
   if (m->fourier_mode == FVSRN_FOURIER_RANDOM) {
     int rc = upload(d->b_matrix, sizeof(float) * m->m * m->fd_in, (void**)&m->d_bmat);
@@ -851,19 +922,18 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
   const bool use_lpt = local_tiles >= 2 * m->num_sms && g_lpt_enabled;
   unsigned* cost = nullptr;
   unsigned* order = nullptr;
-  size_t sb = 0;
   if (use_lpt) {
     const int nl = (int)local_tiles;
-    sb = tile_order_scratch_bytes(nl);
-    CUDA_TRY(cudaMallocAsync(&lpt, 16 * (size_t)nl + sb + 256, s));
+    CUDA_TRY(cudaMallocAsync(&lpt, 8 * (size_t)nl + 256, s));
     cost = (unsigned*)lpt;
-    order = cost + 2 * (size_t)nl;
+    order = cost + (size_t)nl;
     CUDA_TRY(cudaMemsetAsync(cost, 0, sizeof(unsigned) * nl, s));
   }
-  CUDA_TRY(launch_ray_setup(cam, md, sh, nullptr, nullptr, n_slots, rr, d_out, cost,
-                            order ? order + local_tiles : nullptr, s));
+  CUDA_TRY(launch_ray_setup(cam, md, sh, nullptr, nullptr, n_slots, rr, d_out, cost, nullptr, s));
+  count_launch();
   if (use_lpt) {
-    CUDA_TRY(launch_tile_sort((int)local_tiles, cost, order, (char*)lpt + 16 * (size_t)local_tiles, sb, s));
+    CUDA_TRY(launch_tile_sort((int)local_tiles, cost, order, s));
+    count_launch();
     sh.order = order;
   }
   const TFDev* tfp = fs.tf;
@@ -886,6 +956,7 @@ int32_t fvsrn_tiles_to_frame_device(const float* d_gathered, int32_t width, int3
                                     int32_t world, float* d_frame, void* stream) {
   if (!d_gathered || !d_frame || world < 1) return fail(FVSRN_EINVAL, "bad argument");
   CUDA_TRY(launch_tiles_to_frame(d_gathered, width, height, world, d_frame, (cudaStream_t)stream));
+  count_launch();
   return FVSRN_OK;
 }
 
@@ -910,17 +981,23 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
   const size_t bytes = (size_t)c->width * c->height * 16;
+  // A mapped page-locked framebuffer (fvsrn_host_alloc) is written by the kernels
+  // directly over PCIe: each pixel is stored once when its ray ends, so the transfer
+  // overlaps the march instead of following it.  Otherwise render to HBM and copy.
+  float* mapped = mapped_device_ptr(out);
   float* d_out = nullptr;
   unsigned long long* d_cnt = nullptr;
-  CUDA_TRY(cudaMallocAsync(&d_out, bytes + 16, sg.s));
-  d_cnt = (unsigned long long*)((char*)d_out + bytes);
+  void* dbuf = nullptr;
+  CUDA_TRY(cudaMallocAsync(&dbuf, (mapped ? 0 : bytes) + 16, sg.s));
+  d_out = mapped ? mapped : (float*)dbuf;
+  d_cnt = (unsigned long long*)((char*)dbuf + (mapped ? 0 : bytes));
   CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 16, sg.s));
   int rc = render_impl(m, tf, c, st, t, nullptr, d_out, d_cnt, d_cnt + 1, sg.s);
-  if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  if (rc) { cudaFreeAsync(dbuf, sg.s); cudaStreamSynchronize(sg.s); return rc; }
   unsigned long long cnt[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
+  if (!mapped) CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
-  CUDA_TRY(cudaFreeAsync(d_out, sg.s));
+  CUDA_TRY(cudaFreeAsync(dbuf, sg.s));
   CUDA_TRY(cudaStreamSynchronize(sg.s));
   if (eval_count) *eval_count = cnt[0];
   if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
@@ -961,6 +1038,7 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   void* recs = nullptr;
   if ((rc = alloc_recs(m, n_slots, sg.s, rr, recs))) return rc;
   CUDA_TRY(launch_ray_setup(cam, md, sh, d_o, d_d, n_slots, rr, d_out, nullptr, nullptr, sg.s));
+  count_launch();
   int explicit_rays = 1;
   unsigned long long* queue = fs.counters;
   unsigned long long* evc = fs.counters + 1;
@@ -1010,7 +1088,8 @@ static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64
   long long begin = 0, count = n;
   const double* pp = d_p;
   const double* pd = d_d;
-  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out};
+  unsigned long long* bad = nullptr;
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &bad};
   const size_t smem = stage_smem_bytes(net, false, m->k0);
   if ((rc = launch(m, KernelKind::kSample, smem, args, sg.s, n / 32 + 1))) return rc;
   CUDA_TRY(cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
@@ -1029,15 +1108,24 @@ int32_t fvsrn_eval_color(fvsrn_model_t m, const double* p, const double* d, int6
   return eval_common(m, p, d, n, t, out4, FVSRN_HEAD_COLOR);
 }
 
+static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_begin,
+                       int64_t lattice_count, float* d_out, unsigned long long* d_bad, cudaStream_t s);
+
 int32_t fvsrn_decode_density_device(fvsrn_model_t m, int32_t res, double t, int64_t lattice_begin,
                                     int64_t lattice_count, float* d_out, void* stream) {
+  return decode_impl(m, res, t, lattice_begin, lattice_count, d_out, nullptr, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_begin,
+                       int64_t lattice_count, float* d_out, unsigned long long* d_bad, cudaStream_t s) {
   if (!m || !d_out) return fail(FVSRN_EINVAL, "null argument");
   if (m->head != FVSRN_HEAD_DENSITY) return fail(FVSRN_EINVAL, "decode_volume requires a density-head model");
   if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
   if (!m->temporal && !std::isnan(t)) return fail(FVSRN_EINVAL, "timestep supplied to a non-temporal model");
   if (m->temporal && std::isnan(t)) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
   CUDA_TRY(cudaSetDevice(m->device));
-  cudaStream_t s = (cudaStream_t)stream;
   FrameScratch fs;
   int rc = frame_setup(m, t, nullptr, s, fs);
   if (rc) return rc;
@@ -1049,12 +1137,14 @@ int32_t fvsrn_decode_density_device(fvsrn_model_t m, int32_t res, double t, int6
   long long begin = lattice_begin, count = lattice_count;
   const double* pp = nullptr;
   const double* pd = nullptr;
-  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out};
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad};
   const size_t smem = stage_smem_bytes(net, false, m->k0);
   if ((rc = launch(m, KernelKind::kSample, smem, args, s, count / 32 + 1))) return rc;
   CUDA_TRY(cudaFreeAsync(fs.buf, s));
   return FVSRN_OK;
 }
+
+extern "C" {
 
 int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out) {
   if (!m || !out) return fail(FVSRN_EINVAL, "null argument");
@@ -1062,20 +1152,32 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
   const long long count = (long long)res * res * res;
-  float* d_out = nullptr;
-  CUDA_TRY(cudaMallocAsync(&d_out, count * sizeof(float), sg.s));
-  int rc = fvsrn_decode_density_device(m, res, t, 0, count, d_out, sg.s);
-  if (rc) { cudaFreeAsync(d_out, sg.s); cudaStreamSynchronize(sg.s); return rc; }
-  CUDA_TRY(cudaMemcpyAsync(out, d_out, count * sizeof(float), cudaMemcpyDeviceToHost, sg.s));
-  CUDA_TRY(cudaFreeAsync(d_out, sg.s));
+  // mapped page-locked output: the decode kernel's coalesced stores go straight to host
+  float* mapped = mapped_device_ptr(out);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, (mapped ? 0 : count * sizeof(float)) + 16, sg.s));
+  float* d_out = mapped ? mapped : (float*)buf;
+  unsigned long long* d_bad = (unsigned long long*)(buf + (mapped ? 0 : count * sizeof(float)));
+  CUDA_TRY(cudaMemsetAsync(d_bad, 0, 8, sg.s));
+  int rc = decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s);
+  if (rc) {
+    cudaFreeAsync(buf, sg.s);
+    cudaStreamSynchronize(sg.s);
+    return rc;
+  }
+  unsigned long long bad = 0;
+  if (!mapped) CUDA_TRY(cudaMemcpyAsync(out, d_out, count * sizeof(float), cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
   CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (bad) return fail(FVSRN_EINVAL, "volume contains non-finite values");
   return FVSRN_OK;
 }
 
 int32_t fvsrn_host_alloc(uint64_t bytes, void** ptr) {
   if (!ptr) return fail(FVSRN_EINVAL, "null argument");
   *ptr = nullptr;
-  CUDA_TRY(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+  CUDA_TRY(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped));
   return FVSRN_OK;
 }
 
@@ -1171,11 +1273,10 @@ int volume_render_impl(fvsrn_volume_t v, const fvsrn_tf* tf, const fvsrn_camera*
     }
     if (local_tiles >= 2 * v->num_sms && g_lpt_enabled) {
       const int nl = (int)local_tiles;
-      const size_t sb = tile_order_scratch_bytes(nl);
-      CUDA_TRY(cudaMallocAsync(&lpt, 16 * (size_t)nl + sb + 256, s));
+      CUDA_TRY(cudaMallocAsync(&lpt, 12 * (size_t)nl + 256, s));
       unsigned* cost = (unsigned*)lpt;
-      unsigned* order = cost + 2 * (size_t)nl;
-      CUDA_TRY(launch_tile_order(cam, md, sh, nl, cost, order, (char*)lpt + 16 * (size_t)nl, sb, s));
+      unsigned* order = cost + (size_t)nl;
+      CUDA_TRY(launch_tile_order(cam, md, sh, nl, cost, order, s));
       sh.order = order;
     }
   }

@@ -11,7 +11,6 @@
 //   fused_eval_kernel head(mlp(x)) from assembled inputs              fused.py:281-301
 //   blend_grid_kernel per-frame keyframe pre-blend (trilinear is linear) model.py:219-233
 //   tiles_to_frame    reassembles gathered screen-tile shards (multi-GPU)
-#include <cub/cub.cuh>
 
 #include "fvsrn_kernels.cuh"
 #include "fvsrn_geometry.cuh"
@@ -162,7 +161,7 @@ __global__ void ray_setup_kernel(CamDev cam, MarchDev md, ShardDev sh, const dou
       const unsigned sum = __reduce_add_sync(0xffffffffu, n > 0 ? (unsigned)n + 4u : 0u);
       if ((threadIdx.x & 31) == 0) {
         atomicAdd(tile_cost + (s >> 6), sum);
-        if ((s & 63) == 0) iota[s >> 6] = (unsigned)(s >> 6);
+        if (iota && (s & 63) == 0) iota[s >> 6] = (unsigned)(s >> 6);
       }
     }
   }
@@ -179,11 +178,43 @@ cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardD
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, void* scratch,
-                             size_t scratch_bytes, cudaStream_t s) {
-  // cost[0:n] keys, cost[n:2n] sorted keys, order[n:2n] iota -> order[0:n]
-  return cub::DeviceRadixSort::SortPairsDescending(scratch, scratch_bytes, cost, cost + n_local,
-                                                   order + n_local, order, n_local, 0, 32, s);
+// LPT order: local tiles by descending cost, as a one-CTA counting sort over 1024 cost
+// buckets (cost >> shift, shift from the maximum).  Approximate within a bucket, which
+// is all a longest-first schedule needs; one launch instead of a multi-pass radix sort.
+__global__ void __launch_bounds__(1024) lpt_bucket_sort_kernel(const unsigned* __restrict__ cost, int n,
+                                                               unsigned* __restrict__ order) {
+  __shared__ unsigned hist[1024];
+  __shared__ unsigned cmax;
+  const int t = threadIdx.x;
+  hist[t] = 0;
+  if (t == 0) cmax = 0;
+  __syncthreads();
+  unsigned m = 0;
+  for (int i = t; i < n; i += 1024) m = max(m, cost[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((t & 31) == 0) atomicMax(&cmax, m);
+  __syncthreads();
+  int shift = 0;
+  while ((cmax >> shift) >= 1024u) ++shift;
+  for (int i = t; i < n; i += 1024) atomicAdd(&hist[1023 - (cost[i] >> shift)], 1u);
+  __syncthreads();
+  // exclusive scan of the 1024 bucket counts (Hillis-Steele in shared memory)
+  unsigned v = hist[t];
+  for (int off = 1; off < 1024; off <<= 1) {
+    __syncthreads();
+    const unsigned add = t >= off ? hist[t - off] : 0u;
+    __syncthreads();
+    hist[t] += add;
+  }
+  __syncthreads();
+  hist[t] -= v;
+  __syncthreads();
+  for (int i = t; i < n; i += 1024) order[atomicAdd(&hist[1023 - (cost[i] >> shift)], 1u)] = (unsigned)i;
+}
+
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s) {
+  lpt_bucket_sort_kernel<<<1, 1024, 0, s>>>(cost, n_local, order);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- warp-specialised DVR
@@ -330,26 +361,16 @@ __global__ void tile_cost_kernel(CamDev cam, MarchDev md, ShardDev sh, long long
   }
 }
 
-size_t tile_order_scratch_bytes(int n_local) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const unsigned*)nullptr,
-                                            (unsigned*)nullptr, (const unsigned*)nullptr,
-                                            (unsigned*)nullptr, n_local);
-  return bytes;
-}
-
 cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
-                              int n_local, unsigned* cost, unsigned* order, void* scratch,
-                              size_t scratch_bytes, cudaStream_t s) {
-  // cost[0:n] keys, cost[n:2n] sorted keys, order[0:n] values, order[n:2n] iota
+                              int n_local, unsigned* cost, unsigned* order, cudaStream_t s) {
+  // cost[0:n] keys, order[0:n] tile indices (longest first)
   cudaError_t e = cudaMemsetAsync(cost, 0, sizeof(unsigned) * n_local, s);
   if (e != cudaSuccess) return e;
   const long long n_slots = (long long)n_local * 64;
   const int blocks = (int)std::min<long long>((n_slots + 255) / 256, 148 * 16);
   tile_cost_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, n_slots, cost, order + n_local);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  return cub::DeviceRadixSort::SortPairsDescending(scratch, scratch_bytes, cost, cost + n_local,
-                                                   order + n_local, order, n_local, 0, 32, s);
+  return launch_tile_sort(n_local, cost, order, s);
 }
 
 // ---------------------------------------------------------------- decode / eval
@@ -358,7 +379,8 @@ template <int HID, int ACT, int NM, int NL>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID, false>())
 sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, int res, double step,
               long long begin, long long count, const double* __restrict__ pos,
-              const double* __restrict__ dirs, float* __restrict__ out) {
+              const double* __restrict__ dirs, float* __restrict__ out,
+              unsigned long long* __restrict__ bad) {
   const int rs = fd.k0 + 8;
   uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
   stage_setup(net, b0, nullptr, rs, wf_s, b_s, tf, stage, ob);
@@ -392,7 +414,10 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
     if (valid) {
       const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
       if (density) {
-        out[i] = sigmoidf_(o.x);
+        const float v = sigmoidf_(o.x);
+        out[i] = v;
+        // ScalarVolume invariant (volume.py:41-49) checked on the device: finite, in [0,1]
+        if (bad && !(v >= 0.f && v <= 1.f)) atomicAdd(bad, 1ull);
       } else {
         *reinterpret_cast<float4*>(out + 4 * i) =
             make_float4(sigmoidf_(o.x), sigmoidf_(o.y), sigmoidf_(o.z), softplusf_(o.w));

@@ -70,17 +70,15 @@ int fast_layer_count(int hid_pad);
 // LPT schedule: exact per-tile step counts (same f64 geometry as the renderer), then
 // local tiles sorted by descending cost.  `order` receives n_local tile indices.
 cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
-                              int n_local, unsigned* cost, unsigned* order, void* scratch,
-                              size_t scratch_bytes, cudaStream_t s);
-size_t tile_order_scratch_bytes(int n_local);
+                              int n_local, unsigned* cost, unsigned* order, cudaStream_t s);
 // Ray records for n_slots slots (camera rays of this shard, or explicit rays when
 // rays_o != nullptr); tile_cost/iota (may be null) receive the LPT keys / values.
 cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
                              const double* rays_o, const double* rays_d, long long n_slots,
                              const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
                              cudaStream_t s);
-cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, void* scratch,
-                             size_t scratch_bytes, cudaStream_t s);
+// order[0:n] <- local tiles by (bucketed) descending cost[0:n]; one launch
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,

@@ -353,3 +353,15 @@ def set_grid_sampler(name: str) -> str:
     prev = L.lib().fvsrn_set_grid_sampler(GRID_SAMPLERS[name])
     L.check(0 if prev >= 0 else prev)
     return {v: k for k, v in GRID_SAMPLERS.items()}[prev]
+
+
+def kernel_timer(enable: bool = True) -> None:
+    """Start (reset) / stop the calling thread's dominant-kernel timer."""
+    L.check(L.lib().fvsrn_kernel_timer(1 if enable else 0))
+
+
+def kernel_timer_read() -> tuple[float, int, int]:
+    """(dominant-kernel ms, its launches, all library launches) since the last read."""
+    ms, n, tot = C.c_double(), C.c_int64(), C.c_int64()
+    L.check(L.lib().fvsrn_kernel_timer_read(C.byref(ms), C.byref(n), C.byref(tot)))
+    return ms.value, n.value, tot.value

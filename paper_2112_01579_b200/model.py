@@ -188,7 +188,8 @@ def decode_volume(model: FvsrnModel, resolution: int, t: float | None = None, ch
     if model.config.head != "density":
         raise ValueError("decode_volume requires a density-head model")
     vals = _device(model).decode(resolution, t, out=None if out is None else out.reshape(-1))
-    return ScalarVolume(values=vals.reshape((resolution,) * 3))
+    # finite / [0,1] (volume.py:41-49) was checked in the decode kernel (ValueError above)
+    return ScalarVolume._validated(vals.reshape((resolution,) * 3))
 
 
 # ------------------------------------------------------------------ footprint + checkpoints

@@ -26,6 +26,15 @@ class ScalarVolume:
             raise ValueError("volume values must lie in [0,1]")
         object.__setattr__(self, "values", v)
 
+    @classmethod
+    def _validated(cls, values: np.ndarray) -> "ScalarVolume":
+        """Wrap float32 (X,Y,Z) values whose invariants (finite, in [0,1]) were already
+        checked on the device by the decode kernel: no second pass over the host copy."""
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "values", values)
+        object.__setattr__(obj, "f32_range", None)
+        return obj
+
     @property
     def dims(self):
         return self.values.shape
