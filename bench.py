@@ -245,6 +245,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--grid-precision", default="f16", choices=["f16", "u8"],
+                    help="u8: the latent grid round-trips through a u8 .fvsrn checkpoint "
+                         "(grid_quantize, grid.py:157-166) and is sampled as 8-bit codes")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -267,6 +270,12 @@ def main():
 
     cfg = CONFIGS[args.config]
     model = P.model_init(P.ModelConfig(**cfg["model"]))
+    if args.grid_precision == "u8":
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as td:
+            P.checkpoint_save(model, Path(td) / "m.fvsrn", "f16", "u8")
+            model = P.checkpoint_load(Path(td) / "m.fvsrn")
     flops = mlp_flops(cfg["model"])
     t_frame = cfg.get("t")
     res = cfg["res"]
@@ -440,7 +449,7 @@ def main():
                    "ms_per_frame_median": statistics.median(per_ms),
                    "l2": "flushed before every frame (256 MiB memset, outside the events)",
                    "parallelism": f"screen-tile dp{world}" if world > 1 else "1 GPU",
-                   "tf": "grayscale", "t": t_frame},
+                   "tf": "grayscale", "t": t_frame, "grid_precision": args.grid_precision},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "flops_per_eval": flops, "peak_source": peak_src,

@@ -117,6 +117,14 @@ FVSRN_API int32_t fvsrn_set_dvr_kernel(int32_t mode);
  * initial value): 0 auto, 1 texture units (RGBA16F 3D textures, hardware trilinear),
  * 2 LDG.128 + HFMA2 trilinear.  Returns the previous mode, or FVSRN_EINVAL. */
 FVSRN_API int32_t fvsrn_set_grid_sampler(int32_t mode);
+/* Measurement hooks (bench.py): per calling thread, CUDA events around every launch of
+ * the dominant kernel (march / decode) and a count of all library kernel launches.
+ * fvsrn_kernel_timer(1) enables and resets; _read synchronizes the recorded events and
+ * returns the summed dominant-kernel time, its launch count and the total launch count
+ * since the last read, then resets. */
+FVSRN_API int32_t fvsrn_kernel_timer(int32_t enable);
+FVSRN_API int32_t fvsrn_kernel_timer_read(double* dominant_ms, int64_t* dominant_launches,
+                                          int64_t* total_launches);
 
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
 FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);

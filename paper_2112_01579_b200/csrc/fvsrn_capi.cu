@@ -1,3 +1,4 @@
+#include <type_traits>
 #include <array>
 #include <atomic>
 // fvsrn_capi.cu -- the C ABI (include/fvsrn_b200.h): model upload, weight/grid
@@ -188,6 +189,9 @@ struct fvsrn_model {
   // texture path (F padded to 16): per grid 4 RGBA16F 3D arrays + texture objects
   std::vector<cudaArray_t> tex_arrays;
   std::vector<std::array<cudaTextureObject_t, 4>> tex;
+  // u8 grids: the textures hold the codes; per-grid per-channel dequantisation
+  bool tex_u8 = false;
+  std::vector<std::array<float, 16>> qmin, qspan;
   int k0x = 0;
   std::vector<float> b0_static;     // layer-0 bias, padded N0
   std::vector<float> w0_time;       // N0 x T time columns of W0
@@ -235,20 +239,22 @@ int make_devpack(const Pack& pk, int layers, int act, int head, int out_real, De
 
 // 4 RGBA16F 3D arrays (channels 4j..4j+3) of one fp16 (R,R,R,16) grid + texture objects
 // (linear filtering, clamp addressing, unnormalised coordinates).  Array width = grid z.
-int make_grid_textures(fvsrn_model* m, const std::vector<__half>& h) {
+template <typename T>
+int make_grid_textures_t(fvsrn_model* m, const std::vector<T>& h, int F) {
   const int R = m->R;
   const size_t nvox = (size_t)R * R * R;
   std::array<cudaTextureObject_t, 4> t4{};
-  std::vector<__half> plane(nvox * 4);
+  std::vector<T> plane(nvox * 4);
+  const bool u8 = std::is_same<T, uint8_t>::value;
   for (int j = 0; j < 4; ++j) {
     for (size_t v = 0; v < nvox; ++v)
-      for (int c = 0; c < 4; ++c) plane[v * 4 + c] = h[v * 16 + 4 * j + c];
-    cudaChannelFormatDesc cd = cudaCreateChannelDescHalf4();
+      for (int c = 0; c < 4; ++c) plane[v * 4 + c] = (4 * j + c < F) ? h[v * F + 4 * j + c] : T(0);
+    cudaChannelFormatDesc cd = u8 ? cudaCreateChannelDesc<uchar4>() : cudaCreateChannelDescHalf4();
     cudaArray_t arr = nullptr;
     CUDA_TRY(cudaMalloc3DArray(&arr, &cd, make_cudaExtent(R, R, R)));
     m->tex_arrays.push_back(arr);
     cudaMemcpy3DParms cp{};
-    cp.srcPtr = make_cudaPitchedPtr(plane.data(), (size_t)R * 4 * sizeof(__half), R, R);
+    cp.srcPtr = make_cudaPitchedPtr(plane.data(), (size_t)R * 4 * sizeof(T), R, R);
     cp.dstArray = arr;
     cp.extent = make_cudaExtent(R, R, R);
     cp.kind = cudaMemcpyHostToDevice;
@@ -259,13 +265,15 @@ int make_grid_textures(fvsrn_model* m, const std::vector<__half>& h) {
     cudaTextureDesc td{};
     td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
     td.filterMode = cudaFilterModeLinear;
-    td.readMode = cudaReadModeElementType;
+    td.readMode = u8 ? cudaReadModeNormalizedFloat : cudaReadModeElementType;   // u8: code/255
     td.normalizedCoords = 0;
     CUDA_TRY(cudaCreateTextureObject(&t4[j], &rd, &td, nullptr));
   }
   m->tex.push_back(t4);
   return FVSRN_OK;
 }
+
+int make_grid_textures(fvsrn_model* m, const std::vector<__half>& h) { return make_grid_textures_t(m, h, 16); }
 
 std::vector<__half> to_half_padded(const float* src, int R, int F, int f_pad) {
   const size_t nvox = (size_t)R * R * R;
@@ -334,6 +342,7 @@ struct FrameScratch {
   float tex_w = 0.f;
   const cudaTextureObject_t* tex_lo = nullptr;
   const cudaTextureObject_t* tex_hi = nullptr;
+  int q_lo = 0, q_hi = 0;           // grid indices (u8 dequantisation constants)
   float* b0 = nullptr;
   TFDev* tf = nullptr;
   unsigned long long* counters = nullptr;   // [0] queue, [1] evals, [2] non-finite pixels
@@ -375,6 +384,8 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
   if (fs.tex_on) {   // keyframe blend happens in the kernel (two texture sets)
     fs.tex_lo = m->tex[m->temporal ? lo : 0].data();
     fs.tex_hi = m->tex[m->temporal ? hi : 0].data();
+    fs.q_lo = m->temporal ? lo : 0;
+    fs.q_hi = m->temporal ? hi : 0;
     fs.tex_w = (m->temporal && hi != lo) ? (float)w : 0.f;
   }
   const size_t off_tf = 0, off_b0 = (sizeof(TFDev) + 255) / 256 * 256;
@@ -404,6 +415,12 @@ FeatDev feat_for(const fvsrn_model* m, const FrameScratch& fs) {
   fd.tex_on = fs.tex_on ? 1 : 0;
   fd.tex_w = fs.tex_w;
   for (int j = 0; j < 4 && fs.tex_on; ++j) { fd.tex_lo[j] = fs.tex_lo[j]; fd.tex_hi[j] = fs.tex_hi[j]; }
+  fd.tex_u8 = (fs.tex_on && m->tex_u8) ? 1 : 0;
+  if (fd.tex_u8)
+    for (int c = 0; c < 16; ++c) {
+      fd.qmin_lo[c] = m->qmin[fs.q_lo][c]; fd.qspan_lo[c] = m->qspan[fs.q_lo][c];
+      fd.qmin_hi[c] = m->qmin[fs.q_hi][c]; fd.qspan_hi[c] = m->qspan[fs.q_hi][c];
+    }
   fd.grid_res = m->R;
   fd.f_pad = m->f_pad;
   fd.grid = grid;
@@ -742,7 +759,24 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       int rc = upload(h.data(), h.size() * sizeof(__half), (void**)&dg);
       if (rc) return rc;
       m->grids.push_back(dg);
-      if (m->f_pad == 16 && (rc = make_grid_textures(m, h))) return rc;
+      if (m->f_pad == 16) {
+        if (d->grid_precision == FVSRN_GRID_U8) {
+          // sample the 8-bit codes directly: RGBA8 textures + in-kernel
+          // dequantisation with the per-channel (min, max) of grid.py:157-172
+          std::vector<uint8_t> codes(d->grid_codes[gi], d->grid_codes[gi] + nvals);
+          if ((rc = make_grid_textures_t(m, codes, m->F))) return rc;
+          std::array<float, 16> mn{}, sp{};
+          for (int c = 0; c < m->F; ++c) {
+            mn[c] = d->grid_mins[gi][c];
+            sp[c] = d->grid_maxs[gi][c] - d->grid_mins[gi][c];
+          }
+          m->qmin.push_back(mn);
+          m->qspan.push_back(sp);
+          m->tex_u8 = true;
+        } else if ((rc = make_grid_textures(m, h))) {
+          return rc;
+        }
+      }
     }
   }
   // ---- weights: sample pack (device column order, time columns folded out) ...

@@ -55,6 +55,10 @@ struct FeatDev {              // how a lane builds its input row (device column 
   int tex_on;
   float tex_w;
   unsigned long long tex_lo[4], tex_hi[4];
+  // u8-quantised grids (grid.py:157-172): RGBA8 textures read as code/255, dequantised
+  // per channel in the kernel, v = min + (code/255) * (max - min)
+  int tex_u8;
+  float qmin_lo[16], qspan_lo[16], qmin_hi[16], qspan_hi[16];
 };
 
 struct TFDev {
@@ -173,6 +177,28 @@ __device__ __forceinline__ float snake_alt_h_fma(float x) {
   p = fmaf(p, u, 39.46232986450195f);
   p = fmaf(p, u, -1.999928951263428f);
   return x + p;
+}
+
+// sin(2 pi r), cos(2 pi r) for r in [-1/2, 1/2] on the FMA pipe: degree-5 least-
+// squares-minimax polynomials in u = r^2 (|err| < 1.3e-6, MUFU.SIN/COS-class accuracy).
+// 12 FP32 ops instead of FMUL.RZ + MUFU.SIN + MUFU.COS: the DVR path is XU-bound, so
+// the NeRF base angles move to the FMA pipe (FVSRN_FOURIER_POLY=0 restores MUFU).
+#ifndef FVSRN_FOURIER_POLY
+#define FVSRN_FOURIER_POLY 1
+#endif
+__device__ __forceinline__ void sincos_turns(float r, float& s, float& c) {
+  const float u = r * r;
+  float pc = fmaf(-21.0767765045166f, u, 58.794036865234375f);
+  pc = fmaf(pc, u, -85.27239990234375f);
+  pc = fmaf(pc, u, 64.92872619628906f);
+  pc = fmaf(pc, u, -19.738983154296875f);
+  c = fmaf(pc, u, 0.9999992251396179f);
+  float ps = fmaf(-12.473666191101074f, u, 41.34439468383789f);
+  ps = fmaf(ps, u, -76.61480712890625f);
+  ps = fmaf(ps, u, 81.5999755859375f);
+  ps = fmaf(ps, u, -41.341590881347656f);
+  ps = fmaf(ps, u, 6.283185005187988f);
+  s = ps * r;
 }
 
 template <int ACT>
@@ -512,8 +538,20 @@ struct FastRow {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float4 v = tex3D<float4>(fd.tex_lo[j], tx, ty, tz);
+        if (fd.tex_u8) {
+          v.x = fmaf(v.x, fd.qspan_lo[4 * j], fd.qmin_lo[4 * j]);
+          v.y = fmaf(v.y, fd.qspan_lo[4 * j + 1], fd.qmin_lo[4 * j + 1]);
+          v.z = fmaf(v.z, fd.qspan_lo[4 * j + 2], fd.qmin_lo[4 * j + 2]);
+          v.w = fmaf(v.w, fd.qspan_lo[4 * j + 3], fd.qmin_lo[4 * j + 3]);
+        }
         if (fd.tex_w != 0.f) {
-          const float4 u = tex3D<float4>(fd.tex_hi[j], tx, ty, tz);
+          float4 u = tex3D<float4>(fd.tex_hi[j], tx, ty, tz);
+          if (fd.tex_u8) {
+            u.x = fmaf(u.x, fd.qspan_hi[4 * j], fd.qmin_hi[4 * j]);
+            u.y = fmaf(u.y, fd.qspan_hi[4 * j + 1], fd.qmin_hi[4 * j + 1]);
+            u.z = fmaf(u.z, fd.qspan_hi[4 * j + 2], fd.qmin_hi[4 * j + 2]);
+            u.w = fmaf(u.w, fd.qspan_hi[4 * j + 3], fd.qmin_hi[4 * j + 3]);
+          }
           v.x = fmaf(fd.tex_w, u.x - v.x, v.x); v.y = fmaf(fd.tex_w, u.y - v.y, v.y);
           v.z = fmaf(fd.tex_w, u.z - v.z, v.z); v.w = fmaf(fd.tex_w, u.w - v.w, v.w);
         }
@@ -564,7 +602,11 @@ struct FastRow {
       const float pv[3] = {px, py, pz};
       float sn[3], cs[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) __sincosf((pv[a] - rint_fma(pv[a])) * 6.28318548202514648f, &sn[a], &cs[a]);
+      for (int a = 0; a < 3; ++a) {
+        const float r = pv[a] - rint_fma(pv[a]);   // exact, in [-1/2, 1/2]
+        if (FVSRN_FOURIER_POLY) sincos_turns(r, sn[a], cs[a]);
+        else __sincosf(r * 6.28318548202514648f, &sn[a], &cs[a]);
+      }
 #pragma unroll
       for (int i = 0; i < NM; ++i) {
         const int a = i % 3;

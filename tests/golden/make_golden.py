@@ -244,6 +244,15 @@ def main():
         t = 3.0 if back.is_temporal else None
         arrays[f"ckpt_{name}_density"] = eval_density(back, p[:512], t=t)
 
+    # --- u8-quantised grids of the default (fast-path) shapes: the GPU
+    # samples the codes directly (RGBA8 textures, dequantised in the kernel)
+    checkpoint_save(models["cfg1"], HERE / "cfg1_f16_u8.fvsrn", "f16", "u8")
+    checkpoint_save(models["temporal"], HERE / "temporal_f16_u8.fvsrn", "f16", "u8")
+    for name, t in (("cfg1_f16_u8", None), ("temporal_f16_u8", 6.5)):
+        back = checkpoint_load(HERE / f"{name}.fvsrn")
+        arrays[f"ckpt_{name}_density"] = eval_density(back, p[:4096], t=t)
+        add_render(f"ckpt_{name}", back, "grayscale", fib128[2], s128, t=t)
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

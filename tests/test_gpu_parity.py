@@ -355,3 +355,27 @@ def test_dvr_kernel_cfg2_full_frame_and_shards(kernel):
         assert np.array_equal(frame.cpu().numpy(), img)
     finally:
         D.set_dvr_kernel(prev)
+
+
+@pytest.mark.parametrize("sampler", ["tex", "ldg"])
+@pytest.mark.parametrize("name,t", [("cfg1_f16_u8", None), ("temporal_f16_u8", 6.5)])
+def test_u8_checkpoint_sampled_directly(name, t, sampler):
+    """a reference-written checkpoint with a u8-quantised latent grid.  The
+    texture sampler reads the 8-bit codes (RGBA8 textures, dequantised in the kernel);
+    the LDG sampler reads the grid dequantised on upload.  Both match the reference's
+    densities and render."""
+    from paper_2112_01579_b200 import device as D
+
+    prev = D.set_grid_sampler(sampler)
+    try:
+        m = P.checkpoint_load(GOLDEN / f"{name}.fvsrn")
+        assert m.config.grid_resolution > 0
+        got = P.eval_density(m, arrays()["eval_p"][:4096], t=t)
+        assert np.abs(got - arrays()[f"ckpt_{name}_density"]).max() <= DENS_TOL
+        r = meta()["renders"][f"ckpt_{name}"]
+        src = P.ModelSource(m, P.TF_PRESETS[r["tf"]], t=r["t"])
+        img = P.render_image(src, _cam(r["camera"]), P.RenderSettings(stepsize=r["stepsize"]))
+        assert P.metric_psnr(img, arrays()[f"render_ckpt_{name}"]) >= 40.0
+        assert abs(src.last_eval_count - r["count"]) <= max(4, r["count"] // 1000)
+    finally:
+        D.set_grid_sampler(prev)

@@ -189,3 +189,17 @@ def test_library_is_sm100a_cubin():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("name,cfg_name", [("cfg1_f16_u8", "cfg1"), ("temporal_f16_u8", "temporal")])
+def test_checkpoint_u8_codes_match_reference_quantizer(name, cfg_name):
+    """The reference-written u8 checkpoints of the default shapes carry exactly the codes
+    and (min, max) of grid_quantize on the seeded grids (grid.py:157-166) -- the data the
+    GPU texture path samples directly."""
+    m = P.checkpoint_load(GOLDEN / f"{name}.fvsrn")
+    ref = P.model_init(P.ModelConfig(**meta()["models"][cfg_name]["config"]))
+    assert m.quantized is not None and len(m.quantized) == len(ref.grids)
+    for q, g in zip(m.quantized, ref.grids):
+        rq = P.grid_quantize(g)
+        assert np.array_equal(q.codes, rq.codes)
+        assert np.array_equal(q.mins, rq.mins) and np.array_equal(q.maxs, rq.maxs)
