@@ -136,6 +136,12 @@ FVSRN_API int32_t fvsrn_model_info(fvsrn_model_t model, int32_t* k0_pad, int32_t
 FVSRN_API int32_t fvsrn_render(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,
                      const fvsrn_settings* settings, double t, float* out_rgba,
                      uint64_t* eval_count);
+/* render_image followed by png_bytes' 8-bit conversion (imaging.py:74-80:
+ * floor(clip(v,0,1)*255+0.5), bit-identical), done on the device: out is (H,W,4) uint8
+ * (4 B/px over PCIe instead of 16).  The service /render path (service.py:88-129). */
+FVSRN_API int32_t fvsrn_render_rgba8(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,
+                                     const fvsrn_settings* settings, double t, uint8_t* out_rgba8,
+                                     uint64_t* eval_count);
 /* Device framebuffer, stream-ordered; shard may be NULL (whole frame).
  * d_eval_count: device u64 accumulated atomically, may be NULL. */
 FVSRN_API int32_t fvsrn_render_device(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,

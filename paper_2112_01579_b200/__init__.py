@@ -18,6 +18,7 @@ from .model import (CheckpointError, FvsrnModel, ModelConfig, checkpoint_load, c
                     decode_volume, eval_color, eval_density, memory_footprint, model_init)
 from .nn import FourierEncoder, MlpParams, fourier_make, init_params, nerf_rows
 from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays,
-                     fibonacci_cameras, raymarch_forward, render_image, render_rays)
+                     fibonacci_cameras, raymarch_forward, render_image, render_image_rgba8,
+                     render_rays)
 from .transfer import TF_PRESETS, TransferFunction, tf_from_json, tf_load, tf_save
 from .volume import ScalarVolume

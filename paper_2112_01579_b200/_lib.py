@@ -94,6 +94,9 @@ EXPORTS = {
     "fvsrn_render": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),
                                  C.POINTER(SettingsDesc), C.c_double, _f,
                                  C.POINTER(C.c_uint64)]),
+    "fvsrn_render_rgba8": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),
+                                       C.POINTER(SettingsDesc), C.c_double, C.c_void_p,
+                                       C.POINTER(C.c_uint64)]),
     "fvsrn_render_device": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),
                                         C.POINTER(SettingsDesc), C.c_double, C.POINTER(ShardDesc),
                                         C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -1038,6 +1038,35 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   return FVSRN_OK;
 }
 
+int32_t fvsrn_render_rgba8(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
+                           const fvsrn_settings* st, double t, uint8_t* out, uint64_t* eval_count) {
+  if (!m || !c || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+  CUDA_TRY(cudaSetDevice(m->device));
+  StreamGuard sg;
+  const long long n_px = (long long)c->width * c->height;
+  const size_t fb_bytes = (size_t)n_px * 16, u8_bytes = (size_t)n_px * 4;
+  unsigned char* mapped = (unsigned char*)mapped_device_ptr(out);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, fb_bytes + (mapped ? 0 : u8_bytes) + 16, sg.s));
+  float* d_fb = (float*)buf;
+  unsigned char* d_u8 = mapped ? mapped : (unsigned char*)(buf + fb_bytes);
+  unsigned long long* d_cnt = (unsigned long long*)(buf + fb_bytes + (mapped ? 0 : u8_bytes));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 16, sg.s));
+  int rc = render_impl(m, tf, c, st, t, nullptr, d_fb, d_cnt, d_cnt + 1, sg.s);
+  if (rc) { cudaFreeAsync(buf, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  CUDA_TRY(launch_rgba8(d_fb, n_px, d_u8, sg.s));
+  count_launch();
+  unsigned long long cnt[2] = {0, 0};
+  if (!mapped) CUDA_TRY(cudaMemcpyAsync(out, d_u8, u8_bytes, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(buf, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  if (eval_count) *eval_count = cnt[0];
+  if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* origins,
                           const double* dirs, int64_t n, const fvsrn_settings* st, double t,
                           float* out_px, uint64_t* eval_count) {

@@ -466,6 +466,26 @@ __global__ void blend_grid_kernel(const __half* __restrict__ lo, const __half* _
   }
 }
 
+// 8-bit RGBA of a framebuffer exactly as png_bytes/write_png (imaging.py:68-80):
+// floor(clip(v, 0, 1) * 255 + 0.5) with separately rounded f32 ops, as numpy does
+__global__ void rgba8_kernel(const float4* __restrict__ fb, long long n, uchar4* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = fb[i];
+    auto q = [](float c) {
+      return (unsigned char)floorf(__fadd_rn(__fmul_rn(fminf(fmaxf(c, 0.f), 1.f), 255.f), 0.5f));
+    };
+    out[i] = make_uchar4(q(v.x), q(v.y), q(v.z), q(v.w));
+  }
+}
+
+cudaError_t launch_rgba8(const float* fb, long long n_px, unsigned char* out, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((n_px + 255) / 256, 148 * 16);
+  rgba8_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(fb), n_px,
+                                      reinterpret_cast<uchar4*>(out));
+  return cudaGetLastError();
+}
+
 __global__ void tiles_to_frame_kernel(const float4* __restrict__ gathered, int W, int H, int world,
                                       long long per_rank, int tiles_x, int n_tiles,
                                       float4* __restrict__ frame) {

@@ -214,6 +214,20 @@ class DeviceModel:
                                        L.t_arg(t), L.fptr(out), C.byref(cnt)))
         return out, int(cnt.value)
 
+    def render_rgba8(self, tf, cam, settings, t=None, out=None):
+        """(H,W,4) uint8 frame (png_bytes' quantisation, done on the device) + count."""
+        shape = (cam.height, cam.width, 4)
+        if out is None:
+            out = np.empty(shape, dtype=np.uint8)
+        elif out.shape != shape or out.dtype != np.uint8 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous uint8 array of shape {shape}")
+        cnt = C.c_uint64(0)
+        tfd = tf_desc(tf)
+        L.check(self._lib.fvsrn_render_rgba8(self._h, C.byref(tfd.desc) if tfd else None,
+                                             C.byref(camera_desc(cam)), C.byref(settings_desc(settings)),
+                                             L.t_arg(t), C.c_void_p(out.ctypes.data), C.byref(cnt)))
+        return out, int(cnt.value)
+
     def render_rays(self, tf, origins, dirs, settings, t=None):
         o = np.ascontiguousarray(np.asarray(origins, dtype=np.float64).reshape(-1, 3))
         d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))

@@ -183,6 +183,22 @@ def render_image(source, camera: Camera, settings: RenderSettings | None = None,
     return Image._from_device(data)
 
 
+def render_image_rgba8(source, camera: Camera, settings: RenderSettings | None = None,
+                       out: np.ndarray | None = None) -> np.ndarray:
+    """``render_image`` followed by the 8-bit quantisation of ``png_bytes``
+    (imaging.py:74-80, ``floor(clip(v, 0, 1) * 255 + 0.5)``), fused on the device:
+    returns the (H, W, 4) uint8 frame, bit-identical to quantising ``render_image``'s
+    output on the host, with a quarter of the device->host bytes.  New (the service's
+    render path); ``out`` may be a ``pinned_empty(..., np.uint8)`` buffer."""
+    src = _require_model_source(source)
+    if not isinstance(src, ModelSource):
+        raise TypeError("render_image_rgba8 renders ModelSource instances")
+    settings = settings or RenderSettings()
+    data, cnt = src.device_model.render_rgba8(src.tf, camera, settings, src.t, out=out)
+    src.last_eval_count = cnt
+    return data
+
+
 def fibonacci_cameras(n: int, width: int, height: int, radius: float = 2.2,
                       fov_y: float = np.pi / 4, center=(0.5, 0.5, 0.5)) -> list:
     """Deterministic orbit on a Fibonacci sphere (train.py:209-224): the measurement views."""
