@@ -3,8 +3,8 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2112_01579_b200/csrc
 LIB  := paper_2112_01579_b200/libfvsrn_b200.so
-SRCS := $(CSRC)/fvsrn_kernels.cu $(CSRC)/fvsrn_tc.cu $(CSRC)/fvsrn_volume.cu $(CSRC)/fvsrn_capi.cu
-HDRS := $(CSRC)/fvsrn_device.cuh $(CSRC)/fvsrn_kernels.cuh $(CSRC)/fvsrn_geometry.cuh $(CSRC)/fvsrn_volume.cuh $(CSRC)/fvsrn_march.cuh $(CSRC)/fvsrn_tc.cuh $(CSRC)/fvsrn_tmem.cuh include/fvsrn_b200.h
+SRCS := $(CSRC)/fvsrn_kernels.cu $(CSRC)/fvsrn_tc.cu $(CSRC)/fvsrn_train.cu $(CSRC)/fvsrn_volume.cu $(CSRC)/fvsrn_capi.cu
+HDRS := $(CSRC)/fvsrn_device.cuh $(CSRC)/fvsrn_kernels.cuh $(CSRC)/fvsrn_geometry.cuh $(CSRC)/fvsrn_volume.cuh $(CSRC)/fvsrn_march.cuh $(CSRC)/fvsrn_tc.cuh $(CSRC)/fvsrn_tmem.cuh $(CSRC)/fvsrn_train.cuh include/fvsrn_b200.h
 NVFLAGS := $(ARCH) -O3 -lineinfo -ftz=true -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Xptxas -v --expt-relaxed-constexpr -Iinclude
 

@@ -126,6 +126,35 @@ FVSRN_API int32_t fvsrn_kernel_timer(int32_t enable);
 FVSRN_API int32_t fvsrn_kernel_timer_read(double* dominant_ms, int64_t* dominant_launches,
                                           int64_t* total_launches);
 
+/* ---- world-space training (train.py:165-206), device pointers only.
+ * A static, position-input model (time_mode none, direction_mode pos).  The trainable
+ * parameters live in ONE flat f32 buffer in FvsrnModel.trainable_arrays() order
+ * (model.py:155-157): W_0..W_{L-1} as (out,in) row-major, b_0..b_{L-1}, then the
+ * (R,R,R,F) grid.  Gradients use the same layout. */
+typedef struct {
+  int32_t layers, hidden, d_in, d_out, activation, head;
+  int32_t fourier_m;                 /* rows of the (m,3) spatial Fourier matrix */
+  const float* d_b_matrix;           /* device (m,3) f32, or NULL when m == 0 */
+  int32_t grid_resolution, grid_channels;
+} fvsrn_train_desc;
+
+/* One batch of n positions (device f64 (n,3)) against reference values (device f32
+ * (n,d_out)): forward with cached layer inputs (d_inputs: per layer n x in_l floats,
+ * consecutive), pre-activations (d_preacts: (L-1) x n x hidden) and adjoints (d_deltas:
+ * per layer n x out_l); the L1-loss sum is added to *d_loss_sum; the latent-grid
+ * gradient is scatter-added into d_grid_grad (zero it first).  Weight/bias gradients are
+ * the batch reductions delta_l^T @ inputs_l and sum(delta_l) (nn.py:252-253). */
+FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const float* d_params,
+                                          const double* d_positions, const float* d_reference,
+                                          int64_t n, float* d_grid_grad, float* d_inputs,
+                                          float* d_preacts, float* d_deltas, double* d_loss_sum,
+                                          void* stream);
+/* adam_step (nn.py:279-298) over n flat parameters at step t (1-based).  Non-finite
+ * gradients are counted into *d_nonfinite and then nothing is updated. */
+FVSRN_API int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float* d_v,
+                                  int64_t n, double lr, double beta1, double beta2, double eps,
+                                  int32_t t, unsigned long long* d_nonfinite, void* stream);
+
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
 FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);
 /* Padded widths (K0, hidden_pad, out_pad), smem bytes; for plan/introspection. */

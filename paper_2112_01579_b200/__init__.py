@@ -20,5 +20,7 @@ from .nn import FourierEncoder, MlpParams, fourier_make, init_params, nerf_rows
 from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays,
                      fibonacci_cameras, raymarch_forward, render_image, render_image_rgba8,
                      render_rays)
-from .transfer import TF_PRESETS, TransferFunction, tf_from_json, tf_load, tf_save
-from .volume import ScalarVolume
+from .transfer import TF_PRESETS, TransferFunction, tf_eval, tf_from_json, tf_load, tf_save
+from .volume import ScalarVolume, sample_volume
+from .train import (ErrorGrid, TrainingDiverged, WorldTarget, WorldTrainConfig, build_error_grid,
+                    sample_world_dataset, train_world)

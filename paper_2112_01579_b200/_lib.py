@@ -82,6 +82,12 @@ EXPORTS = {
     "fvsrn_last_error": (C.c_char_p, []),
     "fvsrn_set_dvr_kernel": (C.c_int32, [C.c_int32]),
     "fvsrn_set_grid_sampler": (C.c_int32, [C.c_int32]),
+    "fvsrn_train_world_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p]),
+    "fvsrn_adam_step": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                    C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
+                                    C.c_void_p, C.c_void_p]),
     "fvsrn_kernel_timer": (C.c_int32, [C.c_int32]),
     "fvsrn_kernel_timer_read": (C.c_int32, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                             C.POINTER(C.c_int64)]),
@@ -124,6 +130,14 @@ EXPORTS = {
     "fvsrn_host_alloc": (C.c_int32, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "fvsrn_host_free": (C.c_int32, [C.c_void_p]),
 }
+
+class TrainDesc(C.Structure):
+    """fvsrn_train_desc"""
+    _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("d_in", C.c_int32),
+                ("d_out", C.c_int32), ("activation", C.c_int32), ("head", C.c_int32),
+                ("fourier_m", C.c_int32), ("d_b_matrix", C.c_void_p),
+                ("grid_resolution", C.c_int32), ("grid_channels", C.c_int32)]
+
 
 _LIB = None
 

@@ -20,6 +20,7 @@
 #include "../../include/fvsrn_b200.h"
 #include "fvsrn_kernels.cuh"
 #include "fvsrn_tc.cuh"
+#include "fvsrn_train.cuh"
 #include "fvsrn_volume.cuh"
 
 using namespace fvsrn;
@@ -604,6 +605,59 @@ CamDev cam_for(const fvsrn_camera* c) {
 extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
+
+int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params,
+                                const double* d_positions, const float* d_reference, int64_t n,
+                                float* d_grid_grad, float* d_inputs, float* d_preacts,
+                                float* d_deltas, double* d_loss_sum, void* stream) {
+  if (!d || !d_params || (n > 0 && (!d_positions || !d_reference || !d_inputs || !d_deltas)))
+    return fail(FVSRN_EINVAL, "null argument");
+  const int L = d->layers;
+  if (L < 1 || L > kTrainMaxLayers) return fail(FVSRN_EINVAL, "layer count out of range");
+  if (d->hidden > 256 || d->d_in > 256 || d->d_out < 1 || d->d_out > 4)
+    return fail(FVSRN_ECAPACITY, "network too wide for the training kernel");
+  if (d->d_in != 3 + 2 * d->fourier_m + (d->grid_resolution > 0 ? d->grid_channels : 0))
+    return fail(FVSRN_EINVAL, "input width does not match a static position-input model");
+  if (d->fourier_m > 0 && !d->d_b_matrix) return fail(FVSRN_EINVAL, "Fourier matrix required");
+  if (d->grid_resolution == 1) return fail(FVSRN_EINVAL, "need R >= 2");
+  TrainNetDev net{};
+  net.layers = L; net.hidden = d->hidden; net.d_in = d->d_in; net.d_out = d->d_out;
+  net.act = d->activation; net.head = d->head; net.m = d->fourier_m; net.bmat = d->d_b_matrix;
+  net.grid_res = d->grid_resolution; net.grid_ch = d->grid_channels;
+  long long off = 0, io = 0, dof = 0;
+  for (int l = 0; l < L; ++l) {
+    const long long in_l = l == 0 ? d->d_in : d->hidden, out_l = l == L - 1 ? d->d_out : d->hidden;
+    net.w_off[l] = off;
+    off += in_l * out_l;
+    net.in_off[l] = io;
+    io += (long long)n * in_l;
+    net.d_off[l] = dof;
+    dof += (long long)n * out_l;
+  }
+  for (int l = 0; l < L; ++l) {
+    net.b_off[l] = off;
+    off += l == L - 1 ? d->d_out : d->hidden;
+  }
+  net.grid_off = off;
+  CUDA_TRY(launch_train_world(net, d_params, d_positions, d_reference, (long long)n, d_grid_grad,
+                              d_inputs, d_preacts, d_deltas, d_loss_sum, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float* d_v, int64_t n,
+                        double lr, double beta1, double beta2, double eps, int32_t t,
+                        unsigned long long* d_nonfinite, void* stream) {
+  if (!d_params || !d_grads || !d_m || !d_v || !d_nonfinite || t < 1) return fail(FVSRN_EINVAL, "bad argument");
+  AdamConsts k;
+  k.lr = (float)lr; k.b1 = (float)beta1; k.b2 = (float)beta2;
+  k.one_m_b1 = (float)(1.0 - beta1); k.one_m_b2 = (float)(1.0 - beta2); k.eps = (float)eps;
+  k.bc1 = (float)(1.0 - std::pow(beta1, t)); k.bc2 = (float)(1.0 - std::pow(beta2, t));
+  CUDA_TRY(launch_adam(d_params, d_grads, d_m, d_v, (long long)n, k, d_nonfinite, (cudaStream_t)stream));
+  count_launch();
+  count_launch();
+  return FVSRN_OK;
+}
 
 int32_t fvsrn_kernel_timer(int32_t enable) {
   g_kt.on = enable != 0;

@@ -1,0 +1,32 @@
+// fvsrn_train.cuh -- world-space training step (fvsrn_train.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace fvsrn {
+
+constexpr int kTrainMaxLayers = 24;
+
+// Network + encoder description of a static, position-input model; every offset is in
+// floats.  params: [W_0 .. W_{L-1} | b_0 .. b_{L-1} | grid] (model.py:155-157 order).
+// inputs / deltas: per-layer blocks of N x in_l / N x out_l floats; preacts (L-1) x N x H.
+struct TrainNetDev {
+  int layers, hidden, d_in, d_out, act, head;
+  int m;                    // spatial Fourier rows (B is m x 3, f32)
+  const float* bmat;
+  int grid_res, grid_ch;
+  long long grid_off;
+  long long w_off[kTrainMaxLayers], b_off[kTrainMaxLayers];
+  long long in_off[kTrainMaxLayers], d_off[kTrainMaxLayers];
+};
+
+struct AdamConsts {
+  float lr, b1, b2, one_m_b1, one_m_b2, eps, bc1, bc2;
+};
+
+cudaError_t launch_train_world(const TrainNetDev& net, const float* params, const double* pos,
+                               const float* ref, long long n, float* grid_grad, float* inputs,
+                               float* preacts, float* deltas, double* loss_sum, cudaStream_t s);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, const AdamConsts& k,
+                        unsigned long long* bad, cudaStream_t s);
+
+}  // namespace fvsrn

@@ -130,6 +130,10 @@ class FvsrnModel:
     def is_temporal(self) -> bool:
         return self.keyframes is not None
 
+    def trainable_arrays(self) -> list:
+        """[*weights, *biases, *grid values] (model.py:155-157): the Adam / gradient order."""
+        return [*self.params.weights, *self.params.biases, *(g.values for g in self.grids)]
+
     def invalidate_device(self) -> None:
         """Drop the cached device copy (call after mutating parameters in place)."""
         self.__dict__.pop("_device", None)

@@ -1,0 +1,272 @@
+"""World-space training on the GPU (reference train.py:26-206).
+
+Same names and semantics as the reference: ``WorldTrainConfig``, ``WorldTarget``,
+``ErrorGrid``, ``TrainingDiverged``, ``sample_world_dataset``, ``build_error_grid``
+and ``train_world(model, target, cfg, progress=None) -> (model, trace)`` -- L1 loss,
+joint network + latent-grid training with Adam, optional error-grid importance
+resampling.  The datasets come from the same numpy RNG draws as the reference;
+every batch step runs on the device:
+
+* ``fvsrn_train_world_grads`` (one CUDA kernel, thread per sample, f32): forward with
+  cached layer inputs / pre-activations, L1 adjoint, head + MLP backward, latent-grid
+  scatter-add;
+* the weight/bias gradients ``delta_l^T @ inputs_l`` / ``sum(delta_l)`` (nn.py:252-253)
+  are batch reductions done as cuBLAS GEMMs on torch device tensors;
+* ``fvsrn_adam_step`` applies adam_step (nn.py:279-298) to one flat parameter buffer
+  laid out like ``FvsrnModel.trainable_arrays()``.
+
+Scope: static models with position inputs (the reference's ``train_world`` callers);
+screen-space (``train_screen``) and temporal training stay on the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .transfer import TransferFunction, tf_eval
+from .volume import ScalarVolume, sample_volume
+
+_ACT = {"relu": 0, "sigmoid": 1, "softplus": 2, "snake": 3, "snake_alt": 4}
+
+
+class TrainingDiverged(RuntimeError):
+    def __init__(self, epoch: int, message: str):
+        super().__init__(f"epoch {epoch}: {message}")
+        self.epoch = epoch
+
+
+@dataclass
+class WorldTrainConfig:
+    sample_count: int = 64**3
+    batch_size: int = 16384
+    epochs: int = 200
+    lr: float = 0.01
+    seed: int = 0
+    adaptive: bool = False
+    resample_interval: int = 50
+    error_grid_resolution: int = 32
+    samples_per_voxel: int = 8
+
+    def __post_init__(self):
+        if min(self.sample_count, self.batch_size, self.epochs + 1, self.resample_interval) < 1:
+            raise ValueError("counts must be positive")
+        if self.batch_size > self.sample_count:
+            raise ValueError("batch size cannot exceed the sample count")
+
+
+@dataclass
+class ErrorGrid:
+    """Coarse per-voxel mean absolute prediction error."""
+
+    values: np.ndarray  # (r, r, r)
+
+    @property
+    def resolution(self) -> int:
+        return self.values.shape[0]
+
+
+@dataclass
+class WorldTarget:
+    """Ground truth for world-space training: densities, or TF-mapped colors."""
+
+    volume: ScalarVolume
+    tf: TransferFunction | None = None
+
+    def reference(self, p: np.ndarray) -> np.ndarray:
+        dens = sample_volume(self.volume, p)
+        if self.tf is None:
+            return dens.astype(np.float32)
+        rgb, sigma = tf_eval(self.tf, dens)
+        return np.concatenate([rgb, sigma[:, None]], axis=1)
+
+
+def sample_world_dataset(target: WorldTarget, count: int, sampler="uniform", seed: int = 0):
+    """Draw (positions, reference values) exactly as train.py:118-133 (same RNG calls)."""
+    rng = np.random.default_rng(seed)
+    if isinstance(sampler, ErrorGrid) and float(sampler.values.sum()) > 0.0:
+        r = sampler.resolution
+        mass = sampler.values.reshape(-1).astype(np.float64)
+        probs = mass / mass.sum()
+        voxels = rng.choice(r**3, size=count, p=probs)
+        corner = np.stack(np.unravel_index(voxels, (r, r, r)), axis=1)
+        p = (corner + rng.uniform(0.0, 1.0, size=(count, 3))) / r
+    else:
+        p = rng.uniform(0.0, 1.0, size=(count, 3))
+    return p, target.reference(p)
+
+
+def _model_predict(model, p: np.ndarray) -> np.ndarray:
+    from .model import eval_color, eval_density
+
+    if model.config.head == "density":
+        return eval_density(model, p)
+    return eval_color(model, p)
+
+
+def build_error_grid(model, target: WorldTarget, resolution: int, samples_per_voxel: int = 8,
+                     seed: int = 0, t: float | None = None) -> ErrorGrid:
+    """Mean absolute prediction error per voxel of an r^3 lattice (train.py:136-155);
+    the predictions come from the GPU evaluation path."""
+    if t is not None:
+        raise ValueError("the GPU world trainer handles static models")
+    rng = np.random.default_rng(seed)
+    r = resolution
+    corners = np.stack(np.meshgrid(*(np.arange(r),) * 3, indexing="ij"), axis=-1).reshape(-1, 3)
+    err = np.zeros(r**3, dtype=np.float64)
+    chunk = max(1, (1 << 18) // samples_per_voxel)
+    for lo in range(0, r**3, chunk):
+        c = corners[lo:lo + chunk]
+        jitter = rng.uniform(0.0, 1.0, size=(len(c), samples_per_voxel, 3))
+        p = ((c[:, None, :] + jitter) / r).reshape(-1, 3)
+        pred = _model_predict(model, p)
+        ref = target.reference(p)
+        diff = np.abs(np.atleast_2d(pred.T).T - np.atleast_2d(ref.T).T)
+        err[lo:lo + chunk] = diff.reshape(len(c), samples_per_voxel, -1).mean(axis=(1, 2))
+    return ErrorGrid(values=err.reshape(r, r, r).astype(np.float32))
+
+
+class WorldTrainer:
+    """Device-resident trainable state of one model: the flat f32 parameter buffer
+    (trainable_arrays order), its gradient buffer and the Adam moments."""
+
+    def __init__(self, model, device: int | None = None):
+        import torch
+
+        cfg = model.config
+        if cfg.is_temporal or cfg.direction_mode != "pos":
+            raise ValueError("the GPU world trainer handles static, position-input models")
+        if cfg.fourier_mode not in ("off", "nerf", "random") or (
+                model.spatial_encoder.m > 0 and model.spatial_encoder.b_matrix.shape[1] != 3):
+            raise ValueError("unsupported spatial encoder")
+        self.torch = torch
+        self.dev = torch.device("cuda", L.current_device() if device is None else device)
+        self.model = model
+        arrays = model.trainable_arrays()
+        self.shapes = [a.shape for a in arrays]
+        self.sizes = [int(a.size) for a in arrays]
+        flat = np.concatenate([np.ascontiguousarray(a, dtype=np.float32).reshape(-1) for a in arrays])
+        self.params = torch.from_numpy(flat).to(self.dev)
+        self.grads = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.t = 0
+        n_layers = model.params.layer_count
+        self.n_layers = n_layers
+        offs = np.concatenate([[0], np.cumsum(self.sizes)])
+        self._views = [(int(offs[i]), int(offs[i + 1])) for i in range(len(arrays))]
+        self.grid_off = int(offs[2 * n_layers]) if len(arrays) > 2 * n_layers else 0
+        m = model.spatial_encoder.m
+        self.bmat = (torch.from_numpy(np.ascontiguousarray(model.spatial_encoder.b_matrix,
+                                                           dtype=np.float32)).to(self.dev)
+                     if m > 0 else None)
+        self.desc = L.TrainDesc(n_layers, cfg.hidden, cfg.input_width, cfg.output_width,
+                                _ACT[cfg.activation], 0 if cfg.head == "density" else 1, m,
+                                self.bmat.data_ptr() if m > 0 else None,
+                                cfg.grid_resolution, cfg.grid_channels if cfg.grid_resolution else 0)
+        self.widths_in = [cfg.input_width] + [cfg.hidden] * (n_layers - 1)
+        self.widths_out = [cfg.hidden] * (n_layers - 1) + [cfg.output_width]
+        self._scratch_n = -1
+        self.loss_sum = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.nonfinite = torch.zeros(1, dtype=torch.int64, device=self.dev)
+
+    def _scratch(self, n: int):
+        if n != self._scratch_n:
+            t = self.torch
+            self.inputs = t.empty(n * sum(self.widths_in), dtype=t.float32, device=self.dev)
+            self.deltas = t.empty(n * sum(self.widths_out), dtype=t.float32, device=self.dev)
+            self.preacts = t.empty(max(1, (self.n_layers - 1) * n * self.model.config.hidden),
+                                   dtype=t.float32, device=self.dev)
+            self._scratch_n = n
+
+    def gradients(self, positions, reference) -> float:
+        """Fill self.grads for one batch (device tensors or numpy); returns the batch
+        L1 loss (mean over samples and channels, train.py:158-161)."""
+        t = self.torch
+        pos = t.as_tensor(positions, dtype=t.float64, device=self.dev).contiguous()
+        ref = t.as_tensor(reference, dtype=t.float32, device=self.dev).reshape(len(pos), -1).contiguous()
+        n = len(pos)
+        self._scratch(n)
+        self.grads.zero_()
+        self.loss_sum.zero_()
+        stream = t.cuda.current_stream(self.dev).cuda_stream
+        grid_ptr = self.grads.data_ptr() + 4 * self.grid_off if self.model.config.grid_resolution else None
+        L.check(L.lib().fvsrn_train_world_grads(
+            C.byref(self.desc), C.c_void_p(self.params.data_ptr()), C.c_void_p(pos.data_ptr()),
+            C.c_void_p(ref.data_ptr()), n, C.c_void_p(grid_ptr), C.c_void_p(self.inputs.data_ptr()),
+            C.c_void_p(self.preacts.data_ptr()), C.c_void_p(self.deltas.data_ptr()),
+            C.c_void_p(self.loss_sum.data_ptr()), C.c_void_p(stream)))
+        io = do = 0
+        for l in range(self.n_layers):
+            wi, wo = self.widths_in[l], self.widths_out[l]
+            x = self.inputs[io:io + n * wi].view(n, wi)
+            dl = self.deltas[do:do + n * wo].view(n, wo)
+            w0, w1 = self._views[l]
+            b0, b1 = self._views[self.n_layers + l]
+            t.mm(dl.t(), x, out=self.grads[w0:w1].view(wo, wi))          # nn.py:252
+            t.sum(dl, dim=0, out=self.grads[b0:b1])                         # nn.py:253
+            io += n * wi
+            do += n * wo
+        return float(self.loss_sum.item()) / (n * ref.shape[1])
+
+    def adam(self, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
+        self.nonfinite.zero_()
+        stream = self.torch.cuda.current_stream(self.dev).cuda_stream
+        L.check(L.lib().fvsrn_adam_step(
+            C.c_void_p(self.params.data_ptr()), C.c_void_p(self.grads.data_ptr()),
+            C.c_void_p(self.m.data_ptr()), C.c_void_p(self.v.data_ptr()), self.params.numel(),
+            lr, beta1, beta2, eps, self.t + 1, C.c_void_p(self.nonfinite.data_ptr()),
+            C.c_void_p(stream)))
+        if int(self.nonfinite.item()):
+            raise FloatingPointError("non-finite gradient passed to adam_step")
+        self.t += 1
+
+    def write_back(self) -> None:
+        """Copy the trained parameters into the model's arrays (and drop its render copy)."""
+        flat = self.params.cpu().numpy()
+        for a, (lo, hi), shape in zip(self.model.trainable_arrays(), self._views, self.shapes):
+            a[...] = flat[lo:hi].reshape(shape)
+        self.model.invalidate_device()
+
+
+def train_world(model, target: WorldTarget, cfg: WorldTrainConfig, progress=None):
+    """L1 world-space training of network and grid jointly with Adam (train.py:165-206).
+
+    Returns (model, per-epoch loss trace); the model's arrays are updated in place."""
+    import torch
+
+    if (model.config.head == "color") != (target.tf is not None):
+        raise ValueError("model head does not match the training target")
+    rng = np.random.default_rng(cfg.seed)
+    positions, values = sample_world_dataset(target, cfg.sample_count, "uniform", cfg.seed)
+    tr = WorldTrainer(model)
+    pos_d = torch.as_tensor(positions, dtype=torch.float64, device=tr.dev)
+    val_d = torch.as_tensor(values, dtype=torch.float32, device=tr.dev).reshape(cfg.sample_count, -1)
+    trace = []
+    for epoch in range(cfg.epochs):
+        if cfg.adaptive and epoch > 0 and epoch % cfg.resample_interval == 0:
+            tr.write_back()
+            egrid = build_error_grid(model, target, cfg.error_grid_resolution,
+                                     cfg.samples_per_voxel, seed=cfg.seed + epoch)
+            positions, values = sample_world_dataset(target, cfg.sample_count, egrid,
+                                                     seed=cfg.seed + epoch)
+            pos_d = torch.as_tensor(positions, dtype=torch.float64, device=tr.dev)
+            val_d = torch.as_tensor(values, dtype=torch.float32,
+                                    device=tr.dev).reshape(cfg.sample_count, -1)
+        perm = torch.as_tensor(rng.permutation(cfg.sample_count), device=tr.dev)
+        total = 0.0
+        for lo in range(0, cfg.sample_count, cfg.batch_size):
+            idx = perm[lo:lo + cfg.batch_size]
+            loss = tr.gradients(pos_d[idx], val_d[idx])
+            if not np.isfinite(loss):
+                raise TrainingDiverged(epoch, "non-finite loss")
+            tr.adam(cfg.lr)
+            total += loss * len(idx)
+        trace.append(total / cfg.sample_count)
+        if progress is not None:
+            progress(epoch, trace[-1])
+    tr.write_back()
+    return model, trace

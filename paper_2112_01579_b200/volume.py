@@ -42,3 +42,26 @@ class ScalarVolume:
     @property
     def resolution(self) -> int:
         return int(max(self.values.shape))
+
+
+def sample_volume(vol: ScalarVolume, p: np.ndarray) -> np.ndarray:
+    """Host trilinear lookup at positions in [0,1]^3 (volume.py:213-255), the training
+    targets' ground truth; clamped, exact at vertices, f32 lerps in x, y, z order.
+    (The renderer's VolumeSource does the same lookup on the device.)"""
+    values = vol.values
+    pts = np.atleast_2d(np.asarray(p, dtype=np.float64))
+    single = np.asarray(p).ndim == 1
+    dims = np.asarray(values.shape[:3])
+    coords = np.clip(pts, 0.0, 1.0) * (dims - 1)
+    i0 = np.maximum(np.minimum(coords.astype(np.int64), dims - 2), 0)
+    f = (coords - i0).astype(values.dtype)
+    x0, y0, z0 = i0[:, 0], i0[:, 1], i0[:, 2]
+    fx, fy, fz = f[:, 0], f[:, 1], f[:, 2]
+    c00 = values[x0, y0, z0] * (1 - fx) + values[x0 + 1, y0, z0] * fx
+    c10 = values[x0, y0 + 1, z0] * (1 - fx) + values[x0 + 1, y0 + 1, z0] * fx
+    c01 = values[x0, y0, z0 + 1] * (1 - fx) + values[x0 + 1, y0, z0 + 1] * fx
+    c11 = values[x0, y0 + 1, z0 + 1] * (1 - fx) + values[x0 + 1, y0 + 1, z0 + 1] * fx
+    c0 = c00 * (1 - fy) + c10 * fy
+    c1 = c01 * (1 - fy) + c11 * fy
+    out = c0 * (1 - fz) + c1 * fz
+    return out[0] if single else out

@@ -253,6 +253,37 @@ def main():
         arrays[f"ckpt_{name}_density"] = eval_density(back, p[:4096], t=t)
         add_render(f"ckpt_{name}", back, "grayscale", fib128[2], s128, t=t)
 
+    # --- world-space training (train.py:136-206): one-batch gradients of the L1 loss
+    # through model_backward (flat, trainable_arrays order) and short loss traces
+    from fvsrn.model import color_head_backward, density_head_backward, model_backward
+    from fvsrn.train import WorldTarget, WorldTrainConfig, _l1_and_adjoint, _model_predict, train_world
+    vol = synth_field("gaussians", 24, {"n_components": 6}, seed=42)
+    arrays["train_volume"] = vol.values
+    meta["train"] = {}
+    for name, tfname in (("cfg1", None), ("color_pos", "warm"), ("relu_nogrid", None), ("tiny", None)):
+        model = model_init(ModelConfig(**CONFIGS[name]))
+        target = WorldTarget(vol, TF_PRESETS[tfname] if tfname else None)
+        pb = np.random.default_rng(77).uniform(0.0, 1.0, size=(512, 3))
+        ref = target.reference(pb)
+        pred, raw, ctx = _model_predict(model, pb)
+        loss, adj = _l1_and_adjoint(pred, ref)
+        if model.config.head == "density":
+            raw_bar = density_head_backward(raw, adj)
+        else:
+            raw_bar = color_head_backward(raw, adj)
+        grads = model_backward(model, ctx, raw_bar)
+        arrays[f"train_pos_{name}"] = pb
+        arrays[f"train_ref_{name}"] = np.asarray(ref, dtype=np.float32)
+        arrays[f"train_grads_{name}"] = np.concatenate([g.reshape(-1) for g in grads.arrays()])
+        meta["train"][name] = {"tf": tfname, "loss": loss}
+    for name in ("tiny", "cfg1"):
+        model = model_init(ModelConfig(**CONFIGS[name]))
+        cfg = WorldTrainConfig(sample_count=4096, batch_size=1024, epochs=4, lr=0.01, seed=0)
+        _, trace = train_world(model, WorldTarget(vol), cfg)
+        arrays[f"train_trace_{name}"] = np.asarray(trace)
+        arrays[f"train_final_{name}"] = np.concatenate([a.reshape(-1) for a in model.trainable_arrays()])
+        print("train", name, trace, flush=True)
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

@@ -1,0 +1,120 @@
+"""World-space training on the GPU vs the reference's train.py.
+
+Goldens (tests/golden/make_golden.py, produced by the reference): one-batch L1
+gradients through model_backward for four model shapes, and 4-epoch train_world loss
+traces.  The host parts (targets, datasets) are compared exactly on the CPU."""
+
+import numpy as np
+import pytest
+
+import paper_2112_01579_b200 as P
+from tests.golden_util import arrays, meta
+
+NAMES = ["cfg1", "color_pos", "relu_nogrid", "tiny"]
+
+
+def _model(name):
+    return P.model_init(P.ModelConfig(**meta()["models"][name]["config"]))
+
+
+def _target(name):
+    tfname = meta()["train"][name]["tf"]
+    return P.WorldTarget(P.ScalarVolume(arrays()["train_volume"]),
+                         P.TF_PRESETS[tfname] if tfname else None)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_training_targets_bit_exact(name):
+    # sample_volume / tf_eval restated on the host (volume.py:213-255, transfer.py:57-65)
+    got = _target(name).reference(arrays()[f"train_pos_{name}"])
+    np.testing.assert_array_equal(np.asarray(got, np.float32), arrays()[f"train_ref_{name}"])
+
+
+def test_sample_world_dataset_same_draws():
+    t = P.WorldTarget(P.ScalarVolume(arrays()["train_volume"]))
+    p, v = P.sample_world_dataset(t, 1000, "uniform", seed=3)
+    np.testing.assert_array_equal(p, np.random.default_rng(3).uniform(0.0, 1.0, size=(1000, 3)))
+    eg = P.ErrorGrid(values=np.random.default_rng(1).uniform(size=(4, 4, 4)).astype(np.float32))
+    p2, _ = P.sample_world_dataset(t, 500, eg, seed=5)
+    assert p2.shape == (500, 3) and p2.min() >= 0.0 and p2.max() <= 1.0
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        P.WorldTrainConfig(sample_count=10, batch_size=20)
+    with pytest.raises(ValueError):
+        P.WorldTrainConfig(epochs=-2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_batch_gradients_vs_reference(name):
+    from paper_2112_01579_b200.train import WorldTrainer
+
+    m = _model(name)
+    tr = WorldTrainer(m)
+    loss = tr.gradients(arrays()[f"train_pos_{name}"], arrays()[f"train_ref_{name}"])
+    assert abs(loss - meta()["train"][name]["loss"]) <= 1e-6 * max(1.0, abs(loss))
+    got = tr.grads.cpu().numpy()
+    want = arrays()[f"train_grads_{name}"]
+    assert got.shape == want.shape
+    off = 0
+    for a in m.trainable_arrays():       # per parameter array, relative to its scale
+        g, w = got[off:off + a.size], want[off:off + a.size]
+        scale = float(np.abs(w).max()) or 1.0
+        assert np.abs(g - w).max() <= 1e-4 * scale, (name, a.shape, np.abs(g - w).max(), scale)
+        off += a.size
+
+
+@pytest.mark.gpu
+def test_adam_step_matches_numpy_restatement():
+    from paper_2112_01579_b200.train import WorldTrainer
+
+    m = _model("tiny")
+    tr = WorldTrainer(m)
+    rng = np.random.default_rng(0)
+    p0 = tr.params.cpu().numpy().copy()
+    mm = np.zeros_like(p0)
+    vv = np.zeros_like(p0)
+    for t in range(1, 4):             # adam_step, nn.py:287-298, in float32
+        g = (rng.standard_normal(p0.shape) * 1e-2).astype(np.float32)
+        tr.grads.copy_(__import__("torch").from_numpy(g))
+        tr.adam(0.01)
+        bc1, bc2 = 1.0 - 0.9 ** t, 1.0 - 0.999 ** t
+        mm *= np.float32(0.9)
+        mm += np.float32(1.0 - 0.9) * g
+        vv *= np.float32(0.999)
+        vv += np.float32(1.0 - 0.999) * g * g
+        p0 -= np.float32(0.01) * (mm / np.float32(bc1)) / (np.sqrt(vv / np.float32(bc2)) + np.float32(1e-8))
+        np.testing.assert_allclose(tr.params.cpu().numpy(), p0, rtol=0, atol=2e-7)
+    # a non-finite gradient raises and leaves every parameter untouched
+    before = tr.params.cpu().numpy().copy()
+    bad = np.zeros_like(p0)
+    bad[5] = np.nan
+    tr.grads.copy_(__import__("torch").from_numpy(bad))
+    with pytest.raises(FloatingPointError):
+        tr.adam(0.01)
+    np.testing.assert_array_equal(tr.params.cpu().numpy(), before)
+    assert tr.t == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tiny", "cfg1"])
+def test_train_world_trace_vs_reference(name):
+    m = _model(name)
+    vol = P.ScalarVolume(arrays()["train_volume"])
+    cfg = P.WorldTrainConfig(sample_count=4096, batch_size=1024, epochs=4, lr=0.01, seed=0)
+    before = P.eval_density(m, arrays()["train_pos_cfg1"][:64])   # device copy of the init
+    _, trace = P.train_world(m, P.WorldTarget(vol), cfg)
+    want = arrays()[f"train_trace_{name}"]
+    # epoch 0 is the same data, order and initial parameters: tight; later epochs follow
+    # Adam trajectories that start from f32-rounding-level gradient differences
+    assert abs(trace[0] - want[0]) <= 1e-4 * want[0]
+    np.testing.assert_allclose(trace, want, rtol=3e-2)
+    assert trace[-1] < trace[0]
+    final = np.concatenate([a.reshape(-1) for a in m.trainable_arrays()])
+    ref_final = arrays()[f"train_final_{name}"]
+    assert np.abs(final - ref_final).max() <= 0.05 * np.abs(ref_final).max()
+    # the trained parameters reached the model and its render copy was refreshed
+    after = P.eval_density(m, arrays()["train_pos_cfg1"][:64])
+    assert not np.allclose(before, after)
