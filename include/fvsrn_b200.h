@@ -149,6 +149,28 @@ FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const fl
                                           int64_t n, float* d_grid_grad, float* d_inputs,
                                           float* d_preacts, float* d_deltas, double* d_loss_sum,
                                           void* stream);
+/* Screen-space training (train.py:227-262), colour-head models.  Forward:
+ * raymarch_forward(..., want_states=True) (render.py:203-238) of n explicit rays with f32
+ * model evaluation and f64 compositing, no early termination: pixels (n,4) f32, terminal
+ * colour (n,3) / alpha (n) f64 and the per-ray march geometry (tmin, ds, step count). */
+FVSRN_API int32_t fvsrn_train_screen_forward(const fvsrn_train_desc* desc, const float* d_params,
+                                             const double* d_origins, const double* d_dirs, int64_t n,
+                                             const fvsrn_settings* settings, float* d_pixels,
+                                             double* d_color, double* d_alpha, double* d_tmin,
+                                             double* d_ds, int32_t* d_nsteps, void* stream);
+/* raymarch_backward (render.py:241-306): reverse walk per ray with blend inversion; the
+ * cache rows of ray i's step k go to row d_row_offset[i] + k of buffers sized for
+ * cap_rows samples (layout as fvsrn_train_world_grads with n = cap_rows); latent-grid
+ * gradients are scatter-added into d_grid_grad. */
+FVSRN_API int32_t fvsrn_train_screen_backward(const fvsrn_train_desc* desc, const float* d_params,
+                                              const double* d_origins, const double* d_dirs, int64_t n,
+                                              double eps_blend, const double* d_color,
+                                              const double* d_alpha, const double* d_tmin,
+                                              const double* d_ds, const int32_t* d_nsteps,
+                                              const int64_t* d_row_offset, const float* d_image_adjoint,
+                                              const double* d_background, int64_t cap_rows,
+                                              float* d_inputs, float* d_preacts, float* d_deltas,
+                                              float* d_grid_grad, void* stream);
 /* adam_step (nn.py:279-298) over n flat parameters at step t (1-based).  Non-finite
  * gradients are counted into *d_nonfinite and then nothing is updated. */
 FVSRN_API int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float* d_v,

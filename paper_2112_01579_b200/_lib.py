@@ -85,6 +85,11 @@ EXPORTS = {
     "fvsrn_train_world_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p]),
+    "fvsrn_train_screen_forward": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                               C.POINTER(SettingsDesc)] + [C.c_void_p] * 7),
+    "fvsrn_train_screen_backward": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                C.c_double] + [C.c_void_p] * 8 + [C.c_int64] +
+                                               [C.c_void_p] * 5),
     "fvsrn_adam_step": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                     C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
                                     C.c_void_p, C.c_void_p]),

@@ -42,12 +42,13 @@ const bool g_lpt_enabled = [] {
 #define FVSRN_TEX_DEFAULT 1
 #endif
 constexpr bool kTexDefault = FVSRN_TEX_DEFAULT != 0;
-enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3 };
+enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3, kPipe = 4 };
 std::atomic<int> g_dvr_mode_i{[] {
   const char* e = std::getenv("FVSRN_DVR");
   if (e && std::string(e) == "tc") return (int)DvrMode::kTC;
   if (e && std::string(e) == "ws") return (int)DvrMode::kWS;
   if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
+  if (e && std::string(e) == "pipe") return (int)DvrMode::kPipe;
   return (int)DvrMode::kAuto;
 }()};
 // tcgen05 kernel: one 128-ray tile per CTA (default, measured faster), or two tiles in
@@ -541,6 +542,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
   if (dvr_mode() == DvrMode::kWS)
     return launch(m, KernelKind::kDVRWS, ws_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
+  if (dvr_mode() == DvrMode::kPipe && fast_path(m, KernelKind::kDVR))
+    return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   return launch(m, KernelKind::kDVR, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
 }
 
@@ -606,12 +609,7 @@ extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
 
-int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params,
-                                const double* d_positions, const float* d_reference, int64_t n,
-                                float* d_grid_grad, float* d_inputs, float* d_preacts,
-                                float* d_deltas, double* d_loss_sum, void* stream) {
-  if (!d || !d_params || (n > 0 && (!d_positions || !d_reference || !d_inputs || !d_deltas)))
-    return fail(FVSRN_EINVAL, "null argument");
+static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev& net) {
   const int L = d->layers;
   if (L < 1 || L > kTrainMaxLayers) return fail(FVSRN_EINVAL, "layer count out of range");
   if (d->hidden > 256 || d->d_in > 256 || d->d_out < 1 || d->d_out > 4)
@@ -620,7 +618,7 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
     return fail(FVSRN_EINVAL, "input width does not match a static position-input model");
   if (d->fourier_m > 0 && !d->d_b_matrix) return fail(FVSRN_EINVAL, "Fourier matrix required");
   if (d->grid_resolution == 1) return fail(FVSRN_EINVAL, "need R >= 2");
-  TrainNetDev net{};
+  net = TrainNetDev{};
   net.layers = L; net.hidden = d->hidden; net.d_in = d->d_in; net.d_out = d->d_out;
   net.act = d->activation; net.head = d->head; net.m = d->fourier_m; net.bmat = d->d_b_matrix;
   net.grid_res = d->grid_resolution; net.grid_ch = d->grid_channels;
@@ -630,17 +628,72 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
     net.w_off[l] = off;
     off += in_l * out_l;
     net.in_off[l] = io;
-    io += (long long)n * in_l;
+    io += rows * in_l;
     net.d_off[l] = dof;
-    dof += (long long)n * out_l;
+    dof += rows * out_l;
   }
   for (int l = 0; l < L; ++l) {
     net.b_off[l] = off;
     off += l == L - 1 ? d->d_out : d->hidden;
   }
   net.grid_off = off;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params,
+                                const double* d_positions, const float* d_reference, int64_t n,
+                                float* d_grid_grad, float* d_inputs, float* d_preacts,
+                                float* d_deltas, double* d_loss_sum, void* stream) {
+  if (!d || !d_params || (n > 0 && (!d_positions || !d_reference || !d_inputs || !d_deltas)))
+    return fail(FVSRN_EINVAL, "null argument");
+  TrainNetDev net;
+  int rc = make_train_net(d, n, net);
+  if (rc) return rc;
   CUDA_TRY(launch_train_world(net, d_params, d_positions, d_reference, (long long)n, d_grid_grad,
                               d_inputs, d_preacts, d_deltas, d_loss_sum, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_train_screen_forward(const fvsrn_train_desc* d, const float* d_params,
+                                   const double* d_origins, const double* d_dirs, int64_t n,
+                                   const fvsrn_settings* st, float* d_pixels, double* d_color,
+                                   double* d_alpha, double* d_tmin, double* d_ds, int32_t* d_nsteps,
+                                   void* stream) {
+  if (!d || !d_params || !st || (n > 0 && (!d_origins || !d_dirs || !d_pixels || !d_color ||
+                                           !d_alpha || !d_tmin || !d_ds || !d_nsteps)))
+    return fail(FVSRN_EINVAL, "null argument");
+  if (d->head != FVSRN_HEAD_COLOR) return fail(FVSRN_EINVAL, "screen-space training requires a color-head model");
+  int rc = check_settings(st);
+  if (rc) return rc;
+  TrainNetDev net;
+  if ((rc = make_train_net(d, 0, net))) return rc;
+  const MarchDev md = march_for(st);
+  CUDA_TRY(launch_screen_forward(net, d_params, d_origins, d_dirs, (long long)n, md, d_pixels, d_color,
+                                 d_alpha, d_tmin, d_ds, d_nsteps, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_train_screen_backward(const fvsrn_train_desc* d, const float* d_params,
+                                    const double* d_origins, const double* d_dirs, int64_t n,
+                                    double eps_blend, const double* d_color, const double* d_alpha,
+                                    const double* d_tmin, const double* d_ds, const int32_t* d_nsteps,
+                                    const int64_t* d_row_offset, const float* d_image_adjoint,
+                                    const double* d_background, int64_t cap_rows, float* d_inputs,
+                                    float* d_preacts, float* d_deltas, float* d_grid_grad, void* stream) {
+  if (!d || !d_params || (n > 0 && (!d_origins || !d_dirs || !d_color || !d_alpha || !d_tmin ||
+                                    !d_ds || !d_nsteps || !d_row_offset || !d_image_adjoint ||
+                                    !d_background || !d_inputs || !d_deltas)))
+    return fail(FVSRN_EINVAL, "null argument");
+  if (d->head != FVSRN_HEAD_COLOR) return fail(FVSRN_EINVAL, "raymarch_backward trains color-head models only");
+  TrainNetDev net;
+  int rc = make_train_net(d, cap_rows, net);
+  if (rc) return rc;
+  CUDA_TRY(launch_screen_backward(net, d_params, d_origins, d_dirs, (long long)n, eps_blend, d_color,
+                                  d_alpha, d_tmin, d_ds, d_nsteps, (const long long*)d_row_offset,
+                                  d_image_adjoint, d_background, (long long)cap_rows, d_inputs, d_preacts,
+                                  d_deltas, d_grid_grad, (cudaStream_t)stream));
   count_launch();
   return FVSRN_OK;
 }
@@ -688,7 +741,7 @@ int32_t fvsrn_set_grid_sampler(int32_t mode) {
 }
 
 int32_t fvsrn_set_dvr_kernel(int32_t mode) {
-  if (mode < 0 || mode > 3) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..3");
+  if (mode < 0 || mode > 4) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..4");
   return g_dvr_mode_i.exchange(mode);
 }
 const char* fvsrn_version(void) { return "fvsrn_b200 0.1.0 (sm_100a, mma.sync f16/f32)"; }

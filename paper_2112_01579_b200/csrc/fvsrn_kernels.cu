@@ -106,6 +106,90 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
+// ---------------------------------------------------------------- software-pipelined DVR
+// dvr_kernel with the next step's input row built while the MLP of the current step
+// runs: the rows of step k+1 are a pure function of the ray (p_{k+1} = pe + (k+1) dd does
+// not depend on step k's density), so they go to a second stage buffer in the same
+// basic block as step k's MLP.  The scheduler can then interleave texture / FMA feature
+// work with the HMMA + MUFU activation work of the same warp instead of alternating
+// whole phases.  A ray that ends (or a refilled lane) rebuilds its row on the slow path.
+// Default-shape (FastRow) models only.
+template <int HID, int NM, int NL>
+__global__ void __launch_bounds__(kThreads, FVSRN_PIPE_MIN_BLOCKS)
+dvr_pipe_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+                MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+                float* __restrict__ out, unsigned long long* __restrict__ queue,
+                unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  constexpr int rs = FastRow<NM>::kK0 + 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* p = smem;
+  uint2* wf_s = reinterpret_cast<uint2*>(p);
+  p += ((size_t)net.w_total * sizeof(uint2) + 15) / 16 * 16;
+  float* b_s = reinterpret_cast<float*>(p);
+  p += ((size_t)net.b_total * sizeof(float) + 15) / 16 * 16;
+  TFDev* tf = reinterpret_cast<TFDev*>(p);
+  p += (sizeof(TFDev) + 15) / 16 * 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr size_t kStage = (size_t)kWarp * rs * sizeof(__half);
+  unsigned char* wp = p + (size_t)warp * (2 * kStage + kWarp * 4 * sizeof(float));
+  __half* stage[2] = {reinterpret_cast<__half*>(wp), reinterpret_cast<__half*>(wp + kStage)};
+  float* ob = reinterpret_cast<float*>(wp + 2 * kStage);
+  for (int i = threadIdx.x; i < net.w_total; i += blockDim.x) wf_s[i] = net.wfrag[i];
+  for (int i = threadIdx.x; i < net.b_total; i += blockDim.x) b_s[i] = net.bias[i];
+  if (b0) {
+    const int n0q = net.b_off[1] - net.b_off[0];
+    for (int i = threadIdx.x; i < n0q; i += blockDim.x) {
+      const int j = i >> 2;
+      b_s[i] = b0[(j >> 2) * 8 + 2 * (j & 3) + (i & 1)];
+    }
+  }
+  {
+    const int words = sizeof(TFDev) / 4;
+    const int* src = reinterpret_cast<const int*>(tf_g);
+    int* dst = reinterpret_cast<int*>(tf);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  {
+    uint32_t* z = reinterpret_cast<uint32_t*>(wp);
+    for (int i = lane; i < (int)(2 * kStage / 4); i += kWarp) z[i] = 0u;
+  }
+  __syncthreads();
+  const bool density = net.head == 0;
+  RayLane r{};                 // zero state: lanes without a ray build finite dummy rows
+  r.has = false;
+  LaneQueue q{0, 0, false};
+  unsigned long long evals = 0;
+  auto row_at = [&](int k, __half* st) {
+    const float kf = (float)k;
+    FastRow<NM>::template build<1>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1),
+                                   fmaf(kf, r.dd2, r.pe2), st + lane * rs);
+  };
+  int cur = 0;
+  ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+  if (r.has) row_at(r.k, stage[0]);
+  while (true) {
+    const unsigned act = __ballot_sync(0xffffffffu, r.has);
+    if (act == 0) break;
+    evals += __popc(act);
+    __syncwarp();
+    // speculative next row (every lane, no branch: one basic block with the MLP)
+    row_at(r.k + 1, stage[cur ^ 1]);
+    MLPDispatch<HID, 4, NL, fast_kt0<NM>()>::eval32(stage[cur], rs, net, wf_s, b_s, ob, lane);
+    __syncwarp();
+    bool fresh = false;
+    if (r.has) {
+      composite_step(r, *reinterpret_cast<const float4*>(ob + 4 * lane), density, *tf, md, out, nonfinite);
+      fresh = !r.has;
+    }
+    if (__any_sync(0xffffffffu, fresh)) {
+      ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+      if (fresh && r.has) row_at(r.k, stage[cur ^ 1]);   // new ray: its first sample
+    }
+    cur ^= 1;
+  }
+  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+}
+
 // ---------------------------------------------------------------- ray setup
 // One thread per slot, canonical slot order: camera ray (render.py:72-94) or explicit ray,
 // slab test and march geometry (render.py:97-106, 189-200) in f64 with explicit _rn ops,
@@ -511,6 +595,14 @@ constexpr int fast_layers(int hid) { return hid == 64 ? 6 : 4; }
 // fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode, layers =
 // fast_layers(HID)); else generic (runtime layer count and input layout)
 const void* kernel_for(KernelKind kind, int hid, bool fast) {
+  if (kind == KernelKind::kDVRPipe) {
+    if (!fast) return nullptr;
+    switch (hid) {
+      case 32: return (const void*)dvr_pipe_kernel<32, 14, 4>;
+      case 64: return (const void*)dvr_pipe_kernel<64, 30, 6>;
+      default: return nullptr;
+    }
+  }
   switch (hid) {
 #define CASE(H)                                                                              \
   case H:                                                                                    \

@@ -27,6 +27,18 @@ constexpr int min_blocks() {
   return HID <= 32 ? (DVR ? kMinBlocks : FVSRN_MIN_BLOCKS_SAMPLE) : (HID <= 64 ? FVSRN_MIN_BLOCKS_WIDE : 1);
 }
 
+// software-pipelined DVR (dvr_pipe_kernel): CTAs per SM the registers are sized for
+#ifndef FVSRN_PIPE_MIN_BLOCKS
+#define FVSRN_PIPE_MIN_BLOCKS 4
+#endif
+inline size_t pipe_smem_bytes(const NetDev& net, int k0) {
+  size_t b = ((size_t)net.w_total * 8 + 15) / 16 * 16 + ((size_t)net.b_total * 4 + 15) / 16 * 16;
+  b += (sizeof(TFDev) + 15) / 16 * 16;
+  const int rs = k0 + 8;
+  b += (size_t)(kThreads / kWarp) * (2 * (size_t)kWarp * rs * 2 + kWarp * 4 * 4);
+  return b;
+}
+
 // warp-specialised DVR: 4 producer + 4 consumer warps per CTA
 constexpr int kWsThreads = 256;
 constexpr int kWsPairs = 4;
@@ -61,7 +73,7 @@ struct RayRecs {
   float4* d;
 };
 
-enum class KernelKind { kDVR, kDVRWS, kDVRTC, kSample, kFused };
+enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kSample, kFused };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

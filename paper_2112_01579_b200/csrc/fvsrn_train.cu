@@ -17,6 +17,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "fvsrn_geometry.cuh"
 #include "fvsrn_train.cuh"
 
 namespace fvsrn {
@@ -49,6 +50,126 @@ __device__ __forceinline__ float act_grad_f(int kind, float x) {
 
 }  // namespace
 
+// Latent cell of one sample (grid.py:47-53), kept for the backward scatter.
+struct Cell {
+  int x0, y0, z0;
+  float fx, fy, fz;
+};
+
+// Per-sample cache rows: inputs of layer l at in_off[l] + row * in_l, pre-activations of
+// hidden layer l at l * cap * H + row * H, adjoints at d_off[l] + row * out_l (cap rows).
+struct CacheRef {
+  float* inputs;
+  float* preacts;
+  float* deltas;
+  long long row, cap;
+};
+
+// assemble_input (model.py:248-279) + mlp_forward (nn.py:179-192) in f32 (f64 Fourier
+// phases); leaves the raw outputs in x[0..d_out).  Caches when c.inputs != nullptr.
+__device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ params, const double (&p)[3],
+                            const CacheRef& c, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW], Cell& cell) {
+  const int L = net.layers, H = net.hidden, C = net.d_out;
+  int k = 0;
+  for (int a = 0; a < 3; ++a) x[k++] = (float)p[a];
+  for (int j = 0; j < net.m; ++j) {
+    const double ph = (double)net.bmat[3 * j] * p[0] + (double)net.bmat[3 * j + 1] * p[1] +
+                      (double)net.bmat[3 * j + 2] * p[2];
+    x[3 + j] = (float)sin(ph);
+    x[3 + net.m + j] = (float)cos(ph);
+  }
+  k = 3 + 2 * net.m;
+  const float* grid = params + net.grid_off;
+  const int R = net.grid_res, F = net.grid_ch;
+  cell = Cell{0, 0, 0, 0.f, 0.f, 0.f};
+  if (R > 0) {   // _cell_coords (grid.py:47-53) + _gather_kernel
+    const double s = (double)(R - 1);
+    const double cx = fmin(fmax(p[0], 0.0), 1.0) * s, cy = fmin(fmax(p[1], 0.0), 1.0) * s,
+                 cz = fmin(fmax(p[2], 0.0), 1.0) * s;
+    cell.x0 = min((int)cx, R - 2); cell.y0 = min((int)cy, R - 2); cell.z0 = min((int)cz, R - 2);
+    cell.fx = (float)(cx - cell.x0); cell.fy = (float)(cy - cell.y0); cell.fz = (float)(cz - cell.z0);
+    const float fx = cell.fx, fy = cell.fy, fz = cell.fz;
+    const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+    const float w[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                        fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+    const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
+    const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+    const float* b = grid + (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    for (int ch = 0; ch < F; ++ch) {
+      float acc = 0.f;
+      for (int q = 0; q < 8; ++q) acc += w[q] * b[off[q] + ch];
+      x[k + ch] = acc;
+    }
+  }
+  int in_w = net.d_in;
+  for (int l = 0; l < L; ++l) {
+    const int out_w = (l == L - 1) ? C : H;
+    if (c.inputs) {
+      float* inl = c.inputs + net.in_off[l] + c.row * in_w;
+      for (int j = 0; j < in_w; ++j) inl[j] = x[j];
+    }
+    const float* W = params + net.w_off[l];
+    const float* bb = params + net.b_off[l];
+    for (int o = 0; o < out_w; ++o) {
+      float s = bb[o];
+      const float* wr = W + (long long)o * in_w;
+      for (int j = 0; j < in_w; ++j) s = fmaf(x[j], wr[j], s);
+      y[o] = s;
+    }
+    if (l < L - 1) {
+      float* pa = c.preacts ? c.preacts + (long long)l * c.cap * H + c.row * H : nullptr;
+      for (int o = 0; o < out_w; ++o) {
+        if (pa) pa[o] = y[o];
+        x[o] = act_eval_f(net.act, y[o]);
+      }
+    } else {
+      for (int o = 0; o < out_w; ++o) x[o] = y[o];
+    }
+    in_w = out_w;
+  }
+}
+
+// mlp_backward (nn.py:234-255) from raw_bar, writing the adjoints, then the latent-grid
+// scatter (grid.py:87-137) of z_bar = x_bar[-F:] as f32 atomics.
+__device__ void f32_backward(const TrainNetDev& net, const float* __restrict__ params,
+                             const float (&raw_bar)[4], const CacheRef& c, const Cell& cell,
+                             float* __restrict__ grid_grad, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW]) {
+  const int L = net.layers, H = net.hidden, C = net.d_out;
+  for (int ch = 0; ch < C; ++ch) y[ch] = raw_bar[ch];
+  for (int l = L - 1; l >= 0; --l) {
+    const int out_w = (l == L - 1) ? C : H;
+    const int inw = (l == 0) ? net.d_in : H;
+    if (l < L - 1) {
+      const float* pa = c.preacts + (long long)l * c.cap * H + c.row * H;
+      for (int o = 0; o < out_w; ++o) y[o] *= act_grad_f(net.act, pa[o]);
+    }
+    float* dl = c.deltas + net.d_off[l] + c.row * out_w;
+    for (int o = 0; o < out_w; ++o) dl[o] = y[o];
+    const float* W = params + net.w_off[l];
+    for (int j = 0; j < inw; ++j) {
+      float s = 0.f;
+      for (int o = 0; o < out_w; ++o) s = fmaf(y[o], W[(long long)o * inw + j], s);
+      x[j] = s;
+    }
+    for (int j = 0; j < inw; ++j) y[j] = x[j];
+  }
+  const int R = net.grid_res, F = net.grid_ch;
+  if (R > 0) {
+    const float fx = cell.fx, fy = cell.fy, fz = cell.fz;
+    const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+    const float w[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                        fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+    const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
+    const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+    float* g = grid_grad + (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    const int zoff = net.d_in - F;
+    for (int ch = 0; ch < F; ++ch) {
+      const float zb = y[zoff + ch];
+      for (int q = 0; q < 8; ++q) atomicAdd(g + off[q] + ch, w[q] * zb);
+    }
+  }
+}
+
 __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ params,
                                    const double* __restrict__ pos, const float* __restrict__ ref,
                                    long long n, float* __restrict__ grid_grad,
@@ -57,115 +178,139 @@ __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ pa
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   double my_loss = 0.0;
   if (i < n) {
-    const int L = net.layers, H = net.hidden, C = net.d_out;
+    const int C = net.d_out;
     float x[kTrainMaxW], y[kTrainMaxW];
     const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-    // ---- assemble_input: [p | sin(Bp) | cos(Bp) | z]
-    int k = 0;
-    for (int a = 0; a < 3; ++a) x[k++] = (float)p[a];
-    for (int j = 0; j < net.m; ++j) {
-      const double ph = (double)net.bmat[3 * j] * p[0] + (double)net.bmat[3 * j + 1] * p[1] +
-                        (double)net.bmat[3 * j + 2] * p[2];
-      x[3 + j] = (float)sin(ph);
-      x[3 + net.m + j] = (float)cos(ph);
-    }
-    k = 3 + 2 * net.m;
-    int x0 = 0, y0 = 0, z0 = 0;
-    float fx = 0.f, fy = 0.f, fz = 0.f;
-    const float* grid = params + net.grid_off;
-    const int R = net.grid_res, F = net.grid_ch;
-    if (R > 0) {   // _cell_coords (grid.py:47-53) + _gather_kernel
-      const double s = (double)(R - 1);
-      const double cx = fmin(fmax(p[0], 0.0), 1.0) * s, cy = fmin(fmax(p[1], 0.0), 1.0) * s,
-                   cz = fmin(fmax(p[2], 0.0), 1.0) * s;
-      x0 = min((int)cx, R - 2); y0 = min((int)cy, R - 2); z0 = min((int)cz, R - 2);
-      fx = (float)(cx - x0); fy = (float)(cy - y0); fz = (float)(cz - z0);
-      const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
-      const float w[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
-                          fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
-      const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
-      const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
-      const float* b = grid + (((long long)x0 * R + y0) * R + z0) * F;
-      for (int c = 0; c < F; ++c) {
-        float acc = 0.f;
-        for (int q = 0; q < 8; ++q) acc += w[q] * b[off[q] + c];
-        x[k + c] = acc;
-      }
-      k += F;
-    }
-    // ---- mlp_forward (nn.py:179-192), caching layer inputs and pre-activations
-    int in_w = net.d_in;
-    for (int l = 0; l < L; ++l) {
-      const int out_w = (l == L - 1) ? C : H;
-      float* inl = inputs + net.in_off[l] + i * in_w;
-      for (int j = 0; j < in_w; ++j) inl[j] = x[j];
-      const float* W = params + net.w_off[l];
-      const float* bb = params + net.b_off[l];
-      for (int o = 0; o < out_w; ++o) {
-        float s = bb[o];
-        const float* wr = W + (long long)o * in_w;
-        for (int j = 0; j < in_w; ++j) s = fmaf(x[j], wr[j], s);
-        y[o] = s;
-      }
-      if (l < L - 1) {
-        float* pa = preacts + (long long)l * n * H + i * H;
-        for (int o = 0; o < out_w; ++o) { pa[o] = y[o]; x[o] = act_eval_f(net.act, y[o]); }
-      } else {
-        for (int o = 0; o < out_w; ++o) x[o] = y[o];
-      }
-      in_w = out_w;
-    }
+    const CacheRef c{inputs, preacts, deltas, i, n};
+    Cell cell;
+    f32_forward(net, params, p, c, x, y, cell);
     // ---- head, L1 loss and its adjoint (train.py:158-162), head backward
     const float inv = (float)(1.0 / ((double)n * C));
     float raw_bar[4];
-    for (int c = 0; c < C; ++c) {
-      const double r = x[c];
-      const bool softplus_ch = net.head != 0 && c == 3;
+    for (int ch = 0; ch < C; ++ch) {
+      const double r = x[ch];
+      const bool softplus_ch = net.head != 0 && ch == 3;
       const float pred = softplus_ch ? (float)(fmax(r, 0.0) + log1p(exp(-fabs(r)))) : (float)sigmoid_d(r);
-      const float diff = __fsub_rn(pred, ref[i * C + c]);
+      const float diff = __fsub_rn(pred, ref[i * C + ch]);
       my_loss += fabs((double)diff);
       const float adj = (diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f)) * inv;
       // density_head_backward / color_head_backward (model.py:346-365), f32 like numpy
-      raw_bar[c] = softplus_ch ? __fmul_rn(adj, (float)sigmoid_d(r))
-                               : __fmul_rn(__fmul_rn(adj, pred), __fsub_rn(1.f, pred));
+      raw_bar[ch] = softplus_ch ? __fmul_rn(adj, (float)sigmoid_d(r))
+                                : __fmul_rn(__fmul_rn(adj, pred), __fsub_rn(1.f, pred));
     }
-    // ---- mlp_backward (nn.py:234-255)
-    for (int c = 0; c < C; ++c) y[c] = raw_bar[c];
-    for (int l = L - 1; l >= 0; --l) {
-      const int out_w = (l == L - 1) ? C : H;
-      const int inw = (l == 0) ? net.d_in : H;
-      if (l < L - 1) {
-        const float* pa = preacts + (long long)l * n * H + i * H;
-        for (int o = 0; o < out_w; ++o) y[o] *= act_grad_f(net.act, pa[o]);
-      }
-      float* dl = deltas + net.d_off[l] + i * out_w;
-      for (int o = 0; o < out_w; ++o) dl[o] = y[o];
-      const float* W = params + net.w_off[l];
-      for (int j = 0; j < inw; ++j) {
-        float s = 0.f;
-        for (int o = 0; o < out_w; ++o) s = fmaf(y[o], W[(long long)o * inw + j], s);
-        x[j] = s;
-      }
-      for (int j = 0; j < inw; ++j) y[j] = x[j];
-    }
-    // ---- grid_sample_backward (grid.py:87-137): z_bar = x_bar[-F:]
-    if (R > 0) {
-      const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
-      const float w[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
-                          fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
-      const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
-      const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
-      float* g = grid_grad + (((long long)x0 * R + y0) * R + z0) * F;
-      const int zoff = net.d_in - F;
-      for (int c = 0; c < F; ++c) {
-        const float zb = y[zoff + c];
-        for (int q = 0; q < 8; ++q) atomicAdd(g + off[q] + c, w[q] * zb);
-      }
-    }
+    f32_backward(net, params, raw_bar, c, cell, grid_grad, x, y);
   }
   // batch L1 loss sum (train.py:158-161): warp reduce, one f64 atomic per warp
   for (int o = 16; o > 0; o >>= 1) my_loss += __shfl_down_sync(0xffffffffu, my_loss, o);
   if ((threadIdx.x & 31) == 0 && loss_sum) atomicAdd(loss_sum, my_loss);
+}
+
+// ---------------------------------------------------------------- screen space
+// raymarch_forward(ModelSource(colour model), want_states=True) (render.py:203-238):
+// f64 geometry and compositing, f32 model evaluation (the naive ModelSource path), no
+// early termination; terminal (C, A) and the per-ray geometry are kept for backward.
+__global__ void screen_forward_kernel(TrainNetDev net, const float* __restrict__ params,
+                                      const double* __restrict__ org, const double* __restrict__ dir,
+                                      long long n, MarchDev md, float* __restrict__ px,
+                                      double* __restrict__ cst, double* __restrict__ ast,
+                                      double* __restrict__ tmin_o, double* __restrict__ ds_o,
+                                      int* __restrict__ nsteps) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  RayGeom g;
+  for (int a = 0; a < 3; ++a) { g.o[a] = org[3 * i + a]; g.d[a] = dir[3 * i + a]; }
+  int ns = 0;
+  double tmin = 0.0, ds = 0.0;
+  if (march_geometry(md, g)) { ns = g.n; tmin = g.tmin; ds = g.ds; }
+  double C0 = 0.0, C1 = 0.0, C2 = 0.0, A = 0.0;
+  float x[kTrainMaxW], y[kTrainMaxW];
+  const CacheRef none{nullptr, nullptr, nullptr, 0, 0};
+  for (int k = 0; k < ns; ++k) {
+    const double tk = __dadd_rn(tmin, __dmul_rn((double)k + 0.5, ds));
+    const double p[3] = {__dadd_rn(g.o[0], __dmul_rn(tk, g.d[0])), __dadd_rn(g.o[1], __dmul_rn(tk, g.d[1])),
+                         __dadd_rn(g.o[2], __dmul_rn(tk, g.d[2]))};
+    Cell cell;
+    f32_forward(net, params, p, none, x, y, cell);
+    const double r = (float)sigmoid_d(x[0]), gg = (float)sigmoid_d(x[1]), b = (float)sigmoid_d(x[2]);
+    const double sig = (float)(fmax((double)x[3], 0.0) + log1p(exp(-fabs((double)x[3]))));
+    // composite_step (render.py:109-117)
+    double alpha = fmin(1.0 - md.eps_blend, -expm1(-sig * ds));
+    alpha = fmax(alpha, 0.0);
+    const double tr = (1.0 - A) * alpha;
+    C0 += tr * r; C1 += tr * gg; C2 += tr * b;
+    A += tr;
+  }
+  px[4 * i] = (float)(C0 + (1.0 - A) * md.bg[0]);
+  px[4 * i + 1] = (float)(C1 + (1.0 - A) * md.bg[1]);
+  px[4 * i + 2] = (float)(C2 + (1.0 - A) * md.bg[2]);
+  px[4 * i + 3] = (float)A;
+  cst[3 * i] = C0; cst[3 * i + 1] = C1; cst[3 * i + 2] = C2;
+  ast[i] = A;
+  tmin_o[i] = tmin;
+  ds_o[i] = ds;
+  nsteps[i] = ns;
+}
+
+// raymarch_backward (render.py:241-306): each thread walks its ray in reverse step
+// order, re-evaluates the model, inverts the blend to recover the previous state
+// (constant memory per ray), and writes the sample's cache rows at row off[i] + k so the
+// weight-gradient reductions are one GEMM per layer over all samples of the chunk.
+__global__ void screen_backward_kernel(TrainNetDev net, const float* __restrict__ params,
+                                       const double* __restrict__ org, const double* __restrict__ dir,
+                                       long long n, double eps_blend, const double* __restrict__ cst,
+                                       const double* __restrict__ ast, const double* __restrict__ tmin_a,
+                                       const double* __restrict__ ds_a, const int* __restrict__ nsteps,
+                                       const long long* __restrict__ row_off, const float* __restrict__ adj,
+                                       const double* __restrict__ bg, long long cap,
+                                       float* __restrict__ inputs, float* __restrict__ preacts,
+                                       float* __restrict__ deltas, float* __restrict__ grid_grad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ns = nsteps[i];
+  if (ns == 0) return;
+  double c_acc[3] = {cst[3 * i], cst[3 * i + 1], cst[3 * i + 2]};
+  double a_acc = ast[i];
+  const double tmin = tmin_a[i], ds = ds_a[i];
+  double c_bar[3] = {(double)adj[4 * i], (double)adj[4 * i + 1], (double)adj[4 * i + 2]};
+  double a_bar = (double)adj[4 * i + 3] - (c_bar[0] * bg[0] + c_bar[1] * bg[1] + c_bar[2] * bg[2]);
+  float x[kTrainMaxW], y[kTrainMaxW];
+  for (int k = ns - 1; k >= 0; --k) {
+    const double tk = __dadd_rn(tmin, __dmul_rn((double)k + 0.5, ds));
+    const double p[3] = {__dadd_rn(org[3 * i], __dmul_rn(tk, dir[3 * i])),
+                         __dadd_rn(org[3 * i + 1], __dmul_rn(tk, dir[3 * i + 1])),
+                         __dadd_rn(org[3 * i + 2], __dmul_rn(tk, dir[3 * i + 2]))};
+    const CacheRef c{inputs, preacts, deltas, row_off[i] + k, cap};
+    Cell cell;
+    f32_forward(net, params, p, c, x, y, cell);
+    float raw[4] = {x[0], x[1], x[2], x[3]};
+    const float s0 = (float)sigmoid_d(raw[0]), s1 = (float)sigmoid_d(raw[1]), s2 = (float)sigmoid_d(raw[2]);
+    const double rgb[3] = {s0, s1, s2};
+    const double sigma = (float)(fmax((double)raw[3], 0.0) + log1p(exp(-fabs((double)raw[3]))));
+    const double alpha_raw = -expm1(-sigma * ds);
+    const bool clamped = alpha_raw > 1.0 - eps_blend;
+    const double alpha = clamped ? 1.0 - eps_blend : fmax(alpha_raw, 0.0);
+    const double a_prev = (a_acc - alpha) / (1.0 - alpha);
+    const double one_m = 1.0 - a_prev;
+    double c_prev[3], dot = 0.0;
+    for (int q = 0; q < 3; ++q) {
+      c_prev[q] = c_acc[q] - (one_m * alpha) * rgb[q];
+      dot += c_bar[q] * rgb[q];
+    }
+    const double alpha_bar = a_bar * one_m + dot * one_m;
+    const double sigma_bar = clamped ? 0.0 : alpha_bar * ds * exp(-sigma * ds);
+    // color_head_backward (model.py:360-365) on the f32 head adjoint
+    float raw_bar[4];
+    const float s[3] = {s0, s1, s2};
+    for (int q = 0; q < 3; ++q) {
+      const float rb = (float)(c_bar[q] * (alpha * one_m));
+      raw_bar[q] = __fmul_rn(__fmul_rn(rb, s[q]), __fsub_rn(1.f, s[q]));
+    }
+    raw_bar[3] = __fmul_rn((float)sigma_bar, (float)sigmoid_d(raw[3]));
+    f32_backward(net, params, raw_bar, c, cell, grid_grad, x, y);
+    a_bar = a_bar * (1.0 - alpha) - dot * alpha;
+    for (int q = 0; q < 3; ++q) c_acc[q] = c_prev[q];
+    a_acc = a_prev;
+  }
 }
 
 // adam_step (nn.py:279-298) on the flat trainable buffer; non-finite gradients are
@@ -206,6 +351,29 @@ cudaError_t launch_train_world(const TrainNetDev& net, const float* params, cons
   const int threads = 128;
   train_world_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
       net, params, pos, ref, n, grid_grad, inputs, preacts, deltas, loss_sum);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_screen_forward(const TrainNetDev& net, const float* params, const double* org,
+                                  const double* dir, long long n, const MarchDev& md, float* px,
+                                  double* cst, double* ast, double* tmin, double* ds, int* nsteps,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  screen_forward_kernel<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(net, params, org, dir, n, md, px, cst,
+                                                                  ast, tmin, ds, nsteps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_screen_backward(const TrainNetDev& net, const float* params, const double* org,
+                                   const double* dir, long long n, double eps_blend, const double* cst,
+                                   const double* ast, const double* tmin, const double* ds,
+                                   const int* nsteps, const long long* row_off, const float* adj,
+                                   const double* bg, long long cap, float* inputs, float* preacts,
+                                   float* deltas, float* grid_grad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  screen_backward_kernel<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(
+      net, params, org, dir, n, eps_blend, cst, ast, tmin, ds, nsteps, row_off, adj, bg, cap, inputs,
+      preacts, deltas, grid_grad);
   return cudaGetLastError();
 }
 

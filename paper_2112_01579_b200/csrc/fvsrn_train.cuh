@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "fvsrn_kernels.cuh"
+
 namespace fvsrn {
 
 constexpr int kTrainMaxLayers = 24;
@@ -26,6 +28,16 @@ struct AdamConsts {
 cudaError_t launch_train_world(const TrainNetDev& net, const float* params, const double* pos,
                                const float* ref, long long n, float* grid_grad, float* inputs,
                                float* preacts, float* deltas, double* loss_sum, cudaStream_t s);
+cudaError_t launch_screen_forward(const TrainNetDev& net, const float* params, const double* org,
+                                  const double* dir, long long n, const MarchDev& md, float* px,
+                                  double* cst, double* ast, double* tmin, double* ds, int* nsteps,
+                                  cudaStream_t s);
+cudaError_t launch_screen_backward(const TrainNetDev& net, const float* params, const double* org,
+                                   const double* dir, long long n, double eps_blend, const double* cst,
+                                   const double* ast, const double* tmin, const double* ds,
+                                   const int* nsteps, const long long* row_off, const float* adj,
+                                   const double* bg, long long cap, float* inputs, float* preacts,
+                                   float* deltas, float* grid_grad, cudaStream_t s);
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, const AdamConsts& k,
                         unsigned long long* bad, cudaStream_t s);
 

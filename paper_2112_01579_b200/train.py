@@ -1,4 +1,4 @@
-"""World-space training on the GPU (reference train.py:26-206).
+"""World- and screen-space training on the GPU (reference train.py:26-262).
 
 Same names and semantics as the reference: ``WorldTrainConfig``, ``WorldTarget``,
 ``ErrorGrid``, ``TrainingDiverged``, ``sample_world_dataset``, ``build_error_grid``
@@ -15,8 +15,13 @@ every batch step runs on the device:
 * ``fvsrn_adam_step`` applies adam_step (nn.py:279-298) to one flat parameter buffer
   laid out like ``FvsrnModel.trainable_arrays()``.
 
-Scope: static models with position inputs (the reference's ``train_world`` callers);
-screen-space (``train_screen``) and temporal training stay on the reference.
+Screen space (``train_screen``, ``raymarch_backward``): ``fvsrn_train_screen_forward``
+marches each view with f32 model evaluation and f64 compositing keeping the terminal
+states, ``fvsrn_train_screen_backward`` walks every ray in reverse with the blend
+inversion (constant memory per ray) and writes each sample's cache rows, and one GEMM
+per layer reduces the weight gradients over all samples of the view.
+
+Scope: static models with position inputs; temporal training stays on the reference.
 """
 
 from __future__ import annotations
@@ -266,6 +271,181 @@ def train_world(model, target: WorldTarget, cfg: WorldTrainConfig, progress=None
             tr.adam(cfg.lr)
             total += loss * len(idx)
         trace.append(total / cfg.sample_count)
+        if progress is not None:
+            progress(epoch, trace[-1])
+    tr.write_back()
+    return model, trace
+
+
+# ------------------------------------------------------------------ screen space
+@dataclass
+class ScreenTrainConfig:
+    views: int = 96
+    resolution: int = 256
+    stepsize: float = 0.02
+    epochs: int = 100
+    lr: float = 0.01
+    seed: int = 0
+    reference_stepsize_voxels: float = 0.1
+    camera_radius: float = 2.2
+
+    def __post_init__(self):
+        if self.views < 1 or self.stepsize <= 0:
+            raise ValueError("need at least one view and a positive stepsize")
+
+
+@dataclass
+class GradientBuffer:
+    """Gradients in the reference's GradientBuffer shape (nn.py:207-231)."""
+
+    weights: list
+    biases: list
+    grids: list
+
+    def arrays(self) -> list:
+        return [*self.weights, *self.biases, *self.grids]
+
+
+class ScreenTrainer(WorldTrainer):
+    """Adds the screen-space forward (want_states) and constant-memory backward of a
+    colour-head model to the world trainer's device state."""
+
+    CAP_ROWS = 1 << 22          # samples per backward chunk (cache rows)
+
+    def __init__(self, model, device: int | None = None):
+        if model.config.head != "color":
+            raise ValueError("screen-space training requires a color-head model")
+        super().__init__(model, device)
+        self._cap = -1
+
+    def forward(self, origins, dirs, settings):
+        """raymarch_forward(..., want_states=True): (pixels (n,4) f32, state tuple)."""
+        from .device import settings_desc
+
+        t = self.torch
+        o = t.as_tensor(origins, dtype=t.float64, device=self.dev).reshape(-1, 3).contiguous()
+        d = t.as_tensor(dirs, dtype=t.float64, device=self.dev).reshape(-1, 3).contiguous()
+        n = len(o)
+        px = t.empty((n, 4), dtype=t.float32, device=self.dev)
+        col = t.empty((n, 3), dtype=t.float64, device=self.dev)
+        alp, tmin, ds = (t.empty(n, dtype=t.float64, device=self.dev) for _ in range(3))
+        ns = t.empty(n, dtype=t.int32, device=self.dev)
+        stream = t.cuda.current_stream(self.dev).cuda_stream
+        ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+        L.check(L.lib().fvsrn_train_screen_forward(
+            C.byref(self.desc), ptr(self.params), ptr(o), ptr(d), n, C.byref(settings_desc(settings)),
+            ptr(px), ptr(col), ptr(alp), ptr(tmin), ptr(ds), ptr(ns), C.c_void_p(stream)))
+        return px, (o, d, col, alp, tmin, ds, ns)
+
+    def _cache(self, rows: int):
+        if rows > self._cap:
+            t = self.torch
+            self.c_inputs = t.empty(rows * sum(self.widths_in), dtype=t.float32, device=self.dev)
+            self.c_deltas = t.empty(rows * sum(self.widths_out), dtype=t.float32, device=self.dev)
+            self.c_preacts = t.empty(max(1, (self.n_layers - 1) * rows * self.model.config.hidden),
+                                     dtype=t.float32, device=self.dev)
+            self._cap = rows
+
+    def backward(self, state, settings, image_adjoint) -> None:
+        """raymarch_backward (render.py:241-306) into self.grads (zeroed first)."""
+        t = self.torch
+        o, d, col, alp, tmin, ds, ns = state
+        adj = t.as_tensor(image_adjoint, dtype=t.float32, device=self.dev).reshape(-1, 4).contiguous()
+        if not bool(t.isfinite(adj).all()):
+            raise ValueError("non-finite image adjoint")
+        bg = t.tensor(list(settings.background), dtype=t.float64, device=self.dev)
+        self.grads.zero_()
+        steps = ns.to(t.int64)
+        n_host = steps.cpu().numpy()
+        stream = t.cuda.current_stream(self.dev).cuda_stream
+        ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+        grid_ptr = (C.c_void_p(self.grads.data_ptr() + 4 * self.grid_off)
+                    if self.model.config.grid_resolution else None)
+        lo, n = 0, len(n_host)
+        while lo < n:              # ray chunks whose samples fit the cache
+            csum = np.cumsum(n_host[lo:])
+            hi = lo + max(1, int(np.searchsorted(csum, self.CAP_ROWS, side="right")))
+            rows = int(csum[hi - lo - 1])
+            if rows:
+                self._cache(rows)
+                off = t.cumsum(steps[lo:hi], 0) - steps[lo:hi]
+                L.check(L.lib().fvsrn_train_screen_backward(
+                    C.byref(self.desc), ptr(self.params), C.c_void_p(o.data_ptr() + 24 * lo),
+                    C.c_void_p(d.data_ptr() + 24 * lo), hi - lo, float(settings.eps_blend),
+                    C.c_void_p(col.data_ptr() + 24 * lo), C.c_void_p(alp.data_ptr() + 8 * lo),
+                    C.c_void_p(tmin.data_ptr() + 8 * lo), C.c_void_p(ds.data_ptr() + 8 * lo),
+                    C.c_void_p(ns.data_ptr() + 4 * lo), ptr(off), C.c_void_p(adj.data_ptr() + 16 * lo),
+                    ptr(bg), self._cap, ptr(self.c_inputs), ptr(self.c_preacts), ptr(self.c_deltas),
+                    grid_ptr, C.c_void_p(stream)))
+                io = do = 0
+                for l in range(self.n_layers):   # nn.py:252-253 summed over every sample
+                    wi, wo = self.widths_in[l], self.widths_out[l]
+                    x = self.c_inputs[io:io + self._cap * wi].view(self._cap, wi)[:rows]
+                    dl = self.c_deltas[do:do + self._cap * wo].view(self._cap, wo)[:rows]
+                    w0, w1 = self._views[l]
+                    b0, b1 = self._views[self.n_layers + l]
+                    gw = self.grads[w0:w1].view(wo, wi)
+                    gw.addmm_(dl.t(), x)
+                    self.grads[b0:b1].add_(dl.sum(dim=0))
+                    io += self._cap * wi
+                    do += self._cap * wo
+            lo = hi
+
+    def gradient_buffer(self) -> GradientBuffer:
+        flat = self.grads.cpu().numpy()
+        arrs = [flat[lo:hi].reshape(shape) for (lo, hi), shape in zip(self._views, self.shapes)]
+        L_ = self.n_layers
+        return GradientBuffer(arrs[:L_], arrs[L_:2 * L_], arrs[2 * L_:])
+
+
+def raymarch_backward(model, origins, dirs, settings, image_adjoint, terminal_states=None,
+                      t=None, grads=None) -> GradientBuffer:
+    """Adjoint of raymarch_forward for a colour-head model (render.py:241-306) on the GPU:
+    constant memory per ray (blend inversion), f32 model re-evaluation."""
+    if t is not None:
+        raise ValueError("the GPU trainer handles static models")
+    tr = ScreenTrainer(model)
+    _, state = tr.forward(origins, dirs, settings)
+    tr.backward(state, settings, image_adjoint)
+    g = tr.gradient_buffer()
+    if grads is not None:
+        for acc, x in zip(grads.arrays(), g.arrays()):
+            acc += x
+        return grads
+    return g
+
+
+def train_screen(model, volume, tf, cfg: ScreenTrainConfig, progress=None):
+    """Image-space training: L1 against pre-rendered reference views (train.py:227-262)."""
+    import torch
+
+    from .render import RenderSettings, VolumeSource, camera_rays, fibonacci_cameras, raymarch_forward
+
+    if model.config.head != "color":
+        raise ValueError("screen-space training requires a color-head model")
+    cams = fibonacci_cameras(cfg.views, cfg.resolution, cfg.resolution, radius=cfg.camera_radius)
+    ref_settings = RenderSettings.for_voxels(volume.resolution, cfg.reference_stepsize_voxels)
+    tr = ScreenTrainer(model)
+    vsrc = VolumeSource(volume, tf)
+    references = []
+    for cam in cams:
+        o, d = camera_rays(cam)
+        pix, _ = raymarch_forward(vsrc, o, d, ref_settings)
+        references.append((o, d, torch.as_tensor(pix, device=tr.dev)))
+    settings = RenderSettings(stepsize=cfg.stepsize)
+    trace = []
+    for epoch in range(cfg.epochs):
+        total = 0.0
+        for o, d, ref in references:
+            pix, state = tr.forward(o, d, settings)
+            diff = pix - ref
+            loss = float(diff.abs().mean())
+            if not np.isfinite(loss):
+                raise TrainingDiverged(epoch, "non-finite loss")
+            tr.backward(state, settings, torch.sign(diff) / diff.numel())
+            tr.adam(cfg.lr)
+            total += loss
+        trace.append(total / len(references))
         if progress is not None:
             progress(epoch, trace[-1])
     tr.write_back()

@@ -284,6 +284,32 @@ def main():
         arrays[f"train_final_{name}"] = np.concatenate([a.reshape(-1) for a in model.trainable_arrays()])
         print("train", name, trace, flush=True)
 
+    # --- screen-space training (train.py:227-262): raymarch_backward (render.py:241-306)
+    # of a colour model against a VolumeSource reference view, and a short trace
+    from fvsrn.render import raymarch_backward
+    from fvsrn.train import ScreenTrainConfig, train_screen
+
+    model = model_init(ModelConfig(**CONFIGS["color_pos"]))
+    cam = fibonacci_cameras(8, 12, 12)[1]
+    o, d = camera_rays(cam)
+    st = RenderSettings(stepsize=0.05)
+    ref_px, _ = raymarch_forward(VolumeSource(vol, TF_PRESETS["warm"]), o, d,
+                                 RenderSettings.for_voxels(24, 0.5))
+    px, states = raymarch_forward(ModelSource(model), o, d, st, want_states=True)
+    loss, adj = _l1_and_adjoint(px, ref_px)
+    grads = raymarch_backward(model, o, d, st, adj, terminal_states=states)
+    arrays["screen_o"], arrays["screen_d"] = o, d
+    arrays["screen_px"], arrays["screen_ref"], arrays["screen_adj"] = px, ref_px, adj
+    arrays["screen_state_c"], arrays["screen_state_a"] = states.color, states.alpha
+    arrays["screen_grads"] = np.concatenate([g.reshape(-1) for g in grads.arrays()])
+    meta["screen"] = {"stepsize": 0.05, "loss": loss}
+    model = model_init(ModelConfig(**CONFIGS["color_pos"]))
+    _, trace = train_screen(model, vol, TF_PRESETS["warm"],
+                            ScreenTrainConfig(views=2, resolution=12, stepsize=0.05, epochs=3,
+                                              reference_stepsize_voxels=0.5))
+    arrays["screen_trace"] = np.asarray(trace)
+    print("screen", trace, flush=True)
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

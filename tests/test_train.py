@@ -118,3 +118,45 @@ def test_train_world_trace_vs_reference(name):
     # the trained parameters reached the model and its render copy was refreshed
     after = P.eval_density(m, arrays()["train_pos_cfg1"][:64])
     assert not np.allclose(before, after)
+
+
+# ------------------------------------------------------------------ screen space
+@pytest.mark.gpu
+def test_screen_forward_states_and_backward_vs_reference():
+    from paper_2112_01579_b200.train import ScreenTrainer
+
+    a = arrays()
+    m = _model("color_pos")
+    st = P.RenderSettings(stepsize=meta()["screen"]["stepsize"])
+    tr = ScreenTrainer(m)
+    px, state = tr.forward(a["screen_o"], a["screen_d"], st)
+    # raymarch_forward(want_states=True): f32 model, f64 compositing, no ET
+    np.testing.assert_allclose(px.cpu().numpy(), a["screen_px"], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(state[2].cpu().numpy(), a["screen_state_c"], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(state[3].cpu().numpy(), a["screen_state_a"], rtol=0, atol=2e-6)
+    tr.backward(state, st, a["screen_adj"])
+    got, want = tr.grads.cpu().numpy(), a["screen_grads"]
+    off = 0
+    for arr in m.trainable_arrays():
+        g, w = got[off:off + arr.size], want[off:off + arr.size]
+        scale = float(np.abs(w).max()) or 1.0
+        assert np.abs(g - w).max() <= 1e-4 * scale, (arr.shape, np.abs(g - w).max(), scale)
+        off += arr.size
+    # the functional API returns the reference's GradientBuffer shape
+    gb = P.raymarch_backward(m, a["screen_o"], a["screen_d"], st, a["screen_adj"])
+    assert [g.shape for g in gb.arrays()] == [x.shape for x in m.trainable_arrays()]
+
+
+@pytest.mark.gpu
+def test_train_screen_trace_vs_reference():
+    m = _model("color_pos")
+    vol = P.ScalarVolume(arrays()["train_volume"])
+    cfg = P.ScreenTrainConfig(views=2, resolution=12, stepsize=0.05, epochs=3,
+                              reference_stepsize_voxels=0.5)
+    _, trace = P.train_screen(m, vol, P.TF_PRESETS["warm"], cfg)
+    want = arrays()["screen_trace"]
+    assert abs(trace[0] - want[0]) <= 1e-4 * want[0]
+    np.testing.assert_allclose(trace, want, rtol=3e-2)
+    assert trace[-1] < trace[0]
+    with pytest.raises(ValueError):
+        P.train_screen(_model("cfg1"), vol, P.TF_PRESETS["warm"], cfg)

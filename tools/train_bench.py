@@ -50,3 +50,39 @@ for e in range(5):
     print(f"epoch {e} loss {loss:.5f} {1e3 * ts[-1]:.1f} ms")
 print(f"train_world epoch (64^3 samples, batch 16384): median {1e3 * sorted(ts)[2]:.1f} ms "
       f"-> {n / sorted(ts)[2] / 1e6:.1f} M samples/s")
+
+# ---- screen space: colour model (4x32, 32^3x16 grid), 256^2 views, stepsize 0.02
+from paper_2112_01579_b200.train import ScreenTrainer  # noqa: E402
+
+mc = P.model_init(P.ModelConfig(head="color", layers=4, hidden=32, grid_resolution=32,
+                                grid_channels=16, seed=0))
+st = ScreenTrainer(mc)
+settings = P.RenderSettings(stepsize=0.02)
+cams = P.fibonacci_cameras(8, 256, 256)
+vsrc = P.VolumeSource(vol, P.TF_PRESETS["warm"])
+refs = []
+for cam in cams:
+    o, d = P.camera_rays(cam)
+    pix, _ = P.raymarch_forward(vsrc, o, d, P.RenderSettings.for_voxels(64, 0.1))
+    refs.append((o, d, torch.as_tensor(pix, device=st.dev)))
+
+
+def screen_epoch():
+    tot = 0.0
+    for o, d, ref in refs:
+        pix, state = st.forward(o, d, settings)
+        diff = pix - ref
+        tot += float(diff.abs().mean())
+        st.backward(state, settings, torch.sign(diff) / diff.numel())
+        st.adam(0.01)
+    return tot / len(refs)
+
+
+screen_epoch()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(3):
+    loss = screen_epoch()
+torch.cuda.synchronize()
+dt = (time.perf_counter() - t0) / 3
+print(f"train_screen epoch (8 views 256^2, stepsize 0.02): {1e3 * dt:.1f} ms ({1e3 * dt / 8:.2f} ms/view), loss {loss:.5f}")
