@@ -136,16 +136,24 @@ typedef struct {
   int32_t fourier_m;                 /* rows of the (m,3) spatial Fourier matrix */
   const float* d_b_matrix;           /* device (m,3) f32, or NULL when m == 0 */
   int32_t grid_resolution, grid_channels;
+  /* temporal models (model.py:190-245): 0 keyframes = static.  Host pointers. */
+  int32_t n_keyframes;               /* <= 16; the grids follow each other in params */
+  const double* keyframe_times;
+  int32_t time_mode;                 /* 0 none, 1 direct, 2 fourier, 3 both */
+  int32_t time_fourier_count;
+  const float* time_b;               /* (time_fourier_count, 1) */
+  double time_t0, time_t1;           /* normalisation span (time_range or keyframe span) */
 } fvsrn_train_desc;
 
-/* One batch of n positions (device f64 (n,3)) against reference values (device f32
- * (n,d_out)): forward with cached layer inputs (d_inputs: per layer n x in_l floats,
+/* One batch of n positions (device f64 (n,3); timesteps d_times (n) f64 for temporal
+ * models, else NULL) against reference values (device f32 (n,d_out)): forward with cached layer inputs (d_inputs: per layer n x in_l floats,
  * consecutive), pre-activations (d_preacts: (L-1) x n x hidden) and adjoints (d_deltas:
  * per layer n x out_l); the L1-loss sum is added to *d_loss_sum; the latent-grid
  * gradient is scatter-added into d_grid_grad (zero it first).  Weight/bias gradients are
  * the batch reductions delta_l^T @ inputs_l and sum(delta_l) (nn.py:252-253). */
 FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const float* d_params,
-                                          const double* d_positions, const float* d_reference,
+                                          const double* d_positions, const double* d_times,
+                                          const float* d_reference,
                                           int64_t n, float* d_grid_grad, float* d_inputs,
                                           float* d_preacts, float* d_deltas, double* d_loss_sum,
                                           void* stream);

@@ -22,6 +22,6 @@ from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera
                      render_rays)
 from .transfer import TF_PRESETS, TransferFunction, tf_eval, tf_from_json, tf_load, tf_save
 from .volume import ScalarVolume, sample_volume
-from .train import (ErrorGrid, ScreenTrainConfig, TrainingDiverged, WorldTarget, WorldTrainConfig,
-                    build_error_grid, raymarch_backward, sample_world_dataset, train_screen,
-                    train_world)
+from .train import (ErrorGrid, ScreenTrainConfig, TemporalTrainConfig, TrainingDiverged, WorldTarget,
+                    WorldTrainConfig, build_error_grid, raymarch_backward, sample_world_dataset,
+                    train_screen, train_temporal, train_world)

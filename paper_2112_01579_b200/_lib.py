@@ -82,7 +82,8 @@ EXPORTS = {
     "fvsrn_last_error": (C.c_char_p, []),
     "fvsrn_set_dvr_kernel": (C.c_int32, [C.c_int32]),
     "fvsrn_set_grid_sampler": (C.c_int32, [C.c_int32]),
-    "fvsrn_train_world_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+    "fvsrn_train_world_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_int64,
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p]),
     "fvsrn_train_screen_forward": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
@@ -141,7 +142,10 @@ class TrainDesc(C.Structure):
     _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("d_in", C.c_int32),
                 ("d_out", C.c_int32), ("activation", C.c_int32), ("head", C.c_int32),
                 ("fourier_m", C.c_int32), ("d_b_matrix", C.c_void_p),
-                ("grid_resolution", C.c_int32), ("grid_channels", C.c_int32)]
+                ("grid_resolution", C.c_int32), ("grid_channels", C.c_int32),
+                ("n_keyframes", C.c_int32), ("keyframe_times", C.POINTER(C.c_double)),
+                ("time_mode", C.c_int32), ("time_fourier_count", C.c_int32),
+                ("time_b", C.POINTER(C.c_float)), ("time_t0", C.c_double), ("time_t1", C.c_double)]
 
 
 _LIB = None

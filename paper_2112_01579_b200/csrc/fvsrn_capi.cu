@@ -614,14 +614,28 @@ static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev
   if (L < 1 || L > kTrainMaxLayers) return fail(FVSRN_EINVAL, "layer count out of range");
   if (d->hidden > 256 || d->d_in > 256 || d->d_out < 1 || d->d_out > 4)
     return fail(FVSRN_ECAPACITY, "network too wide for the training kernel");
-  if (d->d_in != 3 + 2 * d->fourier_m + (d->grid_resolution > 0 ? d->grid_channels : 0))
-    return fail(FVSRN_EINVAL, "input width does not match a static position-input model");
+  const int tl = d->time_mode == 0 ? 0 : ((d->time_mode & 1) ? 1 : 0) + ((d->time_mode & 2) ? 2 * d->time_fourier_count : 0);
+  if (d->d_in != 3 + 2 * d->fourier_m + tl + (d->grid_resolution > 0 ? d->grid_channels : 0))
+    return fail(FVSRN_EINVAL, "input width does not match a position-input model");
+  if (d->n_keyframes < 0 || d->n_keyframes > 16 || (d->n_keyframes > 0 && !d->keyframe_times))
+    return fail(FVSRN_EINVAL, "keyframes: 0..16 with their times");
+  if (d->n_keyframes > 0 && d->grid_resolution < 2) return fail(FVSRN_EINVAL, "temporal models need a grid");
+  if (d->time_mode < 0 || d->time_mode > 3 || d->time_fourier_count > 16 ||
+      ((d->time_mode & 2) && !d->time_b))
+    return fail(FVSRN_EINVAL, "bad time features");
   if (d->fourier_m > 0 && !d->d_b_matrix) return fail(FVSRN_EINVAL, "Fourier matrix required");
   if (d->grid_resolution == 1) return fail(FVSRN_EINVAL, "need R >= 2");
   net = TrainNetDev{};
   net.layers = L; net.hidden = d->hidden; net.d_in = d->d_in; net.d_out = d->d_out;
   net.act = d->activation; net.head = d->head; net.m = d->fourier_m; net.bmat = d->d_b_matrix;
   net.grid_res = d->grid_resolution; net.grid_ch = d->grid_channels;
+  net.n_kf = d->n_keyframes;
+  for (int k = 0; k < d->n_keyframes; ++k) net.kf_times[k] = d->keyframe_times[k];
+  net.time_mode = d->time_mode;
+  net.time_l = (d->time_mode & 2) ? d->time_fourier_count : 0;
+  for (int j = 0; j < net.time_l; ++j) net.time_b[j] = d->time_b[j];
+  net.t0 = d->time_t0;
+  net.t1 = d->time_t1;
   long long off = 0, io = 0, dof = 0;
   for (int l = 0; l < L; ++l) {
     const long long in_l = l == 0 ? d->d_in : d->hidden, out_l = l == L - 1 ? d->d_out : d->hidden;
@@ -641,7 +655,8 @@ static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev
 }
 
 int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params,
-                                const double* d_positions, const float* d_reference, int64_t n,
+                                const double* d_positions, const double* d_times,
+                                const float* d_reference, int64_t n,
                                 float* d_grid_grad, float* d_inputs, float* d_preacts,
                                 float* d_deltas, double* d_loss_sum, void* stream) {
   if (!d || !d_params || (n > 0 && (!d_positions || !d_reference || !d_inputs || !d_deltas)))
@@ -649,7 +664,9 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
   TrainNetDev net;
   int rc = make_train_net(d, n, net);
   if (rc) return rc;
-  CUDA_TRY(launch_train_world(net, d_params, d_positions, d_reference, (long long)n, d_grid_grad,
+  if (net.n_kf > 0 && n > 0 && !d_times) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
+  CUDA_TRY(launch_train_world(net, d_params, d_positions, net.n_kf > 0 ? d_times : nullptr, d_reference,
+                              (long long)n, d_grid_grad,
                               d_inputs, d_preacts, d_deltas, d_loss_sum, (cudaStream_t)stream));
   count_launch();
   return FVSRN_OK;
@@ -664,6 +681,7 @@ int32_t fvsrn_train_screen_forward(const fvsrn_train_desc* d, const float* d_par
                                            !d_alpha || !d_tmin || !d_ds || !d_nsteps)))
     return fail(FVSRN_EINVAL, "null argument");
   if (d->head != FVSRN_HEAD_COLOR) return fail(FVSRN_EINVAL, "screen-space training requires a color-head model");
+  if (d->n_keyframes > 0 || d->time_mode != 0) return fail(FVSRN_EINVAL, "screen-space training is static");
   int rc = check_settings(st);
   if (rc) return rc;
   TrainNetDev net;

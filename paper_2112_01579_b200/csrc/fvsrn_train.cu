@@ -54,6 +54,8 @@ __device__ __forceinline__ float act_grad_f(int kind, float x) {
 struct Cell {
   int x0, y0, z0;
   float fx, fy, fz;
+  int klo, khi;     // keyframe bracket (temporal), weight wk of khi
+  float wk;
 };
 
 // Per-sample cache rows: inputs of layer l at in_off[l] + row * in_l, pre-activations of
@@ -67,8 +69,22 @@ struct CacheRef {
 
 // assemble_input (model.py:248-279) + mlp_forward (nn.py:179-192) in f32 (f64 Fourier
 // phases); leaves the raw outputs in x[0..d_out).  Caches when c.inputs != nullptr.
+// keyframe bracket of a timestep (model.py:200-209): (lo, hi, w), w = 0 when lo == hi
+__device__ void kf_bracket(const TrainNetDev& net, double t, int& lo, int& hi, float& w) {
+  const int K = net.n_kf;
+  const double tc = fmin(fmax(t, net.kf_times[0]), net.kf_times[K - 1]);
+  int h = 0;
+  while (h < K && net.kf_times[h] < tc) ++h;     // searchsorted(side="left")
+  h = min(h, K - 1);
+  const int l = (h > 0 && net.kf_times[h] != tc) ? h - 1 : h;
+  lo = l;
+  hi = h;
+  w = h > l ? (float)((tc - net.kf_times[l]) / (net.kf_times[h] - net.kf_times[l])) : 0.f;
+}
+
 __device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ params, const double (&p)[3],
-                            const CacheRef& c, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW], Cell& cell) {
+                            double t, const CacheRef& c, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW],
+                            Cell& cell) {
   const int L = net.layers, H = net.hidden, C = net.d_out;
   int k = 0;
   for (int a = 0; a < 3; ++a) x[k++] = (float)p[a];
@@ -79,9 +95,22 @@ __device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ pa
     x[3 + net.m + j] = (float)cos(ph);
   }
   k = 3 + 2 * net.m;
-  const float* grid = params + net.grid_off;
+  if (net.time_mode != 0) {   // _time_features (model.py:236-245)
+    const double tn = net.t1 == net.t0 ? 0.0 : (fmin(fmax(t, net.t0), net.t1) - net.t0) / (net.t1 - net.t0);
+    if (net.time_mode & 1) x[k++] = (float)tn;
+    if (net.time_mode & 2) {
+      for (int j = 0; j < net.time_l; ++j) x[k + j] = (float)sin(tn * (double)net.time_b[j]);
+      for (int j = 0; j < net.time_l; ++j) x[k + net.time_l + j] = (float)cos(tn * (double)net.time_b[j]);
+      k += 2 * net.time_l;
+    }
+  }
   const int R = net.grid_res, F = net.grid_ch;
-  cell = Cell{0, 0, 0, 0.f, 0.f, 0.f};
+  int klo = 0, khi = 0;
+  float wk = 0.f;
+  if (net.n_kf > 0) kf_bracket(net, t, klo, khi, wk);
+  const long long gsz = (long long)R * R * R * F;
+  const float* grid = params + net.grid_off + klo * gsz;
+  cell = Cell{0, 0, 0, 0.f, 0.f, 0.f, klo, khi, wk};
   if (R > 0) {   // _cell_coords (grid.py:47-53) + _gather_kernel
     const double s = (double)(R - 1);
     const double cx = fmin(fmax(p[0], 0.0), 1.0) * s, cy = fmin(fmax(p[1], 0.0), 1.0) * s,
@@ -94,10 +123,17 @@ __device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ pa
                         fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
     const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
     const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
-    const float* b = grid + (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    const long long base = (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    const float* b = grid + base;
+    const float* b2 = params + net.grid_off + khi * gsz + base;
     for (int ch = 0; ch < F; ++ch) {
       float acc = 0.f;
       for (int q = 0; q < 8; ++q) acc += w[q] * b[off[q] + ch];
+      if (khi != klo) {   // (1 - w) z_lo + w z_hi in f32 (model.py:219-233)
+        float acc2 = 0.f;
+        for (int q = 0; q < 8; ++q) acc2 += w[q] * b2[off[q] + ch];
+        acc = __fadd_rn(__fmul_rn(__fsub_rn(1.f, wk), acc), __fmul_rn(wk, acc2));
+      }
       x[k + ch] = acc;
     }
   }
@@ -161,17 +197,27 @@ __device__ void f32_backward(const TrainNetDev& net, const float* __restrict__ p
                         fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
     const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
     const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
-    float* g = grid_grad + (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    const long long gsz = (long long)R * R * R * F;
+    const long long base = (((long long)cell.x0 * R + cell.y0) * R + cell.z0) * F;
+    float* g = grid_grad + cell.klo * gsz + base;
+    float* g2 = grid_grad + cell.khi * gsz + base;
     const int zoff = net.d_in - F;
+    const bool two = cell.khi != cell.klo;   // model.py:318-333: (1-w) zb -> lo, w zb -> hi
     for (int ch = 0; ch < F; ++ch) {
       const float zb = y[zoff + ch];
-      for (int q = 0; q < 8; ++q) atomicAdd(g + off[q] + ch, w[q] * zb);
+      const float zl = two ? __fmul_rn(__fsub_rn(1.f, cell.wk), zb) : zb;
+      for (int q = 0; q < 8; ++q) atomicAdd(g + off[q] + ch, w[q] * zl);
+      if (two) {
+        const float zh = __fmul_rn(cell.wk, zb);
+        for (int q = 0; q < 8; ++q) atomicAdd(g2 + off[q] + ch, w[q] * zh);
+      }
     }
   }
 }
 
 __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ params,
-                                   const double* __restrict__ pos, const float* __restrict__ ref,
+                                   const double* __restrict__ pos, const double* __restrict__ times,
+                                   const float* __restrict__ ref,
                                    long long n, float* __restrict__ grid_grad,
                                    float* __restrict__ inputs, float* __restrict__ preacts,
                                    float* __restrict__ deltas, double* __restrict__ loss_sum) {
@@ -183,7 +229,7 @@ __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ pa
     const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
     const CacheRef c{inputs, preacts, deltas, i, n};
     Cell cell;
-    f32_forward(net, params, p, c, x, y, cell);
+    f32_forward(net, params, p, times ? times[i] : 0.0, c, x, y, cell);
     // ---- head, L1 loss and its adjoint (train.py:158-162), head backward
     const float inv = (float)(1.0 / ((double)n * C));
     float raw_bar[4];
@@ -230,7 +276,7 @@ __global__ void screen_forward_kernel(TrainNetDev net, const float* __restrict__
     const double p[3] = {__dadd_rn(g.o[0], __dmul_rn(tk, g.d[0])), __dadd_rn(g.o[1], __dmul_rn(tk, g.d[1])),
                          __dadd_rn(g.o[2], __dmul_rn(tk, g.d[2]))};
     Cell cell;
-    f32_forward(net, params, p, none, x, y, cell);
+    f32_forward(net, params, p, 0.0, none, x, y, cell);
     const double r = (float)sigmoid_d(x[0]), gg = (float)sigmoid_d(x[1]), b = (float)sigmoid_d(x[2]);
     const double sig = (float)(fmax((double)x[3], 0.0) + log1p(exp(-fabs((double)x[3]))));
     // composite_step (render.py:109-117)
@@ -281,7 +327,7 @@ __global__ void screen_backward_kernel(TrainNetDev net, const float* __restrict_
                          __dadd_rn(org[3 * i + 2], __dmul_rn(tk, dir[3 * i + 2]))};
     const CacheRef c{inputs, preacts, deltas, row_off[i] + k, cap};
     Cell cell;
-    f32_forward(net, params, p, c, x, y, cell);
+    f32_forward(net, params, p, 0.0, c, x, y, cell);
     float raw[4] = {x[0], x[1], x[2], x[3]};
     const float s0 = (float)sigmoid_d(raw[0]), s1 = (float)sigmoid_d(raw[1]), s2 = (float)sigmoid_d(raw[2]);
     const double rgb[3] = {s0, s1, s2};
@@ -345,12 +391,13 @@ __global__ void count_nonfinite_kernel(const float* __restrict__ g, long long n,
 }
 
 cudaError_t launch_train_world(const TrainNetDev& net, const float* params, const double* pos,
-                               const float* ref, long long n, float* grid_grad, float* inputs,
-                               float* preacts, float* deltas, double* loss_sum, cudaStream_t s) {
+                               const double* times, const float* ref, long long n, float* grid_grad,
+                               float* inputs, float* preacts, float* deltas, double* loss_sum,
+                               cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int threads = 128;
   train_world_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
-      net, params, pos, ref, n, grid_grad, inputs, preacts, deltas, loss_sum);
+      net, params, pos, times, ref, n, grid_grad, inputs, preacts, deltas, loss_sum);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,14 @@ struct TrainNetDev {
   int m;                    // spatial Fourier rows (B is m x 3, f32)
   const float* bmat;
   int grid_res, grid_ch;
-  long long grid_off;
+  long long grid_off;           // first grid; keyframe k at grid_off + k * R^3 * F
+  // temporal models (model.py:190-245): keyframe times, time features
+  int n_kf;                     // 0: static
+  double kf_times[16];
+  int time_mode;                // 0 none, 1 direct, 2 fourier, 3 both
+  int time_l;                   // fourier rows (time_fourier_count)
+  float time_b[16];             // time encoder B (L x 1)
+  double t0, t1;                // normalisation span
   long long w_off[kTrainMaxLayers], b_off[kTrainMaxLayers];
   long long in_off[kTrainMaxLayers], d_off[kTrainMaxLayers];
 };
@@ -26,7 +33,7 @@ struct AdamConsts {
 };
 
 cudaError_t launch_train_world(const TrainNetDev& net, const float* params, const double* pos,
-                               const float* ref, long long n, float* grid_grad, float* inputs,
+                               const double* times, const float* ref, long long n, float* grid_grad, float* inputs,
                                float* preacts, float* deltas, double* loss_sum, cudaStream_t s);
 cudaError_t launch_screen_forward(const TrainNetDev& net, const float* params, const double* org,
                                   const double* dir, long long n, const MarchDev& md, float* px,

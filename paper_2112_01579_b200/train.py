@@ -21,13 +21,16 @@ states, ``fvsrn_train_screen_backward`` walks every ray in reverse with the blen
 inversion (constant memory per ray) and writes each sample's cache rows, and one GEMM
 per layer reduces the weight gradients over all samples of the view.
 
-Scope: static models with position inputs; temporal training stays on the reference.
+Temporal models (``train_temporal``): per-sample timesteps drive the time features and
+the keyframe bracket; the latent scatter goes to both bracketing grids.
+
+Scope: position-input models (``train_world`` / ``train_temporal`` targets are positions).
 """
 
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -142,8 +145,8 @@ class WorldTrainer:
         import torch
 
         cfg = model.config
-        if cfg.is_temporal or cfg.direction_mode != "pos":
-            raise ValueError("the GPU world trainer handles static, position-input models")
+        if cfg.direction_mode != "pos":
+            raise ValueError("the GPU world trainer handles position-input models")
         if cfg.fourier_mode not in ("off", "nerf", "random") or (
                 model.spatial_encoder.m > 0 and model.spatial_encoder.b_matrix.shape[1] != 3):
             raise ValueError("unsupported spatial encoder")
@@ -172,6 +175,18 @@ class WorldTrainer:
                                 _ACT[cfg.activation], 0 if cfg.head == "density" else 1, m,
                                 self.bmat.data_ptr() if m > 0 else None,
                                 cfg.grid_resolution, cfg.grid_channels if cfg.grid_resolution else 0)
+        if model.is_temporal:      # model.py:190-245 (host arrays kept alive with the desc)
+            self._kf = np.ascontiguousarray(model.keyframes.times, dtype=np.float64)
+            mode = {"none": 0, "direct": 1, "fourier": 2, "both": 3}[cfg.time_mode]
+            self._tb = (np.ascontiguousarray(model.time_encoder.b_matrix, dtype=np.float32).reshape(-1)
+                        if mode & 2 else np.zeros(1, np.float32))
+            t0, t1 = cfg.time_range if cfg.time_range is not None else model.keyframes.span
+            self.desc.n_keyframes = len(self._kf)
+            self.desc.keyframe_times = L.dptr(self._kf)
+            self.desc.time_mode = mode
+            self.desc.time_fourier_count = cfg.time_fourier_count
+            self.desc.time_b = L.fptr(self._tb)
+            self.desc.time_t0, self.desc.time_t1 = float(t0), float(t1)
         self.widths_in = [cfg.input_width] + [cfg.hidden] * (n_layers - 1)
         self.widths_out = [cfg.hidden] * (n_layers - 1) + [cfg.output_width]
         self._scratch_n = -1
@@ -187,10 +202,15 @@ class WorldTrainer:
                                    dtype=t.float32, device=self.dev)
             self._scratch_n = n
 
-    def gradients(self, positions, reference) -> float:
-        """Fill self.grads for one batch (device tensors or numpy); returns the batch
-        L1 loss (mean over samples and channels, train.py:158-161)."""
+    def gradients(self, positions, reference, times=None) -> float:
+        """Fill self.grads for one batch (device tensors or numpy; ``times`` per sample for
+        temporal models); returns the batch L1 loss (mean over samples and channels,
+        train.py:158-161)."""
         t = self.torch
+        if self.model.is_temporal != (times is not None):
+            raise ValueError("temporal models need per-sample times (and only they)")
+        tt = (t.as_tensor(times, dtype=t.float64, device=self.dev).reshape(-1).contiguous()
+              if times is not None else None)
         pos = t.as_tensor(positions, dtype=t.float64, device=self.dev).contiguous()
         ref = t.as_tensor(reference, dtype=t.float32, device=self.dev).reshape(len(pos), -1).contiguous()
         n = len(pos)
@@ -201,6 +221,7 @@ class WorldTrainer:
         grid_ptr = self.grads.data_ptr() + 4 * self.grid_off if self.model.config.grid_resolution else None
         L.check(L.lib().fvsrn_train_world_grads(
             C.byref(self.desc), C.c_void_p(self.params.data_ptr()), C.c_void_p(pos.data_ptr()),
+            C.c_void_p(tt.data_ptr() if tt is not None else None),
             C.c_void_p(ref.data_ptr()), n, C.c_void_p(grid_ptr), C.c_void_p(self.inputs.data_ptr()),
             C.c_void_p(self.preacts.data_ptr()), C.c_void_p(self.deltas.data_ptr()),
             C.c_void_p(self.loss_sum.data_ptr()), C.c_void_p(stream)))
@@ -271,6 +292,71 @@ def train_world(model, target: WorldTarget, cfg: WorldTrainConfig, progress=None
             tr.adam(cfg.lr)
             total += loss * len(idx)
         trace.append(total / cfg.sample_count)
+        if progress is not None:
+            progress(epoch, trace[-1])
+    tr.write_back()
+    return model, trace
+
+
+# ------------------------------------------------------------------ temporal
+@dataclass
+class TemporalTrainConfig:
+    keyframe_times: list = field(default_factory=lambda: [1, 11, 21])
+    train_times: list = field(default_factory=lambda: [1, 6, 11, 16, 21])
+    world: WorldTrainConfig = field(default_factory=WorldTrainConfig)
+
+    def __post_init__(self):
+        if not self.train_times:
+            raise ValueError("train_times must be non-empty")
+        lo, hi = min(self.train_times), max(self.train_times)
+        if len(self.keyframe_times) > 1 and (lo < self.keyframe_times[0] or hi > self.keyframe_times[-1]):
+            raise ValueError("keyframes must cover the training timestep span")
+
+
+def train_temporal(model, volume_provider, cfg: TemporalTrainConfig, progress=None):
+    """World-space training over (position, timestep) pairs (train.py:265-314): all
+    keyframe grids and the network train jointly; the latent vectors interpolate linearly
+    between keyframes (the kernel scatters (1-w) z_bar / w z_bar into the bracketing pair)."""
+    import torch
+
+    if not model.is_temporal:
+        raise ValueError("train_temporal requires a temporal model")
+    if list(model.keyframes.times) != list(cfg.keyframe_times):
+        raise ValueError("model keyframes do not match the training config")
+    wc = cfg.world
+    volumes = {t: volume_provider(t) for t in cfg.train_times}
+    rng = np.random.default_rng(wc.seed)
+    lo_t, hi_t = model.keyframes.span
+
+    def draw(count, seed):       # the reference's draw (train.py:283-293), same RNG calls
+        r = np.random.default_rng(seed)
+        p = r.uniform(0.0, 1.0, size=(count, 3))
+        t = r.choice(cfg.train_times, size=count)
+        if len(cfg.keyframe_times) > 1:
+            assert t.min() >= lo_t and t.max() <= hi_t
+        v = np.empty(count, dtype=np.float32)
+        for tt in np.unique(t):
+            mask = t == tt
+            v[mask] = sample_volume(volumes[int(tt)], p[mask])
+        return p, t.astype(np.float64), v
+
+    positions, times, values = draw(wc.sample_count, wc.seed)
+    tr = WorldTrainer(model)
+    pos_d = torch.as_tensor(positions, device=tr.dev)
+    tim_d = torch.as_tensor(times, device=tr.dev)
+    val_d = torch.as_tensor(values, device=tr.dev).reshape(-1, 1)
+    trace = []
+    for epoch in range(wc.epochs):
+        perm = torch.as_tensor(rng.permutation(wc.sample_count), device=tr.dev)
+        total = 0.0
+        for lo in range(0, wc.sample_count, wc.batch_size):
+            idx = perm[lo:lo + wc.batch_size]
+            loss = tr.gradients(pos_d[idx], val_d[idx], tim_d[idx])
+            if not np.isfinite(loss):
+                raise TrainingDiverged(epoch, "non-finite loss")
+            tr.adam(wc.lr)
+            total += loss * len(idx)
+        trace.append(total / wc.sample_count)
         if progress is not None:
             progress(epoch, trace[-1])
     tr.write_back()

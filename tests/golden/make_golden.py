@@ -35,7 +35,7 @@ from fvsrn.train import fibonacci_cameras  # noqa: E402
 from fvsrn.transfer import TF_PRESETS, tf_eval  # noqa: E402
 from fvsrn.fused import fused_eval, plan_for_model  # noqa: E402
 from fvsrn.render import VolumeSource  # noqa: E402
-from fvsrn.volume import ScalarVolume, synth_field  # noqa: E402
+from fvsrn.volume import ScalarVolume, sample_volume, synth_field  # noqa: E402
 
 
 def sha(a) -> str:
@@ -309,6 +309,35 @@ def main():
                                               reference_stepsize_voxels=0.5))
     arrays["screen_trace"] = np.asarray(trace)
     print("screen", trace, flush=True)
+
+    # --- temporal training (train.py:265-314): one-batch gradients with per-sample
+    # timesteps (keyframe hits and in-between) and a short train_temporal trace
+    from fvsrn.train import TemporalTrainConfig, train_temporal
+
+    for name in ("temporal", "temporal_both"):
+        model = model_init(ModelConfig(**CONFIGS[name]))
+        rng = np.random.default_rng(91)
+        pb = rng.uniform(0.0, 1.0, size=(384, 3))
+        kt = list(CONFIGS[name]["keyframe_times"])
+        tb = np.concatenate([rng.uniform(kt[0], kt[-1], size=256), rng.choice(kt, size=128)])
+        ref = sample_volume(vol, pb)
+        pred, raw, ctx = _model_predict(model, pb, tb)
+        loss, adj = _l1_and_adjoint(pred, ref)
+        grads = model_backward(model, ctx, density_head_backward(raw, adj))
+        arrays[f"ttrain_pos_{name}"], arrays[f"ttrain_t_{name}"] = pb, tb
+        arrays[f"ttrain_ref_{name}"] = np.asarray(ref, dtype=np.float32)
+        arrays[f"ttrain_grads_{name}"] = np.concatenate([g.reshape(-1) for g in grads.arrays()])
+        meta["train"][f"t_{name}"] = {"loss": loss}
+    model = model_init(ModelConfig(**CONFIGS["temporal"]))
+    tcfg = TemporalTrainConfig(keyframe_times=[1, 11, 21], train_times=[1, 6, 11, 16, 21],
+                               world=WorldTrainConfig(sample_count=4096, batch_size=1024, epochs=3,
+                                                      lr=0.01, seed=0))
+    provider = lambda t: synth_field("gaussians", 20, {"n_components": 5}, t=t / 21.0, seed=42)  # noqa: E731
+    _, trace = train_temporal(model, provider, tcfg)
+    arrays["ttrain_trace"] = np.asarray(trace)
+    for tt in tcfg.train_times:
+        arrays[f"ttrain_vol_{tt}"] = provider(tt).values
+    print("temporal", trace, flush=True)
 
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:

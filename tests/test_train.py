@@ -160,3 +160,49 @@ def test_train_screen_trace_vs_reference():
     assert trace[-1] < trace[0]
     with pytest.raises(ValueError):
         P.train_screen(_model("cfg1"), vol, P.TF_PRESETS["warm"], cfg)
+
+
+# ------------------------------------------------------------------ temporal
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["temporal", "temporal_both"])
+def test_temporal_batch_gradients_vs_reference(name):
+    """Per-sample timesteps (between and exactly on keyframes): time features, keyframe
+    brackets and the two-grid latent scatter (model.py:190-245, 318-333)."""
+    from paper_2112_01579_b200.train import WorldTrainer
+
+    a = arrays()
+    m = _model(name)
+    tr = WorldTrainer(m)
+    loss = tr.gradients(a[f"ttrain_pos_{name}"], a[f"ttrain_ref_{name}"], a[f"ttrain_t_{name}"])
+    assert abs(loss - meta()["train"][f"t_{name}"]["loss"]) <= 1e-6 * max(1.0, abs(loss))
+    got, want = tr.grads.cpu().numpy(), a[f"ttrain_grads_{name}"]
+    off = 0
+    for arr in m.trainable_arrays():
+        g, w = got[off:off + arr.size], want[off:off + arr.size]
+        scale = float(np.abs(w).max()) or 1.0
+        assert np.abs(g - w).max() <= 1e-4 * scale, (name, arr.shape, np.abs(g - w).max(), scale)
+        off += arr.size
+    with pytest.raises(ValueError):
+        tr.gradients(a[f"ttrain_pos_{name}"], a[f"ttrain_ref_{name}"])      # times required
+
+
+@pytest.mark.gpu
+def test_train_temporal_trace_vs_reference():
+    a = arrays()
+    m = _model("temporal")
+    cfg = P.TemporalTrainConfig(keyframe_times=[1, 11, 21], train_times=[1, 6, 11, 16, 21],
+                                world=P.WorldTrainConfig(sample_count=4096, batch_size=1024, epochs=3,
+                                                         lr=0.01, seed=0))
+    _, trace = P.train_temporal(m, lambda t: P.ScalarVolume(a[f"ttrain_vol_{t}"]), cfg)
+    want = a["ttrain_trace"]
+    assert abs(trace[0] - want[0]) <= 1e-4 * want[0]
+    np.testing.assert_allclose(trace, want, rtol=3e-2)
+    with pytest.raises(ValueError):
+        P.train_temporal(_model("cfg1"), lambda t: None, cfg)
+
+
+def test_temporal_config_validation():
+    with pytest.raises(ValueError):
+        P.TemporalTrainConfig(train_times=[])
+    with pytest.raises(ValueError):
+        P.TemporalTrainConfig(keyframe_times=[5, 10], train_times=[1, 10])
