@@ -252,7 +252,20 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
         // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
-        if constexpr (FVSRN_TC_TMEM_A) {
+        if constexpr (FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && HID == 64) {
+          // two 32-column halves: half the live accumulator registers
+          uint32_t acc[32], w[16];
+          tmem_ld<32>(t_row, acc);
+          tmem_wait_ld();
+          act_words<32>(acc, w);
+          tmem_st<16>(t_row + S::kTCols, w);
+          tmem_ld<32>(t_row + 32, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_words<32>(acc, w);
+          tmem_st<16>(t_row + S::kTCols + 16, w);
+        } else if constexpr (FVSRN_TC_TMEM_A) {
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
           tmem_wait_ld();
