@@ -13,4 +13,5 @@ timeout 600 python bench.py > $out/bench_default.json 2> $out/bench_default.err;
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:dvr_kernel -s 3 -c 1 --export $out/ncu_dvr_cfg2 -f python bench.py --config cfg2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:dvr_tc_kernel -s 3 -c 1 --export $out/ncu_tc_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 400 ncu --set full --import-source on --clock-control none -k regex:sample_kernel -s 3 -c 1 --export $out/ncu_decode_cfg4 -f python bench.py --config cfg4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ls $out
