@@ -263,12 +263,19 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # FVSRN_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo (exercises the multi-rank code
+    # paths on a single-GPU box; the timing is then meaningless)
+    one_gpu = os.environ.get("FVSRN_BENCH_ONE_GPU") == "1"
+    dev = 0 if one_gpu else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2112_01579_b200 as P
-    from paper_2112_01579_b200.sharding import TileShardRenderer
+    from paper_2112_01579_b200.sharding import PeerFrameRenderer, TileShardRenderer
 
     cfg = CONFIGS[args.config]
     model = P.model_init(P.ModelConfig(**cfg["model"]))
@@ -288,7 +295,18 @@ def main():
         src = P.ModelSource(model, P.TF_PRESETS["grayscale"], t=t_frame, use_fused=True)
         cams = P.fibonacci_cameras(8, res, res)
         settings = P.RenderSettings(stepsize=cfg["stepsize"])
-        if world > 1:
+        peer = world > 1 and os.environ.get("FVSRN_MULTI", "peer") == "peer"
+        if peer:
+            # tiles stored straight into rank 0's frame over NVLink P2P by the render
+            # kernel (CUDA IPC); no gather / reassembly (sharding.PeerFrameRenderer)
+            renderer = PeerFrameRenderer(src)
+            renderer._frame(res, res)
+
+            def step(i, count_ptr=None):
+                _, ptr, _ = renderer._frame(res, res)
+                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_frame, ptr, count_ptr,
+                                          stream.cuda_stream, rank=rank, world=world, compact=False)
+        elif world > 1:
             renderer = TileShardRenderer(src)
 
             def step(i, count_ptr=None):
@@ -349,7 +367,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     DEV.kernel_timer(True)      # CUDA events around the dominant kernel, launch counts
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         for i in range(args.steps):
             flush.zero_()                      # evict the L2 (outside the events)
             evs[i][0].record(stream)
@@ -377,7 +395,7 @@ def main():
                 fb = P.pinned_empty((res, res, 4))
                 for i in range(2):
                     P.render_image(src, cams[i % 8], settings, out=fb)
-                with ClockSampler(local) as e2e_clocks:
+                with ClockSampler(dev) as e2e_clocks:
                     t0 = time.perf_counter()
                     n_e = 0
                     for i in range(args.steps):
@@ -421,9 +439,16 @@ def main():
                       "(mapped page-locked framebuffer: the kernel stores pixels over PCIe)"
                if cfg["kind"] == "dvr" else "decode_volume(out=pinned) -> fvsrn_decode_density"}
 
-    if rank != 0:
+    def finish():
         if world > 1:
+            dist.barrier()
+            if cfg["kind"] == "dvr" and isinstance(renderer, PeerFrameRenderer):
+                renderer.close()           # release rank 0's frame mapping before it is freed
+                dist.barrier()
             dist.destroy_process_group()
+
+    if rank != 0:
+        finish()
         return
 
     peak, peak_src = measured_peaks()
@@ -435,7 +460,7 @@ def main():
     mc = cfg["model"]
     mufu_per_eval = (mc["layers"] - 1) * mc["hidden"] + 6 + 2
     sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
-    xu_peak = 16 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6
+    xu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
     xu_achieved = rank0_evals * mufu_per_eval / (dom_ms / 1e3)
     kernel_name = {"cfg3": "dvr_tc_kernel<64,30,6> (tcgen05/TMEM)",
                    "cfg4": "sample_kernel<32,4,14,4> (mma.sync)"}.get(
@@ -450,7 +475,11 @@ def main():
                    "evals_per_step_mean": total_evals / args.steps,
                    "ms_per_frame_median": statistics.median(per_ms),
                    "l2": "flushed before every frame (256 MiB memset, outside the events)",
-                   "parallelism": f"screen-tile dp{world}" if world > 1 else "1 GPU",
+                   "parallelism": (f"screen-tile dp{world} ("
+                                   + ("peer-memory frame via CUDA IPC/NVLink"
+                                      if os.environ.get("FVSRN_MULTI", "peer") == "peer"
+                                      else "NCCL gather + reassembly") + ")")
+                   if world > 1 else "1 GPU",
                    "tf": "grayscale", "t": t_frame, "grid_precision": args.grid_precision},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -470,8 +499,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, os.cpu_count() or 1)
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    finish()
 
 
 if __name__ == "__main__":

@@ -185,6 +185,14 @@ FVSRN_API int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* 
                                   int64_t n, double lr, double beta1, double beta2, double eps,
                                   int32_t t, unsigned long long* d_nonfinite, void* stream);
 
+/* ---- peer-memory framebuffer assembly (multi-GPU, one process per GPU).
+ * Rank 0 exports its device framebuffer; every other rank opens it and its kernels
+ * store their screen tiles straight into rank 0's frame over NVLink (P2P), replacing the
+ * gather + reassembly.  64-byte handles (cudaIpcMemHandle_t). */
+FVSRN_API int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64]);
+FVSRN_API int32_t fvsrn_ipc_open(const uint8_t handle[64], int32_t device, void** d_ptr);
+FVSRN_API int32_t fvsrn_ipc_close(void* d_ptr);
+
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);
 FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);
 /* Padded widths (K0, hidden_pad, out_pad), smem bytes; for plan/introspection. */

@@ -730,6 +730,29 @@ int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float
   return FVSRN_OK;
 }
 
+int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64]) {
+  if (!d_ptr || !handle) return fail(FVSRN_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, d_ptr));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_ipc_open(const uint8_t handle[64], int32_t device, void** d_ptr) {
+  if (!handle || !d_ptr) return fail(FVSRN_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_ipc_close(void* d_ptr) {
+  if (d_ptr) CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_kernel_timer(int32_t enable) {
   g_kt.on = enable != 0;
   g_kt.used = 0;
