@@ -65,6 +65,11 @@ std::atomic<int> g_grid_mode{[] {
   return 0;
 }()};
 bool use_tex(const fvsrn_model* m);
+// FVSRN_OCC=n: cap resident CTAs per SM of the persistent kernels (A/B measurements)
+const int g_occ_cap = [] {
+  const char* e = std::getenv("FVSRN_OCC");
+  return e ? std::atoi(e) : 0;
+}();
 // render straight into mapped page-locked framebuffers (FVSRN_ZERO_COPY=0: copy instead)
 const bool g_zero_copy = [] {
   const char* e = std::getenv("FVSRN_ZERO_COPY");
@@ -488,6 +493,15 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
     }
   }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
+  if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
+  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRPipe || kind == KernelKind::kDVRTC) {
+    // Small frames: the frame time is the longest rays' sequential march, and every
+    // co-resident warp slows each step of it.  Keep ~1.75 work slots per lane (measured
+    // at 256^2: 0.456 ms at 5 CTAs/SM -> 0.318 ms at 2); large frames are unaffected.
+    const double rays_per_sm_cta = (double)m->num_sms * threads;
+    const int occ_work = (int)std::lround((double)work_warps * 32.0 / (rays_per_sm_cta * 1.75));
+    occ = std::max(1, std::min(occ, occ_work));
+  }
   long long blocks = (long long)m->num_sms * occ;
   const long long need = (work_warps + (threads / 32) - 1) / (threads / 32);
   if (need < blocks) blocks = std::max(1ll, need);
