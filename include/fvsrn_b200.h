@@ -14,6 +14,11 @@
  *   fvsrn_eval_color        <- eval_color(model, p, d, t)                         model.py:376-382
  *   fvsrn_decode_density    <- decode_volume(model, resolution, t)                model.py:385-398
  *   fvsrn_fused_eval        <- fused_eval(plan, model, x)                         fused.py:281-301
+ *   fvsrn_volume_*          <- render_image / raymarch_forward on a VolumeSource  render.py:132-141
+ *   fvsrn_render_rgba8      <- png_bytes(render_image(...)) pixels (service)      imaging.py:74-80
+ *   fvsrn_train_*, fvsrn_adam_step <- train_world / train_temporal / train_screen batch
+ *                              steps and adam_step      train.py:165-314, render.py:241-306, nn.py:279-298
+ *   fvsrn_ipc_*             <- (new) multi-GPU frame assembly in peer memory
  *
  * Conventions: every function returns an fvsrn_status; on failure
  * fvsrn_last_error() (thread-local) holds a message.  Host-pointer variants are

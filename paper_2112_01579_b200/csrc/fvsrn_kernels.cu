@@ -1,16 +1,24 @@
-// fvsrn_kernels.cu -- sm_100a kernels of the fV-SRN DVR hot path.
+// fvsrn_kernels.cu -- sm_100a kernels of the fV-SRN DVR hot path (mma.sync variants).
 //
-//   dvr_kernel        fused ray march: ray setup (f64, bit-exact geometry) -> per step
-//                     {latent grid, Fourier, MLP on tensor cores, head, TF, compositing,
-//                     early termination}; persistent warps refill lanes from a
-//                     chunked global work queue so MMA tiles stay full.
-//                     render.py:189-238, 314-332
-//   decode_kernel     batched world-space density decode on the vertex lattice
-//                     model.py:385-398
-//   eval_kernel       per-sample density / colour at given positions  model.py:368-382
+//   ray_setup_kernel  per-slot f64 ray setup (camera ray, slab test, march geometry,
+//                     bit-exact) -> f32 ray records; miss pixels; LPT tile costs
+//                     render.py:72-106, 189-200, 224-225
+//   lpt_bucket_sort   one-CTA longest-tile-first order of the local tiles
+//   dvr_kernel        fused ray march: per step {latent grid (texture units or LDG),
+//                     Fourier, MLP on tensor cores (mma.sync), head, TF, compositing,
+//                     early termination}; persistent warps refill lanes from a chunked
+//                     work queue of ray records so MMA tiles stay full.
+//                     render.py:203-238, 314-332
+//   dvr_pipe_kernel / dvr_ws_kernel   software-pipelined / warp-specialised variants
+//                     (A/B switches, measured slower)
+//   sample_kernel     mode 0: lattice decode model.py:385-398; mode 1: eval_density /
+//                     eval_color at given positions model.py:368-382
 //   fused_eval_kernel head(mlp(x)) from assembled inputs              fused.py:281-301
-//   blend_grid_kernel per-frame keyframe pre-blend (trilinear is linear) model.py:219-233
-//   tiles_to_frame    reassembles gathered screen-tile shards (multi-GPU)
+//   blend_grid_kernel per-frame keyframe pre-blend (LDG sampler)     model.py:219-233
+//   rgba8_kernel      png_bytes' 8-bit quantisation on the device    imaging.py:74-80
+//   tiles_to_frame    reassembles gathered screen-tile shards (multi-GPU, gather mode)
+// The tcgen05/TMEM march kernel is in fvsrn_tc.cu, ground-truth volume DVR in
+// fvsrn_volume.cu, the training kernels in fvsrn_train.cu.
 
 #include "fvsrn_kernels.cuh"
 #include "fvsrn_geometry.cuh"
