@@ -142,6 +142,9 @@ constexpr int kActRuntime = -1;
 #ifndef FVSRN_BPAIRS
 #define FVSRN_BPAIRS 0
 #endif
+#ifndef FVSRN_BIAS64
+#define FVSRN_BIAS64 0
+#endif
 // two-point TF coefficients held in registers in the DVR kernel
 #ifndef FVSRN_TF_REGS
 #define FVSRN_TF_REGS 0
@@ -286,8 +289,17 @@ struct WarpMLP {
   // Biases are stored as accumulator quads: for (n-tile nt, quad lane q) the float4
   // {b[nt*8+2q], b[nt*8+2q+1], same, same} at bs[(nt*4 + q)*4] -> one LDS.128 that is
   // the C operand of the layer's first MMA (no register copies).
+  // FVSRN_BIAS64: read only the (b[2q], b[2q+1]) half of the quad (LDS.64) and repeat it
+  // in registers.  Full-bandwidth LDS.128 serialises with MUFU on B200 where LDS.64
+  // overlaps it (tools/microbench/mio_mix.cu), but these broadcast reads (64 B per warp)
+  // measured neutral either way, so the quad load stays the default.
   __device__ static float4 bias_quad(const float* bs, int nt, int q) {
+#if FVSRN_BIAS64
+    const float2 v = *reinterpret_cast<const float2*>(bs + (nt * 4 + q) * 4);
+    return make_float4(v.x, v.y, v.x, v.y);
+#else
     return *reinterpret_cast<const float4*>(bs + (nt * 4 + q) * 4);
+#endif
   }
 
   // m_base: first m16 tile index handled (0, or 0/1 when MT == 1)
