@@ -348,7 +348,11 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
     uint4* az = reinterpret_cast<uint4*>(a_s0);   // pad columns must stay finite
     for (int i = tid; i < 2 * kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
   }
-  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 2 * S::kTCols);
+  constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
+  // per tile: D [0, kTCols) then A (hidden activations, and layer-0 rows when kA0)
+  constexpr uint32_t kTile = S::kTCols + (kA0 ? S::kKA / 2 : HID / 2);
+  constexpr uint32_t kAlloc = 2 * kTile <= 64 ? 64 : 2 * kTile <= 128 ? 128 : 2 * kTile <= 256 ? 256 : 512;
+  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
   if (tid == 0) { mbar_init(smem_u32(mbar), 1); mbar_init(smem_u32(mbar + 1), 1); }
   tc_fence_before();
   __syncthreads();
@@ -357,7 +361,8 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
   const uint32_t w_base = smem_u32(w_s);
   const uint32_t a_base[2] = {smem_u32(a_s0), smem_u32(a_s1)};
   const uint32_t mb[2] = {smem_u32(mbar), smem_u32(mbar + 1)};
-  const uint32_t t_d[2] = {tmem, tmem + (uint32_t)S::kTCols};               // accumulator columns
+  const uint32_t t_d[2] = {tmem, tmem + kTile};                             // accumulator columns
+  const uint32_t t_a[2] = {tmem + S::kTCols, tmem + kTile + S::kTCols};     // A operand columns
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;                     // this warp's lanes
   const int row_off = (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
   __half* myrow[2] = {a_s0 + row_off, a_s1 + row_off};
@@ -380,9 +385,13 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
       const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
       const uint32_t id = idesc_f16(128, N);
 #pragma unroll
-      for (int kk = 0; kk < K / 16; ++kk)
-        umma_f16(t_d[t], smem_desc(a_base[t] + kk * 256u, 128u, S::kSboA),
-                 smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+      for (int kk = 0; kk < K / 16; ++kk) {
+        if (l > 0 || kA0)
+          umma_f16_ts(t_d[t], t_a[t] + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+        else
+          umma_f16(t_d[t], smem_desc(a_base[t] + kk * 256u, 128u, S::kSboA),
+                   smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+      }
       umma_commit(mb[t]);
     }
   };
@@ -392,13 +401,24 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
     ws_refill(r[t], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
     evals += __popc(__ballot_sync(0xffffffffu, r[t].has));
     tmem_bias<HID>(t_d[t] + lane_off, b_s + S::b_off(0));
-    if (r[t].has) {
+    if constexpr (kA0) {          // tcgen05.st is .sync.aligned: every lane stores
+      uint32_t w[FastRow<NM>::kWords];
+      if (r[t].has) {
+        const float kf = (float)r[t].k;
+        FastRow<NM>::words(fd, fmaf(kf, r[t].dd0, r[t].pe0), fmaf(kf, r[t].dd1, r[t].pe1),
+                           fmaf(kf, r[t].dd2, r[t].pe2), w);
+      } else {
+#pragma unroll
+        for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
+      }
+      tmem_st_any<FastRow<NM>::kWords>(t_a[t] + lane_off, w);
+    } else if (r[t].has) {
       const float kf = (float)r[t].k;
       FastRow<NM>::template build<8>(fd, fmaf(kf, r[t].dd0, r[t].pe0), fmaf(kf, r[t].dd1, r[t].pe1),
                                      fmaf(kf, r[t].dd2, r[t].pe2), myrow[t]);
     }
     tmem_wait_st();
-    fence_proxy_async_smem();
+    if constexpr (!kA0) fence_proxy_async_smem();
     tc_fence_before();
     return __syncthreads_or(r[t].has) != 0;
   };
@@ -424,9 +444,10 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
           tmem_wait_ld();
           if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
           else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          act_row<HID>(acc, myrow[t]);
+          uint32_t w[HID / 2];
+          act_words<HID>(acc, w);
+          tmem_st<HID / 2>(t_a[t] + lane_off, w);
           tmem_wait_st();
-          fence_proxy_async_smem();
           tc_fence_before();
           __syncthreads();
           issue(l + 1, t);
@@ -447,7 +468,7 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 2 * S::kTCols);
+  if (warp == 0) tmem_dealloc(tmem, kAlloc);
 }
 
 const void* tc_kernel_for(int hid, bool two_tiles) {
