@@ -6,9 +6,9 @@ namespace fvsrn {
 
 constexpr int kTcThreads = 128;   // 4 warps = 128 rays = one M=128 UMMA tile
 
-// CTAs per SM the register budget is sized for (128 regs for 32-wide, 168 for 64-wide)
+// CTAs per SM the register budget is sized for (96 regs for 32-wide, 168 for 64-wide)
 #ifndef FVSRN_TC_MIN_BLOCKS
-#define FVSRN_TC_MIN_BLOCKS 4
+#define FVSRN_TC_MIN_BLOCKS 5
 #endif
 #ifndef FVSRN_TC_MIN_BLOCKS_WIDE
 #define FVSRN_TC_MIN_BLOCKS_WIDE 3
