@@ -1,26 +1,33 @@
 # Builds the C-ABI shared library in-tree (travels to the GPU box with gpurun).
+# Each .cu compiles to its own object (no cross-TU device code), in parallel.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2112_01579_b200/csrc
 LIB  := paper_2112_01579_b200/libfvsrn_b200.so
 SRCS := $(CSRC)/fvsrn_kernels.cu $(CSRC)/fvsrn_tc.cu $(CSRC)/fvsrn_train.cu $(CSRC)/fvsrn_volume.cu $(CSRC)/fvsrn_capi.cu
+OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS := $(CSRC)/fvsrn_device.cuh $(CSRC)/fvsrn_kernels.cuh $(CSRC)/fvsrn_geometry.cuh $(CSRC)/fvsrn_volume.cuh $(CSRC)/fvsrn_march.cuh $(CSRC)/fvsrn_tc.cuh $(CSRC)/fvsrn_tmem.cuh $(CSRC)/fvsrn_train.cuh include/fvsrn_b200.h
 NVFLAGS := $(ARCH) -O3 -lineinfo -ftz=true -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Xptxas -v --expt-relaxed-constexpr -Iinclude
+LDLIBS := -lcudart_static -ldl -lrt -lpthread
+MAKEFLAGS += -j5
 
 all: $(LIB)
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcudart_static -ldl -lrt -lpthread 2> build/ptxas.log || (cat build/ptxas.log; false)
-	@grep -E "registers|spill" build/ptxas.log | head -40
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
-$(shell mkdir -p build)
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) $(LDLIBS)
+	@cat $(patsubst build/%.o,build/%.ptxas.log,$(OBJS)) > build/ptxas.log
+	@grep -cE "registers" build/ptxas.log | xargs -I{} echo "{} kernels compiled for sm_100a"
 
 # A/B experiment build: make variant VDEFS="-DFVSRN_MIN_BLOCKS=5" VNAME=mb5
 variant: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) $(VDEFS) -shared -o build/libfvsrn_$(VNAME).so $(SRCS) -lcudart_static -ldl -lrt -lpthread 2> build/ptxas_$(VNAME).log || (cat build/ptxas_$(VNAME).log; false)
+	$(NVCC) $(NVFLAGS) $(VDEFS) -shared -o build/libfvsrn_$(VNAME).so $(SRCS) $(LDLIBS) 2> build/ptxas_$(VNAME).log || (cat build/ptxas_$(VNAME).log; false)
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(OBJS)
 
-.PHONY: all clean
+.PHONY: all clean variant
