@@ -86,13 +86,23 @@ __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
 }
 // Waits for the phase with the given parity to complete.  A watchdog traps after ~2^26
 // failed polls (seconds) so a faulted MMA becomes a launch error instead of a hang.
+#ifndef FVSRN_MBAR_SUSPEND_NS
+#define FVSRN_MBAR_SUSPEND_NS 0   // try_wait suspend-time hint (0: hardware default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   uint32_t done = 0, polls = 0;
   while (true) {
+#if FVSRN_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity), "n"(FVSRN_MBAR_SUSPEND_NS) : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+#endif
     if (done) break;
     if (++polls > (1u << 26)) __trap();
   }
