@@ -148,6 +148,8 @@ typedef struct {
   int32_t time_fourier_count;
   const float* time_b;               /* (time_fourier_count, 1) */
   double time_t0, time_t1;           /* normalisation span (time_range or keyframe span) */
+  int32_t raw_width;                 /* raw input block: 3 (p) or 6 (p|d, direction modes); 0 = 3 */
+  int32_t fourier_in;                /* Fourier input width: 3 (p) or 6 (dirF); 0 = 3 */
 } fvsrn_train_desc;
 
 /* One batch of n positions (device f64 (n,3); timesteps d_times (n) f64 for temporal
@@ -184,6 +186,14 @@ FVSRN_API int32_t fvsrn_train_screen_backward(const fvsrn_train_desc* desc, cons
                                               const double* d_background, int64_t cap_rows,
                                               float* d_inputs, float* d_preacts, float* d_deltas,
                                               float* d_grid_grad, void* stream);
+/* Reference-semantics f32 evaluation of model pieces for n samples (device pointers):
+ * stage 0 assemble_input (model.py:248-279) -> (n, d_in); 1 latent vectors grid_sample /
+ * keyframe_sample (grid.py:115-121, 222-230) -> (n, F); 2 raw network outputs of the
+ * positions -> (n, d_out); 3 mlp_eval of given inputs d_x (n, d_in) (nn.py:195-204) ->
+ * (n, d_out).  d_dirs for direction-input models, d_times for temporal ones (else NULL). */
+FVSRN_API int32_t fvsrn_f32_eval(const fvsrn_train_desc* desc, const float* d_params,
+                                 const double* d_positions, const double* d_dirs, const double* d_times,
+                                 const float* d_x, int64_t n, int32_t stage, float* d_out, void* stream);
 /* adam_step (nn.py:279-298) over n flat parameters at step t (1-based).  Non-finite
  * gradients are counted into *d_nonfinite and then nothing is updated. */
 FVSRN_API int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float* d_v,

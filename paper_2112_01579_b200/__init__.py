@@ -12,12 +12,15 @@ __version__ = "0.1.0"
 from ._lib import CapacityError, pinned_empty
 from .fused import FusedPlan, fused_eval, plan_build, plan_for_model, warmup
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
-                   grid_quantize)
+                   grid_quantize, grid_sample, keyframe_bracket, keyframe_sample)
 from .imaging import Camera, Image, metric_psnr, png_bytes, write_png
-from .model import (CheckpointError, FvsrnModel, ModelConfig, checkpoint_load, checkpoint_save,
-                    decode_volume, eval_color, eval_density, memory_footprint, model_init)
-from .nn import FourierEncoder, MlpParams, fourier_make, init_params, nerf_rows
-from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays,
+from .model import (CheckpointError, FvsrnModel, ModelConfig, apply_color_head, apply_density_head,
+                    assemble_input, checkpoint_load, checkpoint_save, decode_volume, eval_color,
+                    eval_density, memory_footprint, model_init)
+from .nn import (FourierEncoder, MlpParams, act_eval, act_grad, fourier_make, init_params, mlp_eval,
+                 nerf_rows)
+from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays, composite_invert,
+                     composite_step, ray_box_intersect,
                      fibonacci_cameras, raymarch_forward, render_image, render_image_rgba8,
                      render_rays)
 from .transfer import TF_PRESETS, TransferFunction, tf_eval, tf_from_json, tf_load, tf_save

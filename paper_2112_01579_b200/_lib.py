@@ -91,6 +91,7 @@ EXPORTS = {
     "fvsrn_train_screen_backward": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                 C.c_double] + [C.c_void_p] * 8 + [C.c_int64] +
                                                [C.c_void_p] * 5),
+    "fvsrn_f32_eval": (C.c_int32, [C.c_void_p] * 6 + [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     "fvsrn_adam_step": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                     C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
                                     C.c_void_p, C.c_void_p]),
@@ -148,7 +149,8 @@ class TrainDesc(C.Structure):
                 ("grid_resolution", C.c_int32), ("grid_channels", C.c_int32),
                 ("n_keyframes", C.c_int32), ("keyframe_times", C.POINTER(C.c_double)),
                 ("time_mode", C.c_int32), ("time_fourier_count", C.c_int32),
-                ("time_b", C.POINTER(C.c_float)), ("time_t0", C.c_double), ("time_t1", C.c_double)]
+                ("time_b", C.POINTER(C.c_float)), ("time_t0", C.c_double), ("time_t1", C.c_double),
+                ("raw_width", C.c_int32), ("fourier_in", C.c_int32)]
 
 
 _LIB = None

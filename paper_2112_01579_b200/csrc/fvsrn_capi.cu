@@ -623,14 +623,17 @@ extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
 
-static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev& net) {
+static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev& net,
+                          bool check_inputs = true) {
   const int L = d->layers;
   if (L < 1 || L > kTrainMaxLayers) return fail(FVSRN_EINVAL, "layer count out of range");
   if (d->hidden > 256 || d->d_in > 256 || d->d_out < 1 || d->d_out > 4)
     return fail(FVSRN_ECAPACITY, "network too wide for the training kernel");
   const int tl = d->time_mode == 0 ? 0 : ((d->time_mode & 1) ? 1 : 0) + ((d->time_mode & 2) ? 2 * d->time_fourier_count : 0);
-  if (d->d_in != 3 + 2 * d->fourier_m + tl + (d->grid_resolution > 0 ? d->grid_channels : 0))
-    return fail(FVSRN_EINVAL, "input width does not match a position-input model");
+  const int rw = d->raw_width ? d->raw_width : 3, fi = d->fourier_in ? d->fourier_in : 3;
+  if ((rw != 3 && rw != 6) || (fi != 3 && fi != 6)) return fail(FVSRN_EINVAL, "raw / Fourier input width must be 3 or 6");
+  if (check_inputs && d->d_in != rw + 2 * d->fourier_m + tl + (d->grid_resolution > 0 ? d->grid_channels : 0))
+    return fail(FVSRN_EINVAL, "input width does not match the model's input layout");
   if (d->n_keyframes < 0 || d->n_keyframes > 16 || (d->n_keyframes > 0 && !d->keyframe_times))
     return fail(FVSRN_EINVAL, "keyframes: 0..16 with their times");
   if (d->n_keyframes > 0 && d->grid_resolution < 2) return fail(FVSRN_EINVAL, "temporal models need a grid");
@@ -642,6 +645,7 @@ static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev
   net = TrainNetDev{};
   net.layers = L; net.hidden = d->hidden; net.d_in = d->d_in; net.d_out = d->d_out;
   net.act = d->activation; net.head = d->head; net.m = d->fourier_m; net.bmat = d->d_b_matrix;
+  net.raw_w = rw; net.fd_in = fi;
   net.grid_res = d->grid_resolution; net.grid_ch = d->grid_channels;
   net.n_kf = d->n_keyframes;
   for (int k = 0; k < d->n_keyframes; ++k) net.kf_times[k] = d->keyframe_times[k];
@@ -665,6 +669,23 @@ static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev
     off += l == L - 1 ? d->d_out : d->hidden;
   }
   net.grid_off = off;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_f32_eval(const fvsrn_train_desc* d, const float* d_params, const double* d_positions,
+                       const double* d_dirs, const double* d_times, const float* d_x, int64_t n,
+                       int32_t stage, float* d_out, void* stream) {
+  if (!d || !d_params || !d_out || stage < 0 || stage > 3) return fail(FVSRN_EINVAL, "bad argument");
+  if (n > 0 && ((stage < 3 && !d_positions) || (stage == 3 && !d_x))) return fail(FVSRN_EINVAL, "null argument");
+  TrainNetDev net;
+  int rc = make_train_net(d, 0, net, stage != 3);
+  if (rc) return rc;
+  if (stage < 3 && net.raw_w == 6 && !d_dirs) return fail(FVSRN_EINVAL, "direction mode requires view directions");
+  if (stage < 3 && net.n_kf > 0 && !d_times) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
+  if (stage == 1 && net.grid_res == 0) return fail(FVSRN_EINVAL, "model has no latent grid");
+  CUDA_TRY(launch_f32_eval(net, d_params, d_positions, d_dirs, d_times, d_x, (long long)n, stage, d_out,
+                           (cudaStream_t)stream));
+  count_launch();
   return FVSRN_OK;
 }
 

@@ -82,19 +82,19 @@ __device__ void kf_bracket(const TrainNetDev& net, double t, int& lo, int& hi, f
   w = h > l ? (float)((tc - net.kf_times[l]) / (net.kf_times[h] - net.kf_times[l])) : 0.f;
 }
 
-__device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ params, const double (&p)[3],
-                            double t, const CacheRef& c, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW],
-                            Cell& cell) {
-  const int L = net.layers, H = net.hidden, C = net.d_out;
-  int k = 0;
-  for (int a = 0; a < 3; ++a) x[k++] = (float)p[a];
+// assemble_input (model.py:248-279) into x[0..d_in): [p | sin | cos | time | z]
+__device__ void assemble_f32(const TrainNetDev& net, const float* __restrict__ params, const double (&p)[3],
+                             const double* d, double t, float (&x)[kTrainMaxW], Cell& cell) {
+  const int rw = net.raw_w, fi = net.fd_in;
+  const double enc[6] = {p[0], p[1], p[2], d ? d[0] : 0.0, d ? d[1] : 0.0, d ? d[2] : 0.0};
+  for (int a = 0; a < rw; ++a) x[a] = (float)enc[a];
   for (int j = 0; j < net.m; ++j) {
-    const double ph = (double)net.bmat[3 * j] * p[0] + (double)net.bmat[3 * j + 1] * p[1] +
-                      (double)net.bmat[3 * j + 2] * p[2];
-    x[3 + j] = (float)sin(ph);
-    x[3 + net.m + j] = (float)cos(ph);
+    double ph = 0.0;
+    for (int a = 0; a < fi; ++a) ph += (double)net.bmat[fi * j + a] * enc[a];
+    x[rw + j] = (float)sin(ph);
+    x[rw + net.m + j] = (float)cos(ph);
   }
-  k = 3 + 2 * net.m;
+  int k = rw + 2 * net.m;
   if (net.time_mode != 0) {   // _time_features (model.py:236-245)
     const double tn = net.t1 == net.t0 ? 0.0 : (fmin(fmax(t, net.t0), net.t1) - net.t0) / (net.t1 - net.t0);
     if (net.time_mode & 1) x[k++] = (float)tn;
@@ -137,6 +137,13 @@ __device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ pa
       x[k + ch] = acc;
     }
   }
+}
+
+// mlp_forward (nn.py:179-192) of x[0..d_in) -> raw outputs in x[0..d_out); caches layer
+// inputs / pre-activations when c.inputs != nullptr
+__device__ void mlp_f32(const TrainNetDev& net, const float* __restrict__ params, const CacheRef& c,
+                        float (&x)[kTrainMaxW], float (&y)[kTrainMaxW]) {
+  const int L = net.layers, H = net.hidden, C = net.d_out;
   int in_w = net.d_in;
   for (int l = 0; l < L; ++l) {
     const int out_w = (l == L - 1) ? C : H;
@@ -163,6 +170,13 @@ __device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ pa
     }
     in_w = out_w;
   }
+}
+
+__device__ void f32_forward(const TrainNetDev& net, const float* __restrict__ params, const double (&p)[3],
+                            double t, const CacheRef& c, float (&x)[kTrainMaxW], float (&y)[kTrainMaxW],
+                            Cell& cell) {
+  assemble_f32(net, params, p, nullptr, t, x, cell);
+  mlp_f32(net, params, c, x, y);
 }
 
 // mlp_backward (nn.py:234-255) from raw_bar, writing the adjoints, then the latent-grid
@@ -421,6 +435,47 @@ cudaError_t launch_screen_backward(const TrainNetDev& net, const float* params, 
   screen_backward_kernel<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(
       net, params, org, dir, n, eps_blend, cst, ast, tmin, ds, nsteps, row_off, adj, bg, cap, inputs,
       preacts, deltas, grid_grad);
+  return cudaGetLastError();
+}
+
+// Reference-semantics f32 evaluation of the pieces of the model (stage 0: assembled
+// inputs, 1: latent vectors (grid_sample / keyframe_sample), 2: raw MLP outputs from
+// positions, 3: raw MLP outputs of given inputs x (mlp_eval)).
+__global__ void f32_eval_kernel(TrainNetDev net, const float* __restrict__ params,
+                                const double* __restrict__ pos, const double* __restrict__ dirs,
+                                const double* __restrict__ times,
+                                const float* __restrict__ xin, long long n, int stage,
+                                float* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float x[kTrainMaxW], y[kTrainMaxW];
+  const CacheRef none{nullptr, nullptr, nullptr, 0, 0};
+  if (stage == 3) {
+    for (int j = 0; j < net.d_in; ++j) x[j] = xin[i * net.d_in + j];
+    mlp_f32(net, params, none, x, y);
+    for (int c = 0; c < net.d_out; ++c) out[i * net.d_out + c] = x[c];
+    return;
+  }
+  const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+  Cell cell;
+  assemble_f32(net, params, p, dirs ? dirs + 3 * i : nullptr, times ? times[i] : 0.0, x, cell);
+  if (stage == 0) {
+    for (int j = 0; j < net.d_in; ++j) out[i * net.d_in + j] = x[j];
+  } else if (stage == 1) {
+    const int F = net.grid_ch;
+    for (int c = 0; c < F; ++c) out[i * F + c] = x[net.d_in - F + c];
+  } else {
+    mlp_f32(net, params, none, x, y);
+    for (int c = 0; c < net.d_out; ++c) out[i * net.d_out + c] = x[c];
+  }
+}
+
+cudaError_t launch_f32_eval(const TrainNetDev& net, const float* params, const double* pos,
+                            const double* dirs, const double* times, const float* xin, long long n,
+                            int stage, float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  f32_eval_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(net, params, pos, dirs, times, xin, n, stage,
+                                                               out);
   return cudaGetLastError();
 }
 

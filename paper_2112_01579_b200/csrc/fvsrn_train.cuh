@@ -13,7 +13,8 @@ constexpr int kTrainMaxLayers = 24;
 // inputs / deltas: per-layer blocks of N x in_l / N x out_l floats; preacts (L-1) x N x H.
 struct TrainNetDev {
   int layers, hidden, d_in, d_out, act, head;
-  int m;                    // spatial Fourier rows (B is m x 3, f32)
+  int m;                    // spatial Fourier rows (B is m x fd_in, f32)
+  int raw_w, fd_in;         // raw input block (3: p, 6: p|d) and Fourier input width
   const float* bmat;
   int grid_res, grid_ch;
   long long grid_off;           // first grid; keyframe k at grid_off + k * R^3 * F
@@ -45,6 +46,9 @@ cudaError_t launch_screen_backward(const TrainNetDev& net, const float* params, 
                                    const int* nsteps, const long long* row_off, const float* adj,
                                    const double* bg, long long cap, float* inputs, float* preacts,
                                    float* deltas, float* grid_grad, cudaStream_t s);
+cudaError_t launch_f32_eval(const TrainNetDev& net, const float* params, const double* pos,
+                            const double* dirs, const double* times, const float* xin, long long n,
+                            int stage, float* out, cudaStream_t s);
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, const AdamConsts& k,
                         unsigned long long* bad, cudaStream_t s);
 

@@ -100,3 +100,55 @@ class KeyframeGrids:
     @property
     def span(self):
         return self.times[0], self.times[-1]
+
+
+def _positions(p) -> tuple[np.ndarray, bool]:
+    arr = np.asarray(p, dtype=np.float64)
+    single = arr.ndim == 1
+    pts = np.atleast_2d(arr)
+    if pts.shape[1] != 3:
+        raise ValueError(f"positions must have 3 components, got {np.shape(p)}")
+    return np.ascontiguousarray(pts), single
+
+
+def grid_sample(grid: LatentGrid, p) -> np.ndarray:
+    """Trilinear lookup at positions (N,3) or (3,) -> (N,F) or (F,) (grid.py:115-121),
+    evaluated on the GPU with the reference's f32 arithmetic."""
+    from .f32ops import NetDesc
+
+    pts, single = _positions(p)
+    F = grid.channels
+    nd = NetDesc([np.zeros((1, 3 + F), np.float32)], [np.zeros(1, np.float32)], "snake_alt", "density",
+                 3 + F, grids=[grid.values])
+    out = nd.run(1, len(pts), F, p=pts)
+    return out[0] if single else out
+
+
+def keyframe_bracket(kfg: "KeyframeGrids", t: float) -> tuple[int, int, float]:
+    """Indices of the bracketing keyframes and the blend weight of the upper one
+    (grid.py:206-219)."""
+    times = kfg.times
+    tc = min(max(float(t), times[0]), times[-1])
+    hi = int(np.searchsorted(times, tc, side="left"))
+    if hi == 0:
+        return 0, 0, 0.0
+    lo = hi - 1
+    if hi >= len(times):
+        return len(times) - 1, len(times) - 1, 0.0
+    if times[hi] == tc:
+        return hi, hi, 0.0
+    return lo, hi, float((tc - times[lo]) / (times[hi] - times[lo]))
+
+
+def keyframe_sample(kfg: "KeyframeGrids", p, t: float) -> np.ndarray:
+    """Latent vectors at positions and a continuous timestep (grid.py:222-230), GPU."""
+    from .f32ops import NetDesc
+
+    if not np.isfinite(t):
+        raise ValueError("timestep must be finite")
+    pts, single = _positions(p)
+    F = kfg.channels
+    nd = NetDesc([np.zeros((1, 3 + F), np.float32)], [np.zeros(1, np.float32)], "snake_alt", "density",
+                 3 + F, grids=[g.values for g in kfg.grids], keyframe_times=list(kfg.times))
+    out = nd.run(1, len(pts), F, p=pts, t=np.full(len(pts), float(t)))
+    return out[0] if single else out

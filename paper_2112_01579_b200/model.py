@@ -308,3 +308,49 @@ def checkpoint_load(path) -> FvsrnModel:
         model.grid = grids[0]
     model.quantized = quant or None
     return model
+
+
+# ------------------------------------------------------------------ standalone pieces
+def assemble_input(model: FvsrnModel, p, d=None, t=None) -> np.ndarray:
+    """Network input batch [raw | sin(Bx) | cos(Bx) | time | z] for positions (and
+    directions / timesteps) (model.py:248-279), evaluated on the GPU in the reference's
+    arithmetic (f64 phases, f32 trilinear latent lookup)."""
+    from .f32ops import NetDesc
+
+    cfg = model.config
+    p = np.atleast_2d(np.asarray(p, dtype=np.float64))
+    n = p.shape[0]
+    if cfg.direction_mode in ("dirP", "dirF"):
+        if d is None:
+            raise ValueError(f"direction mode {cfg.direction_mode!r} requires view directions")
+        d = np.atleast_2d(np.asarray(d, dtype=np.float64))
+        if d.shape != p.shape:
+            raise ValueError("directions must match positions in shape")
+    else:
+        d = None
+    if cfg.is_temporal:
+        if t is None:
+            raise ValueError("temporal model requires timesteps")
+        t = np.broadcast_to(np.asarray(t, dtype=np.float64), (n,))
+    elif t is not None:
+        raise ValueError("timestep supplied to a non-temporal model")
+    return NetDesc.for_model(model).run(0, n, cfg.input_width, p=p, d=d, t=t)
+
+
+def softplus(x: np.ndarray) -> np.ndarray:
+    """Host utility (model.py:338-339); the kernels apply the heads in-kernel."""
+    return np.logaddexp(0.0, x)
+
+
+def apply_density_head(raw: np.ndarray) -> np.ndarray:
+    """sigmoid(raw[:, 0]) (model.py:342-343); host utility on host arrays."""
+    return (1.0 / (1.0 + np.exp(-np.asarray(raw)[:, 0]))).astype(np.asarray(raw).dtype)
+
+
+def apply_color_head(raw: np.ndarray) -> np.ndarray:
+    """sigmoid rgb, softplus sigma (model.py:353-357); host utility on host arrays."""
+    raw = np.asarray(raw)
+    out = np.empty_like(raw)
+    out[:, :3] = 1.0 / (1.0 + np.exp(-raw[:, :3]))
+    out[:, 3] = softplus(raw[:, 3])
+    return out

@@ -114,3 +114,47 @@ def init_params(layer_count: int, hidden: int, d_in: int, d_out: int, seed: int 
         ws.append(gen.uniform(-lim, lim, size=(fan_out, fan_in)).astype(dtype))
         bs.append(np.zeros(fan_out, dtype=dtype))
     return MlpParams(ws, bs, activation)
+
+
+def act_eval(kind: str, x: np.ndarray) -> np.ndarray:
+    """Activation functions (nn.py:18-29); host utility (the kernels evaluate them fused)."""
+    if kind == "relu":
+        return np.maximum(x, 0.0)
+    if kind == "sigmoid":
+        return 1.0 / (1.0 + np.exp(-x))
+    if kind == "softplus":
+        return np.logaddexp(0.0, x)
+    if kind == "snake":
+        return x + np.sin(x) ** 2
+    if kind == "snake_alt":
+        return 0.5 * x + np.sin(x) ** 2
+    raise ValueError(f"unknown activation kind {kind!r}")
+
+
+def act_grad(kind: str, x: np.ndarray) -> np.ndarray:
+    """Activation derivatives (nn.py:32-44); host utility."""
+    if kind == "relu":
+        return (x > 0).astype(x.dtype)
+    if kind == "sigmoid":
+        s = 1.0 / (1.0 + np.exp(-x))
+        return s * (1.0 - s)
+    if kind == "softplus":
+        return 1.0 / (1.0 + np.exp(-x))
+    if kind == "snake":
+        return 1.0 + np.sin(2.0 * x)
+    if kind == "snake_alt":
+        return 0.5 + np.sin(2.0 * x)
+    raise ValueError(f"unknown activation kind {kind!r}")
+
+
+def mlp_eval(params: MlpParams, x: np.ndarray) -> np.ndarray:
+    """Forward pass of the network (nn.py:195-204) on the GPU, f32 like the reference;
+    the last layer stays linear."""
+    from .f32ops import NetDesc
+
+    x = np.asarray(x)
+    d_in = int(params.weights[0].shape[1])
+    if x.ndim != 2 or x.shape[1] != d_in:
+        raise ValueError(f"expected input shape (N, {d_in}), got {x.shape}")
+    nd = NetDesc(params.weights, params.biases, params.activation, "density", d_in)
+    return nd.run(3, x.shape[0], int(params.weights[-1].shape[0]), x=x)

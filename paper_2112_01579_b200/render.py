@@ -109,6 +109,38 @@ class VolumeSource:
                                   "not part of the GPU path")
 
 
+EPS_BLEND = 1e-5
+
+
+def ray_box_intersect(origins: np.ndarray, dirs: np.ndarray):
+    """Entry/exit distances against the unit cube (render.py:97-106); host utility on
+    host arrays (the renderer does this per ray in f64 in ray_setup_kernel)."""
+    d = np.where(np.abs(dirs) < 1e-12, 1e-12, dirs)
+    t_lo = (0.0 - origins) / d
+    t_hi = (1.0 - origins) / d
+    tmin = np.maximum(np.minimum(t_lo, t_hi).max(axis=1), 0.0)
+    tmax = np.maximum(t_lo, t_hi).min(axis=1)
+    return tmin, tmax, tmax > tmin
+
+
+def composite_step(c_acc, a_acc, rgb, sigma, ds, eps_blend: float = EPS_BLEND):
+    """One front-to-back blend step (render.py:109-117); host utility on host arrays
+    (the renderer composites in-kernel)."""
+    alpha = np.maximum(np.minimum(1.0 - eps_blend, -np.expm1(-sigma * ds)), 0.0)
+    trans = (1.0 - a_acc) * alpha
+    return c_acc + trans[..., None] * rgb, a_acc + trans
+
+
+def composite_invert(c_acc, a_acc, rgb, sigma, ds, eps_blend: float = EPS_BLEND):
+    """Exact inverse of composite_step (render.py:120-129); host utility (the GPU
+    raymarch_backward inverts the blend in-kernel)."""
+    alpha = np.maximum(np.minimum(1.0 - eps_blend, -np.expm1(-sigma * ds)), 0.0)
+    if np.any(alpha >= 1.0 - eps_blend / 2 + eps_blend):
+        raise FloatingPointError("blend inversion unstable: alpha too close to 1")
+    a_prev = (a_acc - alpha) / (1.0 - alpha)
+    return c_acc - ((1.0 - a_prev) * alpha)[..., None] * rgb, a_prev
+
+
 def camera_rays(camera: Camera):
     """Per-pixel (origins, unit dirs), row-major from the top-left (render.py:72-94).
 

@@ -379,3 +379,33 @@ def test_u8_checkpoint_sampled_directly(name, t, sampler):
         assert abs(src.last_eval_count - r["count"]) <= max(4, r["count"] // 1000)
     finally:
         D.set_grid_sampler(prev)
+
+
+# ------------------------------------------------------------------ standalone pieces
+ALL_MODELS = ["cfg1", "cfg2", "cfg3", "tiny", "temporal", "temporal_both", "color_dirf", "color_pos",
+              "random_fourier", "relu_nogrid", "snake_f12"]
+
+
+@pytest.mark.parametrize("name", ALL_MODELS)
+def test_assemble_input_and_pieces_vs_reference(name):
+    """assemble_input (model.py:248-279), grid_sample / keyframe_sample (grid.py:115-121,
+    222-230) and mlp_eval + heads (nn.py:195-204, model.py:342-357) through the GPU f32
+    evaluator, against the reference's own outputs."""
+    a = arrays()
+    m = _model(name)
+    p = a["eval_p"][:257]
+    d = a["eval_d"][:257] if m.config.direction_mode != "pos" else None
+    t = 6.5 if m.is_temporal else None
+    x = P.assemble_input(m, p, d, t)
+    want = a[f"assemble_{name}"]
+    assert x.shape == want.shape and x.dtype == np.float32
+    np.testing.assert_allclose(x, want, rtol=0, atol=2e-6)
+    F = m.config.grid_channels if m.config.grid_resolution else 0
+    if F:
+        z = P.keyframe_sample(m.keyframes, p, t) if m.is_temporal else P.grid_sample(m.grid, p)
+        np.testing.assert_allclose(z, want[:, -F:], rtol=0, atol=2e-6)
+    raw = P.mlp_eval(m.params, want)
+    if m.config.head == "density" and not m.is_temporal:
+        np.testing.assert_allclose(P.apply_density_head(raw), a[f"density_{name}"][:257], rtol=0, atol=2e-6)
+    elif m.config.head == "color":
+        np.testing.assert_allclose(P.apply_color_head(raw), a[f"color_{name}"][:257], rtol=0, atol=2e-6)

@@ -203,3 +203,22 @@ def test_checkpoint_u8_codes_match_reference_quantizer(name, cfg_name):
         rq = P.grid_quantize(g)
         assert np.array_equal(q.codes, rq.codes)
         assert np.array_equal(q.mins, rq.mins) and np.array_equal(q.maxs, rq.maxs)
+
+
+def test_host_geometry_and_compositing_utilities():
+    """ray_box_intersect / composite_step / composite_invert (render.py:97-129): host
+    utilities mirroring the reference on host arrays."""
+    from tests.golden_util import arrays as garr
+
+    a = garr()
+    o, d = a["rays_fib0_o"], a["rays_fib0_d"]
+    tmin, tmax, valid = P.ray_box_intersect(o, d)
+    assert valid.sum() == (a["rays_fib0_n"] > 0).sum()
+    rng = np.random.default_rng(0)
+    c = rng.uniform(size=(64, 3)) * 0.3
+    al = rng.uniform(size=64) * 0.5
+    rgb, sig = rng.uniform(size=(64, 3)), rng.uniform(size=64) * 5
+    c2, a2 = P.composite_step(c, al, rgb, sig, 0.01)
+    c3, a3 = P.composite_invert(c2, a2, rgb, sig, 0.01)
+    np.testing.assert_allclose(c3, c, atol=1e-12)
+    np.testing.assert_allclose(a3, al, atol=1e-12)
