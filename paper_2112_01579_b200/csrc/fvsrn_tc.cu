@@ -60,6 +60,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_SPLIT
 #define FVSRN_TC_SPLIT 0
 #endif
+#ifndef FVSRN_TC_WAIT_BAR
+#define FVSRN_TC_WAIT_BAR 0
+#endif
 // hidden-layer A operands in TMEM (tcgen05.st of the packed activations, MMA reads A
 // from TMEM) instead of the shared-memory A tile: removes 2 x 128 B of shared-memory
 // traffic per sample and layer
@@ -246,7 +249,15 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         }
         umma_commit(mb);
       }
-      mbar_wait(mb, phase);
+      if constexpr (FVSRN_TC_WAIT_BAR) {
+        // one thread polls the MMA-completion barrier; the others wait in the hardware
+        // CTA barrier instead of spinning on try_wait (issue slots stay with other CTAs)
+        if (tid == 0) mbar_wait(mb, phase);
+        tc_fence_before();
+        __syncthreads();
+      } else {
+        mbar_wait(mb, phase);
+      }
       phase ^= 1u;
       tc_fence_after();
       if (l < NL - 1) {
