@@ -42,13 +42,14 @@ const bool g_lpt_enabled = [] {
 #define FVSRN_TEX_DEFAULT 1
 #endif
 constexpr bool kTexDefault = FVSRN_TEX_DEFAULT != 0;
-enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3, kPipe = 4 };
+enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3, kPipe = 4, kDual = 5 };
 std::atomic<int> g_dvr_mode_i{[] {
   const char* e = std::getenv("FVSRN_DVR");
   if (e && std::string(e) == "tc") return (int)DvrMode::kTC;
   if (e && std::string(e) == "ws") return (int)DvrMode::kWS;
   if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
   if (e && std::string(e) == "pipe") return (int)DvrMode::kPipe;
+  if (e && std::string(e) == "dual") return (int)DvrMode::kDual;
   return (int)DvrMode::kAuto;
 }()};
 // tcgen05 kernel: one 128-ray tile per CTA (default, measured faster), or two tiles in
@@ -494,7 +495,8 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
-  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRPipe || kind == KernelKind::kDVRTC) {
+  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRPipe || kind == KernelKind::kDVRTC ||
+      kind == KernelKind::kDVRDual) {
     // Small frames: the frame time is the longest rays' sequential march, and every
     // co-resident warp slows each step of it.  Keep ~1.75 work slots per lane (measured
     // at 256^2: 0.456 ms at 5 CTAs/SM -> 0.318 ms at 2); large frames are unaffected.
@@ -556,6 +558,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
   if (dvr_mode() == DvrMode::kWS)
     return launch(m, KernelKind::kDVRWS, ws_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
+  if (dvr_mode() == DvrMode::kDual && fast_path(m, KernelKind::kDVR) && m->hid_pad == 32)
+    return launch(m, KernelKind::kDVRDual, dual_smem_bytes(net, m->k0), args, s, n_slots / 64 + 1);
   if (dvr_mode() == DvrMode::kPipe && fast_path(m, KernelKind::kDVR))
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   return launch(m, KernelKind::kDVR, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
@@ -817,7 +821,7 @@ int32_t fvsrn_set_grid_sampler(int32_t mode) {
 }
 
 int32_t fvsrn_set_dvr_kernel(int32_t mode) {
-  if (mode < 0 || mode > 4) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..4");
+  if (mode < 0 || mode > 5) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..5");
   return g_dvr_mode_i.exchange(mode);
 }
 const char* fvsrn_version(void) { return "fvsrn_b200 0.1.0 (sm_100a, mma.sync f16/f32)"; }

@@ -198,6 +198,82 @@ dvr_pipe_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
+// ---------------------------------------------------------------- two rays per lane
+// dvr_kernel with 64 rays per warp (two per lane): the MLP runs over 64 rows (four m16
+// tiles), so each B-fragment / bias load feeds four MMAs instead of two and the per-step
+// queue / loop overhead is shared by twice the samples; fewer warps, twice the ILP.
+// Default-shape (FastRow) models only.
+template <int HID, int NM, int NL>
+__global__ void __launch_bounds__(kThreads, FVSRN_DUAL_MIN_BLOCKS)
+dvr_dual_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+                MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+                float* __restrict__ out, unsigned long long* __restrict__ queue,
+                unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  constexpr int rs = FastRow<NM>::kK0 + 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* p = smem;
+  uint2* wf_s = reinterpret_cast<uint2*>(p);
+  p += ((size_t)net.w_total * sizeof(uint2) + 15) / 16 * 16;
+  float* b_s = reinterpret_cast<float*>(p);
+  p += ((size_t)net.b_total * sizeof(float) + 15) / 16 * 16;
+  TFDev* tf = reinterpret_cast<TFDev*>(p);
+  p += (sizeof(TFDev) + 15) / 16 * 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr size_t kStage = (size_t)2 * kWarp * rs * sizeof(__half);
+  unsigned char* wp = p + (size_t)warp * (kStage + 2 * kWarp * 4 * sizeof(float));
+  __half* stage = reinterpret_cast<__half*>(wp);
+  float* ob = reinterpret_cast<float*>(wp + kStage);
+  for (int i = threadIdx.x; i < net.w_total; i += blockDim.x) wf_s[i] = net.wfrag[i];
+  for (int i = threadIdx.x; i < net.b_total; i += blockDim.x) b_s[i] = net.bias[i];
+  if (b0) {
+    const int n0q = net.b_off[1] - net.b_off[0];
+    for (int i = threadIdx.x; i < n0q; i += blockDim.x) {
+      const int j = i >> 2;
+      b_s[i] = b0[(j >> 2) * 8 + 2 * (j & 3) + (i & 1)];
+    }
+  }
+  {
+    const int words = sizeof(TFDev) / 4;
+    const int* src = reinterpret_cast<const int*>(tf_g);
+    int* dst = reinterpret_cast<int*>(tf);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  {
+    uint32_t* z = reinterpret_cast<uint32_t*>(stage);
+    for (int i = lane; i < (int)(kStage / 4); i += kWarp) z[i] = 0u;
+  }
+  __syncthreads();
+  const bool density = net.head == 0;
+  RayLane r[2];
+  r[0].has = false;
+  r[1].has = false;
+  LaneQueue q{0, 0, false};
+  unsigned long long evals = 0;
+  while (true) {
+    ws_refill(r[0], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r[1], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    const unsigned a0 = __ballot_sync(0xffffffffu, r[0].has), a1 = __ballot_sync(0xffffffffu, r[1].has);
+    if ((a0 | a1) == 0) break;
+    evals += __popc(a0) + __popc(a1);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+      if (r[g].has) {
+        const float kf = (float)r[g].k;
+        FastRow<NM>::template build<1>(fd, fmaf(kf, r[g].dd0, r[g].pe0), fmaf(kf, r[g].dd1, r[g].pe1),
+                                       fmaf(kf, r[g].dd2, r[g].pe2), stage + (g * kWarp + lane) * rs);
+      }
+    __syncwarp();
+    WarpMLP<HID, 4, 4, NL, fast_kt0<NM>()>::run(stage, rs, net, wf_s, b_s, ob, lane, 0);
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+      if (r[g].has)
+        composite_step(r[g], *reinterpret_cast<const float4*>(ob + 4 * (g * kWarp + lane)), density, *tf, md,
+                       out, nonfinite);
+  }
+  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+}
+
 // ---------------------------------------------------------------- ray setup
 // One thread per slot, canonical slot order: camera ray (render.py:72-94) or explicit ray,
 // slab test and march geometry (render.py:97-106, 189-200) in f64 with explicit _rn ops,
@@ -603,6 +679,10 @@ constexpr int fast_layers(int hid) { return hid == 64 ? 6 : 4; }
 // fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode, layers =
 // fast_layers(HID)); else generic (runtime layer count and input layout)
 const void* kernel_for(KernelKind kind, int hid, bool fast) {
+  if (kind == KernelKind::kDVRDual) {
+    if (!fast || hid != 32) return nullptr;
+    return (const void*)dvr_dual_kernel<32, 14, 4>;
+  }
   if (kind == KernelKind::kDVRPipe) {
     if (!fast) return nullptr;
     switch (hid) {

@@ -39,6 +39,18 @@ inline size_t pipe_smem_bytes(const NetDev& net, int k0) {
   return b;
 }
 
+// two-rays-per-lane DVR (dvr_dual_kernel)
+#ifndef FVSRN_DUAL_MIN_BLOCKS
+#define FVSRN_DUAL_MIN_BLOCKS 3
+#endif
+inline size_t dual_smem_bytes(const NetDev& net, int k0) {
+  size_t b = ((size_t)net.w_total * 8 + 15) / 16 * 16 + ((size_t)net.b_total * 4 + 15) / 16 * 16;
+  b += (sizeof(TFDev) + 15) / 16 * 16;
+  const int rs = k0 + 8;
+  b += (size_t)(kThreads / kWarp) * (2 * (size_t)kWarp * rs * 2 + 2 * kWarp * 4 * 4);
+  return b;
+}
+
 // warp-specialised DVR: 4 producer + 4 consumer warps per CTA
 constexpr int kWsThreads = 256;
 constexpr int kWsPairs = 4;
@@ -73,7 +85,7 @@ struct RayRecs {
   float4* d;
 };
 
-enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kSample, kFused };
+enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

@@ -344,7 +344,7 @@ def shard_slots(width: int, height: int, world: int) -> tuple[int, int]:
     return n_tiles, math.ceil(n_tiles / world) * 64
 
 
-DVR_KERNELS = {"auto": 0, "tc": 1, "ws": 2, "warp": 3, "pipe": 4}
+DVR_KERNELS = {"auto": 0, "tc": 1, "ws": 2, "warp": 3, "pipe": 4, "dual": 5}
 
 
 def set_dvr_kernel(name: str) -> str:

@@ -269,7 +269,7 @@ def test_model_vs_dense_decode_on_gpu():
 
 
 @pytest.mark.parametrize("sampler", ["tex", "ldg"])
-@pytest.mark.parametrize("kernel", ["tc", "ws", "warp", "pipe"])
+@pytest.mark.parametrize("kernel", ["tc", "ws", "warp", "pipe", "dual"])
 @pytest.mark.parametrize("tag", ["cfg1_v1_peaks_bg", "cfg2_v2_gray", "cfg3_v0_gray_48", "inside_gray",
                                  "temporal_t6.5"])
 def test_dvr_kernel_variants(kernel, tag, sampler):
@@ -318,7 +318,7 @@ def test_grid_sampler_density_and_decode(sampler):
         D.set_grid_sampler(prev)
 
 
-@pytest.mark.parametrize("kernel", ["tc", "warp", "pipe"])
+@pytest.mark.parametrize("kernel", ["tc", "warp", "pipe", "dual"])
 def test_dvr_kernel_cfg2_full_frame_and_shards(kernel):
     """Full 1024^2 config-2 frame per kernel vs the oracle on sampled rows, explicit-ray
     marching, and shard reassembly bit-identical to the 1-GPU frame."""
