@@ -287,6 +287,12 @@ def main():
             model = P.checkpoint_load(Path(td) / "m.fvsrn")
     flops = mlp_flops(cfg["model"])
     t_frame = cfg.get("t")
+    # temporal configs animate: every frame is at a different timestep, so every frame
+    # re-blends its keyframe pair (the latent interpolation is inside the timed region)
+    t_cycle = [t_frame + 0.75 * k for k in range(8)] if t_frame is not None else [None] * 8
+
+    def t_of(i):
+        return t_cycle[i % 8]
     res = cfg["res"]
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
@@ -304,13 +310,13 @@ def main():
 
             def step(i, count_ptr=None):
                 _, ptr, _ = renderer._frame(res, res)
-                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_frame, ptr, count_ptr,
+                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_of(i), ptr, count_ptr,
                                           stream.cuda_stream, rank=rank, world=world, compact=False)
         elif world > 1:
             renderer = TileShardRenderer(src)
 
             def step(i, count_ptr=None):
-                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_frame,
+                renderer.dm.render_device(src.tf, cams[i % 8], settings, t_of(i),
                                           renderer._buffers(res, res)[0].data_ptr(), count_ptr,
                                           stream.cuda_stream, rank=rank, world=world, compact=True)
                 local_buf, gathered, frame, _ = renderer._buffers(res, res)
@@ -325,7 +331,7 @@ def main():
             frame = torch.empty((res, res, 4), dtype=torch.float32, device="cuda")
 
             def step(i, count_ptr=None):
-                src.device_model.render_device(src.tf, cams[i % 8], settings, t_frame,
+                src.device_model.render_device(src.tf, cams[i % 8], settings, t_of(i),
                                                frame.data_ptr(), count_ptr, stream.cuda_stream)
     else:  # decode: lattice split in contiguous slabs across ranks
         total = res ** 3
@@ -399,6 +405,7 @@ def main():
                     t0 = time.perf_counter()
                     n_e = 0
                     for i in range(args.steps):
+                        src.t = t_of(i)
                         P.render_image(src, cams[i % 8], settings, out=fb)
                         n_e += src.last_eval_count
                     dt = time.perf_counter() - t0
@@ -411,6 +418,7 @@ def main():
                 t0 = time.perf_counter()
                 n_e = 0
                 for i in range(args.steps):
+                    src.t = t_of(i)
                     out = renderer.render(cams[i % 8], settings, count=True)
                     n_e += renderer.last_eval_count
                     if rank == 0:
@@ -480,7 +488,8 @@ def main():
                                       if os.environ.get("FVSRN_MULTI", "peer") == "peer"
                                       else "NCCL gather + reassembly") + ")")
                    if world > 1 else "1 GPU",
-                   "tf": "grayscale", "t": t_frame, "grid_precision": args.grid_precision},
+                   "tf": "grayscale", "t": t_cycle if t_frame is not None else None,
+                   "grid_precision": args.grid_precision},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "flops_per_eval": flops, "peak_source": peak_src,

@@ -1,3 +1,4 @@
+#include <thread>
 #include <type_traits>
 #include <array>
 #include <atomic>
@@ -70,6 +71,12 @@ bool use_tex(const fvsrn_model* m);
 const int g_occ_cap = [] {
   const char* e = std::getenv("FVSRN_OCC");
   return e ? std::atoi(e) : 0;
+}();
+// temporal texture path: pre-blend the bracketing keyframes once per frame
+// (FVSRN_TEX_PREBLEND=0: blend both texture sets per sample in the march kernel)
+const bool g_tex_preblend = [] {
+  const char* e = std::getenv("FVSRN_TEX_PREBLEND");
+  return !(e && e[0] == '0');
 }();
 // render straight into mapped page-locked framebuffers (FVSRN_ZERO_COPY=0: copy instead)
 const bool g_zero_copy = [] {
@@ -200,6 +207,16 @@ struct fvsrn_model {
   // u8 grids: the textures hold the codes; per-grid per-channel dequantisation
   bool tex_u8 = false;
   std::vector<std::array<float, 16>> qmin, qspan;
+  // temporal texture path: per-(host thread, stream) pre-blended keyframe array set
+  struct BlendSet {
+    cudaArray_t arr[4] = {};
+    cudaSurfaceObject_t surf[4] = {};
+    cudaTextureObject_t tex[4] = {};
+    int lo = -1, hi = -1;
+    float w = -1.f;
+  };
+  mutable std::mutex blend_mu;
+  mutable std::map<std::pair<std::thread::id, cudaStream_t>, std::unique_ptr<BlendSet>> blend_sets;
   int k0x = 0;
   std::vector<float> b0_static;     // layer-0 bias, padded N0
   std::vector<float> w0_time;       // N0 x T time columns of W0
@@ -215,6 +232,12 @@ struct fvsrn_model {
     for (auto& t4 : tex)
       for (auto t : t4) cudaDestroyTextureObject(t);
     for (auto a : tex_arrays) cudaFreeArray(a);
+    for (auto& kv : blend_sets)
+      for (int j = 0; j < 4; ++j) {
+        cudaDestroyTextureObject(kv.second->tex[j]);
+        cudaDestroySurfaceObject(kv.second->surf[j]);
+        cudaFreeArray(kv.second->arr[j]);
+      }
   }
 };
 
@@ -350,6 +373,7 @@ struct FrameScratch {
   float tex_w = 0.f;
   const cudaTextureObject_t* tex_lo = nullptr;
   const cudaTextureObject_t* tex_hi = nullptr;
+  bool tex_u8 = false;
   int q_lo = 0, q_hi = 0;           // grid indices (u8 dequantisation constants)
   float* b0 = nullptr;
   TFDev* tf = nullptr;
@@ -360,6 +384,53 @@ bool use_tex(const fvsrn_model* m) {
   if (m->tex.empty()) return false;
   const int g = g_grid_mode.load(std::memory_order_relaxed);
   return g == 1 || (g == 0 && kTexDefault);
+}
+
+// Pre-blend keyframes (lo, hi, w) into this (thread, stream)'s array set; reuses the set
+// when the bracket is unchanged.  Stream order makes the blend finish before the march.
+int preblend(const fvsrn_model* m, int lo, int hi, float w, cudaStream_t s,
+             const fvsrn_model::BlendSet*& out) {
+  fvsrn_model::BlendSet* b = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(m->blend_mu);
+    auto& slot = m->blend_sets[std::make_pair(std::this_thread::get_id(), s)];
+    if (!slot) {
+      slot.reset(new fvsrn_model::BlendSet());
+      const int R = m->R;
+      for (int j = 0; j < 4; ++j) {
+        cudaChannelFormatDesc cd = cudaCreateChannelDescHalf4();
+        CUDA_TRY(cudaMalloc3DArray(&slot->arr[j], &cd, make_cudaExtent(R, R, R), cudaArraySurfaceLoadStore));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = slot->arr[j];
+        CUDA_TRY(cudaCreateSurfaceObject(&slot->surf[j], &rd));
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModeLinear;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CUDA_TRY(cudaCreateTextureObject(&slot->tex[j], &rd, &td, nullptr));
+      }
+    }
+    b = slot.get();
+  }
+  if (b->lo != lo || b->hi != hi || b->w != w) {
+    TexBlendArgs a{};
+    for (int j = 0; j < 4; ++j) { a.lo[j] = m->tex[lo][j]; a.hi[j] = m->tex[hi][j]; a.out[j] = b->surf[j]; }
+    a.R = m->R;
+    a.u8 = m->tex_u8 ? 1 : 0;
+    a.w = w;
+    if (m->tex_u8)
+      for (int c = 0; c < 16; ++c) {
+        a.qmin_lo[c] = m->qmin[lo][c]; a.qspan_lo[c] = m->qspan[lo][c];
+        a.qmin_hi[c] = m->qmin[hi][c]; a.qspan_hi[c] = m->qspan[hi][c];
+      }
+    CUDA_TRY(launch_tex_blend(a, s));
+    count_launch();
+    b->lo = lo; b->hi = hi; b->w = w;
+  }
+  out = b;
+  return FVSRN_OK;
 }
 
 // Per-call device scratch: effective layer-0 bias (time folded), TF table,
@@ -389,12 +460,21 @@ int frame_setup(const fvsrn_model* m, double t, const fvsrn_tf* tf, cudaStream_t
     bracket(m->kf_times, t, lo, hi, w);
     if (hi != lo && !fs.tex_on) grid_bytes = (size_t)m->R * m->R * m->R * m->f_pad * sizeof(__half);
   }
-  if (fs.tex_on) {   // keyframe blend happens in the kernel (two texture sets)
+  if (fs.tex_on) {   // keyframe blend in the kernel (two texture sets) or pre-blended
     fs.tex_lo = m->tex[m->temporal ? lo : 0].data();
     fs.tex_hi = m->tex[m->temporal ? hi : 0].data();
     fs.q_lo = m->temporal ? lo : 0;
     fs.q_hi = m->temporal ? hi : 0;
     fs.tex_w = (m->temporal && hi != lo) ? (float)w : 0.f;
+    fs.tex_u8 = m->tex_u8;
+    if (fs.tex_w != 0.f && g_tex_preblend) {
+      const fvsrn_model::BlendSet* b = nullptr;
+      int rc = preblend(m, lo, hi, (float)w, s, b);
+      if (rc) return rc;
+      fs.tex_lo = fs.tex_hi = b->tex;
+      fs.tex_w = 0.f;
+      fs.tex_u8 = false;
+    }
   }
   const size_t off_tf = 0, off_b0 = (sizeof(TFDev) + 255) / 256 * 256;
   const size_t off_ct = off_b0 + 1024, off_grid = off_ct + 256;
@@ -423,7 +503,7 @@ FeatDev feat_for(const fvsrn_model* m, const FrameScratch& fs) {
   fd.tex_on = fs.tex_on ? 1 : 0;
   fd.tex_w = fs.tex_w;
   for (int j = 0; j < 4 && fs.tex_on; ++j) { fd.tex_lo[j] = fs.tex_lo[j]; fd.tex_hi[j] = fs.tex_hi[j]; }
-  fd.tex_u8 = (fs.tex_on && m->tex_u8) ? 1 : 0;
+  fd.tex_u8 = (fs.tex_on && fs.tex_u8) ? 1 : 0;
   if (fd.tex_u8)
     for (int c = 0; c < 16; ++c) {
       fd.qmin_lo[c] = m->qmin[fs.q_lo][c]; fd.qspan_lo[c] = m->qspan[fs.q_lo][c];

@@ -625,6 +625,40 @@ fused_eval_kernel(NetDev net, int d_in, int k0, const float* __restrict__ x, lon
   }
 }
 
+// Temporal texture path: per-frame keyframe pre-blend (1-w) G_lo + w G_hi (model.py:219-233,
+// trilinear is linear in the grid values) written into one RGBA16F array set through
+// surfaces, so the march kernel fetches 4 texels per sample instead of 8.  u8 grids are
+// dequantised here (grid.py:170-172).
+__global__ void tex_blend_kernel(TexBlendArgs a) {
+  const long long n = (long long)a.R * a.R * a.R;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n * 4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % 4);
+    const long long v = i / 4;
+    const int z = (int)(v % a.R), y = (int)((v / a.R) % a.R), x = (int)(v / ((long long)a.R * a.R));
+    float4 lo = tex3D<float4>(a.lo[j], z + 0.5f, y + 0.5f, x + 0.5f);   // texel centre: exact
+    float4 hi = tex3D<float4>(a.hi[j], z + 0.5f, y + 0.5f, x + 0.5f);
+    if (a.u8) {
+      lo = make_float4(fmaf(lo.x, a.qspan_lo[4 * j], a.qmin_lo[4 * j]), fmaf(lo.y, a.qspan_lo[4 * j + 1], a.qmin_lo[4 * j + 1]),
+                       fmaf(lo.z, a.qspan_lo[4 * j + 2], a.qmin_lo[4 * j + 2]), fmaf(lo.w, a.qspan_lo[4 * j + 3], a.qmin_lo[4 * j + 3]));
+      hi = make_float4(fmaf(hi.x, a.qspan_hi[4 * j], a.qmin_hi[4 * j]), fmaf(hi.y, a.qspan_hi[4 * j + 1], a.qmin_hi[4 * j + 1]),
+                       fmaf(hi.z, a.qspan_hi[4 * j + 2], a.qmin_hi[4 * j + 2]), fmaf(hi.w, a.qspan_hi[4 * j + 3], a.qmin_hi[4 * j + 3]));
+    }
+    const float w = a.w, u = 1.f - w;
+    uint2 bits;
+    bits.x = pack_half2(fmaf(u, lo.x, w * hi.x), fmaf(u, lo.y, w * hi.y));
+    bits.y = pack_half2(fmaf(u, lo.z, w * hi.z), fmaf(u, lo.w, w * hi.w));
+    surf3Dwrite(bits, a.out[j], z * (int)sizeof(uint2), y, x);
+  }
+}
+
+cudaError_t launch_tex_blend(const TexBlendArgs& a, cudaStream_t s) {
+  const long long n = (long long)a.R * a.R * a.R * 4;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  tex_blend_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 __global__ void blend_grid_kernel(const __half* __restrict__ lo, const __half* __restrict__ hi,
                                   float w, long long n, __half* __restrict__ dst) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;

@@ -105,6 +105,13 @@ cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardD
 cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
+struct TexBlendArgs {
+  unsigned long long lo[4], hi[4], out[4];   // texture objects in, surface objects out
+  int R, u8;
+  float w;
+  float qmin_lo[16], qspan_lo[16], qmin_hi[16], qspan_hi[16];
+};
+cudaError_t launch_tex_blend(const TexBlendArgs& a, cudaStream_t s);
 cudaError_t launch_rgba8(const float* fb, long long n_px, unsigned char* out, cudaStream_t s);
 cudaError_t launch_tiles_to_frame(const float* gathered, int W, int H, int world, float* frame,
                                   cudaStream_t s);
