@@ -1,3 +1,4 @@
+#include <chrono>
 #include <thread>
 #include <type_traits>
 #include <array>
@@ -108,6 +109,23 @@ thread_local KernelTimer g_kt;
 void count_launch() {
   if (g_kt.on) ++g_kt.launches;
 }
+
+// FVSRN_DEBUG_TIMING=1: host-side phase timestamps of fvsrn_render to stderr (diagnostics)
+const bool g_debug_timing = std::getenv("FVSRN_DEBUG_TIMING") != nullptr;
+struct HostPhases {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string out;
+  void mark(const char* what) {
+    if (!g_debug_timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    out += std::string(" ") + what + "=" +
+           std::to_string(std::chrono::duration<double, std::micro>(now - last).count()).substr(0, 6) + "us";
+    last = now;
+  }
+  ~HostPhases() {
+    if (g_debug_timing) std::fprintf(stderr, "fvsrn_render phases:%s\n", out.c_str());
+  }
+};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -1287,7 +1305,9 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   // A mapped page-locked framebuffer (fvsrn_host_alloc) is written by the kernels
   // directly over PCIe: each pixel is stored once when its ray ends, so the transfer
   // overlaps the march instead of following it.  Otherwise render to HBM and copy.
+  HostPhases ph;
   float* mapped = mapped_device_ptr(out);
+  ph.mark("ptrattr");
   float* d_out = nullptr;
   unsigned long long* d_cnt = nullptr;
   void* dbuf = nullptr;
@@ -1295,13 +1315,17 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   d_out = mapped ? mapped : (float*)dbuf;
   d_cnt = (unsigned long long*)((char*)dbuf + (mapped ? 0 : bytes));
   CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 16, sg.s));
+  ph.mark("alloc");
   int rc = render_impl(m, tf, c, st, t, nullptr, d_out, d_cnt, d_cnt + 1, sg.s);
   if (rc) { cudaFreeAsync(dbuf, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  ph.mark("enqueue");
   unsigned long long cnt[2] = {0, 0};
   if (!mapped) CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaFreeAsync(dbuf, sg.s));
+  ph.mark("tail");
   CUDA_TRY(cudaStreamSynchronize(sg.s));
+  ph.mark("sync");
   if (eval_count) *eval_count = cnt[0];
   if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
   return FVSRN_OK;
