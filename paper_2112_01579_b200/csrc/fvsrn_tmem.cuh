@@ -86,6 +86,9 @@ __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
 }
 // Waits for the phase with the given parity to complete.  A watchdog traps after ~2^26
 // failed polls (seconds) so a faulted MMA becomes a launch error instead of a hang.
+#ifndef FVSRN_MBAR_BACKOFF_NS
+#define FVSRN_MBAR_BACKOFF_NS 0   // sleep between failed polls (0: spin)
+#endif
 #ifndef FVSRN_MBAR_SUSPEND_NS
 #define FVSRN_MBAR_SUSPEND_NS 0   // try_wait suspend-time hint (0: hardware default)
 #endif
@@ -105,6 +108,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
 #endif
     if (done) break;
     if (++polls > (1u << 26)) __trap();
+#if FVSRN_MBAR_BACKOFF_NS > 0
+    __nanosleep(FVSRN_MBAR_BACKOFF_NS);   // give the issue slots to other warps
+#endif
   }
 }
 
