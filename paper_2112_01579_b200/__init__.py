@@ -10,7 +10,8 @@ sm_100a CUDA kernels behind the C ABI of ``include/fvsrn_b200.h``.
 __version__ = "0.1.0"
 
 from ._lib import CapacityError, pinned_empty
-from .fused import FusedPlan, fused_eval, plan_build, plan_for_model, warmup
+from .fused import (FusedPlan, bench_compare, bench_csv, fused_eval, naive_eval_model, plan_build,
+                    plan_for_model, warmup)
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
                    grid_quantize, grid_sample, keyframe_bracket, keyframe_sample)
 from .imaging import Camera, Image, metric_psnr, png_bytes, write_png

@@ -82,3 +82,44 @@ def fused_eval(plan: FusedPlan, model, x: np.ndarray, python_tiles: bool = False
 
 def warmup(plan: FusedPlan, model) -> None:
     fused_eval(plan, model, np.zeros((TILE_SAMPLES, plan.d_in), dtype=np.float32))
+
+
+def naive_eval_model(model, x: np.ndarray) -> np.ndarray:
+    """Layer-by-layer evaluator (fused.py:304-312): head(mlp_eval(x)) with the reference's
+    f32 arithmetic on the GPU f32 evaluator (the fused path is ``fused_eval``)."""
+    from .model import apply_color_head, apply_density_head
+    from .nn import mlp_eval
+
+    raw = mlp_eval(model.params, np.asarray(x, dtype=np.float32))
+    return apply_density_head(raw) if model.config.head == "density" else apply_color_head(raw)
+
+
+def bench_compare(model, batch_sizes: list, runs: int = 5, seed: int = 0) -> list:
+    """Median throughput of the naive (f32) and fused (fp16 tensor-core) evaluators per
+    batch size (fused.py:320-343); host-synchronous calls including transfers."""
+    import time
+
+    plan = plan_for_model(model)
+    warmup(plan, model)
+    rng = np.random.default_rng(seed)
+    rows = []
+    for batch in batch_sizes:
+        x = rng.uniform(-1.0, 1.0, size=(batch, plan.d_in)).astype(np.float32)
+        naive_eval_model(model, x)
+        for name, fn in (("naive", lambda: naive_eval_model(model, x)),
+                         ("fused", lambda: fused_eval(plan, model, x))):
+            times = []
+            for _ in range(max(runs, 5)):
+                t0 = time.perf_counter()
+                fn()
+                times.append(time.perf_counter() - t0)
+            rows.append({"batch": batch, "evaluator": name,
+                         "samples_per_sec": batch / sorted(times)[len(times) // 2]})
+    return rows
+
+
+def bench_csv(rows: list) -> str:
+    lines = ["batch,evaluator,samples_per_sec"]
+    for r in rows:
+        lines.append(f"{r['batch']},{r['evaluator']},{r['samples_per_sec']:.1f}")
+    return "\n".join(lines) + "\n"

@@ -409,3 +409,16 @@ def test_assemble_input_and_pieces_vs_reference(name):
         np.testing.assert_allclose(P.apply_density_head(raw), a[f"density_{name}"][:257], rtol=0, atol=2e-6)
     elif m.config.head == "color":
         np.testing.assert_allclose(P.apply_color_head(raw), a[f"color_{name}"][:257], rtol=0, atol=2e-6)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "color_pos", "random_fourier"])
+def test_naive_vs_fused_eval(name):
+    """naive_eval_model (f32, fused.py:304-312) vs fused_eval (fp16 tensor cores) vs the
+    reference's fused outputs; bench_compare rows are well formed."""
+    m = _model(name)
+    x = arrays()[f"fused_x_{name}"]
+    naive = P.naive_eval_model(m, x)
+    assert np.abs(naive - arrays()[f"fused_y_{name}"]).max() <= 1e-4      # fused.py tolerance
+    rows = P.bench_compare(m, [1024], runs=2)
+    assert {r["evaluator"] for r in rows} == {"naive", "fused"} and all(r["samples_per_sec"] > 0 for r in rows)
+    assert P.bench_csv(rows).startswith("batch,evaluator,samples_per_sec")
