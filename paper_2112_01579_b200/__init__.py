@@ -14,7 +14,7 @@ from .fused import (FusedPlan, bench_compare, bench_csv, fused_eval, naive_eval_
                     plan_for_model, warmup)
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
                    grid_quantize, grid_sample, keyframe_bracket, keyframe_sample)
-from .imaging import Camera, Image, metric_psnr, png_bytes, write_png
+from .imaging import Camera, Image, metric_psnr, metric_ssim, png_bytes, write_png
 from .model import (CheckpointError, FvsrnModel, ModelConfig, apply_color_head, apply_density_head,
                     assemble_input, checkpoint_load, checkpoint_save, decode_volume, eval_color,
                     eval_density, memory_footprint, model_init)
@@ -27,5 +27,5 @@ from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera
 from .transfer import TF_PRESETS, TransferFunction, tf_eval, tf_from_json, tf_load, tf_save
 from .volume import ScalarVolume, sample_volume
 from .train import (ErrorGrid, ScreenTrainConfig, TemporalTrainConfig, TrainingDiverged, WorldTarget,
-                    WorldTrainConfig, build_error_grid, raymarch_backward, sample_world_dataset,
-                    train_screen, train_temporal, train_world)
+                    WorldTrainConfig, build_error_grid, evaluate_views, loss_csv, metrics_csv,
+                    raymarch_backward, sample_world_dataset, train_screen, train_temporal, train_world)

@@ -104,3 +104,44 @@ def png_bytes(img: Image) -> bytes:
 def write_png(img: Image, path) -> None:
     with open(path, "wb") as f:
         f.write(png_bytes(img))
+
+
+# ------------------------------------------------------------------ SSIM (host metric)
+_SSIM_WIN, _SSIM_SIGMA, _SSIM_C1, _SSIM_C2 = 11, 1.5, 0.01 ** 2, 0.03 ** 2
+
+
+def _luma(a: np.ndarray) -> np.ndarray:
+    """Rec. 709 luminance of the rgb channels, or the array itself if 2-D (f64)."""
+    if a.ndim == 3:
+        return (0.2126 * a[:, :, 0] + 0.7152 * a[:, :, 1] + 0.0722 * a[:, :, 2]).astype(np.float64)
+    return a.astype(np.float64)
+
+
+def _gauss_mean(img: np.ndarray) -> np.ndarray:
+    """Separable normalised Gaussian window mean, zero padding, fully supported windows."""
+    from scipy.ndimage import correlate1d
+
+    r = np.arange(_SSIM_WIN, dtype=np.float64) - (_SSIM_WIN - 1) / 2.0
+    k = np.exp(-(r ** 2) / (2.0 * _SSIM_SIGMA ** 2))
+    k /= k.sum()
+    out = correlate1d(correlate1d(img, k, axis=0, mode="constant"), k, axis=1, mode="constant")
+    h = (_SSIM_WIN - 1) // 2
+    return out[h:-h, h:-h]
+
+
+def metric_ssim(a, b) -> float:
+    """Mean local SSIM of the luminance, 11x11 Gaussian window, sigma 1.5, K = (0.01, 0.03)
+    on a unit dynamic range (imaging.py:156-177); a host metric like metric_psnr."""
+    x = a.data if isinstance(a, Image) else np.asarray(getattr(a, "values", a))
+    y = b.data if isinstance(b, Image) else np.asarray(getattr(b, "values", b))
+    if x.shape != y.shape:
+        raise ValueError(f"shape mismatch: {x.shape} vs {y.shape}")
+    gx, gy = _luma(x), _luma(y)
+    if min(gx.shape) < _SSIM_WIN:
+        raise ValueError(f"image smaller than the {_SSIM_WIN}x{_SSIM_WIN} SSIM window")
+    mx, my = _gauss_mean(gx), _gauss_mean(gy)
+    vx = _gauss_mean(gx * gx) - mx ** 2
+    vy = _gauss_mean(gy * gy) - my ** 2
+    cxy = _gauss_mean(gx * gy) - mx * my
+    s = ((2 * mx * my + _SSIM_C1) * (2 * cxy + _SSIM_C2)) / ((mx ** 2 + my ** 2 + _SSIM_C1) * (vx + vy + _SSIM_C2))
+    return float(s.mean())

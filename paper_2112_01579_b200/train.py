@@ -536,3 +536,42 @@ def train_screen(model, volume, tf, cfg: ScreenTrainConfig, progress=None):
             progress(epoch, trace[-1])
     tr.write_back()
     return model, trace
+
+
+
+# ------------------------------------------------------------------ evaluation
+def evaluate_views(model, volume, tf, n_views: int = 64, resolution: int = 512,
+                   stepsize_voxels: float = 1.0, t: float | None = None, use_fused: bool = True) -> list:
+    """Render a deterministic orbit from the model and from the ground-truth volume, both
+    on the GPU (ModelSource / VolumeSource), and score each view with PSNR and SSIM
+    (train.py:317-341).  One row per view plus a trailing "mean" row."""
+    from .imaging import metric_psnr, metric_ssim
+    from .render import ModelSource, RenderSettings, VolumeSource, fibonacci_cameras, render_image
+
+    cams = fibonacci_cameras(n_views, resolution, resolution)
+    settings = RenderSettings.for_voxels(volume.resolution, stepsize_voxels)
+    ref_source = VolumeSource(volume, tf)
+    model_source = ModelSource(model, tf=tf if model.config.head == "density" else None, t=t,
+                               use_fused=use_fused)
+    rows = []
+    for i, cam in enumerate(cams):
+        ref = render_image(ref_source, cam, settings)
+        img = render_image(model_source, cam, settings)
+        rows.append({"view": i, "psnr": metric_psnr(img, ref), "ssim": metric_ssim(img, ref)})
+    rows.append({"view": "mean", "psnr": float(np.mean([r["psnr"] for r in rows])),
+                 "ssim": float(np.mean([r["ssim"] for r in rows]))})
+    return rows
+
+
+def metrics_csv(rows: list) -> str:
+    lines = ["view,psnr,ssim"]
+    for r in rows:
+        lines.append(f"{r['view']},{r['psnr']:.4f},{r['ssim']:.6f}")
+    return "\n".join(lines) + "\n"
+
+
+def loss_csv(trace: list) -> str:
+    lines = ["epoch,loss"]
+    for i, v in enumerate(trace):
+        lines.append(f"{i},{v:.8f}")
+    return "\n".join(lines) + "\n"

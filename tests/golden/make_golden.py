@@ -24,7 +24,7 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import fvsrn  # noqa: E402
-from fvsrn.imaging import Camera  # noqa: E402
+from fvsrn.imaging import Camera, Image  # noqa: E402
 from fvsrn.model import (  # noqa: E402
     ModelConfig, assemble_input, checkpoint_save, decode_volume, eval_color,
     eval_density, model_init)
@@ -338,6 +338,24 @@ def main():
     for tt in tcfg.train_times:
         arrays[f"ttrain_vol_{tt}"] = provider(tt).values
     print("temporal", trace, flush=True)
+
+    # --- evaluation metrics (imaging.py:156-177, train.py:317-341): SSIM of seeded image
+    # pairs (rgb, gray, identical) and a 2-view evaluate_views of cfg1 vs the train volume
+    from fvsrn.imaging import metric_ssim
+    from fvsrn.train import evaluate_views, metrics_csv
+
+    rng = np.random.default_rng(123)
+    a = rng.uniform(0, 1, size=(24, 20, 4)).astype(np.float32)
+    b = np.clip(a + rng.normal(0, 0.1, size=a.shape), 0, 1).astype(np.float32)
+    g1, g2 = rng.uniform(0, 1, size=(16, 33)), rng.uniform(0, 1, size=(16, 33))
+    arrays["ssim_a"], arrays["ssim_b"], arrays["ssim_g1"], arrays["ssim_g2"] = a, b, g1, g2
+    meta["ssim"] = {"rgb": metric_ssim(Image(a), Image(b)), "gray": metric_ssim(g1, g2),
+                    "same": metric_ssim(Image(a), Image(a))}
+    model = model_init(ModelConfig(**CONFIGS["cfg1"]))
+    rows = evaluate_views(model, vol, TF_PRESETS["grayscale"], n_views=2, resolution=32)
+    meta["evaluate_views"] = {"model": "cfg1", "tf": "grayscale", "n_views": 2, "resolution": 32,
+                              "rows": rows, "csv": metrics_csv(rows)}
+    print("evaluate_views", rows, flush=True)
 
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:

@@ -222,3 +222,21 @@ def test_host_geometry_and_compositing_utilities():
     c3, a3 = P.composite_invert(c2, a2, rgb, sig, 0.01)
     np.testing.assert_allclose(c3, c, atol=1e-12)
     np.testing.assert_allclose(a3, al, atol=1e-12)
+
+
+def test_metric_ssim_vs_reference():
+    # imaging.py:156-177 restated on the host (luminance, Gaussian window, K1/K2)
+    a, g = arrays(), meta()["ssim"]
+    assert P.metric_ssim(P.Image(a["ssim_a"]), P.Image(a["ssim_b"])) == pytest.approx(g["rgb"], abs=1e-12)
+    assert P.metric_ssim(a["ssim_g1"], a["ssim_g2"]) == pytest.approx(g["gray"], abs=1e-12)
+    assert P.metric_ssim(P.Image(a["ssim_a"]), P.Image(a["ssim_a"])) == pytest.approx(1.0, abs=1e-12)
+    with pytest.raises(ValueError):
+        P.metric_ssim(a["ssim_g1"], a["ssim_g1"][:, :20])
+    with pytest.raises(ValueError):
+        P.metric_ssim(np.zeros((10, 40)), np.zeros((10, 40)))
+
+
+def test_metrics_and_loss_csv_format():
+    rows = meta()["evaluate_views"]["rows"]
+    assert P.metrics_csv(rows) == meta()["evaluate_views"]["csv"]
+    assert P.loss_csv([0.5, 0.25]) == "epoch,loss\n0,0.50000000\n1,0.25000000\n"

@@ -206,3 +206,17 @@ def test_temporal_config_validation():
         P.TemporalTrainConfig(train_times=[])
     with pytest.raises(ValueError):
         P.TemporalTrainConfig(keyframe_times=[5, 10], train_times=[1, 10])
+
+
+@pytest.mark.gpu
+def test_evaluate_views_vs_reference():
+    # train.py:317-341: GPU renders of model (ModelSource) and ground truth (VolumeSource)
+    g = meta()["evaluate_views"]
+    m = _model(g["model"])
+    rows = P.evaluate_views(m, P.ScalarVolume(arrays()["train_volume"]), P.TF_PRESETS[g["tf"]],
+                            n_views=g["n_views"], resolution=g["resolution"])
+    assert [r["view"] for r in rows] == [r["view"] for r in g["rows"]]
+    for got, ref in zip(rows, g["rows"]):
+        # fp16 network in the kernel vs f32 reference evaluation: metric-level tolerance
+        assert got["psnr"] == pytest.approx(ref["psnr"], abs=0.05)
+        assert got["ssim"] == pytest.approx(ref["ssim"], abs=5e-3)
