@@ -135,8 +135,10 @@ int fail(int code, const std::string& msg) {
 #define CUDA_TRY(expr)                                                                  \
   do {                                                                                  \
     cudaError_t _e = (expr);                                                            \
-    if (_e != cudaSuccess)                                                              \
+    if (_e != cudaSuccess) {                                                            \
+      (void)cudaGetLastError(); /* do not leak a non-sticky error into the next call */ \
       return fail(FVSRN_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+    }                                                                                   \
   } while (0)
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -552,8 +554,11 @@ bool fast_path(const fvsrn_model* m, KernelKind kind) {
 
 // (kernel, device, smem) -> resident CTAs per SM; the attribute + occupancy queries run
 // once per configuration instead of on every launch.
+// The dynamic-smem attribute is per (kernel, device) and only ever raised: lowering it
+// for a smaller configuration would invalidate a cached larger one.
 std::mutex g_occ_mu;
 std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+std::map<std::pair<const void*, int>, size_t> g_smem_attr;
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
@@ -568,7 +573,11 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
     auto key = std::make_tuple(fn, m->device, smem);
     auto it = g_occ.find(key);
     if (it == g_occ.end()) {
-      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      size_t& attr = g_smem_attr[std::make_pair(fn, m->device)];
+      if (smem > attr) {
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+      }
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
       if (kind == KernelKind::kDVRTC) {
         // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; the real

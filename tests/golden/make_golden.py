@@ -192,6 +192,11 @@ def main():
                RenderSettings(stepsize=1 / 128))
     add_render("cfg3_v0_gray_48", models["cfg3"], "grayscale", fibonacci_cameras(8, 48, 48)[0],
                RenderSettings(stepsize=1 / 192), fused=False)  # CapacityError on fused
+    # ragged frame (neither side a multiple of the 8x8 screen tile), rays capped by
+    # max_steps (render.py:196), ET off, coloured background
+    add_render("cfg2_ragged_cap", models["cfg2"], "warm", fibonacci_cameras(8, 100, 36)[3],
+               RenderSettings(stepsize=1 / 200, max_steps=60, early_term_alpha=1.0,
+                              background=(0.05, 0.1, 0.15)))
 
     # --- ground-truth DVR through VolumeSource (render.py:132-141, volume.py:213-255)
     vols = {
