@@ -30,7 +30,28 @@ def camera_basis(cam):
     return fwd, right, up, float(half_w), float(half_h)
 
 
+_CAM_CACHE: dict = {}
+_TF_CACHE: dict = {}
+_CACHE_MAX = 64
+
+
+def _cache_put(cache: dict, key, value):
+    if len(cache) >= _CACHE_MAX:
+        cache.pop(next(iter(cache)))
+    cache[key] = value
+    return value
+
+
 def camera_desc(cam) -> L.CameraDesc:
+    """Descriptor with the numpy-evaluated basis; cached per camera value (the basis
+    costs ~50 us of numpy per frame, more than the C entry's whole host path)."""
+    key = (tuple(map(float, cam.eye)), tuple(map(float, cam.target)), tuple(map(float, cam.up)),
+           float(cam.fov_y), int(cam.width), int(cam.height))
+    d = _CAM_CACHE.get(key)
+    return d if d is not None else _cache_put(_CAM_CACHE, key, _camera_desc(cam))
+
+
+def _camera_desc(cam) -> L.CameraDesc:
     d = L.CameraDesc()
     d.eye[:] = [float(v) for v in cam.eye]
     d.target[:] = [float(v) for v in cam.target]
@@ -57,7 +78,19 @@ class _TF:
 
 
 def tf_desc(tf):
-    return None if tf is None else _TF(tf)
+    """TF descriptor.  Reused per TF object when its arrays are already float32 and
+    contiguous: the descriptor then points at the caller's arrays, so in-place edits
+    are still seen (the C entry reads the TF on every call)."""
+    if tf is None:
+        return None
+    hit = _TF_CACHE.get(id(tf))
+    if hit is not None and hit[0] is tf and hit[1].xs is tf.xs and hit[1].rgbs is tf.rgbs \
+            and hit[1].sigmas is tf.sigmas:
+        return hit[1]
+    d = _TF(tf)
+    if d.xs is tf.xs and d.rgbs is tf.rgbs and d.sigmas is tf.sigmas:
+        _cache_put(_TF_CACHE, id(tf), (tf, d))
+    return d
 
 
 def settings_desc(s) -> L.SettingsDesc:
