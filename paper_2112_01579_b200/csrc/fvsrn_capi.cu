@@ -94,6 +94,19 @@ float* mapped_device_ptr(void* host) {
   cudaGetLastError();
   return nullptr;
 }
+// Per-thread page-locked landing slot for the per-frame counters: the D2H copy is then a
+// plain DMA (a pageable destination goes through a driver staging buffer).
+unsigned long long* pinned_counters() {
+  thread_local struct Slot {
+    unsigned long long* p = nullptr;
+    ~Slot() { if (p) cudaFreeHost(p); }
+  } slot;
+  if (!slot.p && cudaMallocHost((void**)&slot.p, 64) != cudaSuccess) {
+    cudaGetLastError();
+    slot.p = nullptr;
+  }
+  return slot.p;
+}
 inline DvrMode dvr_mode() { return (DvrMode)g_dvr_mode_i.load(std::memory_order_relaxed); }
 bool use_tc(const fvsrn_model* m);
 
@@ -112,6 +125,13 @@ void count_launch() {
 
 // FVSRN_DEBUG_TIMING=1: host-side phase timestamps of fvsrn_render to stderr (diagnostics)
 const bool g_debug_timing = std::getenv("FVSRN_DEBUG_TIMING") != nullptr;
+// Miss pixels are stored by the march kernel's refill rather than by ray_setup (so the
+// stores into a mapped host framebuffer overlap the march); FVSRN_DEFER_MISS=0 restores
+// the ray_setup stores (A/B switch).
+const int g_defer_miss = [] {
+  const char* e = std::getenv("FVSRN_DEFER_MISS");
+  return (e && e[0] == '0') ? 0 : 1;
+}();
 struct HostPhases {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
   std::string out;
@@ -1259,7 +1279,7 @@ static int render_impl(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* 
     order = cost + (size_t)nl;
     CUDA_TRY(cudaMemsetAsync(cost, 0, sizeof(unsigned) * nl, s));
   }
-  CUDA_TRY(launch_ray_setup(cam, md, sh, nullptr, nullptr, n_slots, rr, d_out, cost, nullptr, s));
+  CUDA_TRY(launch_ray_setup(cam, md, sh, nullptr, nullptr, n_slots, rr, d_out, cost, nullptr, g_defer_miss, s));
   count_launch();
   if (use_lpt) {
     CUDA_TRY(launch_tile_sort((int)local_tiles, cost, order, s));
@@ -1328,7 +1348,17 @@ int32_t fvsrn_render(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c,
   int rc = render_impl(m, tf, c, st, t, nullptr, d_out, d_cnt, d_cnt + 1, sg.s);
   if (rc) { cudaFreeAsync(dbuf, sg.s); cudaStreamSynchronize(sg.s); return rc; }
   ph.mark("enqueue");
-  unsigned long long cnt[2] = {0, 0};
+  if (g_debug_timing) {   // host time at which the march kernel has finished
+    cudaEvent_t done;
+    cudaEventCreate(&done);
+    cudaEventRecord(done, sg.s);
+    cudaEventSynchronize(done);
+    cudaEventDestroy(done);
+    ph.mark("kernels");
+  }
+  unsigned long long stack_cnt[2] = {0, 0};
+  unsigned long long* cnt = pinned_counters();
+  if (!cnt) cnt = stack_cnt;
   if (!mapped) CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaFreeAsync(dbuf, sg.s));
@@ -1402,7 +1432,7 @@ int32_t fvsrn_render_rays(fvsrn_model_t m, const fvsrn_tf* tf, const double* ori
   RayRecs rr{};
   void* recs = nullptr;
   if ((rc = alloc_recs(m, n_slots, sg.s, rr, recs))) return rc;
-  CUDA_TRY(launch_ray_setup(cam, md, sh, d_o, d_d, n_slots, rr, d_out, nullptr, nullptr, sg.s));
+  CUDA_TRY(launch_ray_setup(cam, md, sh, d_o, d_d, n_slots, rr, d_out, nullptr, nullptr, g_defer_miss, sg.s));
   count_launch();
   int explicit_rays = 1;
   unsigned long long* queue = fs.counters;

@@ -94,7 +94,7 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   unsigned long long evals = 0;
 
   while (true) {
-    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     const unsigned act = __ballot_sync(0xffffffffu, r.has);
     if (act == 0) break;
     evals += __popc(act);
@@ -173,7 +173,7 @@ dvr_pipe_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
                                    fmaf(kf, r.dd2, r.pe2), st + lane * rs);
   };
   int cur = 0;
-  ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+  ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
   if (r.has) row_at(r.k, stage[0]);
   while (true) {
     const unsigned act = __ballot_sync(0xffffffffu, r.has);
@@ -190,7 +190,7 @@ dvr_pipe_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       fresh = !r.has;
     }
     if (__any_sync(0xffffffffu, fresh)) {
-      ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+      ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
       if (fresh && r.has) row_at(r.k, stage[cur ^ 1]);   // new ray: its first sample
     }
     cur ^= 1;
@@ -250,8 +250,8 @@ dvr_dual_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
   while (true) {
-    ws_refill(r[0], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
-    ws_refill(r[1], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r[0], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
+    ws_refill(r[1], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     const unsigned a0 = __ballot_sync(0xffffffffu, r[0].has), a1 = __ballot_sync(0xffffffffu, r[1].has);
     if ((a0 | a1) == 0) break;
     evals += __popc(a0) + __popc(a1);
@@ -283,7 +283,7 @@ dvr_dual_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
 __global__ void ray_setup_kernel(CamDev cam, MarchDev md, ShardDev sh, const double* __restrict__ rays_o,
                                  const double* __restrict__ rays_d, long long n_slots, RayRecs rr,
                                  float* __restrict__ out, unsigned* __restrict__ tile_cost,
-                                 unsigned* __restrict__ iota) {
+                                 unsigned* __restrict__ iota, int defer_miss) {
   for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
        s += (long long)gridDim.x * blockDim.x) {
     RayGeom g;
@@ -317,6 +317,8 @@ __global__ void ray_setup_kernel(CamDev cam, MarchDev md, ShardDev sh, const dou
         rb = make_float4((float)__dmul_rn(g.ds, g.d[0]), (float)__dmul_rn(g.ds, g.d[1]),
                          (float)__dmul_rn(g.ds, g.d[2]), (float)g.ds);
         if (rr.d) rr.d[s] = make_float4((float)g.d[0], (float)g.d[1], (float)g.d[2], 0.f);
+      } else if (defer_miss) {
+        n = -1;   // the march kernel's refill stores the background (ws_refill)
       } else {
         *reinterpret_cast<float4*>(out + 4 * dst) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
       }
@@ -338,11 +340,11 @@ __global__ void ray_setup_kernel(CamDev cam, MarchDev md, ShardDev sh, const dou
 cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
                              const double* rays_o, const double* rays_d, long long n_slots,
                              const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
-                             cudaStream_t s) {
+                             int defer_miss, cudaStream_t s) {
   if (n_slots <= 0) return cudaSuccess;
   // blocks of 256 keep the tile-cost warp reduction inside one 64-slot tile
   const int blocks = (int)std::min<long long>((n_slots + 255) / 256, 148 * 32);
-  ray_setup_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, rays_o, rays_d, n_slots, rr, out, tile_cost, iota);
+  ray_setup_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, rays_o, rays_d, n_slots, rr, out, tile_cost, iota, defer_miss);
   return cudaGetLastError();
 }
 
@@ -364,7 +366,10 @@ __global__ void __launch_bounds__(1024) lpt_bucket_sort_kernel(const unsigned* _
   __syncthreads();
   int shift = 0;
   while ((cmax >> shift) >= 1024u) ++shift;
-  for (int i = t; i < n; i += 1024) atomicAdd(&hist[1023 - (cost[i] >> shift)], 1u);
+  // zero-cost tiles (all rays miss) go first with the heaviest: their only work is the
+  // deferred background stores, which then drain over PCIe under the march
+  auto bucket = [&](unsigned c) { return c == 0u ? 0u : 1023u - (c >> shift); };
+  for (int i = t; i < n; i += 1024) atomicAdd(&hist[bucket(cost[i])], 1u);
   __syncthreads();
   // exclusive scan of the 1024 bucket counts (Hillis-Steele in shared memory)
   unsigned v = hist[t];
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(1024) lpt_bucket_sort_kernel(const unsigned* _
   __syncthreads();
   hist[t] -= v;
   __syncthreads();
-  for (int i = t; i < n; i += 1024) order[atomicAdd(&hist[1023 - (cost[i] >> shift)], 1u)] = (unsigned)i;
+  for (int i = t; i < n; i += 1024) order[atomicAdd(&hist[bucket(cost[i])], 1u)] = (unsigned)i;
 }
 
 cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s) {
@@ -470,7 +475,7 @@ dvr_ws_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const floa
   };
   // refill group i and write its next input rows; returns whether any lane is active
   auto produce = [&](RayLane& r, __half* stage) -> bool {
-    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     const unsigned a = __ballot_sync(0xffffffffu, r.has);
     evals += __popc(a);
     if (r.has) {

@@ -100,7 +100,7 @@ cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const Shard
 cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardDev& sh,
                              const double* rays_o, const double* rays_d, long long n_slots,
                              const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
-                             cudaStream_t s);
+                             int defer_miss, cudaStream_t s);
 // order[0:n] <- local tiles by (bucketed) descending cost[0:n]; one launch
 cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,

@@ -34,7 +34,8 @@ __device__ __forceinline__ void named_bar_sync(unsigned id, unsigned count) {
 // Refill free lanes of one ray group from the warp's chunk of the global queue.
 __device__ __forceinline__ void ws_refill(RayLane& r, LaneQueue& q, int lane, const CamDev& cam,
                                           const ShardDev& sh, bool explicit_rays, const RayRecs& rr,
-                                          long long n_slots, unsigned long long* __restrict__ queue) {
+                                          long long n_slots, unsigned long long* __restrict__ queue,
+                                          const MarchDev& md, float* __restrict__ out) {
   while (true) {
     unsigned need = __ballot_sync(0xffffffffu, !r.has);
     if (need == 0) break;
@@ -69,6 +70,12 @@ __device__ __forceinline__ void ws_refill(RayLane& r, LaneQueue& q, int lane, co
           r.dx = r.dy = r.dz = 0.f;
         }
         r.C0 = r.C1 = r.C2 = r.A = 0.f;
+      } else if (n < 0) {
+        // a ray that misses the volume (ray_setup deferred its pixel): store the
+        // background here, so the stores of a mapped host framebuffer drain over PCIe
+        // while the march runs instead of serialising before it
+        const long long o = (explicit_rays || sh.compact) ? s : slot_pixel(cam, sh, s);
+        *reinterpret_cast<float4*>(out + 4 * o) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
       }
     }
     q.chunk_base += take;

@@ -206,7 +206,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   uint32_t phase = 0;
 
   while (true) {
-    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
     tmem_bias<HID>(t_row, b_s + S::b_off(0));
@@ -409,7 +409,7 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
   // refill tile t, pre-load its layer-0 bias, write its rows; returns (CTA-wide) whether
   // the tile has any ray, after the fences + barrier that make the rows MMA-visible
   auto start = [&](int t) -> bool {
-    ws_refill(r[t], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue);
+    ws_refill(r[t], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     evals += __popc(__ballot_sync(0xffffffffu, r[t].has));
     tmem_bias<HID>(t_d[t] + lane_off, b_s + S::b_off(0));
     if constexpr (kA0) {          // tcgen05.st is .sync.aligned: every lane stores
