@@ -1484,7 +1484,8 @@ static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64
   const double* pp = d_p;
   const double* pd = d_d;
   unsigned long long* bad = nullptr;
-  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &bad};
+  const float* coords = nullptr;
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &bad, &coords};
   const size_t smem = stage_smem_bytes(net, false, m->k0);
   if ((rc = launch(m, KernelKind::kSample, smem, args, sg.s, n / 32 + 1))) return rc;
   CUDA_TRY(cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, sg.s));
@@ -1532,9 +1533,17 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
   long long begin = lattice_begin, count = lattice_count;
   const double* pp = nullptr;
   const double* pd = nullptr;
-  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad};
+  // lattice coordinates as numpy's linspace(0, 1, res) then float32 (model.py:385-398):
+  // i * step for i < res - 1, the last exactly 1.0
+  std::vector<float> hc((size_t)res);
+  for (int i = 0; i < res; ++i) hc[i] = i == res - 1 ? 1.f : (float)((double)i * step);
+  float* coords = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&coords, hc.size() * sizeof(float), s));
+  CUDA_TRY(cudaMemcpyAsync(coords, hc.data(), hc.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad, &coords};
   const size_t smem = stage_smem_bytes(net, false, m->k0);
   if ((rc = launch(m, KernelKind::kSample, smem, args, s, count / 32 + 1))) return rc;
+  CUDA_TRY(cudaFreeAsync(coords, s));
   CUDA_TRY(cudaFreeAsync(fs.buf, s));
   return FVSRN_OK;
 }
