@@ -52,13 +52,14 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 
 // Activation of element e of a row: every FVSRN_TC_POLY-th element evaluates its cosine
 // on the FMA pipe instead of the XU (MUFU) pipe.  The tcgen05 kernels are XU-bound in
-// their activation phases with issue slots to spare, so moving ~1/3 of the cosines
-// balances the two (0 disables).
+// their activation phases with issue slots to spare (6x64 at 4 CTAs/SM: issue 46%,
+// XU 67%), so moving every 6th cosine balances the two (cfg 3: 28.2 -> 26.9 ms;
+// every 3rd 28.9, 4th 27.8, 8th 27.1, 12th 27.2, 16th 27.3).  0 disables.
 #ifndef FVSRN_TC_POLY
-#define FVSRN_TC_POLY 0
+#define FVSRN_TC_POLY 6
 #endif
 #ifndef FVSRN_TC_SPLIT
-#define FVSRN_TC_SPLIT 0
+#define FVSRN_TC_SPLIT 1
 #endif
 #ifndef FVSRN_TC_WAIT_BAR
 #define FVSRN_TC_WAIT_BAR 0
@@ -69,11 +70,8 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_TMEM_A
 #define FVSRN_TC_TMEM_A 1
 #endif
-// layer-0 input rows in TMEM too (no shared-memory A tile at all): 1 on, 0 off,
-// 2 = 32-wide only (measured: faster at 32-wide, slower at 64-wide)
-#ifndef FVSRN_TC_TMEM_A0
-#define FVSRN_TC_TMEM_A0 2
-#endif
+// FVSRN_TC_TMEM_A0 (fvsrn_tc.cuh): layer-0 input rows in TMEM too (measured at 3
+// CTAs/SM: faster at 32-wide, slower at 64-wide)
 // snake_alt activations of one accumulator row -> fp16 chunks of the A tile row
 // (chunk c = columns 8c..8c+7 at +128 B per chunk in the canonical layout)
 template <int HID>
@@ -179,10 +177,12 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     const int* ts = reinterpret_cast<const int*>(tf_g);
     int* td = reinterpret_cast<int*>(tf);
     for (int i = tid; i < words; i += kTcThreads) td[i] = ts[i];
-    uint4* az = reinterpret_cast<uint4*>(a_s);   // pad columns must stay finite
-    for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
+    if constexpr (!S::kA0) {
+      uint4* az = reinterpret_cast<uint4*>(a_s);   // pad columns must stay finite
+      for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
+    }
   }
-  constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
+  constexpr bool kA0 = S::kA0;
   // TMEM columns: D [0, kTCols), A [kTCols, kTCols + max(K0, HID)/2)
   constexpr uint32_t kAcols = kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
   constexpr uint32_t kNeed = S::kTCols + kAcols;

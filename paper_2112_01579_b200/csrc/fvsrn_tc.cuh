@@ -11,7 +11,7 @@ constexpr int kTcThreads = 128;   // 4 warps = 128 rays = one M=128 UMMA tile
 #define FVSRN_TC_MIN_BLOCKS 5
 #endif
 #ifndef FVSRN_TC_MIN_BLOCKS_WIDE
-#define FVSRN_TC_MIN_BLOCKS_WIDE 3
+#define FVSRN_TC_MIN_BLOCKS_WIDE 4
 #endif
 template <int HID>
 constexpr int tc_min_blocks() {
@@ -42,6 +42,12 @@ struct TcNetDev {
 
 __host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / m * m; }
 
+// layer-0 input rows in TMEM (no shared-memory A tile at all): 1 on, 0 off,
+// 2 = 32-wide only.  On: at 64-wide it frees the 20 KB A tile, which with the split
+// epilogue (128 registers) lets 4 CTAs share an SM (cfg 3: 30.0 -> 28.2 ms)
+#ifndef FVSRN_TC_TMEM_A0
+#define FVSRN_TC_TMEM_A0 1
+#endif
 template <int HID, int NM, int NL>
 struct TcShape {
   static constexpr int kK0 = tc_round(16 + 2 * NM + 3, 16);   // FastRow<NM>::kK0
@@ -59,7 +65,9 @@ struct TcShape {
   static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
   static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
   static constexpr int kATile = kTcThreads * kKA * 2;
-  static constexpr int kMbarOff = kAOff + kATile;
+  // with layer-0 rows in TMEM the one-tile kernel has no shared-memory A tile
+  static constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
+  static constexpr int kMbarOff = kA0 ? kAOff : kAOff + kATile;
   static constexpr int kSmem = kMbarOff + 16;
   static constexpr int kSmem2 = kAOff + 2 * kATile + 32;   // two-tile variant
 };
