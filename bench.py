@@ -304,9 +304,17 @@ def main():
         peer = world > 1 and os.environ.get("FVSRN_MULTI", "peer") == "peer"
         if peer:
             # tiles stored straight into rank 0's frame over NVLink P2P by the render
-            # kernel (CUDA IPC); no gather / reassembly (sharding.PeerFrameRenderer)
+            # kernel (CUDA IPC); no gather / reassembly (sharding.PeerFrameRenderer).
+            # If any rank cannot map the frame, all ranks fall back to the NCCL gather.
+            from paper_2112_01579_b200.sharding import PeerUnavailable
             renderer = PeerFrameRenderer(src)
-            renderer._frame(res, res)
+            try:
+                renderer._frame(res, res)
+            except PeerUnavailable as e:
+                if rank == 0:
+                    print(f"bench: {e}; using the NCCL gather path", file=sys.stderr)
+                peer = False
+        if peer:
 
             def step(i, count_ptr=None):
                 _, ptr, _ = renderer._frame(res, res)

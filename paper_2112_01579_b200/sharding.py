@@ -120,6 +120,10 @@ def _shard_len(width, height, world):
     return n_tiles, math.ceil(n_tiles / world) * TILE * TILE
 
 
+class PeerUnavailable(RuntimeError):
+    """Raised on every rank when any rank cannot map rank 0's framebuffer."""
+
+
 class PeerFrameRenderer:
     """Screen-tile sharding with the frame assembled in peer memory.
 
@@ -156,16 +160,32 @@ class PeerFrameRenderer:
             frame = t.empty((height, width, 4), dtype=t.float32, device="cuda") if self.rank == 0 else None
             ptr = frame.data_ptr() if frame is not None else None
             if self.world > 1:
-                obj = [None]
+                # every rank reaches the same collectives even when a step fails, and all
+                # ranks agree on the outcome (PeerUnavailable everywhere, so a caller can
+                # fall back to TileShardRenderer without a hang)
+                obj, err = [None], None
                 if self.rank == 0:
-                    h = C.create_string_buffer(64)
-                    L.check(L.lib().fvsrn_ipc_export(C.c_void_p(ptr), h))
-                    obj = [h.raw]
+                    try:
+                        h = C.create_string_buffer(64)
+                        L.check(L.lib().fvsrn_ipc_export(C.c_void_p(ptr), h))
+                        obj = [h.raw]
+                    except Exception as e:          # noqa: BLE001 -- reported below
+                        err = e
                 self.dist.broadcast_object_list(obj, src=0, group=self.group)
-                if self.rank != 0:
-                    p = C.c_void_p()
-                    L.check(L.lib().fvsrn_ipc_open(obj[0], t.cuda.current_device(), C.byref(p)))
-                    ptr = p.value
+                if self.rank != 0 and obj[0] is not None:
+                    try:
+                        p = C.c_void_p()
+                        L.check(L.lib().fvsrn_ipc_open(obj[0], t.cuda.current_device(), C.byref(p)))
+                        ptr = p.value
+                    except Exception as e:          # noqa: BLE001
+                        err = e
+                dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+                ok = t.tensor([0 if (err is not None or obj[0] is None) else 1], device=dev)
+                self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self.group)
+                if not int(ok.item()):
+                    if self.rank != 0 and err is None and obj[0] is not None:
+                        L.lib().fvsrn_ipc_close(C.c_void_p(ptr))
+                    raise PeerUnavailable(f"peer framebuffer unavailable on some rank ({err})")
             cnt = t.zeros(1, dtype=t.int64, device="cuda")
             self._frames[key] = (frame, ptr, cnt)
         return self._frames[key]
