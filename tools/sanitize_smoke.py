@@ -1,0 +1,29 @@
+"""Small invocations of every kernel family, for compute-sanitizer runs:
+    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py"""
+import os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np
+import paper_2112_01579_b200 as P
+from paper_2112_01579_b200 import device as D
+
+cam = P.fibonacci_cameras(8, 40, 24)[2]
+s = P.RenderSettings(stepsize=1 / 64)
+for kw in (dict(layers=4, hidden=32, grid_resolution=8, seed=0),
+           dict(layers=6, hidden=64, grid_resolution=8, fourier_m=30, seed=0),
+           dict(layers=3, hidden=32, grid_resolution=6, grid_channels=8, keyframe_times=[1, 6, 11],
+                time_mode="both", seed=3)):
+    m = P.model_init(P.ModelConfig(**kw))
+    t = 3.0 if m.is_temporal else None
+    src = P.ModelSource(m, P.TF_PRESETS["warm"], t=t)
+    for k in ("auto", "warp", "tc"):
+        D.set_dvr_kernel(k)
+        P.render_image(src, cam, s)
+    D.set_dvr_kernel("auto")
+    p = np.random.default_rng(0).uniform(0, 1, (100, 3))
+    P.eval_density(m, p, t=t)
+    P.decode_volume(m, 12, t=t)
+vol = P.ScalarVolume(np.random.default_rng(1).uniform(0, 1, (9, 7, 5)).astype(np.float32))
+P.render_image(P.VolumeSource(vol, P.TF_PRESETS["grayscale"]), cam, s)
+m = P.model_init(P.ModelConfig(layers=3, hidden=32, grid_resolution=8, seed=0))
+P.train_world(m, P.WorldTarget(vol), P.WorldTrainConfig(sample_count=2048, batch_size=512, epochs=1))
+print("sanitize smoke done")
