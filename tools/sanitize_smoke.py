@@ -26,4 +26,10 @@ vol = P.ScalarVolume(np.random.default_rng(1).uniform(0, 1, (9, 7, 5)).astype(np
 P.render_image(P.VolumeSource(vol, P.TF_PRESETS["grayscale"]), cam, s)
 m = P.model_init(P.ModelConfig(layers=3, hidden=32, grid_resolution=8, seed=0))
 P.train_world(m, P.WorldTarget(vol), P.WorldTrainConfig(sample_count=2048, batch_size=512, epochs=1))
+mc = P.model_init(P.ModelConfig(head="color", layers=3, hidden=32, grid_resolution=8, seed=11))
+P.train_screen(mc, vol, P.TF_PRESETS["warm"],
+               P.ScreenTrainConfig(views=2, resolution=12, stepsize=0.05, epochs=1, reference_stepsize_voxels=0.5))
+mt = P.model_init(P.ModelConfig(layers=3, hidden=32, grid_resolution=6, keyframe_times=[1, 11], seed=0))
+P.train_temporal(mt, lambda t: vol, P.TemporalTrainConfig(keyframe_times=[1, 11], train_times=[1, 6, 11],
+                 world=P.WorldTrainConfig(sample_count=1024, batch_size=512, epochs=1)))
 print("sanitize smoke done")
