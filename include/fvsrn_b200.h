@@ -164,6 +164,16 @@ FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const fl
                                           int64_t n, float* d_grid_grad, float* d_inputs,
                                           float* d_preacts, float* d_deltas, double* d_loss_sum,
                                           void* stream);
+/* model_backward (model.py:300-335): gradients of sum(raw_bar * raw) for n samples with
+ * given raw-output adjoints d_raw_bar (n, d_out) f32, any head and input encoding (view
+ * directions d_dirs (n,3) for direction modes, per-sample d_times for temporal models).
+ * Same caches as fvsrn_train_world_grads (weight/bias gradients are the caller's GEMMs
+ * over d_inputs / d_deltas); latent-grid gradients are scatter-added into d_grid_grad. */
+FVSRN_API int32_t fvsrn_model_grads(const fvsrn_train_desc* desc, const float* d_params,
+                                    const double* d_positions, const double* d_dirs,
+                                    const double* d_times, const float* d_raw_bar, int64_t n,
+                                    float* d_grid_grad, float* d_inputs, float* d_preacts,
+                                    float* d_deltas, void* stream);
 /* Screen-space training (train.py:227-262), colour-head models.  Forward:
  * raymarch_forward(..., want_states=True) (render.py:203-238) of n explicit rays with f32
  * model evaluation and f64 compositing, no early termination: pixels (n,4) f32, terminal

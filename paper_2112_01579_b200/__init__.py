@@ -15,9 +15,10 @@ from .fused import (FusedPlan, bench_compare, bench_csv, fused_eval, naive_eval_
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
                    grid_quantize, grid_sample, keyframe_bracket, keyframe_sample)
 from .imaging import Camera, Image, metric_psnr, metric_ssim, png_bytes, write_png
-from .model import (CheckpointError, FvsrnModel, ModelConfig, apply_color_head, apply_density_head,
-                    assemble_input, checkpoint_load, checkpoint_save, decode_volume, eval_color,
-                    eval_density, memory_footprint, model_init)
+from .model import (CheckpointError, FvsrnModel, ModelConfig, ModelForwardContext, apply_color_head,
+                    apply_density_head, assemble_input, checkpoint_load, checkpoint_save,
+                    color_head_backward, decode_volume, density_head_backward, eval_color,
+                    eval_density, memory_footprint, model_backward, model_forward, model_init)
 from .nn import (FourierEncoder, MlpParams, act_eval, act_grad, fourier_make, init_params, mlp_eval,
                  nerf_rows)
 from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays, composite_invert,

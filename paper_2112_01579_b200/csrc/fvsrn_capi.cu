@@ -838,6 +838,24 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
   return FVSRN_OK;
 }
 
+int32_t fvsrn_model_grads(const fvsrn_train_desc* d, const float* d_params, const double* d_positions,
+                          const double* d_dirs, const double* d_times, const float* d_raw_bar, int64_t n,
+                          float* d_grid_grad, float* d_inputs, float* d_preacts, float* d_deltas,
+                          void* stream) {
+  if (!d || !d_params || (n > 0 && (!d_positions || !d_raw_bar || !d_inputs || !d_deltas)))
+    return fail(FVSRN_EINVAL, "null argument");
+  TrainNetDev net;
+  int rc = make_train_net(d, n, net);
+  if (rc) return rc;
+  if (net.n_kf > 0 && n > 0 && !d_times) return fail(FVSRN_EINVAL, "temporal model requires timesteps");
+  if (d->raw_width > 3 && n > 0 && !d_dirs) return fail(FVSRN_EINVAL, "direction mode requires view directions");
+  CUDA_TRY(launch_model_grads(net, d_params, d_positions, d->raw_width > 3 ? d_dirs : nullptr,
+                              net.n_kf > 0 ? d_times : nullptr, d_raw_bar, (long long)n, d_grid_grad,
+                              d_inputs, d_preacts, d_deltas, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_train_screen_forward(const fvsrn_train_desc* d, const float* d_params,
                                    const double* d_origins, const double* d_dirs, int64_t n,
                                    const fvsrn_settings* st, float* d_pixels, double* d_color,

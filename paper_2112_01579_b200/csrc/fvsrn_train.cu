@@ -265,6 +265,40 @@ __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ pa
   if ((threadIdx.x & 31) == 0 && loss_sum) atomicAdd(loss_sum, my_loss);
 }
 
+// model_backward (model.py:300-335): gradients of sum(raw_bar * raw) for given per-sample
+// raw-output adjoints (any head, any input encoding incl. view directions).  The forward
+// is recomputed with its caches (deterministic, identical to model_forward's); weight /
+// bias reductions are GEMMs on the host side, the latent-grid adjoint is scattered here.
+__global__ void model_grads_kernel(TrainNetDev net, const float* __restrict__ params,
+                                   const double* __restrict__ pos, const double* __restrict__ dirs,
+                                   const double* __restrict__ times, const float* __restrict__ raw_bar_in,
+                                   long long n, float* __restrict__ grid_grad,
+                                   float* __restrict__ inputs, float* __restrict__ preacts,
+                                   float* __restrict__ deltas) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float x[kTrainMaxW], y[kTrainMaxW];
+  const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+  const CacheRef c{inputs, preacts, deltas, i, n};
+  Cell cell;
+  assemble_f32(net, params, p, dirs ? dirs + 3 * i : nullptr, times ? times[i] : 0.0, x, cell);
+  mlp_f32(net, params, c, x, y);
+  float raw_bar[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int ch = 0; ch < net.d_out && ch < 4; ++ch) raw_bar[ch] = raw_bar_in[i * net.d_out + ch];
+  f32_backward(net, params, raw_bar, c, cell, grid_grad, x, y);
+}
+
+cudaError_t launch_model_grads(const TrainNetDev& net, const float* params, const double* pos,
+                               const double* dirs, const double* times, const float* raw_bar, long long n,
+                               float* grid_grad, float* inputs, float* preacts, float* deltas,
+                               cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int threads = 128;
+  model_grads_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
+      net, params, pos, dirs, times, raw_bar, n, grid_grad, inputs, preacts, deltas);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- screen space
 // raymarch_forward(ModelSource(colour model), want_states=True) (render.py:203-238):
 // f64 geometry and compositing, f32 model evaluation (the naive ModelSource path), no

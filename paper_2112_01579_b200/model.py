@@ -337,6 +337,113 @@ def assemble_input(model: FvsrnModel, p, d=None, t=None) -> np.ndarray:
     return NetDesc.for_model(model).run(0, n, cfg.input_width, p=p, d=d, t=t)
 
 
+def _check_inputs(model, p, d, t):
+    cfg = model.config
+    p = np.atleast_2d(np.asarray(p, dtype=np.float64))
+    n = p.shape[0]
+    if cfg.direction_mode in ("dirP", "dirF"):
+        if d is None:
+            raise ValueError(f"direction mode {cfg.direction_mode!r} requires view directions")
+        d = np.atleast_2d(np.asarray(d, dtype=np.float64))
+        if d.shape != p.shape:
+            raise ValueError("directions must match positions in shape")
+    else:
+        d = None
+    if cfg.is_temporal:
+        if t is None:
+            raise ValueError("temporal model requires timesteps")
+        t = np.broadcast_to(np.asarray(t, dtype=np.float64), (n,)).copy()
+    elif t is not None:
+        raise ValueError("timestep supplied to a non-temporal model")
+    return p, d, t
+
+
+@dataclass
+class ModelForwardContext:
+    """What model_backward needs (model.py:280-288).  The GPU backward recomputes the
+    layer caches from the positions (same f32 arithmetic), so ``cache`` is None; the
+    view directions are kept for direction-mode models."""
+
+    inputs: np.ndarray
+    cache: object
+    positions: np.ndarray
+    times: np.ndarray | None
+    dirs: np.ndarray | None = None
+
+
+def model_forward(model: FvsrnModel, p, d=None, t=None):
+    """Raw (pre-head) outputs plus the context for model_backward (model.py:290-299),
+    on the GPU f32 evaluator.  ``t`` may be a scalar or one timestep per sample."""
+    from .f32ops import NetDesc
+
+    p, d, t = _check_inputs(model, p, d, t)
+    nd = NetDesc.for_model(model)
+    n, cfg = p.shape[0], model.config
+    x = nd.run(0, n, cfg.input_width, p=p, d=d, t=t)
+    raw = nd.run(2, n, cfg.output_width, p=p, d=d, t=t)
+    return raw, ModelForwardContext(inputs=x, cache=None, positions=p, times=t, dirs=d)
+
+
+def model_backward(model: FvsrnModel, ctx: ModelForwardContext, raw_bar, grads=None):
+    """Accumulate the gradients of sum(raw_bar * raw) into a GradientBuffer
+    (model.py:302-335): one CUDA kernel recomputes the forward with its caches, runs the
+    MLP backward and scatter-adds the latent-grid adjoint (both bracketing keyframe grids
+    for temporal models, weights 1-w / w); the weight and bias reductions are GEMMs."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib as L
+    from .f32ops import NetDesc
+    from .train import GradientBuffer
+
+    cfg = model.config
+    p, d, t = ctx.positions, ctx.dirs, ctx.times
+    n = p.shape[0]
+    rb = np.ascontiguousarray(np.asarray(raw_bar, dtype=np.float32).reshape(n, cfg.output_width))
+    nd = NetDesc.for_model(model)
+    dev = nd.dev
+    L_ = model.params.layer_count
+    w_in = [cfg.input_width] + [cfg.hidden] * (L_ - 1)
+    w_out = [cfg.hidden] * (L_ - 1) + [cfg.output_width]
+    f64 = lambda a: None if a is None else torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)  # noqa: E731
+    pd, dd, td = f64(p), f64(d), f64(t)
+    rbd = torch.as_tensor(rb, device=dev)
+    inputs = torch.empty(max(1, n * sum(w_in)), dtype=torch.float32, device=dev)
+    deltas = torch.empty(max(1, n * sum(w_out)), dtype=torch.float32, device=dev)
+    preacts = torch.empty(max(1, (L_ - 1) * n * cfg.hidden), dtype=torch.float32, device=dev)
+    gsizes = [int(g.values.size) for g in model.grids]
+    ggrad = torch.zeros(max(1, sum(gsizes)), dtype=torch.float32, device=dev)
+    ptr = lambda a: C.c_void_p(a.data_ptr() if a is not None else None)  # noqa: E731
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    L.check(L.lib().fvsrn_model_grads(C.byref(nd.desc), ptr(nd.params), ptr(pd), ptr(dd), ptr(td),
+                                      ptr(rbd), n, C.c_void_p(ggrad.data_ptr() if gsizes else None),
+                                      ptr(inputs), ptr(preacts), ptr(deltas), C.c_void_p(stream)))
+    gw, gb = [], []
+    io = do = 0
+    for l in range(L_):
+        x = inputs[io:io + n * w_in[l]].view(n, w_in[l])
+        dl = deltas[do:do + n * w_out[l]].view(n, w_out[l])
+        gw.append((dl.t() @ x).cpu().numpy())                 # nn.py:252
+        gb.append(dl.sum(dim=0).cpu().numpy())                # nn.py:253
+        io += n * w_in[l]
+        do += n * w_out[l]
+    gg, off = [], 0
+    host = ggrad.cpu().numpy()
+    for g, sz in zip(model.grids, gsizes):
+        gg.append(host[off:off + sz].reshape(g.values.shape))
+        off += sz
+    if grads is None:
+        return GradientBuffer(weights=gw, biases=gb, grids=gg)
+    for acc, g in zip(grads.weights, gw):
+        acc += g
+    for acc, g in zip(grads.biases, gb):
+        acc += g
+    for acc, g in zip(grads.grids, gg):
+        acc += g
+    return grads
+
+
 def softplus(x: np.ndarray) -> np.ndarray:
     """Host utility (model.py:338-339); the kernels apply the heads in-kernel."""
     return np.logaddexp(0.0, x)
@@ -345,6 +452,25 @@ def softplus(x: np.ndarray) -> np.ndarray:
 def apply_density_head(raw: np.ndarray) -> np.ndarray:
     """sigmoid(raw[:, 0]) (model.py:342-343); host utility on host arrays."""
     return (1.0 / (1.0 + np.exp(-np.asarray(raw)[:, 0]))).astype(np.asarray(raw).dtype)
+
+
+def density_head_backward(raw: np.ndarray, y_bar: np.ndarray) -> np.ndarray:
+    """Adjoint of apply_density_head (model.py:346-350); host utility on host arrays."""
+    raw = np.asarray(raw)
+    s = 1.0 / (1.0 + np.exp(-raw[:, 0]))
+    out = np.zeros_like(raw)
+    out[:, 0] = y_bar * s * (1.0 - s)
+    return out
+
+
+def color_head_backward(raw: np.ndarray, y_bar: np.ndarray) -> np.ndarray:
+    """Adjoint of apply_color_head (model.py:360-365); host utility on host arrays."""
+    raw = np.asarray(raw)
+    out = np.empty_like(raw)
+    s = 1.0 / (1.0 + np.exp(-raw[:, :3]))
+    out[:, :3] = y_bar[:, :3] * s * (1.0 - s)
+    out[:, 3] = y_bar[:, 3] * (1.0 / (1.0 + np.exp(-raw[:, 3])))
+    return out
 
 
 def apply_color_head(raw: np.ndarray) -> np.ndarray:

@@ -220,3 +220,51 @@ def test_evaluate_views_vs_reference():
         # fp16 network in the kernel vs f32 reference evaluation: metric-level tolerance
         assert got["psnr"] == pytest.approx(ref["psnr"], abs=0.05)
         assert got["ssim"] == pytest.approx(ref["ssim"], abs=5e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES + ["t_temporal", "t_temporal_both"])
+def test_model_forward_backward_vs_reference(name):
+    # model_forward / model_backward (model.py:290-335) with the reference's L1 adjoint
+    # through the head backward (train.py:158-162, model.py:346-365)
+    a = arrays()
+    if name.startswith("t_"):
+        key = name[2:]
+        m = P.model_init(P.ModelConfig(**meta()["models"][key]["config"]))
+        pb, tb, ref = a[f"ttrain_pos_{key}"], a[f"ttrain_t_{key}"], a[f"ttrain_ref_{key}"]
+        want = a[f"ttrain_grads_{key}"]
+    else:
+        m, pb, tb, ref = _model(name), a[f"train_pos_{name}"], None, a[f"train_ref_{name}"]
+        want = a[f"train_grads_{name}"]
+    raw, ctx = P.model_forward(m, pb, t=tb)
+    assert ctx.inputs.shape == (len(pb), m.config.input_width)
+    dens = m.config.head == "density"
+    pred = P.apply_density_head(raw) if dens else P.apply_color_head(raw)
+    diff = pred - np.asarray(ref).reshape(pred.shape)
+    adj = (np.sign(diff) / diff.size).astype(np.float32)
+    raw_bar = P.density_head_backward(raw, adj) if dens else P.color_head_backward(raw, adj)
+    g = P.model_backward(m, ctx, raw_bar)
+    got = np.concatenate([x.reshape(-1) for x in g.arrays()])
+    assert got.shape == want.shape
+    off = 0
+    for arr in m.trainable_arrays():
+        gg, ww = got[off:off + arr.size], want[off:off + arr.size]
+        scale = float(np.abs(ww).max()) or 1.0
+        assert np.abs(gg - ww).max() <= 1e-4 * scale, (name, arr.shape, np.abs(gg - ww).max(), scale)
+        off += arr.size
+    # accumulation into an existing buffer doubles it
+    g2 = P.model_backward(m, ctx, raw_bar, grads=P.model_backward(m, ctx, raw_bar))
+    np.testing.assert_allclose(np.concatenate([x.reshape(-1) for x in g2.arrays()]), 2 * got,
+                               rtol=1e-5, atol=1e-9)
+
+
+def test_head_backward_host_utilities():
+    raw = np.random.default_rng(0).normal(size=(7, 4)).astype(np.float32)
+    yb = np.random.default_rng(1).normal(size=(7, 4)).astype(np.float32)
+    s = 1 / (1 + np.exp(-raw))
+    d = P.density_head_backward(raw, yb[:, 0])
+    np.testing.assert_allclose(d[:, 0], yb[:, 0] * s[:, 0] * (1 - s[:, 0]), rtol=1e-6)
+    assert np.all(d[:, 1:] == 0)
+    c = P.color_head_backward(raw, yb)
+    np.testing.assert_allclose(c[:, :3], yb[:, :3] * s[:, :3] * (1 - s[:, :3]), rtol=1e-6)
+    np.testing.assert_allclose(c[:, 3], yb[:, 3] * s[:, 3], rtol=1e-6)
