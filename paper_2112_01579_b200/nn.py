@@ -158,3 +158,64 @@ def mlp_eval(params: MlpParams, x: np.ndarray) -> np.ndarray:
         raise ValueError(f"expected input shape (N, {d_in}), got {x.shape}")
     nd = NetDesc(params.weights, params.biases, params.activation, "density", d_in)
     return nd.run(3, x.shape[0], int(params.weights[-1].shape[0]), x=x)
+
+
+@dataclass
+class AdamState:
+    """First/second moment accumulators, one per parameter array (nn.py:258-276)."""
+
+    m: list
+    v: list
+    t: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    @classmethod
+    def for_arrays(cls, arrays, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> "AdamState":
+        return cls(m=[np.zeros_like(a) for a in arrays], v=[np.zeros_like(a) for a in arrays],
+                   beta1=beta1, beta2=beta2, eps=eps)
+
+
+def adam_step(arrays: list, grads: list, state: AdamState, lr: float) -> None:
+    """One bias-corrected Adam update of host arrays, in place (nn.py:279-298), by the
+    CUDA Adam kernel (``fvsrn_adam_step``) over one flat device buffer; the arrays and
+    the moments are written back.  A non-finite gradient raises FloatingPointError and
+    updates nothing (the step counter included)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib as L
+
+    if len(arrays) != len(state.m) or len(grads) != len(arrays) or len(state.v) != len(arrays):
+        raise ValueError("parameter/gradient/state lengths disagree")
+    for p, g in zip(arrays, grads):
+        if np.shape(p) != np.shape(g):
+            raise ValueError(f"gradient shape {np.shape(g)} does not match parameter {np.shape(p)}")
+    if not arrays:
+        state.t += 1
+        return
+    dev = torch.device("cuda", L.current_device())
+
+    def flat(xs):
+        return torch.from_numpy(np.concatenate([np.asarray(x, dtype=np.float32).reshape(-1) for x in xs])).to(dev)
+
+    P, G, M, V = flat(arrays), flat(grads), flat(state.m), flat(state.v)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    L.check(L.lib().fvsrn_adam_step(C.c_void_p(P.data_ptr()), C.c_void_p(G.data_ptr()),
+                                    C.c_void_p(M.data_ptr()), C.c_void_p(V.data_ptr()), P.numel(),
+                                    float(lr), float(state.beta1), float(state.beta2), float(state.eps),
+                                    state.t + 1, C.c_void_p(bad.data_ptr()), C.c_void_p(stream)))
+    if int(bad.item()):
+        raise FloatingPointError("non-finite gradient passed to adam_step")
+    state.t += 1
+    off = 0
+    hp, hm, hv = P.cpu().numpy(), M.cpu().numpy(), V.cpu().numpy()
+    for p, m, v in zip(arrays, state.m, state.v):
+        k = int(np.size(p))
+        p[...] = hp[off:off + k].reshape(np.shape(p))
+        m[...] = hm[off:off + k].reshape(np.shape(m))
+        v[...] = hv[off:off + k].reshape(np.shape(v))
+        off += k

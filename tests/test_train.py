@@ -268,3 +268,33 @@ def test_head_backward_host_utilities():
     c = P.color_head_backward(raw, yb)
     np.testing.assert_allclose(c[:, :3], yb[:, :3] * s[:, :3] * (1 - s[:, :3]), rtol=1e-6)
     np.testing.assert_allclose(c[:, 3], yb[:, 3] * s[:, 3], rtol=1e-6)
+
+
+@pytest.mark.gpu
+def test_adam_step_host_api_matches_reference_semantics():
+    # adam_step / AdamState (nn.py:258-298) on host arrays through the CUDA Adam kernel
+    rng = np.random.default_rng(4)
+    arrays = [rng.normal(size=(3, 5)).astype(np.float32), rng.normal(size=(5,)).astype(np.float32)]
+    ref = [a.copy() for a in arrays]
+    st = P.AdamState.for_arrays(arrays)
+    m = [np.zeros_like(a) for a in arrays]
+    v = [np.zeros_like(a) for a in arrays]
+    for t in range(1, 4):
+        grads = [(rng.normal(size=a.shape) * 1e-2).astype(np.float32) for a in arrays]
+        P.adam_step(arrays, grads, st, 0.01)
+        bc1, bc2 = 1 - 0.9 ** t, 1 - 0.999 ** t
+        for p, g, mm, vv in zip(ref, grads, m, v):
+            mm *= np.float32(0.9); mm += np.float32(0.1) * g
+            vv *= np.float32(0.999); vv += np.float32(0.001) * g * g
+            p -= np.float32(0.01) * (mm / np.float32(bc1)) / (np.sqrt(vv / np.float32(bc2)) + np.float32(1e-8))
+        for a, r in zip(arrays, ref):
+            np.testing.assert_allclose(a, r, rtol=0, atol=2e-7)
+    assert st.t == 3
+    before = [a.copy() for a in arrays]
+    bad = [np.zeros_like(a) for a in arrays]
+    bad[1][2] = np.inf
+    with pytest.raises(FloatingPointError):
+        P.adam_step(arrays, bad, st, 0.01)
+    assert st.t == 3 and all(np.array_equal(a, b) for a, b in zip(arrays, before))
+    with pytest.raises(ValueError):
+        P.adam_step(arrays, bad[:1], st, 0.01)
