@@ -164,6 +164,11 @@ FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const fl
                                           int64_t n, float* d_grid_grad, float* d_inputs,
                                           float* d_preacts, float* d_deltas, double* d_loss_sum,
                                           void* stream);
+/* grid_sample_backward (grid.py:123-137): scatter-add of trilinear-weighted adjoints
+ * d_z_bar (n, channels) f32 at positions (n,3) f64 into d_grad (res^3 * channels) f32. */
+FVSRN_API int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels,
+                                             const double* d_positions, const float* d_z_bar,
+                                             int64_t n, float* d_grad, void* stream);
 /* model_backward (model.py:300-335): gradients of sum(raw_bar * raw) for n samples with
  * given raw-output adjoints d_raw_bar (n, d_out) f32, any head and input encoding (view
  * directions d_dirs (n,3) for direction modes, per-sample d_times for temporal models).

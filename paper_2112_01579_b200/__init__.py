@@ -13,7 +13,7 @@ from ._lib import CapacityError, pinned_empty
 from .fused import (FusedPlan, bench_compare, bench_csv, fused_eval, naive_eval_model, plan_build,
                     plan_for_model, warmup)
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
-                   grid_quantize, grid_sample, keyframe_bracket, keyframe_sample)
+                   grid_quantize, grid_sample, grid_sample_backward, keyframe_bracket, keyframe_sample)
 from .imaging import Camera, Image, metric_psnr, metric_ssim, png_bytes, write_png
 from .model import (CheckpointError, FvsrnModel, ModelConfig, ModelForwardContext, apply_color_head,
                     apply_density_head, assemble_input, checkpoint_load, checkpoint_save,

@@ -838,6 +838,16 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
   return FVSRN_OK;
 }
 
+int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels, const double* d_positions,
+                                   const float* d_z_bar, int64_t n, float* d_grad, void* stream) {
+  if (resolution < 2 || channels < 1) return fail(FVSRN_EINVAL, "grid must have resolution >= 2 and channels >= 1");
+  if (n > 0 && (!d_positions || !d_z_bar || !d_grad)) return fail(FVSRN_EINVAL, "null argument");
+  CUDA_TRY(launch_grid_scatter(resolution, channels, d_positions, d_z_bar, (long long)n, d_grad,
+                               (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_model_grads(const fvsrn_train_desc* d, const float* d_params, const double* d_positions,
                           const double* d_dirs, const double* d_times, const float* d_raw_bar, int64_t n,
                           float* d_grid_grad, float* d_inputs, float* d_preacts, float* d_deltas,

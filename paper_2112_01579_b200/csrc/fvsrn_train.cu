@@ -265,6 +265,38 @@ __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ pa
   if ((threadIdx.x & 31) == 0 && loss_sum) atomicAdd(loss_sum, my_loss);
 }
 
+// grid_sample_backward (grid.py:123-137): trilinear-weighted scatter-add of per-sample
+// adjoints z_bar (n, F) into a gradient grid shaped like the latent grid (R, R, R, F).
+// Same cell arithmetic as the lookup (_cell_coords in f64, f32 weights); atomics replace
+// the reference's sequential loop, so sums agree to rounding order.
+__global__ void grid_scatter_kernel(int R, int F, const double* __restrict__ pos,
+                                    const float* __restrict__ z_bar, long long n, float* __restrict__ grad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double s = (double)(R - 1);
+  const double cx = fmin(fmax(pos[3 * i], 0.0), 1.0) * s, cy = fmin(fmax(pos[3 * i + 1], 0.0), 1.0) * s,
+               cz = fmin(fmax(pos[3 * i + 2], 0.0), 1.0) * s;
+  const int x0 = min((int)cx, R - 2), y0 = min((int)cy, R - 2), z0 = min((int)cz, R - 2);
+  const float fx = (float)(cx - x0), fy = (float)(cy - y0), fz = (float)(cz - z0);
+  const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+  const float w[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                      fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+  const long long sz = F, sy = (long long)R * F, sx = (long long)R * R * F;
+  const long long off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+  float* g = grad + (((long long)x0 * R + y0) * R + z0) * F;
+  for (int ch = 0; ch < F; ++ch) {
+    const float zb = z_bar[i * F + ch];
+    for (int q = 0; q < 8; ++q) atomicAdd(g + off[q] + ch, w[q] * zb);
+  }
+}
+
+cudaError_t launch_grid_scatter(int R, int F, const double* pos, const float* z_bar, long long n,
+                                float* grad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  grid_scatter_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(R, F, pos, z_bar, n, grad);
+  return cudaGetLastError();
+}
+
 // model_backward (model.py:300-335): gradients of sum(raw_bar * raw) for given per-sample
 // raw-output adjoints (any head, any input encoding incl. view directions).  The forward
 // is recomputed with its caches (deterministic, identical to model_forward's); weight /

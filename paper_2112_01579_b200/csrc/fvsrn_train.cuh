@@ -33,6 +33,8 @@ struct AdamConsts {
   float lr, b1, b2, one_m_b1, one_m_b2, eps, bc1, bc2;
 };
 
+cudaError_t launch_grid_scatter(int R, int F, const double* pos, const float* z_bar, long long n,
+                                float* grad, cudaStream_t s);
 cudaError_t launch_model_grads(const TrainNetDev& net, const float* params, const double* pos,
                                const double* dirs, const double* times, const float* raw_bar, long long n,
                                float* grid_grad, float* inputs, float* preacts, float* deltas,

@@ -124,6 +124,34 @@ def grid_sample(grid: LatentGrid, p) -> np.ndarray:
     return out[0] if single else out
 
 
+def grid_sample_backward(grid: LatentGrid, p, z_bar, grad: np.ndarray) -> None:
+    """Scatter-add trilinear-weighted adjoints into ``grad`` (shaped like grid.values), in
+    place (grid.py:123-137), by a CUDA scatter kernel (``fvsrn_grid_sample_backward``).
+    Positions receive no gradient.  Device atomics replace the reference's sequential
+    loop: sums agree up to f32 rounding order."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib as L
+
+    if grad.shape != grid.values.shape:
+        raise ValueError(f"gradient shape {grad.shape} does not match grid {grid.values.shape}")
+    pts, _ = _positions(p)
+    zb = np.atleast_2d(np.asarray(z_bar, dtype=np.float32))
+    if zb.shape != (len(pts), grid.channels):
+        raise ValueError(f"adjoint shape {zb.shape} does not match (N,{grid.channels})")
+    dev = torch.device("cuda", L.current_device())
+    pd = torch.as_tensor(np.ascontiguousarray(pts, dtype=np.float64), device=dev)
+    zd = torch.as_tensor(np.ascontiguousarray(zb), device=dev)
+    gd = torch.as_tensor(np.ascontiguousarray(grad, dtype=np.float32), device=dev).contiguous()
+    L.check(L.lib().fvsrn_grid_sample_backward(int(grid.resolution), int(grid.channels),
+                                               C.c_void_p(pd.data_ptr()), C.c_void_p(zd.data_ptr()),
+                                               len(pts), C.c_void_p(gd.data_ptr()),
+                                               C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    grad[...] = gd.cpu().numpy().reshape(grad.shape)
+
+
 def keyframe_bracket(kfg: "KeyframeGrids", t: float) -> tuple[int, int, float]:
     """Indices of the bracketing keyframes and the blend weight of the upper one
     (grid.py:206-219)."""

@@ -362,6 +362,19 @@ def main():
                               "rows": rows, "csv": metrics_csv(rows)}
     print("evaluate_views", rows, flush=True)
 
+    # --- grid_sample_backward (grid.py:123-137) on cfg1's latent grid: positions incl.
+    # the faces / corners / outside the cube (clamped), random adjoints
+    from fvsrn.grid import grid_sample_backward
+
+    g1 = models["cfg1"].grid
+    rng = np.random.default_rng(55)
+    gp = rng.uniform(-0.1, 1.1, size=(300, 3))
+    gp[:4] = [[0, 0, 0], [1, 1, 1], [1, 0, 0.5], [0.999999, 1e-9, 0.25]]
+    gz = rng.normal(size=(300, g1.channels)).astype(np.float32)
+    gg = np.zeros_like(g1.values)
+    grid_sample_backward(g1, gp, gz, gg)
+    arrays["gsb_pos"], arrays["gsb_zbar"], arrays["gsb_grad"] = gp, gz, gg
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

@@ -298,3 +298,22 @@ def test_adam_step_host_api_matches_reference_semantics():
     assert st.t == 3 and all(np.array_equal(a, b) for a, b in zip(arrays, before))
     with pytest.raises(ValueError):
         P.adam_step(arrays, bad[:1], st, 0.01)
+
+
+@pytest.mark.gpu
+def test_grid_sample_backward_vs_reference():
+    # grid.py:123-137 scatter-add, incl. clamped positions outside the cube; atomics vs the
+    # reference's sequential loop: equal up to f32 summation order
+    a = arrays()
+    m = _model("cfg1")
+    g = np.zeros_like(m.grid.values)
+    P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"], g)
+    want = a["gsb_grad"]
+    assert np.abs(g - want).max() <= 1e-5 * float(np.abs(want).max())
+    # accumulates in place
+    P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"], g)
+    assert np.abs(g - 2 * want).max() <= 2e-5 * float(np.abs(want).max())
+    with pytest.raises(ValueError):
+        P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"][:, :3], g)
+    with pytest.raises(ValueError):
+        P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"], g[:2])
