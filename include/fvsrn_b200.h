@@ -164,6 +164,13 @@ FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const fl
                                           int64_t n, float* d_grid_grad, float* d_inputs,
                                           float* d_preacts, float* d_deltas, double* d_loss_sum,
                                           void* stream);
+/* mlp_forward / mlp_backward (nn.py:179-193, 234-256) of a plain MLP (desc without grid)
+ * on given inputs d_x (n, d_in) f32: outputs d_y (n, d_out), caches (layout as
+ * fvsrn_train_world_grads) and, when d_y_bar (n, d_out) is given, the per-layer deltas. */
+FVSRN_API int32_t fvsrn_mlp_forward_backward(const fvsrn_train_desc* desc, const float* d_params,
+                                             const float* d_x, const float* d_y_bar, int64_t n,
+                                             float* d_y, float* d_inputs, float* d_preacts,
+                                             float* d_deltas, void* stream);
 /* grid_sample_backward (grid.py:123-137): scatter-add of trilinear-weighted adjoints
  * d_z_bar (n, channels) f32 at positions (n,3) f64 into d_grad (res^3 * channels) f32. */
 FVSRN_API int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels,

@@ -838,6 +838,22 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
   return FVSRN_OK;
 }
 
+int32_t fvsrn_mlp_forward_backward(const fvsrn_train_desc* d, const float* d_params, const float* d_x,
+                                   const float* d_y_bar, int64_t n, float* d_y, float* d_inputs,
+                                   float* d_preacts, float* d_deltas, void* stream) {
+  if (!d || !d_params || (n > 0 && (!d_x || !d_y || !d_inputs || (d_y_bar && !d_deltas))))
+    return fail(FVSRN_EINVAL, "null argument");
+  if (d->grid_resolution != 0 || d->n_keyframes != 0) return fail(FVSRN_EINVAL, "plain MLP: no grid / keyframes");
+  if (d_y_bar && d->d_out > 4) return fail(FVSRN_EINVAL, "backward: output width must be <= 4");
+  TrainNetDev net;
+  int rc = make_train_net(d, n, net, false);
+  if (rc) return rc;
+  CUDA_TRY(launch_mlp_grads(net, d_params, d_x, d_y_bar, (long long)n, d_y, d_inputs, d_preacts,
+                            d_deltas, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels, const double* d_positions,
                                    const float* d_z_bar, int64_t n, float* d_grad, void* stream) {
   if (resolution < 2 || channels < 1) return fail(FVSRN_EINVAL, "grid must have resolution >= 2 and channels >= 1");

@@ -265,6 +265,38 @@ __global__ void train_world_kernel(TrainNetDev net, const float* __restrict__ pa
   if ((threadIdx.x & 31) == 0 && loss_sum) atomicAdd(loss_sum, my_loss);
 }
 
+// mlp_forward / mlp_backward (nn.py:179-193, 234-256) of given inputs x (n, d_in): the
+// forward with its caches (layer inputs, hidden pre-activations) and outputs; with y_bar,
+// the reverse pass writes the per-layer deltas (weight/bias/input adjoints are the
+// caller's GEMMs over the caches).
+__global__ void mlp_grads_kernel(TrainNetDev net, const float* __restrict__ params,
+                                 const float* __restrict__ x_in, const float* __restrict__ y_bar,
+                                 long long n, float* __restrict__ y_out, float* __restrict__ inputs,
+                                 float* __restrict__ preacts, float* __restrict__ deltas) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float x[kTrainMaxW], y[kTrainMaxW];
+  for (int j = 0; j < net.d_in; ++j) x[j] = x_in[i * net.d_in + j];
+  const CacheRef c{inputs, preacts, deltas, i, n};
+  mlp_f32(net, params, c, x, y);
+  for (int o = 0; o < net.d_out; ++o) y_out[i * net.d_out + o] = y[o];
+  if (y_bar) {
+    float rb[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int o = 0; o < net.d_out && o < 4; ++o) rb[o] = y_bar[i * net.d_out + o];
+    const Cell cell{0, 0, 0, 0.f, 0.f, 0.f, 0, 0, 0.f};
+    f32_backward(net, params, rb, c, cell, nullptr, x, y);
+  }
+}
+
+cudaError_t launch_mlp_grads(const TrainNetDev& net, const float* params, const float* x, const float* y_bar,
+                             long long n, float* y_out, float* inputs, float* preacts, float* deltas,
+                             cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  mlp_grads_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(net, params, x, y_bar, n, y_out, inputs,
+                                                                 preacts, deltas);
+  return cudaGetLastError();
+}
+
 // grid_sample_backward (grid.py:123-137): trilinear-weighted scatter-add of per-sample
 // adjoints z_bar (n, F) into a gradient grid shaped like the latent grid (R, R, R, F).
 // Same cell arithmetic as the lookup (_cell_coords in f64, f32 weights); atomics replace

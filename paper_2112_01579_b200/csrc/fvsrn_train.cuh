@@ -33,6 +33,9 @@ struct AdamConsts {
   float lr, b1, b2, one_m_b1, one_m_b2, eps, bc1, bc2;
 };
 
+cudaError_t launch_mlp_grads(const TrainNetDev& net, const float* params, const float* x, const float* y_bar,
+                             long long n, float* y_out, float* inputs, float* preacts, float* deltas,
+                             cudaStream_t s);
 cudaError_t launch_grid_scatter(int R, int F, const double* pos, const float* z_bar, long long n,
                                 float* grad, cudaStream_t s);
 cudaError_t launch_model_grads(const TrainNetDev& net, const float* params, const double* pos,

@@ -161,6 +161,94 @@ def mlp_eval(params: MlpParams, x: np.ndarray) -> np.ndarray:
 
 
 @dataclass
+class MlpCache:
+    """Per-layer inputs and pre-activations of a forward pass (nn.py:172-176)."""
+
+    inputs: list
+    preacts: list
+
+
+def _mlp_run(params: MlpParams, x: np.ndarray, y_bar=None):
+    """One fvsrn_mlp_forward_backward call: outputs, caches and (with y_bar) the weight /
+    bias / input adjoints as cuBLAS GEMMs over the cached deltas (nn.py:248-255)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib as L
+    from .f32ops import NetDesc
+
+    n, d_in = x.shape
+    Lc = params.layer_count
+    d_out = int(params.weights[-1].shape[0])
+    H = int(params.weights[0].shape[0]) if Lc > 1 else 1
+    nd = NetDesc(params.weights, params.biases, params.activation, "density", d_in)
+    dev = nd.dev
+    w_in = [d_in] + [H] * (Lc - 1)
+    w_out = [H] * (Lc - 1) + [d_out]
+    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32), device=dev)
+    yd = torch.empty((max(n, 1), d_out), dtype=torch.float32, device=dev)
+    inputs = torch.empty(max(1, n * sum(w_in)), dtype=torch.float32, device=dev)
+    preacts = torch.empty(max(1, (Lc - 1) * n * H), dtype=torch.float32, device=dev)
+    deltas = torch.empty(max(1, n * sum(w_out)), dtype=torch.float32, device=dev)
+    yb = (None if y_bar is None else
+          torch.as_tensor(np.ascontiguousarray(y_bar, dtype=np.float32), device=dev))
+    ptr = lambda a: C.c_void_p(a.data_ptr() if a is not None else None)  # noqa: E731
+    L.check(L.lib().fvsrn_mlp_forward_backward(
+        C.byref(nd.desc), ptr(nd.params), ptr(xd), ptr(yb), n, ptr(yd), ptr(inputs), ptr(preacts),
+        ptr(deltas), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    y = yd[:n].cpu().numpy()
+    ins, pre = [], []
+    io = 0
+    for l in range(Lc):
+        ins.append(inputs[io:io + n * w_in[l]].view(n, w_in[l]).cpu().numpy())
+        io += n * w_in[l]
+        pre.append(preacts[l * n * H:(l + 1) * n * H].view(n, H).cpu().numpy() if l < Lc - 1 else y.copy())
+    if y_bar is None:
+        return y, MlpCache(inputs=ins, preacts=pre), None, None
+    gw, gb = [], []
+    io = do = 0
+    x_bar = None
+    for l in range(Lc):
+        xi = inputs[io:io + n * w_in[l]].view(n, w_in[l])
+        dl = deltas[do:do + n * w_out[l]].view(n, w_out[l])
+        gw.append((dl.t() @ xi).cpu().numpy())
+        gb.append(dl.sum(dim=0).cpu().numpy())
+        if l == 0:
+            x_bar = (dl @ torch.as_tensor(np.ascontiguousarray(params.weights[0], dtype=np.float32),
+                                          device=dev)).cpu().numpy()
+        io += n * w_in[l]
+        do += n * w_out[l]
+    return y, MlpCache(inputs=ins, preacts=pre), gw, (gb, x_bar)
+
+
+def mlp_forward(params: MlpParams, x: np.ndarray):
+    """Evaluate the network keeping the per-layer caches (nn.py:179-193), on the GPU in
+    f32; the last layer stays linear.  Returns (y, MlpCache)."""
+    x = np.asarray(x)
+    d_in = int(params.weights[0].shape[1])
+    if x.ndim != 2 or x.shape[1] != d_in:
+        raise ValueError(f"expected input shape (N, {d_in}), got {x.shape}")
+    y, cache, _, _ = _mlp_run(params, x)
+    return y, cache
+
+
+def mlp_backward(params: MlpParams, cache: MlpCache, y_bar: np.ndarray):
+    """Reverse pass for sum(y_bar * y) (nn.py:234-256): returns the input adjoints and a
+    GradientBuffer of weight / bias gradients (grids empty).  The deltas come from one
+    CUDA kernel (forward recomputed from cache.inputs[0]); the reductions are GEMMs."""
+    from .train import GradientBuffer
+
+    if len(cache.inputs) != params.layer_count:
+        raise ValueError("cache does not match the parameter set")
+    y_bar = np.asarray(y_bar)
+    if y_bar.shape != np.shape(cache.preacts[-1]):
+        raise ValueError(f"adjoint shape {y_bar.shape} does not match output {np.shape(cache.preacts[-1])}")
+    _, _, gw, (gb, x_bar) = _mlp_run(params, np.asarray(cache.inputs[0]), y_bar)
+    return x_bar, GradientBuffer(weights=gw, biases=gb, grids=[])
+
+
+@dataclass
 class AdamState:
     """First/second moment accumulators, one per parameter array (nn.py:258-276)."""
 

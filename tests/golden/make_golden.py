@@ -375,6 +375,27 @@ def main():
     grid_sample_backward(g1, gp, gz, gg)
     arrays["gsb_pos"], arrays["gsb_zbar"], arrays["gsb_grad"] = gp, gz, gg
 
+    # --- mlp_forward / mlp_backward (nn.py:179-193, 234-256) of plain MLPs
+    from fvsrn.nn import init_params, mlp_backward, mlp_forward
+
+    for tag, (lc, hid, din, dout, act) in {"snake4": (3, 16, 10, 4, "snake_alt"),
+                                          "relu1": (4, 24, 7, 1, "relu"),
+                                          "snake2": (2, 8, 5, 2, "snake"), "softplus3": (3, 12, 6, 3, "softplus")}.items():
+        prm = init_params(lc, hid, din, dout, seed=3, activation=act)
+        rng = np.random.default_rng(66)
+        for b in prm.biases:
+            b[...] = rng.normal(scale=0.1, size=b.shape).astype(np.float32)
+        xm = rng.normal(size=(64, din)).astype(np.float32)
+        ym, cm = mlp_forward(prm, xm)
+        yb = rng.normal(size=ym.shape).astype(np.float32)
+        xb, gm = mlp_backward(prm, cm, yb)
+        arrays[f"mlp_{tag}_x"], arrays[f"mlp_{tag}_y"], arrays[f"mlp_{tag}_ybar"] = xm, ym, yb
+        arrays[f"mlp_{tag}_xbar"] = xb
+        arrays[f"mlp_{tag}_grads"] = np.concatenate([g.reshape(-1) for g in gm.arrays()])
+        arrays[f"mlp_{tag}_biases"] = np.concatenate([b.reshape(-1) for b in prm.biases])
+        arrays[f"mlp_{tag}_pre0"] = cm.preacts[0]
+        meta.setdefault("mlp", {})[tag] = [lc, hid, din, dout, act]
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

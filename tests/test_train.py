@@ -317,3 +317,31 @@ def test_grid_sample_backward_vs_reference():
         P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"][:, :3], g)
     with pytest.raises(ValueError):
         P.grid_sample_backward(m.grid, a["gsb_pos"], a["gsb_zbar"], g[:2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["snake4", "relu1", "snake2", "softplus3"])
+def test_mlp_forward_backward_vs_reference(tag):
+    # nn.py:179-193, 234-256 on the GPU (f32 FMA order vs numpy matmul: tolerance)
+    a = arrays()
+    lc, hid, din, dout, act = meta()["mlp"][tag]
+    prm = P.init_params(lc, hid, din, dout, seed=3, activation=act)
+    off = 0
+    bias = a[f"mlp_{tag}_biases"]
+    for b in prm.biases:
+        b[...] = bias[off:off + b.size]
+        off += b.size
+    y, cache = P.mlp_forward(prm, a[f"mlp_{tag}_x"])
+    want = a[f"mlp_{tag}_y"]
+    assert np.abs(y - want).max() <= 2e-5 * max(1.0, float(np.abs(want).max()))
+    assert len(cache.inputs) == lc and len(cache.preacts) == lc
+    np.testing.assert_allclose(cache.preacts[0], a[f"mlp_{tag}_pre0"], rtol=0, atol=2e-5)
+    x_bar, g = P.mlp_backward(prm, cache, a[f"mlp_{tag}_ybar"])
+    wx = a[f"mlp_{tag}_xbar"]
+    assert np.abs(x_bar - wx).max() <= 1e-4 * max(1.0, float(np.abs(wx).max()))
+    got = np.concatenate([x.reshape(-1) for x in g.arrays()])
+    wg = a[f"mlp_{tag}_grads"]
+    assert got.shape == wg.shape and g.grids == []
+    assert np.abs(got - wg).max() <= 1e-4 * float(np.abs(wg).max())
+    with pytest.raises(ValueError):
+        P.mlp_backward(prm, cache, a[f"mlp_{tag}_ybar"][:, :1].repeat(dout + 1, axis=1))
