@@ -20,7 +20,7 @@ from .model import (CheckpointError, FvsrnModel, ModelConfig, ModelForwardContex
                     color_head_backward, decode_volume, density_head_backward, eval_color,
                     eval_density, memory_footprint, model_backward, model_forward, model_init)
 from .nn import (AdamState, FourierEncoder, MlpCache, MlpParams, act_eval, act_grad, adam_step,
-                 fourier_make, init_params, mlp_backward, mlp_eval, mlp_forward, nerf_rows)
+                 fourier_encode, fourier_make, init_params, mlp_backward, mlp_eval, mlp_forward, nerf_rows)
 from .render import (ModelSource, RayState, RenderSettings, VolumeSource, camera_rays, composite_invert,
                      composite_step, ray_box_intersect,
                      fibonacci_cameras, raymarch_forward, render_image, render_image_rgba8,

@@ -134,6 +134,12 @@ class FvsrnModel:
         """[*weights, *biases, *grid values] (model.py:155-157): the Adam / gradient order."""
         return [*self.params.weights, *self.params.biases, *(g.values for g in self.grids)]
 
+    def grad_buffer(self):
+        """Zero GradientBuffer shaped like the trainable set (model.py:159-162)."""
+        from .train import GradientBuffer
+
+        return GradientBuffer.zeros_like_params(self.params, grid_shapes=[g.values.shape for g in self.grids])
+
     def invalidate_device(self) -> None:
         """Drop the cached device copy (call after mutating parameters in place)."""
         self.__dict__.pop("_device", None)

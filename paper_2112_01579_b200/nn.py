@@ -59,6 +59,18 @@ def fourier_make(mode: str, m: int, d_in: int, sigma: float = 1.0, seed: int = 0
     raise ValueError(f"unknown fourier mode {mode!r}")
 
 
+def fourier_encode(enc: FourierEncoder, v) -> np.ndarray:
+    """[v | sin(v B^T) | cos(v B^T)] in v's dtype; mode "off" passes through (nn.py:96-105).
+    Host utility on host arrays (the render / training kernels encode on chip)."""
+    v = np.atleast_2d(np.asarray(v))
+    if v.shape[1] != enc.d_in:
+        raise ValueError(f"expected {enc.d_in} input components, got {v.shape[1]}")
+    if enc.m == 0:
+        return v
+    phase = v @ enc.b_matrix.T.astype(v.dtype)
+    return np.concatenate([v, np.sin(phase), np.cos(phase)], axis=1)
+
+
 @dataclass
 class MlpParams:
     """(out, in) weight matrices + biases; hidden layers share one activation."""

@@ -386,10 +386,23 @@ class GradientBuffer:
 
     weights: list
     biases: list
-    grids: list
+    grids: list = field(default_factory=list)
+
+    @classmethod
+    def zeros_like_params(cls, params, grid_shapes=()) -> "GradientBuffer":
+        return cls(weights=[np.zeros_like(w) for w in params.weights],
+                   biases=[np.zeros_like(b) for b in params.biases],
+                   grids=[np.zeros(s, dtype=np.float32) for s in grid_shapes])
 
     def arrays(self) -> list:
         return [*self.weights, *self.biases, *self.grids]
+
+    def add_scaled(self, other: "GradientBuffer", scale: float = 1.0) -> None:
+        for a, b in zip(self.arrays(), other.arrays()):
+            a += scale * b
+
+    def all_finite(self) -> bool:
+        return all(np.all(np.isfinite(a)) for a in self.arrays())
 
 
 class ScreenTrainer(WorldTrainer):

@@ -396,6 +396,16 @@ def main():
         arrays[f"mlp_{tag}_pre0"] = cm.preacts[0]
         meta.setdefault("mlp", {})[tag] = [lc, hid, din, dout, act]
 
+    # --- fourier_encode (nn.py:96-105), f64 and f32 inputs
+    from fvsrn.nn import fourier_encode, fourier_make
+
+    fv = np.random.default_rng(12).uniform(-1, 2, size=(33, 3))
+    arrays["fenc_v"] = fv
+    for mode, mm in (("nerf", 12), ("random", 7)):
+        enc = fourier_make(mode, mm, 3, sigma=2.0, seed=5)
+        arrays[f"fenc_{mode}_f64"] = fourier_encode(enc, fv)
+        arrays[f"fenc_{mode}_f32"] = fourier_encode(enc, fv.astype(np.float32))
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     with open(HERE / "golden.json", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

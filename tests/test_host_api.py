@@ -240,3 +240,32 @@ def test_metrics_and_loss_csv_format():
     rows = meta()["evaluate_views"]["rows"]
     assert P.metrics_csv(rows) == meta()["evaluate_views"]["csv"]
     assert P.loss_csv([0.5, 0.25]) == "epoch,loss\n0,0.50000000\n1,0.25000000\n"
+
+
+def test_fourier_encode_vs_reference():
+    a = arrays()
+    for mode, mm in (("nerf", 12), ("random", 7)):
+        enc = P.fourier_make(mode, mm, 3, sigma=2.0, seed=5)
+        got64 = P.fourier_encode(enc, a["fenc_v"])
+        got32 = P.fourier_encode(enc, a["fenc_v"].astype(np.float32))
+        assert got64.dtype == np.float64 and got32.dtype == np.float32
+        np.testing.assert_array_equal(got64, a[f"fenc_{mode}_f64"])
+        np.testing.assert_array_equal(got32, a[f"fenc_{mode}_f32"])
+    with pytest.raises(ValueError):
+        P.fourier_encode(P.fourier_make("nerf", 12, 3), np.zeros((2, 4)))
+
+
+def test_gradient_buffer_helpers():
+    from paper_2112_01579_b200.train import GradientBuffer
+
+    m = P.model_init(P.ModelConfig(layers=3, hidden=16, grid_resolution=4, grid_channels=4, seed=1))
+    g = m.grad_buffer()
+    assert [x.shape for x in g.arrays()] == [x.shape for x in m.trainable_arrays()]
+    assert g.all_finite()
+    h = GradientBuffer.zeros_like_params(m.params, [x.values.shape for x in m.grids])
+    for x in h.arrays():
+        x += 1.0
+    g.add_scaled(h, 0.5)
+    assert all(np.all(x == 0.5) for x in g.arrays())
+    g.weights[0][0, 0] = np.nan
+    assert not g.all_finite()
