@@ -8,7 +8,10 @@
 
 namespace fvsrn {
 
-constexpr int kThreads = 128;  // 4 independent warps per CTA; weights shared in smem
+#ifndef FVSRN_THREADS
+#define FVSRN_THREADS 128
+#endif
+constexpr int kThreads = FVSRN_THREADS;  // 4 independent warps per CTA; weights shared in smem
 // CTAs per SM the register budget is sized for (A/B-measured on B200):
 // DVR 5 (<= 102 regs, 20 warps/SM), decode/eval 4 (<= 128 regs).
 #ifndef FVSRN_MIN_BLOCKS
