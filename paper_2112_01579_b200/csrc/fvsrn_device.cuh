@@ -609,6 +609,41 @@ struct FastRow {
         for (int j = 0; j < 4; ++j) w[4 * c8 + j] = *reinterpret_cast<uint32_t*>(&acc[j]);
       }
     }
+    fourier_words(px, py, pz, w);
+  }
+
+  // texture-unit latent lookup of a static fp16 grid (fd.tex_on, no u8 codes, no keyframe
+  // blend): the four raw RGBA16F fetches, so a caller can issue them early and consume
+  // them later (words_from_tex)
+  __device__ static void tex_fetch(const FeatDev& fd, float px, float py, float pz, float4 (&v)[4]) {
+    const float s = (float)(fd.grid_res - 1);
+    const float tz = fmaf(fminf(fmaxf(px, 0.f), 1.f), s, 0.5f);
+    const float ty = fmaf(fminf(fmaxf(py, 0.f), 1.f), s, 0.5f);
+    const float tx = fmaf(fminf(fmaxf(pz, 0.f), 1.f), s, 0.5f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = tex3D<float4>(fd.tex_lo[j], tx, ty, tz);
+  }
+
+  // the 16 latent channels of tex_fetch as 8 packed fp16 pairs
+  __device__ static void tex_words(const FeatDev& fd, float px, float py, float pz, uint32_t (&z)[8]) {
+    float4 v[4];
+    tex_fetch(fd, px, py, pz, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      z[2 * j] = pack_half2(v[j].x, v[j].y);
+      z[2 * j + 1] = pack_half2(v[j].z, v[j].w);
+    }
+  }
+
+  __device__ static void words_from_z(const uint32_t (&z)[8], float px, float py, float pz,
+                                      uint32_t (&w)[kWords]) {
+#pragma unroll
+    for (int i = 0; i < kWords; ++i) w[i] = i < 8 ? z[i] : 0u;
+    fourier_words(px, py, pz, w);
+  }
+
+  // NeRF Fourier pairs and the raw position (columns 16 .. kWidth-1)
+  __device__ static void fourier_words(float px, float py, float pz, uint32_t (&w)[kWords]) {
     // NeRF Fourier pairs: base angle f32(2 pi) * (p - rint p), then doubling
     {
       const float pv[3] = {px, py, pz};

@@ -61,6 +61,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_SPLIT
 #define FVSRN_TC_SPLIT 1
 #endif
+#ifndef FVSRN_TC_PREFETCH
+#define FVSRN_TC_PREFETCH 0
+#endif
 #ifndef FVSRN_TC_WAIT_BAR
 #define FVSRN_TC_WAIT_BAR 0
 #endif
@@ -204,6 +207,11 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
   uint32_t phase = 0;
+  // FVSRN_TC_PREFETCH: the next sample's latent-grid texture fetches are issued before the
+  // last layer's MMA wait, so their latency hides under it (static fp16 texture grids)
+  const bool prefetch = FVSRN_TC_PREFETCH && kA0 && fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
+  uint32_t pre[8];
+  int pre_k = -1;
 
   while (true) {
     ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
@@ -215,7 +223,9 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       uint32_t w[FastRow<NM>::kWords];
       if (r.has) {
         const float kf = (float)r.k;
-        FastRow<NM>::words(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2), w);
+        const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
+        if (prefetch && pre_k == r.k) FastRow<NM>::words_from_z(pre, px, py, pz, w);
+        else FastRow<NM>::words(fd, px, py, pz, w);
       } else {
 #pragma unroll
         for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
@@ -248,6 +258,14 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
                      smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
         }
         umma_commit(mb);
+      }
+      if (prefetch && l == NL - 1) {
+        pre_k = -1;
+        if (r.has && r.k + 1 < r.n) {
+          const float kf = (float)(r.k + 1);
+          FastRow<NM>::tex_words(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2), pre);
+          pre_k = r.k + 1;
+        }
       }
       if constexpr (FVSRN_TC_WAIT_BAR) {
         // one thread polls the MMA-completion barrier; the others wait in the hardware
