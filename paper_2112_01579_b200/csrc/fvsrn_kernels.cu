@@ -20,6 +20,8 @@
 // The tcgen05/TMEM march kernel is in fvsrn_tc.cu, ground-truth volume DVR in
 // fvsrn_volume.cu, the training kernels in fvsrn_train.cu.
 
+#include <cstdlib>
+
 #include "fvsrn_kernels.cuh"
 #include "fvsrn_geometry.cuh"
 #include "fvsrn_march.cuh"
@@ -352,7 +354,7 @@ cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardD
 // buckets (cost >> shift, shift from the maximum).  Approximate within a bucket, which
 // is all a longest-first schedule needs; one launch instead of a multi-pass radix sort.
 __global__ void __launch_bounds__(1024) lpt_bucket_sort_kernel(const unsigned* __restrict__ cost, int n,
-                                                               unsigned* __restrict__ order) {
+                                                               unsigned* __restrict__ order, int zigzag /* filler tiles kept at the end; 0 = pure LPT */) {
   __shared__ unsigned hist[1024];
   __shared__ unsigned cmax;
   const int t = threadIdx.x;
@@ -382,11 +384,20 @@ __global__ void __launch_bounds__(1024) lpt_bucket_sort_kernel(const unsigned* _
   __syncthreads();
   hist[t] -= v;
   __syncthreads();
-  for (int i = t; i < n; i += 1024) order[atomicAdd(&hist[bucket(cost[i])], 1u)] = (unsigned)i;
+  // zigzag (percent of tiles kept as pure-LPT fillers at the end): the first part is
+  // reordered heaviest, lightest, 2nd heaviest, 2nd lightest, ... so the pixel stores of
+  // cheap tiles spread over the frame instead of bunching at its end
+  const unsigned nz = zigzag > 0 ? (unsigned)n - min((unsigned)n, (unsigned)zigzag) : 0u;
+  const unsigned h = (nz + 1) / 2;
+  for (int i = t; i < n; i += 1024) {
+    unsigned k = atomicAdd(&hist[bucket(cost[i])], 1u);
+    if (k < nz) k = k < h ? 2u * k : 2u * (nz - 1u - k) + 1u;
+    order[k] = (unsigned)i;
+  }
 }
 
-cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s) {
-  lpt_bucket_sort_kernel<<<1, 1024, 0, s>>>(cost, n_local, order);
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, int fillers, cudaStream_t s) {
+  lpt_bucket_sort_kernel<<<1, 1024, 0, s>>>(cost, n_local, order, fillers);
   return cudaGetLastError();
 }
 
@@ -543,7 +554,7 @@ cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const Shard
   const int blocks = (int)std::min<long long>((n_slots + 255) / 256, 148 * 16);
   tile_cost_kernel<<<blocks, 256, 0, s>>>(cam, md, sh, n_slots, cost, order + n_local);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  return launch_tile_sort(n_local, cost, order, s);
+  return launch_tile_sort(n_local, cost, order, 0, s);
 }
 
 // ---------------------------------------------------------------- decode / eval

@@ -105,7 +105,7 @@ cudaError_t launch_ray_setup(const CamDev& cam, const MarchDev& md, const ShardD
                              const RayRecs& rr, float* out, unsigned* tile_cost, unsigned* iota,
                              int defer_miss, cudaStream_t s);
 // order[0:n] <- local tiles by (bucketed) descending cost[0:n]; one launch
-cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, cudaStream_t s);
+cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, int fillers, cudaStream_t s);
 cudaError_t launch_blend(const __half* lo, const __half* hi, float w, long long n, __half* dst,
                          cudaStream_t s);
 struct TexBlendArgs {
