@@ -438,3 +438,17 @@ def test_naive_vs_fused_eval(name):
     rows = P.bench_compare(m, [1024], runs=2)
     assert {r["evaluator"] for r in rows} == {"naive", "fused"} and all(r["samples_per_sec"] > 0 for r in rows)
     assert P.bench_csv(rows).startswith("batch,evaluator,samples_per_sec")
+
+
+def test_mapped_framebuffer_tile_order_bit_identical():
+    # a mapped page-locked frame uses the filler/zigzag tile order (fvsrn_capi.cu
+    # render_impl), a pageable one pure LPT: the pixels must not depend on the order
+    m = _model("cfg1")
+    src = P.ModelSource(m, P.TF_PRESETS["warm"])
+    cam = P.fibonacci_cameras(8, 1024, 1024)[5]
+    s = P.RenderSettings(stepsize=1 / 128)
+    fb = P.pinned_empty((1024, 1024, 4))
+    a = P.render_image(src, cam, s, out=fb).data.copy()
+    na = src.last_eval_count
+    b = P.render_image(src, cam, s).data
+    assert np.array_equal(a, b) and na == src.last_eval_count
