@@ -452,3 +452,12 @@ def test_mapped_framebuffer_tile_order_bit_identical():
     na = src.last_eval_count
     b = P.render_image(src, cam, s).data
     assert np.array_equal(a, b) and na == src.last_eval_count
+
+
+def test_decode_into_pinned_volume_matches():
+    # a page-locked output volume takes the chunked decode + overlapped copy path
+    m = _model("cfg1")
+    vb = P.pinned_empty((128, 128, 128))
+    a = P.decode_volume(m, 128, out=vb).values.copy()
+    b = P.decode_volume(m, 128).values
+    assert np.array_equal(a, b)
