@@ -1659,8 +1659,13 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
   float* d_out = mapped ? mapped : (float*)buf;
   unsigned long long* d_bad = (unsigned long long*)(buf + (mapped ? 0 : count * sizeof(float)));
   CUDA_TRY(cudaMemsetAsync(d_bad, 0, 8, sg.s));
-  thread_local cudaStream_t copy_s = nullptr;
-  if (pipelined && !copy_s) CUDA_TRY(cudaStreamCreateWithFlags(&copy_s, cudaStreamNonBlocking));
+  thread_local std::map<int, cudaStream_t> copy_streams;   // one copy stream per (thread, device)
+  cudaStream_t copy_s = nullptr;
+  if (pipelined) {
+    cudaStream_t& cs = copy_streams[m->device];
+    if (!cs) CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    copy_s = cs;
+  }
   int rc = pipelined ? decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s, g_decode_chunks, out, copy_s)
                      : decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s);
   if (rc) {
