@@ -225,9 +225,12 @@ FVSRN_API int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* 
 /* ---- peer-memory framebuffer assembly (multi-GPU, one process per GPU).
  * Rank 0 exports its device framebuffer; every other rank opens it and its kernels
  * store their screen tiles straight into rank 0's frame over NVLink (P2P), replacing the
- * gather + reassembly.  64-byte handles (cudaIpcMemHandle_t). */
-FVSRN_API int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64]);
-FVSRN_API int32_t fvsrn_ipc_open(const uint8_t handle[64], int32_t device, void** d_ptr);
+ * gather + reassembly.  64-byte handles (cudaIpcMemHandle_t) plus the byte offset of d_ptr
+ * from its allocation base (IPC maps whole allocations; a pointer inside a caching
+ * allocator's segment is reopened as base + offset).  fvsrn_ipc_close takes the pointer
+ * fvsrn_ipc_open returned. */
+FVSRN_API int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64], uint64_t* offset);
+FVSRN_API int32_t fvsrn_ipc_open(const uint8_t handle[64], uint64_t offset, int32_t device, void** d_ptr);
 FVSRN_API int32_t fvsrn_ipc_close(void* d_ptr);
 
 FVSRN_API int32_t fvsrn_model_create(const fvsrn_model_desc* desc, int32_t device, fvsrn_model_t* out);

@@ -103,8 +103,8 @@ EXPORTS = {
                                     C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
                                     C.c_void_p, C.c_void_p]),
     "fvsrn_kernel_timer": (C.c_int32, [C.c_int32]),
-    "fvsrn_ipc_export": (C.c_int32, [C.c_void_p, C.c_char_p]),
-    "fvsrn_ipc_open": (C.c_int32, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "fvsrn_ipc_export": (C.c_int32, [C.c_void_p, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "fvsrn_ipc_open": (C.c_int32, [C.c_char_p, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p)]),
     "fvsrn_ipc_close": (C.c_int32, [C.c_void_p]),
     "fvsrn_kernel_timer_read": (C.c_int32, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                             C.POINTER(C.c_int64)]),

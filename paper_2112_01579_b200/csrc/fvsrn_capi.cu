@@ -166,6 +166,31 @@ int fail(int code, const std::string& msg) {
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// IPC: opened mapping (base + offset) -> the base cudaIpcOpenMemHandle returned
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_bases;
+
+// [base, base + size) of the device allocation containing p (driver cuMemGetAddressRange,
+// fetched through the runtime so the library does not link libcuda).
+int alloc_range(void* p, void** base, size_t* size) {
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return (GetRange)f;
+  }();
+  if (!fn) return fail(FVSRN_ECUDA, "cuMemGetAddressRange unavailable");
+  unsigned long long b = 0;
+  if (int r = fn(&b, size, (unsigned long long)p)) return fail(FVSRN_ECUDA, "cuMemGetAddressRange failed (" + std::to_string(r) + ")");
+  *base = (void*)b;
+  return FVSRN_OK;
+}
+
+
 struct Pack {                     // fragment-ordered weights + padded biases
   std::vector<uint2> frag;
   std::vector<float> bias;
@@ -943,26 +968,46 @@ int32_t fvsrn_adam_step(float* d_params, const float* d_grads, float* d_m, float
   return FVSRN_OK;
 }
 
-int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64]) {
-  if (!d_ptr || !handle) return fail(FVSRN_EINVAL, "null argument");
+int32_t fvsrn_ipc_export(void* d_ptr, uint8_t handle[64], uint64_t* offset) {
+  if (!d_ptr || !handle || !offset) return fail(FVSRN_EINVAL, "null argument");
+  // cudaIpcGetMemHandle names the whole cudaMalloc allocation and cudaIpcOpenMemHandle
+  // maps its BASE, so a pointer carved from a caching allocator's segment travels as
+  // (handle, offset from the allocation base).
+  void* base = nullptr;
+  size_t size = 0;
+  if (int rc = alloc_range(d_ptr, &base, &size)) return rc;
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, d_ptr));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
   std::memcpy(handle, &h, 64);
+  *offset = (uint64_t)((char*)d_ptr - (char*)base);
   return FVSRN_OK;
 }
 
-int32_t fvsrn_ipc_open(const uint8_t handle[64], int32_t device, void** d_ptr) {
+int32_t fvsrn_ipc_open(const uint8_t handle[64], uint64_t offset, int32_t device, void** d_ptr) {
   if (!handle || !d_ptr) return fail(FVSRN_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(device));
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, 64);
-  CUDA_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_ptr = (char*)base + offset;
+  std::lock_guard<std::mutex> g(g_ipc_mu);
+  g_ipc_bases[*d_ptr] = base;
   return FVSRN_OK;
 }
 
 int32_t fvsrn_ipc_close(void* d_ptr) {
-  if (d_ptr) CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+  if (!d_ptr) return FVSRN_OK;
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_ipc_mu);
+    auto it = g_ipc_bases.find(d_ptr);
+    if (it == g_ipc_bases.end()) return fail(FVSRN_EINVAL, "pointer was not opened by fvsrn_ipc_open");
+    base = it->second;
+    g_ipc_bases.erase(it);
+  }
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
   return FVSRN_OK;
 }
 
@@ -1669,6 +1714,9 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
   int rc = pipelined ? decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s, g_decode_chunks, out, copy_s)
                      : decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s);
   if (rc) {
+    // chunks already queued on copy_s may still read buf and write out: drain them
+    // before the buffer goes back to the pool and before the caller regains `out`
+    if (copy_s) cudaStreamSynchronize(copy_s);
     cudaFreeAsync(buf, sg.s);
     cudaStreamSynchronize(sg.s);
     return rc;

@@ -33,13 +33,55 @@ def camera_basis(cam):
 _CAM_CACHE: dict = {}
 _TF_CACHE: dict = {}
 _CACHE_MAX = 64
+_desc_lock = threading.Lock()
 
 
 def _cache_put(cache: dict, key, value):
-    if len(cache) >= _CACHE_MAX:
-        cache.pop(next(iter(cache)))
-    cache[key] = value
+    """Insert with FIFO eviction; the descriptor caches are shared by every thread that
+    renders (service workers), so eviction and insertion happen under one lock."""
+    with _desc_lock:
+        while len(cache) >= _CACHE_MAX:
+            cache.pop(next(iter(cache)), None)
+        cache[key] = value
     return value
+
+
+def _words(a) -> np.ndarray:
+    a = np.ascontiguousarray(a)
+    return a.reshape(-1).view(np.uint8)
+
+
+def grid_fingerprint(grids, sampled: bool = False) -> tuple:
+    """Cheap content fingerprint of latent grids: the XOR of all 64-bit words plus the
+    byte length (0.1 ms for a 2 MiB f32 grid), or with ``sampled`` a CRC of every
+    4099th value (microseconds; used per frame by ModelSource)."""
+    import zlib
+
+    out = []
+    for g in grids:
+        v = np.ascontiguousarray(g.values if hasattr(g, "values") else g, dtype=np.float32).reshape(-1)
+        if sampled:
+            out.append((v.size, zlib.crc32(v[::4099].tobytes())))
+        else:
+            head = v[: v.size - v.size % 2]
+            out.append((v.size, int(np.bitwise_xor.reduce(head.view(np.uint64))) if head.size else 0,
+                        float(v[-1]) if v.size % 2 else 0.0))
+    return tuple(out)
+
+
+def param_fingerprint(model, sampled_grids: bool = False) -> tuple:
+    """What the device copy of ``model`` was built from: array identities, an exact CRC of
+    every weight and bias (<= 90 KB) and a grid fingerprint.  device_model() compares it
+    on every call so in-place edits (adam_step, trainers, direct writes) are picked up;
+    the reference re-reads the arrays on every call."""
+    import zlib
+
+    p = model.params
+    crc = 0
+    for a in (*p.weights, *p.biases):
+        crc = zlib.crc32(np.ascontiguousarray(a, dtype=np.float32), crc)
+    ids = tuple(id(a) for a in model.trainable_arrays())
+    return ids, crc, grid_fingerprint(model.grids, sampled_grids)
 
 
 def camera_desc(cam) -> L.CameraDesc:
@@ -150,6 +192,10 @@ class DeviceModel:
             d.keyframe_times = L.dptr(kt)
         if grids:
             quant = getattr(model, "quantized", None)
+            # the u8 codes are uploaded only while the grids still hold exactly the values
+            # they were loaded as (training or an edit since then makes them stale)
+            if quant and getattr(model, "quantized_fp", None) != grid_fingerprint(grids):
+                quant = model.quantized = None
             if quant:
                 d.grid_precision = L.GRID_U8
                 codes = [np.ascontiguousarray(q.codes, dtype=np.uint8) for q in quant]
@@ -353,14 +399,18 @@ class DeviceVolume:
 _cache_lock = threading.Lock()
 
 
-def device_model(model, device: int | None = None) -> DeviceModel:
-    """Cached upload of ``model`` (invalidate with ``model.invalidate_device()``)."""
+def device_model(model, device: int | None = None, sampled_grids: bool = False) -> DeviceModel:
+    """Cached upload of ``model``, rebuilt when its parameters changed since the upload
+    (param_fingerprint; ``model.invalidate_device()`` forces a rebuild)."""
     dev = L.current_device() if device is None else int(device)
+    fp = param_fingerprint(model, sampled_grids)
     with _cache_lock:
         cache = model.__dict__.setdefault("_device", {})
-        dm = cache.get(dev)
-        if dm is None:
-            dm = cache[dev] = DeviceModel(model, dev)
+        hit = cache.get(dev)
+        if hit is not None and hit[1 if sampled_grids else 2] == fp:
+            return hit[0]
+        dm = DeviceModel(model, dev)
+        cache[dev] = (dm, param_fingerprint(model, True), param_fingerprint(model, False))
         return dm
 
 

@@ -117,8 +117,10 @@ class FvsrnModel:
     time_encoder: FourierEncoder | None = None
     grid: LatentGrid | None = None
     keyframes: KeyframeGrids | None = None
-    # u8 codes as loaded from a checkpoint (uploaded as-is; see device.py)
+    # u8 codes as loaded from a checkpoint (uploaded as-is while the grids still equal
+    # their dequantised values, i.e. quantized_fp matches; see device.py)
     quantized: list | None = None
+    quantized_fp: tuple | None = None
 
     @property
     def grids(self) -> list:
@@ -313,6 +315,10 @@ def checkpoint_load(path) -> FvsrnModel:
     elif grids:
         model.grid = grids[0]
     model.quantized = quant or None
+    if quant:
+        from .device import grid_fingerprint
+
+        model.quantized_fp = grid_fingerprint(model.grids)
     return model
 
 

@@ -76,8 +76,16 @@ class ModelSource:
         self.tf = tf
         self.t = t
         self.use_fused = use_fused
-        self.device_model = device_model(model, device)
+        self._device = device
+        device_model(model, device)            # upload now (the per-frame path only checks)
         self.last_eval_count = 0
+
+    @property
+    def device_model(self):
+        """The model's device copy, re-validated on every call with the cheap parameter
+        fingerprint (exact weights/biases, sampled grids: microseconds), so a source bound
+        before an optimiser step renders the updated model as the reference would."""
+        return device_model(self.model, self._device, sampled_grids=True)
 
     def sample(self, p, d):
         """The per-sample source protocol (render.py:182-186), evaluated on the GPU."""

@@ -127,14 +127,22 @@ class PeerUnavailable(RuntimeError):
 class PeerFrameRenderer:
     """Screen-tile sharding with the frame assembled in peer memory.
 
-    Rank 0 exports its (H,W,4) device framebuffer (CUDA IPC); every other rank opens it
-    and its fused kernel stores each finished pixel of its round-robin tiles straight
-    into rank 0's frame over NVLink P2P -- the "gather" happens inside the render
-    kernel, tile by tile, overlapped with the ray marching; there is no separate
-    collective and no reassembly kernel.  After each rank's stream completes, a
-    process-group barrier publishes the frame.  Pixels are produced by the same per-ray
-    code as the 1-GPU path, so the frame is bit-identical to a single-GPU render.
+    Rank 0 exports its (H,W,4) device framebuffers (CUDA IPC: handle + offset from the
+    allocation base); every other rank opens them and its fused kernel stores each
+    finished pixel of its round-robin tiles straight into rank 0's frame over NVLink
+    P2P -- the "gather" happens inside the render kernel, tile by tile, overlapped with
+    the ray marching; there is no separate collective and no reassembly kernel.  After
+    each rank's stream completes, a process-group barrier publishes the frame.  Pixels
+    are produced by the same per-ray code as the 1-GPU path, so the frame is
+    bit-identical to a single-GPU render.
+
+    Frames alternate between two exported buffers.  The frame ``render`` returns on rank
+    0 stays valid until the second following ``render`` call: a peer rank can only start
+    writing frame N+2 (the same buffer) after the barrier that ends frame N+1, which rank
+    0 reaches after it has finished with frame N.
     """
+
+    NBUF = 2
 
     def __init__(self, source, group=None):
         import torch
@@ -147,53 +155,69 @@ class PeerFrameRenderer:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.dm = source.device_model
         self._frames = {}
+        self._opened = []
+        self._seq = 0
         self.last_eval_count = 0
 
-    def _frame(self, width, height):
+    def _export(self, frame):
+        """rank 0: (handle bytes, offset); others: open it -> peer pointer.  Every rank
+        reaches the same collectives and agrees on failure (PeerUnavailable everywhere)."""
         import ctypes as C
 
         from . import _lib as L
 
+        t = self.torch
+        ptr = frame.data_ptr() if frame is not None else None
+        obj, err = [None], None
+        if self.rank == 0:
+            try:
+                h = C.create_string_buffer(64)
+                off = C.c_uint64()
+                L.check(L.lib().fvsrn_ipc_export(C.c_void_p(ptr), h, C.byref(off)))
+                obj = [(h.raw, int(off.value))]
+            except Exception as e:          # noqa: BLE001 -- reported below
+                err = e
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        if self.rank != 0 and obj[0] is not None:
+            try:
+                p = C.c_void_p()
+                L.check(L.lib().fvsrn_ipc_open(obj[0][0], obj[0][1], t.cuda.current_device(),
+                                               C.byref(p)))
+                ptr = p.value
+                self._opened.append(ptr)
+            except Exception as e:          # noqa: BLE001
+                err = e
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        ok = t.tensor([0 if (err is not None or obj[0] is None) else 1], device=dev)
+        self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self.group)
+        if not int(ok.item()):
+            self.close()
+            raise PeerUnavailable(f"peer framebuffer unavailable on some rank ({err})")
+        return ptr
+
+    def _frame(self, width, height, slot: int = 0):
         key = (width, height)
         if key not in self._frames:
             t = self.torch
-            frame = t.empty((height, width, 4), dtype=t.float32, device="cuda") if self.rank == 0 else None
-            ptr = frame.data_ptr() if frame is not None else None
-            if self.world > 1:
-                # every rank reaches the same collectives even when a step fails, and all
-                # ranks agree on the outcome (PeerUnavailable everywhere, so a caller can
-                # fall back to TileShardRenderer without a hang)
-                obj, err = [None], None
-                if self.rank == 0:
-                    try:
-                        h = C.create_string_buffer(64)
-                        L.check(L.lib().fvsrn_ipc_export(C.c_void_p(ptr), h))
-                        obj = [h.raw]
-                    except Exception as e:          # noqa: BLE001 -- reported below
-                        err = e
-                self.dist.broadcast_object_list(obj, src=0, group=self.group)
-                if self.rank != 0 and obj[0] is not None:
-                    try:
-                        p = C.c_void_p()
-                        L.check(L.lib().fvsrn_ipc_open(obj[0], t.cuda.current_device(), C.byref(p)))
-                        ptr = p.value
-                    except Exception as e:          # noqa: BLE001
-                        err = e
-                dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
-                ok = t.tensor([0 if (err is not None or obj[0] is None) else 1], device=dev)
-                self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self.group)
-                if not int(ok.item()):
-                    if self.rank != 0 and err is None and obj[0] is not None:
-                        L.lib().fvsrn_ipc_close(C.c_void_p(ptr))
-                    raise PeerUnavailable(f"peer framebuffer unavailable on some rank ({err})")
+            bufs = []
+            for _ in range(self.NBUF):
+                frame = (t.empty((height, width, 4), dtype=t.float32, device="cuda")
+                         if self.rank == 0 else None)
+                ptr = self._export(frame) if self.world > 1 else frame.data_ptr()
+                bufs.append((frame, ptr))
             cnt = t.zeros(1, dtype=t.int64, device="cuda")
-            self._frames[key] = (frame, ptr, cnt)
-        return self._frames[key]
+            self._frames[key] = (bufs, cnt)
+        bufs, cnt = self._frames[key]
+        frame, ptr = bufs[slot % self.NBUF]
+        return frame, ptr, cnt
 
-    def render_async(self, camera, settings, count: bool = False):
-        """Launch this rank's share on the current stream (no synchronisation)."""
+    def render_async(self, camera, settings, count: bool = False, slot: int | None = None):
+        """Launch this rank's share on the current stream (no synchronisation) into buffer
+        ``slot`` (default: the next one in the ping-pong)."""
         t = self.torch
-        frame, ptr, cnt = self._frame(camera.width, camera.height)
+        if slot is None:
+            slot, self._seq = self._seq, self._seq + 1
+        frame, ptr, cnt = self._frame(camera.width, camera.height, slot)
         if count:
             cnt.zero_()
         self.dm.render_device(self.source.tf, camera, settings, self.source.t, ptr,
@@ -215,7 +239,7 @@ class PeerFrameRenderer:
     def close(self):
         from . import _lib as L
 
-        if self.rank != 0:
-            for _, ptr, _ in self._frames.values():
-                L.lib().fvsrn_ipc_close(__import__("ctypes").c_void_p(ptr))
+        for ptr in self._opened:
+            L.lib().fvsrn_ipc_close(__import__("ctypes").c_void_p(ptr))
+        self._opened.clear()
         self._frames.clear()

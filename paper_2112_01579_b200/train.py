@@ -255,6 +255,7 @@ class WorldTrainer:
         flat = self.params.cpu().numpy()
         for a, (lo, hi), shape in zip(self.model.trainable_arrays(), self._views, self.shapes):
             a[...] = flat[lo:hi].reshape(shape)
+        self.model.quantized = None        # the u8 codes no longer describe the grids
         self.model.invalidate_device()
 
 
@@ -293,6 +294,7 @@ def train_world(model, target: WorldTarget, cfg: WorldTrainConfig, progress=None
             total += loss * len(idx)
         trace.append(total / cfg.sample_count)
         if progress is not None:
+            tr.write_back()            # the reference updates the model in place every step
             progress(epoch, trace[-1])
     tr.write_back()
     return model, trace
@@ -358,6 +360,7 @@ def train_temporal(model, volume_provider, cfg: TemporalTrainConfig, progress=No
             total += loss * len(idx)
         trace.append(total / wc.sample_count)
         if progress is not None:
+            tr.write_back()            # the reference updates the model in place every step
             progress(epoch, trace[-1])
     tr.write_back()
     return model, trace
@@ -546,6 +549,7 @@ def train_screen(model, volume, tf, cfg: ScreenTrainConfig, progress=None):
             total += loss
         trace.append(total / len(references))
         if progress is not None:
+            tr.write_back()            # the reference updates the model in place every step
             progress(epoch, trace[-1])
     tr.write_back()
     return model, trace

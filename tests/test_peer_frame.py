@@ -33,11 +33,19 @@ def _worker(rank, world, port, q):
 
     m = P.model_init(P.ModelConfig(layers=4, hidden=32, grid_resolution=16, seed=0))
     src = P.ModelSource(m, P.TF_PRESETS["warm"])
+    # a live allocation first, so rank 0's frames sit at a non-zero offset inside the
+    # caching allocator's segment (IPC maps the segment base; the offset must travel)
+    pad = torch.empty(40000, dtype=torch.float32, device="cuda")
     r = PeerFrameRenderer(src)
-    cam = P.fibonacci_cameras(8, 203, 157)[3]
-    out = r.render(cam, P.RenderSettings(stepsize=1 / 128), count=True)
+    cams = P.fibonacci_cameras(8, 203, 157)
+    got = []
+    for v in (3, 4, 5):     # three frames through the two ping-pong buffers
+        out = r.render(cams[v], P.RenderSettings(stepsize=1 / 128), count=True)
+        if rank == 0:
+            got.append((out.cpu().numpy(), r.last_eval_count))
     if rank == 0:
-        q.put((out.cpu().numpy(), r.last_eval_count))
+        q.put(got)
+    del pad
     dist.barrier()
     r.close()
     dist.barrier()
@@ -53,15 +61,36 @@ def test_peer_frame_two_processes_bit_identical():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    frame, count = q.get(timeout=300)
+    got = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     m = P.model_init(P.ModelConfig(layers=4, hidden=32, grid_resolution=16, seed=0))
     src = P.ModelSource(m, P.TF_PRESETS["warm"])
-    img = P.render_image(src, P.fibonacci_cameras(8, 203, 157)[3], P.RenderSettings(stepsize=1 / 128))
-    assert np.array_equal(frame, img.data)
-    assert count == src.last_eval_count
+    cams = P.fibonacci_cameras(8, 203, 157)
+    for (frame, count), v in zip(got, (3, 4, 5)):
+        img = P.render_image(src, cams[v], P.RenderSettings(stepsize=1 / 128))
+        assert np.array_equal(frame, img.data)
+        assert count == src.last_eval_count
+
+
+def test_ipc_export_reports_offset_from_allocation_base():
+    import ctypes as C
+
+    import torch
+
+    from paper_2112_01579_b200 import _lib as L
+
+    a = torch.empty(4096, dtype=torch.float32, device="cuda")
+    b = torch.empty(4096, dtype=torch.float32, device="cuda")
+    offs = []
+    for t in (a, b):
+        h, off = C.create_string_buffer(64), C.c_uint64()
+        L.check(L.lib().fvsrn_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)))
+        offs.append(off.value)
+    # both live in one caching-allocator segment: offsets differ by their address gap
+    assert offs[1] - offs[0] == b.data_ptr() - a.data_ptr()
+    assert offs[1] > 0
 
 
 def _fallback_worker(rank, world, port, q):
@@ -76,7 +105,7 @@ def _fallback_worker(rank, world, port, q):
     from paper_2112_01579_b200.sharding import PeerFrameRenderer, PeerUnavailable
 
     if rank == 1:   # this rank cannot map rank 0's framebuffer
-        L.lib().fvsrn_ipc_open = lambda *a: 3
+        L.lib().fvsrn_ipc_open = lambda *a: 3   # noqa: E731
     m = P.model_init(P.ModelConfig(layers=4, hidden=32, grid_resolution=16, seed=0))
     src = P.ModelSource(m, P.TF_PRESETS["warm"])
     raised = False
