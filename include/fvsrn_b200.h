@@ -9,10 +9,12 @@
  *                              (weights/B/grid(s) of FvsrnModel                   model.py:136-162)
  *   fvsrn_render            <- render_image(ModelSource(...), camera, settings)   render.py:314-332
  *   fvsrn_render_device     <- same, device framebuffer / screen-tile subset      (multi-GPU)
+ *   fvsrn_render_multi      <- same, split over several GPUs of one process       (SURVEY 8b device_ids[])
  *   fvsrn_render_rays       <- raymarch_forward(source, origins, dirs, settings)  render.py:203-238
  *   fvsrn_eval_density      <- eval_density(model, p, t)                          model.py:368-373
  *   fvsrn_eval_color        <- eval_color(model, p, d, t)                         model.py:376-382
  *   fvsrn_decode_density    <- decode_volume(model, resolution, t)                model.py:385-398
+ *   fvsrn_decode_density_multi <- same, lattice slabs over several GPUs            (SURVEY 8b n_devices)
  *   fvsrn_fused_eval        <- fused_eval(plan, model, x)                         fused.py:281-301
  *   fvsrn_volume_*          <- render_image / raymarch_forward on a VolumeSource  render.py:132-141
  *   fvsrn_render_rgba8      <- png_bytes(render_image(...)) pixels (service)      imaging.py:74-80
@@ -130,6 +132,10 @@ FVSRN_API int32_t fvsrn_set_grid_sampler(int32_t mode);
 FVSRN_API int32_t fvsrn_kernel_timer(int32_t enable);
 FVSRN_API int32_t fvsrn_kernel_timer_read(double* dominant_ms, int64_t* dominant_launches,
                                           int64_t* total_launches);
+/* The last kernel the timer recorded on this thread: template instantiation, MMA path and
+ * latent-grid sampler (e.g. "dvr_kernel<32,4,14,4> (mma.sync m16n8k16); grid: texture
+ * units, RGBA16F, ...").  NUL-terminated, truncated to cap bytes. */
+FVSRN_API int32_t fvsrn_kernel_timer_info(char* buf, int32_t cap);
 
 /* ---- world-space training (train.py:165-206), device pointers only.
  * A static, position-input model (time_mode none, direction_mode pos).  The trainable
@@ -269,6 +275,28 @@ FVSRN_API int32_t fvsrn_decode_density(fvsrn_model_t model, int32_t resolution, 
 FVSRN_API int32_t fvsrn_decode_density_device(fvsrn_model_t model, int32_t resolution, double t,
                                     int64_t lattice_begin, int64_t lattice_count,
                                     float* d_out, void* stream);
+/* ---- one process, several GPUs: SURVEY 8b's minimum export set asks for
+ * fvsrn_render(..., device_ids[], n_devices) and fvsrn_decode_density(..., n_devices).
+ * replicas[i] is the model uploaded with fvsrn_model_create(desc, device_ids[i], ...)
+ * (same parameters on every device; a replica handle carries its device id).
+ *
+ * fvsrn_render_multi  <- render_image(source, camera, settings)       render.py:314-332
+ *   Screen tiles (8x8) go round-robin to the replicas, tile k -> replica k mod n
+ *   (SURVEY 8e).  Each replica's march kernel stores its finished pixels straight into
+ *   the frame: into out itself, over each GPU's own link, when out is mapped page-locked
+ *   memory (fvsrn_host_alloc); otherwise into one framebuffer on replicas[0]'s device
+ *   over NVLink P2P, followed by a single device->host copy (page-locked staging if a
+ *   pair has no P2P path).  Bit-identical to fvsrn_render on one device; eval_count is
+ *   the sum over replicas.  n_devices == 1 is fvsrn_render.
+ * fvsrn_decode_density_multi  <- decode_volume(model, resolution, t)  model.py:385-398
+ *   Contiguous lattice slabs per replica, each decoded in its device's HBM and copied to
+ *   out + slab begin over its own link. */
+FVSRN_API int32_t fvsrn_render_multi(const fvsrn_model_t* replicas, int32_t n_devices,
+                                     const fvsrn_tf* tf, const fvsrn_camera* cam,
+                                     const fvsrn_settings* settings, double t, float* out_rgba,
+                                     uint64_t* eval_count);
+FVSRN_API int32_t fvsrn_decode_density_multi(const fvsrn_model_t* replicas, int32_t n_devices,
+                                             int32_t resolution, double t, float* out);
 /* Page-locked host buffers (e.g. reusable framebuffers: the D2H of fvsrn_render
  * into pinned memory runs at full PCIe/C2C bandwidth). */
 FVSRN_API int32_t fvsrn_host_alloc(uint64_t bytes, void** ptr);

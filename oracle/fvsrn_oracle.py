@@ -416,6 +416,38 @@ def decode_volume(model: OModel, res, t=None, chunk=1 << 16):
     return out.reshape((res,) * 3)
 
 
+def checkpoint_load(path) -> OModel:
+    """model.py:475-528: 'FVSR' magic, <u32 version, <u32 header length>, JSON header
+    (config, sections {name, dtype, shape, offset, bytes}, grid_precision), payload.
+    Weights/biases are cast to f32; u8 grids dequantised as grid.py:170-172
+    (v = min + code/255 * (max - min), f32)."""
+    import json
+    import struct
+
+    with open(path, "rb") as f:
+        raw = f.read()
+    _version, hlen = struct.unpack_from("<II", raw, 4)
+    header = json.loads(raw[12:12 + hlen].decode("utf-8"))
+    payload = raw[12 + hlen:]
+    sec = {}
+    for s in header["sections"]:
+        a = np.frombuffer(payload[s["offset"]:s["offset"] + s["bytes"]], dtype=s["dtype"])
+        sec[s["name"]] = a.reshape(s["shape"])
+    model = model_init(OConfig(**header["config"]))
+    for i in range(len(model.weights)):
+        model.weights[i] = sec[f"w{i}"].astype(np.float32)
+        model.biases[i] = sec[f"b{i}"].astype(np.float32)
+    for gi in range(len(model.grids)):
+        if header["grid_precision"] == "u8":
+            mins = sec[f"grid{gi}_mins"].astype(np.float32)
+            maxs = sec[f"grid{gi}_maxs"].astype(np.float32)
+            codes = sec[f"grid{gi}_codes"].astype(np.float32)
+            model.grids[gi] = (mins + codes / 255.0 * (maxs - mins)).astype(np.float32)
+        else:
+            model.grids[gi] = sec[f"grid{gi}"].astype(np.float32)
+    return model
+
+
 # --------------------------------------------------------------------------
 # transfer function (transfer.py:57-65, 89-113)
 # --------------------------------------------------------------------------

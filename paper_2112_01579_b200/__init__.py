@@ -9,7 +9,7 @@ sm_100a CUDA kernels behind the C ABI of ``include/fvsrn_b200.h``.
 
 __version__ = "0.1.0"
 
-from ._lib import CapacityError, pinned_empty
+from ._lib import CapacityError, pinned_empty, pooled_empty
 from .fused import (FusedPlan, bench_compare, bench_csv, fused_eval, naive_eval_model, plan_build,
                     plan_for_model, warmup)
 from .grid import (KeyframeGrids, LatentGrid, QuantizedLatentGrid, grid_dequantize, grid_init,
@@ -30,3 +30,4 @@ from .volume import ScalarVolume, sample_volume
 from .train import (ErrorGrid, ScreenTrainConfig, TemporalTrainConfig, TrainingDiverged, WorldTarget,
                     WorldTrainConfig, build_error_grid, evaluate_views, loss_csv, metrics_csv,
                     raymarch_backward, sample_world_dataset, train_screen, train_temporal, train_world)
+from .device import set_devices, set_dvr_kernel, set_grid_sampler  # noqa: E402

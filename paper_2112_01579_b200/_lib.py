@@ -108,6 +108,7 @@ EXPORTS = {
     "fvsrn_ipc_close": (C.c_int32, [C.c_void_p]),
     "fvsrn_kernel_timer_read": (C.c_int32, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                             C.POINTER(C.c_int64)]),
+    "fvsrn_kernel_timer_info": (C.c_int32, [C.c_char_p, C.c_int32]),
     "fvsrn_version": (C.c_char_p, []),
     "fvsrn_device_count": (C.c_int32, []),
     "fvsrn_model_create": (C.c_int32, [C.POINTER(ModelDesc), C.c_int32, C.POINTER(C.c_void_p)]),
@@ -144,6 +145,11 @@ EXPORTS = {
                                                C.c_void_p, C.c_void_p]),
     "fvsrn_volume_render_rays": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), _d, _d, C.c_int64,
                                              C.POINTER(SettingsDesc), _f, C.POINTER(C.c_uint64)]),
+    "fvsrn_render_multi": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(TFDesc),
+                                       C.POINTER(CameraDesc), C.POINTER(SettingsDesc), C.c_double,
+                                       _f, C.POINTER(C.c_uint64)]),
+    "fvsrn_decode_density_multi": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32,
+                                               C.c_double, _f]),
     "fvsrn_host_alloc": (C.c_int32, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "fvsrn_host_free": (C.c_int32, [C.c_void_p]),
 }
@@ -230,6 +236,82 @@ def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
     buf = (C.c_char * nbytes).from_address(p.value)
     buf._owner = _PinnedOwner(p.value)     # lives exactly as long as the buffer object
     return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype)[:int(np.prod(shape))].reshape(shape)
+
+
+class _PooledOwner:
+    """Returns a pooled page-locked block to ``_POOL`` when the last numpy view of it dies."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = ptr, nbytes
+
+    def __del__(self):
+        try:
+            _POOL.give(self.ptr, self.nbytes)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+class _PinnedPool:
+    """Page-locked (portable, mapped) host blocks recycled by size for the arrays the stock
+    API returns (``render_image(src, cam, settings)`` without ``out=``): the render kernels
+    store each finished pixel straight into the returned frame over PCIe instead of a
+    pageable device->host copy after the march.  A block goes back to the pool when the
+    caller drops the last view of it.  At most ``CAP`` bytes are handed out at once
+    (beyond that arrays are ordinary pageable memory) and ``IDLE`` bytes kept idle."""
+
+    CAP = 4 << 30
+    IDLE = 1 << 30
+
+    def __init__(self):
+        import threading
+
+        self.lock = threading.Lock()
+        self.free: dict[int, list[int]] = {}
+        self.out_bytes = 0
+        self.idle_bytes = 0
+
+    def take(self, nbytes: int):
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                self.idle_bytes -= nbytes
+                self.out_bytes += nbytes
+                return lst.pop()
+            if self.out_bytes + nbytes > self.CAP:
+                return None
+            self.out_bytes += nbytes
+        p = C.c_void_p()
+        if lib().fvsrn_host_alloc(nbytes, C.byref(p)) != FVSRN_OK:
+            with self.lock:
+                self.out_bytes -= nbytes
+            return None
+        return p.value
+
+    def give(self, ptr: int, nbytes: int):
+        with self.lock:
+            self.out_bytes -= nbytes
+            if self.idle_bytes + nbytes <= self.IDLE:
+                self.free.setdefault(nbytes, []).append(ptr)
+                self.idle_bytes += nbytes
+                return
+        lib().fvsrn_host_free(C.c_void_p(ptr))
+
+
+_POOL = _PinnedPool()
+
+
+def pooled_empty(shape, dtype=np.float32) -> np.ndarray:
+    """Like ``pinned_empty`` but from the recycling pool (pageable ``np.empty`` when the
+    pool's cap is reached)."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape))
+    nbytes = max(1, count * dtype.itemsize)
+    ptr = _POOL.take(nbytes)
+    if ptr is None:
+        return np.empty(shape, dtype=dtype)
+    buf = (C.c_char * nbytes).from_address(ptr)
+    buf._owner = _PooledOwner(ptr, nbytes)
+    return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype)[:count].reshape(shape)
 
 
 def current_device() -> int:

@@ -1,4 +1,8 @@
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <future>
 #include <thread>
 #include <type_traits>
 #include <array>
@@ -117,6 +121,7 @@ bool use_tc(const fvsrn_model* m);
 // dominant kernel (the march / decode kernel) and a count of all library launches.
 struct KernelTimer {
   bool on = false;
+  std::string name;              // the last timed launch: kernel instantiation + grid sampler
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   size_t used = 0;
   long long launches = 0;
@@ -608,6 +613,34 @@ std::mutex g_occ_mu;
 std::map<std::tuple<const void*, int, size_t>, int> g_occ;
 std::map<std::pair<const void*, int>, size_t> g_smem_attr;
 
+// What `launch` runs, for the measurement record (fvsrn_kernel_timer_info): the template
+// instantiation, the MMA path and the latent-grid sampler.
+std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
+  const int h = m->hid_pad;
+  const bool fast = fast_path(m, kind);
+  const std::string tmpl = fast ? std::to_string(h) + ",4," + std::to_string((h - 4) / 2) + "," +
+                                      std::to_string(m->layers)
+                                : std::to_string(h) + ",-1,0,0";
+  std::string k;
+  switch (kind) {
+    case KernelKind::kDVRTC:
+      k = std::string(g_tc_two_tiles ? "dvr_tc2_kernel<" : "dvr_tc_kernel<") + std::to_string(h) + "," +
+          std::to_string((h - 4) / 2) + "," + std::to_string(m->layers) +
+          "> (tcgen05.mma kind::f16, TMEM accumulators)";
+      break;
+    case KernelKind::kDVRWS: k = "dvr_ws_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+    case KernelKind::kDVRPipe: k = "dvr_pipe_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+    case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+    case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+    default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+  }
+  const char* grid = m->R <= 0 ? "no latent grid"
+                     : use_tex(m) ? (m->tex_u8 ? "texture units, RGBA8 u8 codes, hardware trilinear (8-bit weights)"
+                                               : "texture units, RGBA16F, hardware trilinear (8-bit weights)")
+                                  : "LDG.128 fp16 + HFMA2 trilinear";
+  return k + "; grid: " + grid;
+}
+
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
   const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
@@ -664,6 +697,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   if (need < blocks) blocks = std::max(1ll, need);
   std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
   if (g_kt.on && kind != KernelKind::kFused) {
+    g_kt.name = kernel_desc(m, kind);
     if (g_kt.used == g_kt.ev.size()) {
       std::pair<cudaEvent_t, cudaEvent_t> p;
       CUDA_TRY(cudaEventCreate(&p.first));
@@ -1031,6 +1065,12 @@ int32_t fvsrn_kernel_timer_read(double* dominant_ms, int64_t* dominant_launches,
   if (total_launches) *total_launches = g_kt.launches;
   g_kt.used = 0;
   g_kt.launches = 0;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_kernel_timer_info(char* buf, int32_t cap) {
+  if (!buf || cap < 1) return fail(FVSRN_EINVAL, "null buffer");
+  std::snprintf(buf, (size_t)cap, "%s", g_kt.name.c_str());
   return FVSRN_OK;
 }
 
@@ -1688,12 +1728,14 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
 
 extern "C" {
 
-int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out) {
-  if (!m || !out) return fail(FVSRN_EINVAL, "null argument");
-  if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
+}  // extern "C"
+
+// Lattice slab [begin, begin + count) of the res^3 decode into host memory `out` (the
+// slab's first element), on the calling thread's per-thread stream of m's device.
+static int decode_host_slab(fvsrn_model_t m, int32_t res, double t, long long begin, long long count,
+                            float* out) {
   CUDA_TRY(cudaSetDevice(m->device));
   StreamGuard sg;
-  const long long count = (long long)res * res * res;
   // page-locked output: either chunked decode into HBM with the copies overlapped on a
   // second stream (default), or the decode kernel storing straight into the mapped buffer
   float* mapped = mapped_device_ptr(out);
@@ -1711,8 +1753,8 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
     if (!cs) CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     copy_s = cs;
   }
-  int rc = pipelined ? decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s, g_decode_chunks, out, copy_s)
-                     : decode_impl(m, res, t, 0, count, d_out, d_bad, sg.s);
+  int rc = pipelined ? decode_impl(m, res, t, begin, count, d_out, d_bad, sg.s, g_decode_chunks, out, copy_s)
+                     : decode_impl(m, res, t, begin, count, d_out, d_bad, sg.s);
   if (rc) {
     // chunks already queued on copy_s may still read buf and write out: drain them
     // before the buffer goes back to the pool and before the caller regains `out`
@@ -1721,12 +1763,275 @@ int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out)
     cudaStreamSynchronize(sg.s);
     return rc;
   }
-  unsigned long long bad = 0;
+  unsigned long long* bad = pinned_counters();
+  unsigned long long stack_bad = 0;
+  if (!bad) bad = &stack_bad;
   if (!mapped && !pipelined) CUDA_TRY(cudaMemcpyAsync(out, d_out, count * sizeof(float), cudaMemcpyDeviceToHost, sg.s));
-  CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaMemcpyAsync(bad, d_bad, 8, cudaMemcpyDeviceToHost, sg.s));
   CUDA_TRY(cudaFreeAsync(buf, sg.s));
   CUDA_TRY(cudaStreamSynchronize(sg.s));
-  if (bad) return fail(FVSRN_EINVAL, "volume contains non-finite values");
+  if (*bad) return fail(FVSRN_EINVAL, "volume contains non-finite values");
+  return FVSRN_OK;
+}
+
+// ---------------------------------------------------------------- several GPUs, one process
+namespace {
+
+// One persistent host thread per device for the multi-device entries: every device's
+// enqueue (ray setup, tile sort, march, copies) and its stream synchronisation run
+// concurrently, each on the worker's own per-thread default stream.  Workers live for
+// the process (never joined at exit, when the CUDA runtime may already be gone).
+class DeviceWorker {
+ public:
+  explicit DeviceWorker(int dev) : dev_(dev), th_([this] { loop(); }) { th_.detach(); }
+  using Result = std::pair<int, std::string>;
+  std::future<Result> submit(std::function<int()> fn) {
+    auto task = std::make_shared<std::packaged_task<Result()>>([fn, this] {
+      const cudaError_t e = cudaSetDevice(dev_);
+      const int rc = e != cudaSuccess ? fail(FVSRN_ECUDA, cudaGetErrorString(e)) : fn();
+      return Result(rc, rc ? g_err : std::string());
+    });
+    auto fut = task->get_future();
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      q_.emplace_back([task] { (*task)(); });
+    }
+    cv_.notify_one();
+    return fut;
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> f;
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return !q_.empty(); });
+        f = std::move(q_.front());
+        q_.pop_front();
+      }
+      f();
+    }
+  }
+  int dev_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+  std::thread th_;
+};
+
+std::mutex g_workers_mu;
+DeviceWorker* worker_for(int dev) {
+  static auto* workers = new std::map<int, DeviceWorker*>();
+  auto it = workers->find(dev);
+  if (it == workers->end()) it = workers->emplace(dev, new DeviceWorker(dev)).first;
+  return it->second;
+}
+
+// Runs fns[i] on the worker of replica i's device; all submitted under one lock so every
+// worker queue sees concurrent calls in the same order.  Returns the first failure.
+int run_on_devices(const fvsrn_model_t* reps, int n, const std::vector<std::function<int()>>& fns) {
+  std::vector<std::future<DeviceWorker::Result>> futs;
+  {
+    std::lock_guard<std::mutex> l(g_workers_mu);
+    for (int i = 0; i < n; ++i) futs.push_back(worker_for(reps[i]->device)->submit(fns[i]));
+  }
+  int rc = FVSRN_OK;
+  std::string msg;
+  for (auto& f : futs) {
+    auto r = f.get();
+    if (r.first && !rc) { rc = r.first; msg = r.second; }
+  }
+  return rc ? fail(rc, msg) : FVSRN_OK;
+}
+
+int check_replicas(const fvsrn_model_t* reps, int n) {
+  if (!reps || n < 1) return fail(FVSRN_EINVAL, "need at least one model replica");
+  for (int i = 0; i < n; ++i) {
+    if (!reps[i]) return fail(FVSRN_EINVAL, "null model replica");
+    const fvsrn_model& a = *reps[i];
+    const fvsrn_model& b = *reps[0];
+    if (a.head != b.head || a.temporal != b.temporal || a.layers != b.layers || a.hidden != b.hidden ||
+        a.d_in != b.d_in || a.d_out != b.d_out || a.act != b.act || a.R != b.R || a.F != b.F ||
+        a.k0 != b.k0)
+      return fail(FVSRN_EINVAL, "model replicas differ in shape");
+  }
+  return FVSRN_OK;
+}
+
+// peer access from `dev` to `home` (once per pair); false when the pair has no P2P path
+bool enable_peer(int dev, int home) {
+  if (dev == home) return true;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> state;
+  std::lock_guard<std::mutex> l(mu);
+  auto key = std::make_pair(dev, home);
+  auto it = state.find(key);
+  if (it != state.end()) return it->second;
+  int can = 0;
+  bool ok = cudaDeviceCanAccessPeer(&can, dev, home) == cudaSuccess && can;
+  if (ok) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(home, 0);
+    ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+    cudaSetDevice(prev);
+  }
+  cudaGetLastError();
+  state[key] = ok;
+  return ok;
+}
+
+// Framebuffers on a home device that peers store into (cudaMalloc memory: P2P-mappable,
+// unlike the stream-ordered pool's), recycled across calls.
+struct FrameCache {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> free;
+  void* take(int dev, size_t bytes) {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      auto& v = free[{dev, bytes}];
+      if (!v.empty()) { void* p = v.back(); v.pop_back(); return p; }
+    }
+    void* p = nullptr;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
+    cudaSetDevice(prev);
+    return p;
+  }
+  void give(int dev, size_t bytes, void* p) {
+    std::lock_guard<std::mutex> l(mu);
+    free[{dev, bytes}].push_back(p);
+  }
+};
+FrameCache& frame_cache() {
+  static auto* c = new FrameCache();
+  return *c;
+}
+
+// one replica's round-robin tiles into `d_frame` (full-frame layout), synchronised;
+// adds its evaluated-sample count to *evals
+int render_share(fvsrn_model_t m, const fvsrn_tf* tf, const fvsrn_camera* c, const fvsrn_settings* st,
+                 double t, int rank, int world, float* d_frame, bool frame_mapped,
+                 std::atomic<unsigned long long>* evals) {
+  StreamGuard sg;
+  unsigned long long* d_cnt = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d_cnt, 16, sg.s));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 16, sg.s));
+  fvsrn_shard sh{rank, world, 0};
+  g_out_mapped = frame_mapped;
+  int rc = render_impl(m, tf, c, st, t, &sh, d_frame, d_cnt, d_cnt + 1, sg.s);
+  g_out_mapped = false;
+  if (rc) { cudaFreeAsync(d_cnt, sg.s); cudaStreamSynchronize(sg.s); return rc; }
+  unsigned long long stack_cnt[2] = {0, 0};
+  unsigned long long* cnt = pinned_counters();
+  if (!cnt) cnt = stack_cnt;
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sg.s));
+  CUDA_TRY(cudaFreeAsync(d_cnt, sg.s));
+  CUDA_TRY(cudaStreamSynchronize(sg.s));
+  evals->fetch_add(cnt[0]);
+  if (cnt[1]) return fail(FVSRN_EINVAL, "image contains non-finite values");
+  return FVSRN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fvsrn_decode_density(fvsrn_model_t m, int32_t res, double t, float* out) {
+  if (!m || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
+  return decode_host_slab(m, res, t, 0, (long long)res * res * res, out);
+}
+
+int32_t fvsrn_decode_density_multi(const fvsrn_model_t* reps, int32_t n, int32_t res, double t,
+                                   float* out) {
+  int rc = check_replicas(reps, n);
+  if (rc) return rc;
+  if (!out) return fail(FVSRN_EINVAL, "null argument");
+  if (res < 2) return fail(FVSRN_EINVAL, "resolution must be >= 2");
+  if (n == 1) return fvsrn_decode_density(reps[0], res, t, out);
+  // contiguous lattice slabs (multiples of 32 entries: whole warps) per replica
+  const long long total = (long long)res * res * res;
+  const long long per = ((total + n - 1) / n + 31) / 32 * 32;
+  std::vector<std::function<int()>> fns;
+  for (int i = 0; i < n; ++i) {
+    const long long b = std::min(total, i * per), cnt = std::min(per, total - b);
+    fvsrn_model_t m = reps[i];
+    fns.push_back([=] { return cnt > 0 ? decode_host_slab(m, res, t, b, cnt, out + b) : (int)FVSRN_OK; });
+  }
+  return run_on_devices(reps, n, fns);
+}
+
+int32_t fvsrn_render_multi(const fvsrn_model_t* reps, int32_t n, const fvsrn_tf* tf,
+                           const fvsrn_camera* c, const fvsrn_settings* st, double t, float* out,
+                           uint64_t* eval_count) {
+  int rc = check_replicas(reps, n);
+  if (rc) return rc;
+  if (!c || !out) return fail(FVSRN_EINVAL, "null argument");
+  if (c->width < 1 || c->height < 1) return fail(FVSRN_EINVAL, "image dimensions must be positive");
+  if (n == 1) return fvsrn_render(reps[0], tf, c, st, t, out, eval_count);
+  const size_t bytes = (size_t)c->width * c->height * 16;
+  std::atomic<unsigned long long> evals{0};
+  // (1) page-locked out (fvsrn_host_alloc: portable + mapped): every GPU stores its own
+  // tiles' pixels straight into the host frame over its own link, overlapped with its march
+  if (mapped_device_ptr(out)) {
+    std::vector<std::function<int()>> fns;
+    for (int i = 0; i < n; ++i) {
+      fvsrn_model_t m = reps[i];
+      fns.push_back([=, &evals] {
+        float* d = mapped_device_ptr(out);
+        if (!d) return fail(FVSRN_ECUDA, "framebuffer is not mapped on this device");
+        return render_share(m, tf, c, st, t, i, n, d, true, &evals);
+      });
+    }
+    if ((rc = run_on_devices(reps, n, fns))) return rc;
+    if (eval_count) *eval_count = evals.load();
+    return FVSRN_OK;
+  }
+  // (2) pageable out: the replicas store into one framebuffer on replicas[0]'s device over
+  // NVLink P2P, then one device->host copy.  Without a P2P path: a page-locked staging frame.
+  const int home = reps[0]->device;
+  bool p2p = true;
+  for (int i = 1; i < n; ++i) p2p = p2p && enable_peer(reps[i]->device, home);
+  float* frame = nullptr;
+  void* staging = nullptr;
+  if (p2p) {
+    frame = (float*)frame_cache().take(home, bytes);
+    if (!frame) return fail(FVSRN_ECUDA, "cannot allocate the shared framebuffer");
+  } else {
+    CUDA_TRY(cudaHostAlloc(&staging, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  }
+  std::vector<std::function<int()>> fns;
+  for (int i = 0; i < n; ++i) {
+    fvsrn_model_t m = reps[i];
+    fns.push_back([=, &evals] {
+      float* d = p2p ? frame : mapped_device_ptr(staging);
+      return render_share(m, tf, c, st, t, i, n, d, !p2p, &evals);
+    });
+  }
+  rc = run_on_devices(reps, n, fns);
+  if (!rc) {
+    if (p2p) {
+      cudaSetDevice(home);
+      StreamGuard sg;
+      const cudaError_t e1 = cudaMemcpyAsync(out, frame, bytes, cudaMemcpyDeviceToHost, sg.s);
+      const cudaError_t e2 = cudaStreamSynchronize(sg.s);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        cudaGetLastError();
+        rc = fail(FVSRN_ECUDA, std::string("frame copy: ") + cudaGetErrorString(e1 ? e1 : e2));
+      }
+    } else {
+      std::memcpy(out, staging, bytes);
+    }
+  }
+  if (frame) frame_cache().give(home, bytes, frame);
+  if (staging) cudaFreeHost(staging);
+  if (rc) return rc;
+  if (eval_count) *eval_count = evals.load();
   return FVSRN_OK;
 }
 

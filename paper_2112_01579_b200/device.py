@@ -261,7 +261,7 @@ class DeviceModel:
     def decode(self, res: int, t=None, out=None) -> np.ndarray:
         n = int(res) ** 3
         if out is None:
-            out = np.empty(n, dtype=np.float32)
+            out = L.pooled_empty(n)
         elif out.size != n or out.dtype != np.float32 or not out.flags.c_contiguous:
             raise ValueError(f"out must be a C-contiguous float32 array of {n} elements")
         L.check(self._lib.fvsrn_decode_density(self._h, int(res), L.t_arg(t), L.fptr(out)))
@@ -283,7 +283,7 @@ class DeviceModel:
         (e.g. ``pinned_empty`` for full-bandwidth reads)."""
         shape = (cam.height, cam.width, 4)
         if out is None:
-            out = np.empty(shape, dtype=np.float32)
+            out = L.pooled_empty(shape)
         elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
             raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
         cnt = C.c_uint64(0)
@@ -396,6 +396,80 @@ class DeviceVolume:
             C.byref(sh), C.c_void_p(out_ptr), C.c_void_p(stream_ptr)))
 
 
+def _handles(dms):
+    return (C.c_void_p * len(dms))(*[dm.handle.value for dm in dms])
+
+
+def render_multi(dms, tf, cam, settings, t=None, out=None):
+    """One frame across the devices of ``dms`` (one DeviceModel per GPU, same model):
+    fvsrn_render_multi, round-robin 8x8 screen tiles; returns (frame, summed count)."""
+    shape = (cam.height, cam.width, 4)
+    if out is None:
+        out = L.pooled_empty(shape)
+    elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+    cnt = C.c_uint64(0)
+    tfd = tf_desc(tf)
+    L.check(L.lib().fvsrn_render_multi(_handles(dms), len(dms), C.byref(tfd.desc) if tfd else None,
+                                       C.byref(camera_desc(cam)), C.byref(settings_desc(settings)),
+                                       L.t_arg(t), L.fptr(out), C.byref(cnt)))
+    return out, int(cnt.value)
+
+
+def decode_multi(dms, res: int, t=None, out=None) -> np.ndarray:
+    """decode_volume across the devices of ``dms`` (contiguous lattice slabs per GPU)."""
+    n = int(res) ** 3
+    if out is None:
+        out = L.pooled_empty(n)
+    elif out.size != n or out.dtype != np.float32 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float32 array of {n} elements")
+    L.check(L.lib().fvsrn_decode_density_multi(_handles(dms), len(dms), int(res), L.t_arg(t),
+                                               L.fptr(out)))
+    return out
+
+
+_DEFAULT_DEVICES: list | None = None
+
+
+def _parse_devices(spec):
+    if spec is None:
+        return None
+    if isinstance(spec, str):
+        spec = spec.strip()
+        if not spec:
+            return None
+        if spec == "all":
+            return list(range(max(1, int(L.lib().fvsrn_device_count()))))
+        return [int(x) for x in spec.split(",") if x.strip()]
+    if isinstance(spec, int):
+        return [spec]
+    return [int(x) for x in spec]
+
+
+def set_devices(devices) -> list | None:
+    """Default GPU set for render_image / decode_volume calls that pass no ``devices=``:
+    a list of device ids, "all", or None (one GPU, the current device).  The environment
+    variable FVSRN_DEVICES ("all" or "0,1,2,...") sets the initial default, so reference
+    callers (service, CLI, evaluate_views) render on several GPUs unchanged.  Returns the
+    previous setting."""
+    global _DEFAULT_DEVICES
+    prev = _DEFAULT_DEVICES
+    _DEFAULT_DEVICES = _parse_devices(devices)
+    return prev
+
+
+def resolve_devices(devices=None) -> list | None:
+    """The device list a call should use (None = the single-device path)."""
+    import os
+
+    devs = _parse_devices(devices) if devices is not None else _DEFAULT_DEVICES
+    if devs is None and devices is None:
+        devs = _parse_devices(os.environ.get("FVSRN_DEVICES"))
+    if devs is not None and not devs:
+        raise ValueError("devices must name at least one GPU")
+    return devs
+
+
 _cache_lock = threading.Lock()
 
 
@@ -462,3 +536,10 @@ def kernel_timer_read() -> tuple[float, int, int]:
     ms, n, tot = C.c_double(), C.c_int64(), C.c_int64()
     L.check(L.lib().fvsrn_kernel_timer_read(C.byref(ms), C.byref(n), C.byref(tot)))
     return ms.value, n.value, tot.value
+
+
+def kernel_timer_info() -> str:
+    """The kernel (instantiation, MMA path, grid sampler) the timer last recorded."""
+    buf = C.create_string_buffer(512)
+    L.check(L.lib().fvsrn_kernel_timer_info(buf, 512))
+    return buf.value.decode()

@@ -188,18 +188,28 @@ def eval_color(model: FvsrnModel, p, d=None, t=None) -> np.ndarray:
 
 
 def decode_volume(model: FvsrnModel, resolution: int, t: float | None = None, chunk: int = 1 << 16,
-                  out: np.ndarray | None = None):
+                  out: np.ndarray | None = None, devices=None):
     """Dense density on the linspace(0,1,res)^3 vertex lattice (model.py:385-398).
 
     ``chunk`` is accepted for signature compatibility; the GPU decodes the
     whole lattice in one launch.  ``out`` (optional): float32 host buffer of
-    res^3 values (e.g. ``pinned_empty``) to decode into.
+    res^3 values (e.g. ``pinned_empty``) to decode into.  ``devices`` (optional): GPU ids
+    (or "all") to split the lattice over in contiguous slabs (fvsrn_decode_density_multi);
+    default ``set_devices`` / FVSRN_DEVICES, else one GPU.
     """
+    from .device import decode_multi, device_model, resolve_devices
     from .volume import ScalarVolume
 
     if model.config.head != "density":
         raise ValueError("decode_volume requires a density-head model")
-    vals = _device(model).decode(resolution, t, out=None if out is None else out.reshape(-1))
+    flat = None if out is None else out.reshape(-1)
+    devs = resolve_devices(devices)
+    if devs is not None and len(devs) > 1:
+        vals = decode_multi([device_model(model, d) for d in devs], resolution, t, out=flat)
+    elif devs is not None:
+        vals = device_model(model, devs[0]).decode(resolution, t, out=flat)
+    else:
+        vals = _device(model).decode(resolution, t, out=flat)
     # finite / [0,1] (volume.py:41-49) was checked in the decode kernel (ValueError above)
     return ScalarVolume._validated(vals.reshape((resolution,) * 3))
 

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .device import DeviceVolume, device_model
+from .device import DeviceVolume, decode_multi, device_model, render_multi, resolve_devices
 from .imaging import Camera, Image
 
 EPS_BLEND = 1e-5
@@ -86,6 +86,10 @@ class ModelSource:
         fingerprint (exact weights/biases, sampled grids: microseconds), so a source bound
         before an optimiser step renders the updated model as the reference would."""
         return device_model(self.model, self._device, sampled_grids=True)
+
+    def device_models(self, devices):
+        """One device copy per GPU in ``devices`` (uploaded on first use, re-validated)."""
+        return [device_model(self.model, d, sampled_grids=True) for d in devices]
 
     def sample(self, p, d):
         """The per-sample source protocol (render.py:182-186), evaluated on the GPU."""
@@ -203,7 +207,7 @@ def render_rays(source, origins, dirs, settings: RenderSettings) -> np.ndarray:
 
 
 def render_image(source, camera: Camera, settings: RenderSettings | None = None,
-                 out: np.ndarray | None = None) -> Image:
+                 out: np.ndarray | None = None, devices=None) -> Image:
     """Full frame through the fused DVR kernel (render.py:314-332).
 
     ``settings.threads`` is ignored (the GPU parallelises over rays); the output
@@ -212,11 +216,20 @@ def render_image(source, camera: Camera, settings: RenderSettings | None = None,
     new): a float32 (H,W,4) host buffer to render into -- with
     ``pinned_empty`` an interactive viewer reuses one page-locked framebuffer and
     the device->host read runs at full bandwidth; the returned Image views it.
+    ``devices`` (optional, new): GPU ids (or "all") to split the frame over by 8x8 screen
+    tiles in this process (fvsrn_render_multi); default ``set_devices`` /
+    FVSRN_DEVICES, else one GPU.  The frame is bit-identical to the 1-GPU render.
     """
     src = _require_model_source(source)
     settings = settings or RenderSettings()
+    devs = resolve_devices(devices)
     if isinstance(src, VolumeSource):
         data, cnt = src.device_volume.render(src.tf, camera, settings, out=out)
+    elif devs is not None and len(devs) > 1:
+        data, cnt = render_multi(src.device_models(devs), src.tf, camera, settings, src.t, out=out)
+    elif devs is not None:
+        data, cnt = device_model(src.model, devs[0], sampled_grids=True).render(
+            src.tf, camera, settings, src.t, out=out)
     else:
         data, cnt = src.device_model.render(src.tf, camera, settings, src.t, out=out)
     src.last_eval_count = cnt

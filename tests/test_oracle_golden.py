@@ -130,3 +130,45 @@ def test_volume_source_render_matches_reference(tag):
     img = O.render_image(vol, O.TF_PRESETS[r["tf"]], _cam(r["camera"]), r["stepsize"],
                          r["max_steps"], tuple(r["background"]), r["et"])
     assert O.metric_psnr(img, arrays()[f"render_{tag}"]) > 90.0
+
+
+# ---- shape-exact fixtures (tests/golden/make_golden_shapes.py) -----------------------
+def _shapes():
+    import json
+
+    from tests.golden_util import GOLDEN
+
+    with np.load(GOLDEN / "golden_shapes.npz") as z:
+        a = {k: z[k] for k in z.files}
+    with open(GOLDEN / "golden_shapes.json") as f:
+        return GOLDEN, a, json.load(f)
+
+
+@pytest.mark.parametrize("ckpt,key,n", [("trained_cfg2.fvsrn", "trained_density", 8192),
+                                        ("trained_cfg3.fvsrn", "trained3_density", 2048)])
+def test_oracle_trained_checkpoint_density(ckpt, key, n):
+    # the oracle's checkpoint reader + evaluator vs the reference on the trained weights
+    g, a, _ = _shapes()
+    om = O.checkpoint_load(g / ckpt)
+    np.testing.assert_allclose(O.eval_density(om, a["trained_p"][:n]), a[key][:n], atol=2e-6)
+
+
+@pytest.mark.parametrize("tag", ["cfg2_v3", "trained_v5", "cfg5_t16.25"])
+def test_oracle_shape_rows(tag):
+    # one row of a full-size reference frame through the oracle's raymarch (same rays)
+    g, a, m = _shapes()
+    r = m["renders"][tag]
+    if r["model"] == "trained":
+        om = O.checkpoint_load(g / "trained_cfg2.fvsrn")
+    else:
+        om = O.model_init(O.OConfig(**m["models"][r["model"]]))
+    c = r["camera"]
+    cam = O.OCamera(np.array(c["eye"]), np.array(c["target"]), np.array(c["up"]), c["fov_y"],
+                    c["width"], c["height"])
+    rows = a[f"rows_{tag}"]
+    k = len(rows) // 2
+    cnt = [0]
+    img = O.render_image(om, O.TF_PRESETS[r["tf"]], cam, r["stepsize"], t=r["t"], counter=cnt,
+                         rows=rows[k:k + 1])
+    want = a[f"px_{tag}"].reshape(len(rows), c["width"], 4)[k]
+    assert O.metric_psnr(img[rows[k]], want) > 80.0
