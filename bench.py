@@ -15,11 +15,21 @@ Weights are random-init (ModelConfig seed 0); there is no dataset.
             framebuffer device->host inside the timed region).
 * roofline -- tensor-core FLOPs of the unpadded MLP per eval (7,168 at 4x32)
             x evals per frame / frame time, vs MEASURED_PEAKS.json bf16 burst.
-* cpu_baseline -- the CPU oracle port (numpy + numba, thread pool like
-            render.py:320-331) on a bounded row sample of the same frame.
+* cpu_baseline -- the reference itself (staged into oracle/_ref by oracle/stage_ref.sh;
+            the numpy/numba port when absent) on the box's host cores: all cores on the
+            same bounded row sample the reference arm times, plus one `taskset -c 0`
+            single-core run; CPU model stated (oracle/ref_runner.py).
+* --impl reference -- the reference arm: the same reference code on all host cores,
+            each step that row sample of view (step mod 8), rank 0 only.
 
-Under torchrun (N > 1) every rank renders its round-robin share of 8x8 screen
-tiles and one NCCL gather brings the tiles to rank 0.
+`--gpus N` without WORLD_SIZE in the environment re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU; it fails if fewer than N GPUs exist,
+unless FVSRN_BENCH_ONE_GPU=1 puts every rank on GPU 0 to exercise the multi-rank path).
+Under torchrun (N > 1) every rank renders its round-robin share of 8x8 screen tiles
+straight into rank 0's frame in peer memory (CUDA IPC over NVLink; FVSRN_MULTI=gather:
+NCCL gather + reassembly), and every timed frame ends with a device-side cross-rank
+completion (an NCCL all-reduce on each rank's stream), so rank 0's frame time covers
+every rank's tiles.
 """
 
 from __future__ import annotations
@@ -129,6 +139,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
+    """MUFU (XU-pipe) instructions per evaluation in the launched kernel: one MUFU.COS per
+    hidden activation except the ones evaluated on the FMA pipe (tcgen05 kernel: every 6th
+    element of a row, FVSRN_TC_POLY; mma.sync kernels: none, FVSRN_POLY_EVERY=0), plus
+    MUFU.TANH for the sigmoid head and MUFU.EX2 for alpha.  The NeRF base sin/cos run on
+    the FMA pipe (FVSRN_FOURIER_POLY=1)."""
+    layers, hid = model_cfg["layers"], model_cfg["hidden"]
+    per_row = hid - hid // 6 if kernel.startswith("dvr_tc") else hid
+    return (layers - 1) * per_row + 2
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -148,96 +169,145 @@ def ncu_traffic(config: str):
     return None, {}
 
 
-# ------------------------------------------------------------------ CPU (oracle port)
-def cpu_render_sample(cfg_name: str, view: int, row_stride: int, threads: int):
-    """Oracle port on every row_stride-th row of one view; returns (evals, seconds)."""
-    from oracle import fvsrn_oracle as O
-
-    cfg = CONFIGS[cfg_name]
-    O.set_threads(threads)
-    m = O.model_init(O.OConfig(**cfg["model"]))
-    cam = O.fibonacci_cameras(8, cfg["res"], cfg["res"])[view % 8]
-    rows = np.arange(0, cfg["res"], row_stride)
-    cnt = [0]
-    t0 = time.perf_counter()
-    O.render_image(m, O.TF_PRESETS["grayscale"], cam, cfg["stepsize"], t=cfg.get("t"),
-                   counter=cnt, rows=rows, threads=threads)
-    return cnt[0], time.perf_counter() - t0
+# ------------------------------------------------------------------ CPU legs (reference)
+# Bounded sample of one frame per config: every k-th row of a view (rays are independent,
+# so the rows cost what they cost inside the full frame); cfg 1 and the cfg 4 decode are
+# timed whole.  The reference arm and the all-core cpu_baseline use the same sample.
+CPU_ROW_STRIDE = {"cfg1": 1, "cfg2": 4, "cfg3": 64, "cfg5": 128}
+CPU_SINGLE_STRIDE = {"cfg1": 4, "cfg2": 64, "cfg3": 256, "cfg5": 512, "cfg4": 32}
+CPU_DECODE_ARM_STRIDE = 16          # reference arm, cfg 4: x slabs [::16] per step
 
 
-def cpu_decode_sample(cfg_name: str, fraction: int, threads: int):
-    from oracle import fvsrn_oracle as O
-
-    cfg = CONFIGS[cfg_name]
-    O.set_threads(threads)
-    m = O.model_init(O.OConfig(**cfg["model"]))
-    res = cfg["res"]
-    axis = np.linspace(0.0, 1.0, res)
-    xs = axis[::fraction]
-    gx, gy, gz = np.meshgrid(xs, axis, axis, indexing="ij")
-    pts = np.stack([gx, gy, gz], -1).reshape(-1, 3)
-    t0 = time.perf_counter()
-    for lo in range(0, len(pts), 1 << 16):
-        O.eval_density(m, pts[lo:lo + (1 << 16)])
-    return len(pts), time.perf_counter() - t0
+def ref_threads(cores: int, kind: str = "dvr") -> tuple[int, int]:
+    """(render_image `threads`, NUMBA_NUM_THREADS) for the reference on `cores` cores.
+    Measured on 8 cores for the cfg-2 row sample (oracle/ref_runner.py): threads=8 with
+    single-threaded numba kernels 4.11 M evals/s, threads=8 x numba 8 2.78 M/s
+    (oversubscribed), threads=1 x numba 8 0.71 M/s (small wavefronts) -- so the
+    reference's best is one render thread per core over single-threaded numba kernels.
+    decode_volume has no thread pool (model.py:392-398): its parallelism is numba's, so
+    decode uses NUMBA_NUM_THREADS = cores.  FVSRN_REF_THREADS / FVSRN_REF_NUMBA override."""
+    if kind == "decode":
+        return 1, int(os.environ.get("FVSRN_REF_NUMBA", cores))
+    return (int(os.environ.get("FVSRN_REF_THREADS", cores)),
+            int(os.environ.get("FVSRN_REF_NUMBA", 1)))
 
 
-def cpu_baseline(cfg_name: str, threads: int):
-    cfg = CONFIGS[cfg_name]
-    if cfg["kind"] == "decode":
-        cpu_decode_sample(cfg_name, 64, threads)       # JIT warm-up
-        n, dt = cpu_decode_sample(cfg_name, 8, threads)
-        sample = f"{cfg_name}: lattice slabs x[::8] of the {cfg['res']}^3 decode ({n} evals)"
-    else:
-        stride = max(1, cfg["res"] // 256)
-        cpu_render_sample(cfg_name, 0, cfg["res"] // 8, threads)   # JIT warm-up
-        n, dt = cpu_render_sample(cfg_name, 0, stride, threads)
-        sample = (f"{cfg_name} view 0, every {stride}th row ({cfg['res'] // stride} of "
-                  f"{cfg['res']} rows, {n} evals), {threads} threads")
-    return {"value": n / dt, "unit": "evals/s", "cores": threads, "kind": "port",
-            "sample": sample, "seconds": dt,
-            "note": "numpy+numba restatement of render.py/model.py (oracle/fvsrn_oracle.py); the "
-                    "reference itself measured 3.2 M evals/s on 8 cores of the build container"}
+def cpu_leg(config: str, cores: int, row_stride: int, view: int = 0, single: bool = False,
+            timeout: float = 240.0):
+    """oracle/ref_runner.py in a subprocess (its own NUMBA_NUM_THREADS; `taskset -c 0`
+    for the single-core run); returns its JSON result or {"error": ...}."""
+    import subprocess
+
+    threads, numba = (1, 1) if single else ref_threads(cores, CONFIGS[config]["kind"])
+    env = dict(os.environ, NUMBA_NUM_THREADS=str(numba), PYTHONDONTWRITEBYTECODE="1")
+    cmd = [sys.executable, "-m", "oracle.ref_runner", "--config", config,
+           "--threads", str(threads), "--view", str(view)]
+    cmd += ["--full"] if row_stride == 1 else ["--row-stride", str(row_stride)]
+    if single:
+        cmd = ["taskset", "-c", "0"] + cmd
+    try:
+        r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def cpu_baseline(config: str):
+    cores = os.cpu_count() or 1
+    kind = CONFIGS[config]["kind"]
+    allc = cpu_leg(config, cores, 1 if kind == "decode" else CPU_ROW_STRIDE[config],
+                   timeout=420.0)
+    one = cpu_leg(config, 1, CPU_SINGLE_STRIDE[config], single=True)
+    if "error" in allc:
+        return {"value": None, "unit": "evals/s", "cores": cores, "kind": "unavailable",
+                "sample": allc["error"]}
+    out = {"value": allc["value"], "unit": "evals/s", "cores": cores, "kind": allc["kind"],
+           "sample": allc["sample"] + (f", render_image threads={allc['threads']}, "
+                                       f"NUMBA_NUM_THREADS={ref_threads(cores)[1]}"
+                                       if kind == "dvr" else
+                                       f", NUMBA_NUM_THREADS={ref_threads(cores, kind)[1]}"),
+           "seconds": allc["seconds"], "cpu_model": allc.get("cpu_model"),
+           "single_core": ({"value": one["value"], "cores": 1, "sample": one["sample"] +
+                            ", taskset -c 0, NUMBA_NUM_THREADS=1", "seconds": one["seconds"]}
+                           if "error" not in one else one),
+           "note": ("the reference package itself (fvsrn 0.1.0 staged into oracle/_ref), "
+                    "through camera_rays + render_rays chunks exactly as render_image composes "
+                    "them (render.py:314-332), ModelSource(use_fused=" +
+                    ("True" if CONFIGS[config]["model"]["hidden"] <= 32 else "False") + ")")
+           if allc["kind"] == "reference" else "numpy+numba port (oracle/fvsrn_oracle.py)"}
+    return out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU path on the host cores (oracle port), rank 0 only."""
+    """--impl reference: the reference's CPU path on the host cores, rank 0 only."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
+    cores = os.cpu_count() or 1
+    threads, numba = ref_threads(cores, CONFIGS[args.config]["kind"])
+    os.environ["NUMBA_NUM_THREADS"] = str(numba)       # before numba is imported
+    from oracle.ref_runner import Runner, cpu_model
+
     cfg = CONFIGS[args.config]
-    # 128 rows of a view per step: large enough that the port's per-step numpy overhead
-    # does not understate the CPU (64 rows measured 1.6 vs 4.7 M evals/s), ~2 s per step
-    stride = max(1, cfg["res"] // 128) if cfg["kind"] == "dvr" else 32
-    runner = ((lambda v: cpu_render_sample(args.config, v, stride, threads))
-              if cfg["kind"] == "dvr" else (lambda v: cpu_decode_sample(args.config, stride, threads)))
+    runner = Runner(args.config, threads)
+    runner.warm()
+    if cfg["kind"] == "dvr":
+        stride = CPU_ROW_STRIDE[args.config]
+        rows = np.arange(0, cfg["res"], stride)
+        step = lambda i: runner.render_rows(i % 8, rows)          # noqa: E731
+        sample = (f"{args.config}: every {stride}th row ({len(rows)} of {cfg['res']}) of view "
+                  f"(step mod 8), render_image threads={runner.threads}, NUMBA_NUM_THREADS={numba}")
+    else:
+        stride = CPU_DECODE_ARM_STRIDE
+        step = lambda i: runner.decode(stride)                   # noqa: E731
+        sample = (f"{args.config}: decode_volume's chunked eval_density over lattice x slabs "
+                  f"[::{stride}], NUMBA_NUM_THREADS={numba}")
     for i in range(args.warmup):
-        runner(i)
+        if cfg["kind"] == "dvr":
+            runner.render_rows(i % 8, rows[len(rows) // 2: len(rows) // 2 + 1])
+        else:
+            runner.decode(cfg["res"] // 2)
     tot_n = tot_t = 0.0
-    per = []
     for i in range(args.steps):
-        n, dt = runner(i)
+        n, dt = step(i)
         tot_n += n
         tot_t += dt
-        per.append(dt)
     value = tot_n / tot_t
-    sample = (f"{args.config}: every {stride}th row of view (step mod 8), oracle port, "
-              f"{threads} threads" if cfg["kind"] == "dvr"
-              else f"{args.config}: lattice x[::{stride}] slab set, {threads} threads")
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (random-init weights, ModelConfig seed 0)",
-            "config": {"workload": cfg["desc"], "sample_rows_stride": stride},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 MLP, f64 ray setup/compositing (reference numpy + numba)",
+            "data": "synthetic (random-init weights, ModelConfig seed 0; fibonacci_cameras(8) views)",
+            "config": {"workload": cfg["desc"], "sample": sample,
+                       "evals_per_step_mean": tot_n / args.steps},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores,
+                             "kind": runner.kind, "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU
+def relaunch(n: int):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N
+    ranks on this node (rendezvous on 127.0.0.1).  Fails if fewer than N GPUs are visible,
+    unless FVSRN_BENCH_ONE_GPU=1 (all ranks share GPU 0: tests the multi-rank path only)."""
+    import socket
+
+    if os.environ.get("FVSRN_BENCH_ONE_GPU") != "1":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            sys.exit(f"bench.py --gpus {n}: only {have} GPU(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -253,6 +323,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus)          # does not return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -317,7 +389,7 @@ def main():
         if peer:
 
             def step(i, count_ptr=None):
-                _, ptr, _ = renderer._frame(res, res)
+                _, ptr, _ = renderer._frame(res, res, slot=i % renderer.NBUF)
                 renderer.dm.render_device(src.tf, cams[i % 8], settings, t_of(i), ptr, count_ptr,
                                           stream.cuda_stream, rank=rank, world=world, compact=False)
         elif world > 1:
@@ -377,6 +449,20 @@ def main():
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    done = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def complete():
+        """Cross-rank frame completion inside the timed region: every rank's tiles have
+        landed before this rank's end event (NCCL: an all-reduce ordered after the render
+        on every rank's stream; gloo test mode: host synchronisation + barrier)."""
+        if world == 1:
+            return
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(done)
+        else:
+            torch.cuda.synchronize()
+            dist.barrier()
+
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -386,11 +472,13 @@ def main():
             flush.zero_()                      # evict the L2 (outside the events)
             evs[i][0].record(stream)
             step(i)
+            complete()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     dom_ms, dom_launches, lib_launches = DEV.kernel_timer_read()
+    kernel_desc = DEV.kernel_timer_info()
     DEV.kernel_timer(False)
     per_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = torch.tensor([sum(per_ms)], dtype=torch.float64, device="cuda")
@@ -401,22 +489,39 @@ def main():
     ms_per_step = tot_ms / args.steps
 
     # ---- end-to-end through the public API (host buffers, copies inside the timing)
-    e2e = None
+    e2e = e2e_viewer = None
     if not args.no_e2e:
         if cfg["kind"] == "dvr":
             if world == 1:
-                # an interactive viewer's loop: one reusable page-locked framebuffer
-                fb = P.pinned_empty((res, res, 4))
+                # (1) the stock call a reference caller makes, render_image(src, cam,
+                # settings): a fresh Image every frame (its array is page-locked memory
+                # recycled by the library once the previous frame is dropped)
+                img = None
                 for i in range(2):
-                    P.render_image(src, cams[i % 8], settings, out=fb)
+                    img = P.render_image(src, cams[i % 8], settings)
                 with ClockSampler(dev) as e2e_clocks:
                     t0 = time.perf_counter()
                     n_e = 0
                     for i in range(args.steps):
                         src.t = t_of(i)
-                        P.render_image(src, cams[i % 8], settings, out=fb)
+                        img = P.render_image(src, cams[i % 8], settings)
                         n_e += src.last_eval_count
                     dt = time.perf_counter() - t0
+                del img
+                # (2) an interactive viewer's loop: one caller-owned page-locked framebuffer
+                fb = P.pinned_empty((res, res, 4))
+                for i in range(2):
+                    P.render_image(src, cams[i % 8], settings, out=fb)
+                t1 = time.perf_counter()
+                n_v = 0
+                for i in range(args.steps):
+                    src.t = t_of(i)
+                    P.render_image(src, cams[i % 8], settings, out=fb)
+                    n_v += src.last_eval_count
+                dtv = time.perf_counter() - t1
+                e2e_viewer = {"value": n_v / dtv, "unit": "evals/s", "ms_per_step": 1e3 * dtv / args.steps,
+                              "api": "render_image(ModelSource, cam, settings, out=pinned_empty(...)) "
+                                     "(one reused caller-owned page-locked framebuffer)"}
                 h2d = 4356 + 4 * 32
                 d2h = res * res * 16 + 8
             else:
@@ -439,21 +544,24 @@ def main():
                 h2d = 4356 + 4 * 32
                 d2h = res * res * 16 if rank == 0 else 0
         else:
-            vb = P.pinned_empty((res, res, res))
-            P.decode_volume(model, res, t=t_frame, out=vb)
+            vol = P.decode_volume(model, res, t=t_frame)
             t0 = time.perf_counter()
             for i in range(max(2, args.steps // 4)):
-                P.decode_volume(model, res, t=t_frame, out=vb)
+                vol = P.decode_volume(model, res, t=t_frame)
             dt = time.perf_counter() - t0
+            del vol
             n_e = max(2, args.steps // 4) * res ** 3
             h2d, d2h = 4 * 32, res ** 3 * 4
         e2e = {"value": n_e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                **({"clocks": e2e_clocks.summary()} if cfg["kind"] == "dvr" and world == 1 else {}),
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * dt / args.steps
                if cfg["kind"] == "dvr" else 1e3 * dt / max(2, args.steps // 4),
-               "api": "render_image(ModelSource, out=pinned framebuffer) -> fvsrn_render "
-                      "(mapped page-locked framebuffer: the kernel stores pixels over PCIe)"
-               if cfg["kind"] == "dvr" else "decode_volume(out=pinned) -> fvsrn_decode_density"}
+               "api": ("render_image(ModelSource(model, tf), cam, settings) -> fvsrn_render: host "
+                       "frame returned per call; the kernels store each pixel into it over PCIe "
+                       "(page-locked, recycled)" if world == 1 else
+                       "PeerFrameRenderer.render + rank-0 host copy (torchrun ranks)")
+               if cfg["kind"] == "dvr" else "decode_volume(model, 256) -> fvsrn_decode_density "
+                                            "(host volume returned per call)"}
 
     def finish():
         if world > 1:
@@ -473,14 +581,10 @@ def main():
     rank0_evals = total_evals / world
     achieved = rank0_evals * flops / (dom_ms / 1e3) / 1e12
     traffic, ncu = ncu_traffic(args.config)
-    mc = cfg["model"]
-    mufu_per_eval = (mc["layers"] - 1) * mc["hidden"] + 6 + 2
+    mufu_per_eval = mufu_per_eval_of(cfg["model"], kernel_desc)
     sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
     xu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
     xu_achieved = rank0_evals * mufu_per_eval / (dom_ms / 1e3)
-    kernel_name = {"cfg3": "dvr_tc_kernel<64,30,6> (tcgen05/TMEM)",
-                   "cfg4": "sample_kernel<32,4,14,4> (mma.sync)"}.get(
-        args.config, "dvr_kernel<32,4,14,4> (mma.sync)")
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -501,20 +605,23 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "flops_per_eval": flops, "peak_source": peak_src,
-                     "kernel": kernel_name, "kernel_ms_per_launch": dom_ms / max(1, dom_launches),
+                     "kernel": kernel_desc, "kernel_ms_per_launch": dom_ms / max(1, dom_launches),
                      "kernel_share_of_step": dom_ms / tot_ms if world == 1 else None,
                      "xu_pipe": {"mufu_per_eval": mufu_per_eval, "achieved_Gops": xu_achieved / 1e9,
                                  "peak_Gops": xu_peak / 1e9, "frac": xu_achieved / xu_peak,
-                                 "note": "MUFU (16/clk/SM) is the binding pipe: one cos per "
-                                         "hidden activation; see DESIGN.md section 4"},
+                                 "note": "MUFU (16/clk/SM): one cos per hidden activation not "
+                                         "moved to the FMA pipe, one tanh (sigmoid head), one "
+                                         "ex2 (alpha); see DESIGN.md section 4"},
                      **({"ncu": ncu} if ncu else {})},
         "gpu_launches": lib_launches,
         "clocks": clocks.summary(),
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if e2e_viewer is not None:
+        line["e2e_viewer"] = e2e_viewer
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, os.cpu_count() or 1)
+        line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
     finish()
 

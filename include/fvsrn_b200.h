@@ -245,6 +245,11 @@ FVSRN_API int32_t fvsrn_model_destroy(fvsrn_model_t model);
 FVSRN_API int32_t fvsrn_model_info(fvsrn_model_t model, int32_t* k0_pad, int32_t* hidden_pad,
                          int32_t* smem_bytes);
 
+/* Latent-grid sampler admitted at upload: tex_ok = 1 when the upload-time probe found
+ * max |texture - exact-weight| <= 1e-3 on 2^18 positions (auto mode then uses the texture
+ * units), probe_err = that maximum. */
+FVSRN_API int32_t fvsrn_model_sampler(fvsrn_model_t model, int32_t* tex_ok, float* probe_err);
+
 /* Full frame into host RGBA f32 (H,W,4); eval_count may be NULL. */
 FVSRN_API int32_t fvsrn_render(fvsrn_model_t model, const fvsrn_tf* tf, const fvsrn_camera* cam,
                      const fvsrn_settings* settings, double t, float* out_rgba,

@@ -113,6 +113,7 @@ EXPORTS = {
     "fvsrn_device_count": (C.c_int32, []),
     "fvsrn_model_create": (C.c_int32, [C.POINTER(ModelDesc), C.c_int32, C.POINTER(C.c_void_p)]),
     "fvsrn_model_destroy": (C.c_int32, [C.c_void_p]),
+    "fvsrn_model_sampler": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     "fvsrn_model_info": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32)]),
     "fvsrn_render": (C.c_int32, [C.c_void_p, C.POINTER(TFDesc), C.POINTER(CameraDesc),

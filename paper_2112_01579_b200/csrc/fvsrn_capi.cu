@@ -280,6 +280,10 @@ struct fvsrn_model {
   // u8 grids: the textures hold the codes; per-grid per-channel dequantisation
   bool tex_u8 = false;
   std::vector<std::array<float, 16>> qmin, qspan;
+  // texture sampler admitted for this model by the upload-time accuracy probe
+  // (probe_texture_sampler); tex_probe_err = max |tex - ldg| of the probe outputs
+  bool tex_ok = true;
+  float tex_probe_err = 0.f;
   // temporal texture path: per-(host thread, stream) pre-blended keyframe array set
   struct BlendSet {
     cudaArray_t arr[4] = {};
@@ -453,10 +457,20 @@ struct FrameScratch {
   unsigned long long* counters = nullptr;   // [0] queue, [1] evals, [2] non-finite pixels
 };
 
+// per-thread sampler override used by the upload-time probe (0 none, 1 tex, 2 ldg)
+thread_local int g_sampler_override = 0;
+
+// Texture units for the latent grid when: forced (FVSRN_GRID=tex / mode 1), or in auto
+// mode when the model passed the upload-time accuracy probe.  The texture filter's 8-bit
+// fractional weights perturb each latent channel by up to |v1 - v0| / 512 per axis; for
+// random-init grids that stays ~5e-4 in density, for trained grids with sharp latent
+// features it reached 4e-3 (trained cfg-2 shape) and 1.0e-2 (trained cfg-3 shape, u8
+// grid) at 2^20 positions, so those models render with the exact-weight LDG sampler.
 bool use_tex(const fvsrn_model* m) {
   if (m->tex.empty()) return false;
+  if (g_sampler_override) return g_sampler_override == 1;
   const int g = g_grid_mode.load(std::memory_order_relaxed);
-  return g == 1 || (g == 0 && kTexDefault);
+  return g == 1 || (g == 0 && kTexDefault && m->tex_ok);
 }
 
 // Pre-blend keyframes (lo, hi, w) into this (thread, stream)'s array set; reuses the set
@@ -1091,6 +1105,63 @@ int32_t fvsrn_device_count(void) {
   return n;
 }
 
+static int eval_common(fvsrn_model_t m, const double* p, const double* dd, int64_t n, double t,
+                       float* out, int want_head);
+
+// Upload-time accuracy probe of the texture sampler: the model's outputs at 2^18
+// deterministic uniform positions (and unit directions), once through the texture units
+// and once through the exact-weight LDG sampler, per keyframe time for temporal models.
+// Auto mode keeps the texture units only if max |tex - ldg| <= FVSRN_TEX_TOL (default
+// 1e-3, a tenth of the density tolerance).  ~2 ms per upload.
+static int probe_texture_sampler(fvsrn_model_t m) {
+  m->tex_ok = false;
+  if (m->tex.empty()) return FVSRN_OK;
+  static const double tol = [] {
+    const char* e = std::getenv("FVSRN_TEX_TOL");
+    return e ? std::atof(e) : 1e-3;
+  }();
+  const int64_t n = 1 << 18;
+  const int oc = m->head == FVSRN_HEAD_DENSITY ? 1 : 4;
+  std::vector<double> p((size_t)n * 3), d((size_t)n * 3);
+  uint64_t x = 0x9E3779B97F4A7C15ull;
+  auto next = [&x] {          // splitmix64 -> [0, 1)
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return (double)((z ^ (z >> 31)) >> 11) * (1.0 / 9007199254740992.0);
+  };
+  for (auto& v : p) v = next();
+  for (int64_t i = 0; i < n; ++i) {
+    double a = 2.0 * next() - 1.0, b = 6.283185307179586 * next(), r = std::sqrt(1.0 - a * a);
+    d[3 * i] = r * std::cos(b); d[3 * i + 1] = r * std::sin(b); d[3 * i + 2] = a;
+  }
+  std::vector<float> a((size_t)n * oc), b((size_t)n * oc);
+  std::vector<double> ts;
+  if (m->temporal) ts = m->kf_times;
+  else ts.push_back(std::nan(""));
+  float err = 0.f;
+  const double* dd = m->dir_mode != FVSRN_DIR_POS ? d.data() : nullptr;
+  for (double t : ts) {
+    g_sampler_override = 1;
+    int rc = eval_common(m, p.data(), dd, n, t, a.data(), m->head);
+    g_sampler_override = 2;
+    if (!rc) rc = eval_common(m, p.data(), dd, n, t, b.data(), m->head);
+    g_sampler_override = 0;
+    if (rc) return rc;
+    for (size_t i = 0; i < a.size(); ++i) err = std::max(err, std::fabs(a[i] - b[i]));
+  }
+  m->tex_probe_err = err;
+  m->tex_ok = err <= tol;
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_model_sampler(fvsrn_model_t m, int32_t* tex_ok, float* probe_err) {
+  if (!m) return fail(FVSRN_EINVAL, "null model");
+  if (tex_ok) *tex_ok = m->tex_ok ? 1 : 0;
+  if (probe_err) *probe_err = m->tex_probe_err;
+  return FVSRN_OK;
+}
+
 int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_model_t* out) {
   if (!d || !out) return fail(FVSRN_EINVAL, "null argument");
   *out = nullptr;
@@ -1326,6 +1397,7 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
   if (rc) return rc;
   rc = make_devpack(pkx, L, m->act, m->head, d_out, m->px);
   if (rc) return rc;
+  if ((rc = probe_texture_sampler(m))) return rc;
   *out = guard.release();
   return FVSRN_OK;
 }

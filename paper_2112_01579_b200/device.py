@@ -233,7 +233,10 @@ class DeviceModel:
     def info(self):
         k0, hp, sm = C.c_int32(), C.c_int32(), C.c_int32()
         L.check(self._lib.fvsrn_model_info(self._h, C.byref(k0), C.byref(hp), C.byref(sm)))
-        return {"k0_pad": k0.value, "hidden_pad": hp.value, "smem_bytes": sm.value}
+        ok, err = C.c_int32(), C.c_float()
+        L.check(self._lib.fvsrn_model_sampler(self._h, C.byref(ok), C.byref(err)))
+        return {"k0_pad": k0.value, "hidden_pad": hp.value, "smem_bytes": sm.value,
+                "texture_sampler_ok": bool(ok.value), "texture_probe_err": err.value}
 
     # ---------------------------------------------------------------- calls
     def eval_density(self, p, t=None) -> np.ndarray:
