@@ -317,6 +317,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--check-frame", action="store_true",
+                    help="N>1: compare the assembled frame with a 1-GPU render on rank 0")
     ap.add_argument("--grid-precision", default="f16", choices=["f16", "u8"],
                     help="u8: the latent grid round-trips through a u8 .fvsrn checkpoint "
                          "(grid_quantize, grid.py:157-166) and is sampled as 8-bit codes")
@@ -563,6 +565,14 @@ def main():
                if cfg["kind"] == "dvr" else "decode_volume(model, 256) -> fvsrn_decode_density "
                                             "(host volume returned per call)"}
 
+    frame_check = None
+    if args.check_frame and world > 1 and cfg["kind"] == "dvr":
+        src.t = t_of(0)
+        got = renderer.render(cams[0], settings)      # every rank takes part
+        if rank == 0:
+            want, _ = src.device_model.render(src.tf, cams[0], settings, src.t)
+            frame_check = bool(np.array_equal(got.cpu().numpy(), want))
+
     def finish():
         if world > 1:
             dist.barrier()
@@ -620,6 +630,8 @@ def main():
         line["e2e"] = e2e
     if e2e_viewer is not None:
         line["e2e_viewer"] = e2e_viewer
+    if frame_check is not None:
+        line["config"]["frame_bit_identical_to_1gpu"] = frame_check
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)

@@ -116,9 +116,13 @@ class VolumeSource:
         self.last_eval_count = 0
 
     def sample(self, p, d):
-        raise NotImplementedError("the B200 VolumeSource renders whole frames / ray batches "
-                                  "(render_image, raymarch_forward); per-sample host calls are "
-                                  "not part of the GPU path")
+        """The per-sample source protocol (render.py:139-141) on host arrays: trilinear
+        density (volume.py:213-255) through the TF.  Frames and ray batches do not come
+        through here; they render on the GPU (fvsrn_volume_render)."""
+        from .transfer import tf_eval
+        from .volume import sample_volume
+
+        return tf_eval(self.tf, sample_volume(self.volume, p))
 
 
 EPS_BLEND = 1e-5
@@ -172,11 +176,50 @@ def camera_rays(camera: Camera):
     return np.broadcast_to(camera.eye, dirs.shape).copy(), dirs
 
 
-def _require_model_source(source):
-    if not isinstance(source, (ModelSource, VolumeSource)):
-        raise TypeError("the B200 renderer draws ModelSource or VolumeSource instances; "
-                        f"got {type(source).__name__}")
+def _is_gpu_source(source) -> bool:
+    return isinstance(source, (ModelSource, VolumeSource))
+
+
+def _require_sampler(source):
+    if not callable(getattr(source, "sample", None)):
+        raise TypeError(f"{type(source).__name__} has no sample(p, d) method (render.py:226)")
     return source
+
+
+def _march_host_source(source, origins, dirs, settings: RenderSettings, want_states: bool):
+    """render.py:203-238 for a caller-defined source: any object with ``sample(p, d) ->
+    (rgb (N,3), sigma (N,))`` (the reference's duck-typed protocol).  Its sample() is the
+    caller's host code, so the march is a host wavefront: the rays still active at step k
+    are sampled together at t = tmin + (k + 1/2) ds and blended front to back in f64
+    (composite_step), with early termination unless ``want_states``.  ModelSource and
+    VolumeSource never come here: they march on the GPU."""
+    o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
+    d = np.asarray(dirs, dtype=np.float64).reshape(-1, 3)
+    tmin, tmax, hit = ray_box_intersect(o, d)
+    span = np.where(hit, tmax - tmin, 0.0)
+    steps = np.zeros(len(o), dtype=np.int64)
+    steps[hit] = np.maximum(np.minimum(np.ceil(span[hit] / settings.stepsize).astype(np.int64),
+                                       settings.max_steps), 1)
+    ds = np.where(steps > 0, span / np.maximum(steps, 1), 0.0)
+    color = np.zeros((len(o), 3))
+    alpha = np.zeros(len(o))
+    live = steps > 0
+    for k in range(int(steps.max()) if len(o) else 0):
+        live &= k < steps
+        idx = np.flatnonzero(live)
+        if idx.size == 0:
+            break
+        pos = o[idx] + (tmin[idx] + (k + 0.5) * ds[idx])[:, None] * d[idx]
+        rgb, sigma = source.sample(pos, d[idx])
+        color[idx], alpha[idx] = composite_step(color[idx], alpha[idx], np.asarray(rgb, np.float64),
+                                                np.asarray(sigma, np.float64), ds[idx],
+                                                settings.eps_blend)
+        if not want_states:
+            live[idx] &= ~(alpha[idx] > settings.early_term_alpha)
+    px = np.empty((len(o), 4), dtype=np.float32)
+    px[:, :3] = color + (1.0 - alpha)[:, None] * np.asarray(settings.background, dtype=np.float64)
+    px[:, 3] = alpha
+    return px, (RayState(color, alpha) if want_states else None)
 
 
 def raymarch_forward(source, origins, dirs, settings: RenderSettings, want_states: bool = False):
@@ -185,7 +228,9 @@ def raymarch_forward(source, origins, dirs, settings: RenderSettings, want_state
     With ``want_states`` early termination is disabled (as in the reference) and
     the terminal (C, A) pair is returned.
     """
-    src = _require_model_source(source)
+    if not _is_gpu_source(source):
+        return _march_host_source(_require_sampler(source), origins, dirs, settings, want_states)
+    src = source
     if want_states:
         settings = RenderSettings(settings.stepsize, settings.max_steps, settings.background,
                                   1.0, settings.eps_blend)
@@ -220,8 +265,12 @@ def render_image(source, camera: Camera, settings: RenderSettings | None = None,
     tiles in this process (fvsrn_render_multi); default ``set_devices`` /
     FVSRN_DEVICES, else one GPU.  The frame is bit-identical to the 1-GPU render.
     """
-    src = _require_model_source(source)
     settings = settings or RenderSettings()
+    if not _is_gpu_source(source):
+        o, d = camera_rays(camera)
+        px, _ = _march_host_source(_require_sampler(source), o, d, settings, False)
+        return Image(data=px.reshape(camera.height, camera.width, 4))
+    src = source
     devs = resolve_devices(devices)
     if isinstance(src, VolumeSource):
         data, cnt = src.device_volume.render(src.tf, camera, settings, out=out)
@@ -243,7 +292,7 @@ def render_image_rgba8(source, camera: Camera, settings: RenderSettings | None =
     returns the (H, W, 4) uint8 frame, bit-identical to quantising ``render_image``'s
     output on the host, with a quarter of the device->host bytes.  New (the service's
     render path); ``out`` may be a ``pinned_empty(..., np.uint8)`` buffer."""
-    src = _require_model_source(source)
+    src = source
     if not isinstance(src, ModelSource):
         raise TypeError("render_image_rgba8 renders ModelSource instances")
     settings = settings or RenderSettings()
