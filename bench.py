@@ -317,6 +317,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--csv", default=None,
+                    help="append a row to this benchmark.csv (SURVEY section 5 columns) and write "
+                         "manifest.json beside it")
     ap.add_argument("--check-frame", action="store_true",
                     help="N>1: compare the assembled frame with a 1-GPU render on rank 0")
     ap.add_argument("--grid-precision", default="f16", choices=["f16", "u8"],
@@ -635,7 +638,37 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_csv(args.csv, args.config, world, line)
     finish()
+
+
+def write_csv(path: str, config: str, world: int, line: dict) -> None:
+    """benchmark.csv + manifest.json, the reference's artefact convention (cli.py:64-76):
+    columns config,gpus,res,spr,evals,ms_per_frame,evals_per_s,roofline_frac."""
+    import platform
+
+    cfg = CONFIGS[config]
+    p = Path(path)
+    p.parent.mkdir(parents=True, exist_ok=True)
+    new = not p.exists()
+    spr = round(1.0 / cfg["stepsize"]) if cfg["kind"] == "dvr" else ""
+    with open(p, "a") as f:
+        if new:
+            f.write("config,gpus,res,spr,evals,ms_per_frame,evals_per_s,roofline_frac\n")
+        f.write(f"{config},{world},{cfg['res']},{spr},{line['config']['evals_per_step_mean']:.0f},"
+                f"{line['ms_per_step']:.4f},{line['value']:.6g},{line['roofline']['frac']:.4f}\n")
+    import torch
+
+    manifest = {"config": {k: v for k, v in cfg.items() if k != "desc"}, "workload": cfg["desc"],
+                "seed": cfg["model"].get("seed", 0), "gpus": world,
+                "versions": {"fvsrn_b200": __import__("paper_2112_01579_b200").__version__,
+                             "torch": torch.__version__, "cuda": torch.version.cuda,
+                             "python": platform.python_version(),
+                             "device": torch.cuda.get_device_name(0)},
+                "kernel": line["roofline"].get("kernel")}
+    with open(p.parent / "manifest.json", "w") as f:
+        json.dump(manifest, f, indent=1)
 
 
 if __name__ == "__main__":

@@ -118,11 +118,12 @@ FVSRN_API int32_t fvsrn_device_count(void);
 /* DVR kernel selection for the default fV-SRN shapes (no reference counterpart: a
  * measurement / A-B switch; the environment variable FVSRN_DVR sets the initial value).
  * 0 auto (measured faster per width), 1 tcgen05/TMEM, 2 warp-specialised mma.sync,
- * 3 single-role mma.sync.  Returns the previous mode, or FVSRN_EINVAL. */
+ * 3 single-role mma.sync (4 pipelined, 5 two rays per lane, 2 warp-specialised: A/B builds
+ * only).  Returns the previous mode, or -FVSRN_EINVAL (negative) on failure. */
 FVSRN_API int32_t fvsrn_set_dvr_kernel(int32_t mode);
 /* Latent-grid sampler for 16-channel grids (measurement switch; env FVSRN_GRID sets the
  * initial value): 0 auto, 1 texture units (RGBA16F 3D textures, hardware trilinear),
- * 2 LDG.128 + HFMA2 trilinear.  Returns the previous mode, or FVSRN_EINVAL. */
+ * 2 LDG.128 + HFMA2 trilinear.  Returns the previous mode, or -FVSRN_EINVAL on failure. */
 FVSRN_API int32_t fvsrn_set_grid_sampler(int32_t mode);
 /* Measurement hooks (bench.py): per calling thread, CUDA events around every launch of
  * the dominant kernel (march / decode) and a count of all library kernel launches.
@@ -161,9 +162,10 @@ typedef struct {
 /* One batch of n positions (device f64 (n,3); timesteps d_times (n) f64 for temporal
  * models, else NULL) against reference values (device f32 (n,d_out)): forward with cached layer inputs (d_inputs: per layer n x in_l floats,
  * consecutive), pre-activations (d_preacts: (L-1) x n x hidden) and adjoints (d_deltas:
- * per layer n x out_l); the L1-loss sum is added to *d_loss_sum; the latent-grid
- * gradient is scatter-added into d_grid_grad (zero it first).  Weight/bias gradients are
- * the batch reductions delta_l^T @ inputs_l and sum(delta_l) (nn.py:252-253). */
+ * per layer n x out_l); the L1-loss sum is added to *d_loss_sum (fixed-order reduction);
+ * the latent-grid gradient is added into d_grid_grad by the deterministic scatter: every
+ * vertex sums its contributions in the reference's order and arithmetic (grid.py:86-112).
+ * Weight/bias gradients: fvsrn_layer_grads over the caches (nn.py:252-253). */
 FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const float* d_params,
                                           const double* d_positions, const double* d_times,
                                           const float* d_reference,
@@ -172,21 +174,33 @@ FVSRN_API int32_t fvsrn_train_world_grads(const fvsrn_train_desc* desc, const fl
                                           void* stream);
 /* mlp_forward / mlp_backward (nn.py:179-193, 234-256) of a plain MLP (desc without grid)
  * on given inputs d_x (n, d_in) f32: outputs d_y (n, d_out), caches (layout as
- * fvsrn_train_world_grads) and, when d_y_bar (n, d_out) is given, the per-layer deltas. */
+ * fvsrn_train_world_grads) and, when d_y_bar (n, d_out) is given, the per-layer deltas and
+ * (d_x_bar != NULL) the input adjoint delta_0 @ W_0 (n, d_in). */
 FVSRN_API int32_t fvsrn_mlp_forward_backward(const fvsrn_train_desc* desc, const float* d_params,
                                              const float* d_x, const float* d_y_bar, int64_t n,
                                              float* d_y, float* d_inputs, float* d_preacts,
-                                             float* d_deltas, void* stream);
+                                             float* d_deltas, float* d_x_bar, void* stream);
+/* Weight / bias gradients of every layer from the caches of the calls above
+ * (nn.py:252-253: delta_l^T @ inputs_l, sum over rows of delta_l) for the first n of
+ * cap_rows cache rows, into d_grads laid out like the parameters ([W_0..W_{L-1} |
+ * b_0..b_{L-1}], trainable_arrays order); accumulate != 0 adds to d_grads.  Tensor cores
+ * (mma.sync TF32, 3xTF32 split) over fixed 256-row chunks, chunk partials summed in order:
+ * bit-identical run to run.  Replaces the caller-side GEMMs. */
+FVSRN_API int32_t fvsrn_layer_grads(const fvsrn_train_desc* desc, const float* d_inputs,
+                                    const float* d_deltas, int64_t cap_rows, int64_t n,
+                                    float* d_grads, int32_t accumulate, void* stream);
 /* grid_sample_backward (grid.py:123-137): scatter-add of trilinear-weighted adjoints
- * d_z_bar (n, channels) f32 at positions (n,3) f64 into d_grad (res^3 * channels) f32. */
+ * d_z_bar (n, channels) f32 at positions (n,3) f64 into d_grad (res^3 * channels) f32,
+ * deterministic (per-vertex sums in sample order, the reference's sequential order). */
 FVSRN_API int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels,
                                              const double* d_positions, const float* d_z_bar,
                                              int64_t n, float* d_grad, void* stream);
 /* model_backward (model.py:300-335): gradients of sum(raw_bar * raw) for n samples with
  * given raw-output adjoints d_raw_bar (n, d_out) f32, any head and input encoding (view
  * directions d_dirs (n,3) for direction modes, per-sample d_times for temporal models).
- * Same caches as fvsrn_train_world_grads (weight/bias gradients are the caller's GEMMs
- * over d_inputs / d_deltas); latent-grid gradients are scatter-added into d_grid_grad. */
+ * Same caches as fvsrn_train_world_grads (weight/bias gradients: fvsrn_layer_grads);
+ * latent-grid gradients are added into d_grid_grad by the deterministic scatter
+ * (per-vertex sums in model_backward's order: bracket pair, then sample). */
 FVSRN_API int32_t fvsrn_model_grads(const fvsrn_train_desc* desc, const float* d_params,
                                     const double* d_positions, const double* d_dirs,
                                     const double* d_times, const float* d_raw_bar, int64_t n,
@@ -204,7 +218,8 @@ FVSRN_API int32_t fvsrn_train_screen_forward(const fvsrn_train_desc* desc, const
 /* raymarch_backward (render.py:241-306): reverse walk per ray with blend inversion; the
  * cache rows of ray i's step k go to row d_row_offset[i] + k of buffers sized for
  * cap_rows samples (layout as fvsrn_train_world_grads with n = cap_rows); latent-grid
- * gradients are scatter-added into d_grid_grad. */
+ * gradients are added into d_grid_grad by the deterministic scatter in
+ * raymarch_backward's order (steps from the last, rays in index order). */
 FVSRN_API int32_t fvsrn_train_screen_backward(const fvsrn_train_desc* desc, const float* d_params,
                                               const double* d_origins, const double* d_dirs, int64_t n,
                                               double eps_blend, const double* d_color,

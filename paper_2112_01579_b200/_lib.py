@@ -83,7 +83,10 @@ EXPORTS = {
     "fvsrn_set_dvr_kernel": (C.c_int32, [C.c_int32]),
     "fvsrn_set_grid_sampler": (C.c_int32, [C.c_int32]),
     "fvsrn_mlp_forward_backward": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
-                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_void_p]),
+    "fvsrn_layer_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                      C.c_void_p, C.c_int32, C.c_void_p]),
     "fvsrn_grid_sample_backward": (C.c_int32, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                                                C.c_void_p, C.c_void_p]),
     "fvsrn_model_grads": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

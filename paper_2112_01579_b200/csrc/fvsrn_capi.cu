@@ -52,17 +52,17 @@ enum class DvrMode : int { kAuto = 0, kTC = 1, kWS = 2, kWarp = 3, kPipe = 4, kD
 std::atomic<int> g_dvr_mode_i{[] {
   const char* e = std::getenv("FVSRN_DVR");
   if (e && std::string(e) == "tc") return (int)DvrMode::kTC;
-  if (e && std::string(e) == "ws") return (int)DvrMode::kWS;
   if (e && std::string(e) == "warp") return (int)DvrMode::kWarp;
-  if (e && std::string(e) == "pipe") return (int)DvrMode::kPipe;
-  if (e && std::string(e) == "dual") return (int)DvrMode::kDual;
+  if (FVSRN_AB_VARIANTS && e && std::string(e) == "ws") return (int)DvrMode::kWS;
+  if (FVSRN_AB_VARIANTS && e && std::string(e) == "pipe") return (int)DvrMode::kPipe;
+  if (FVSRN_AB_VARIANTS && e && std::string(e) == "dual") return (int)DvrMode::kDual;
   return (int)DvrMode::kAuto;
 }()};
 // tcgen05 kernel: one 128-ray tile per CTA (default, measured faster), or two tiles in
 // ping-pong (FVSRN_TC_TILES=2)
 const bool g_tc_two_tiles = [] {
   const char* e = std::getenv("FVSRN_TC_TILES");
-  return e && e[0] == '2';
+  return FVSRN_AB_VARIANTS && e && e[0] == '2';
 }();
 // latent-grid sampler for F = 16 grids: 0 auto, 1 texture units, 2 LDG + HFMA2
 std::atomic<int> g_grid_mode{[] {
@@ -830,8 +830,26 @@ extern "C" {
 
 const char* fvsrn_last_error(void) { return g_err.c_str(); }
 
+// The stream-ordered pool of the calling thread's device keeps freed blocks (per-call
+// scratch would otherwise be unmapped and remapped at every synchronisation).
+static void keep_pool_blocks() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
+  std::lock_guard<std::mutex> l(mu);
+  for (int d : done) if (d == dev) return;
+  cudaMemPool_t pool;
+  uint64_t keep = UINT64_MAX;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  cudaGetLastError();
+  done.push_back(dev);
+}
+
 static int make_train_net(const fvsrn_train_desc* d, long long rows, TrainNetDev& net,
                           bool check_inputs = true) {
+  keep_pool_blocks();
   const int L = d->layers;
   if (L < 1 || L > kTrainMaxLayers) return fail(FVSRN_EINVAL, "layer count out of range");
   if (d->hidden > 256 || d->d_in > 256 || d->d_out < 1 || d->d_out > 4)
@@ -916,7 +934,7 @@ int32_t fvsrn_train_world_grads(const fvsrn_train_desc* d, const float* d_params
 
 int32_t fvsrn_mlp_forward_backward(const fvsrn_train_desc* d, const float* d_params, const float* d_x,
                                    const float* d_y_bar, int64_t n, float* d_y, float* d_inputs,
-                                   float* d_preacts, float* d_deltas, void* stream) {
+                                   float* d_preacts, float* d_deltas, float* d_x_bar, void* stream) {
   if (!d || !d_params || (n > 0 && (!d_x || !d_y || !d_inputs || (d_y_bar && !d_deltas))))
     return fail(FVSRN_EINVAL, "null argument");
   if (d->grid_resolution != 0 || d->n_keyframes != 0) return fail(FVSRN_EINVAL, "plain MLP: no grid / keyframes");
@@ -925,13 +943,27 @@ int32_t fvsrn_mlp_forward_backward(const fvsrn_train_desc* d, const float* d_par
   int rc = make_train_net(d, n, net, false);
   if (rc) return rc;
   CUDA_TRY(launch_mlp_grads(net, d_params, d_x, d_y_bar, (long long)n, d_y, d_inputs, d_preacts,
-                            d_deltas, (cudaStream_t)stream));
+                            d_deltas, d_y_bar ? d_x_bar : nullptr, (cudaStream_t)stream));
+  count_launch();
+  return FVSRN_OK;
+}
+
+int32_t fvsrn_layer_grads(const fvsrn_train_desc* d, const float* d_inputs, const float* d_deltas,
+                          int64_t cap_rows, int64_t n, float* d_grads, int32_t accumulate, void* stream) {
+  if (!d || (n > 0 && (!d_inputs || !d_deltas || !d_grads))) return fail(FVSRN_EINVAL, "null argument");
+  if (n > cap_rows) return fail(FVSRN_EINVAL, "more rows than the caches hold");
+  TrainNetDev net;
+  int rc = make_train_net(d, cap_rows, net, false);
+  if (rc) return rc;
+  CUDA_TRY(launch_layer_grads(net, d_inputs, d_deltas, (long long)n, d_grads, accumulate != 0,
+                              (cudaStream_t)stream));
   count_launch();
   return FVSRN_OK;
 }
 
 int32_t fvsrn_grid_sample_backward(int32_t resolution, int32_t channels, const double* d_positions,
                                    const float* d_z_bar, int64_t n, float* d_grad, void* stream) {
+  keep_pool_blocks();
   if (resolution < 2 || channels < 1) return fail(FVSRN_EINVAL, "grid must have resolution >= 2 and channels >= 1");
   if (n > 0 && (!d_positions || !d_z_bar || !d_grad)) return fail(FVSRN_EINVAL, "null argument");
   CUDA_TRY(launch_grid_scatter(resolution, channels, d_positions, d_z_bar, (long long)n, d_grad,
@@ -1089,12 +1121,16 @@ int32_t fvsrn_kernel_timer_info(char* buf, int32_t cap) {
 }
 
 int32_t fvsrn_set_grid_sampler(int32_t mode) {
-  if (mode < 0 || mode > 2) return fail(FVSRN_EINVAL, "grid sampler mode must be 0..2");
+  if (mode < 0 || mode > 2) return -fail(FVSRN_EINVAL, "grid sampler mode must be 0..2");
   return g_grid_mode.exchange(mode);
 }
 
 int32_t fvsrn_set_dvr_kernel(int32_t mode) {
-  if (mode < 0 || mode > 5) return fail(FVSRN_EINVAL, "DVR kernel mode must be 0..5");
+  // failures are negative (-FVSRN_EINVAL): every non-negative value is a previous mode
+  if (mode < 0 || mode > 5) return -fail(FVSRN_EINVAL, "DVR kernel mode must be 0..5");
+  if (!FVSRN_AB_VARIANTS && (mode == (int)DvrMode::kWS || mode == (int)DvrMode::kPipe ||
+                             mode == (int)DvrMode::kDual))
+    return -fail(FVSRN_EINVAL, "DVR variant not in this build (A/B builds: -DFVSRN_AB_VARIANTS=1)");
   return g_dvr_mode_i.exchange(mode);
 }
 const char* fvsrn_version(void) { return "fvsrn_b200 0.1.0 (sm_100a, mma.sync f16/f32)"; }

@@ -230,6 +230,29 @@ __device__ __forceinline__ float act_h(float x) {
 }
 
 // ---------------------------------------------------------------- warp MLP
+// FVSRN_BREG=1: the B fragments of the hidden layers live in registers for the whole
+// kernel (loaded once per warp) instead of one LDS.64 per MMA per step (A/B switch).
+#ifndef FVSRN_BREG
+#define FVSRN_BREG 0
+#endif
+template <int HID, int NL>
+struct HiddenB {
+  static constexpr int NLH = NL > 2 ? NL - 2 : 1;
+  static constexpr bool kOn = FVSRN_BREG != 0 && NL > 2;
+  uint2 f[kOn ? NLH : 1][kOn ? HID / 16 : 1][kOn ? HID / 8 : 1];
+  __device__ void load(const uint2* wf, const NetDev& net, int lane) {
+    if constexpr (kOn) {
+#pragma unroll
+      for (int l = 0; l < NLH; ++l)
+#pragma unroll
+        for (int kt = 0; kt < HID / 16; ++kt)
+#pragma unroll
+          for (int nt = 0; nt < HID / 8; ++nt)
+            f[l][kt][nt] = wf[net.w_off[l + 1] + (kt * (HID / 8) + nt) * 32 + lane];
+    }
+  }
+};
+
 // Evaluates the whole network for the 32 rows staged in `stage` (row stride `rs`
 // halfs) and writes head inputs (pre-head raw outputs, up to 4 per row) to
 // `outbuf[row*4 + c]`.  MT = number of m16 tiles held at once (2 -> all 32 rows).
@@ -302,9 +325,14 @@ struct WarpMLP {
 #endif
   }
 
-  // m_base: first m16 tile index handled (0, or 0/1 when MT == 1)
   __device__ static void run(const __half* stage, int rs, const NetDev& net, const uint2* wf,
                              const float* bs, float* outbuf, int lane, int m_base) {
+    run(stage, rs, net, wf, bs, outbuf, lane, m_base, HiddenB<HID, 0>{});
+  }
+  // m_base: first m16 tile index handled (0, or 0/1 when MT == 1)
+  template <class HB>
+  __device__ static void run(const __half* stage, int rs, const NetDev& net, const uint2* wf,
+                             const float* bs, float* outbuf, int lane, int m_base, const HB& hb) {
     const int g = lane >> 2, q = lane & 3;
     const int arow = lane & 15, acol = (lane >> 4) * 8;
     float out_acc[MT][4];
@@ -362,7 +390,9 @@ struct WarpMLP {
         for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const uint2 b = bfrag(wf + net.w_off[l], kt, nt, lane);
+            uint2 b;
+            if constexpr (HB::kOn) b = hb.f[l - 1][kt][nt];
+            else b = bfrag(wf + net.w_off[l], kt, nt, lane);
             if (kt == 0) {
               const float4 bq = bias_quad(bl, nt, q);
 #pragma unroll
@@ -399,14 +429,25 @@ struct WarpMLP {
   }
 };
 
+// m16 tiles held at once by the warp MLP for 32-wide networks (FVSRN_MT32=1: one tile at a
+// time, half the accumulator registers, weights read twice; A/B switch)
+#ifndef FVSRN_MT32
+#define FVSRN_MT32 2
+#endif
 template <int HID, int ACT, int NL = 0, int KT0 = 0>
 struct MLPDispatch {
-  static constexpr int MT = HID <= 64 ? 2 : 1;
+  static constexpr int MT = HID <= 32 ? FVSRN_MT32 : (HID <= 64 ? 2 : 1);
+  using HB = HiddenB<HID, NL>;
   __device__ static void eval32(const __half* stage, int rs, const NetDev& net, const uint2* wf,
-                                const float* bs, float* outbuf, int lane) {
+                                const float* bs, float* outbuf, int lane, const HB& hb) {
 #pragma unroll
     for (int mb = 0; mb < 2; mb += MT)
-      WarpMLP<HID, MT, ACT, NL, KT0>::run(stage, rs, net, wf, bs, outbuf, lane, mb);
+      WarpMLP<HID, MT, ACT, NL, KT0>::run(stage, rs, net, wf, bs, outbuf, lane, mb, hb);
+  }
+  __device__ static void eval32(const __half* stage, int rs, const NetDev& net, const uint2* wf,
+                                const float* bs, float* outbuf, int lane) {
+    HB hb;
+    eval32(stage, rs, net, wf, bs, outbuf, lane, hb);
   }
 };
 

@@ -94,6 +94,9 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   r.has = false;
   LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
+  using MLP = MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>;
+  typename MLP::HB hb;
+  hb.load(wf_s, net, lane);
 
   while (true) {
     ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
@@ -107,7 +110,7 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
                          use_dir ? r.dx : 0.f, use_dir ? r.dy : 0.f, use_dir ? r.dz : 0.f, myrow);
     }
     __syncwarp();
-    MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    MLP::eval32(stage, rs, net, wf_s, b_s, ob, lane, hb);
     __syncwarp();
     // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
     if (r.has)
@@ -116,6 +119,7 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
+#if FVSRN_AB_VARIANTS   // measured-slower A/B variants, off by default
 // ---------------------------------------------------------------- software-pipelined DVR
 // dvr_kernel with the next step's input row built while the MLP of the current step
 // runs: the rows of step k+1 are a pure function of the ray (p_{k+1} = pe + (k+1) dd does
@@ -276,6 +280,8 @@ dvr_dual_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
+#endif  // FVSRN_AB_VARIANTS
+
 // ---------------------------------------------------------------- ray setup
 // One thread per slot, canonical slot order: camera ray (render.py:72-94) or explicit ray,
 // slab test and march geometry (render.py:97-106, 189-200) in f64 with explicit _rn ops,
@@ -401,6 +407,7 @@ cudaError_t launch_tile_sort(int n_local, unsigned* cost, unsigned* order, int f
   return cudaGetLastError();
 }
 
+#if FVSRN_AB_VARIANTS
 // ---------------------------------------------------------------- warp-specialised DVR
 // The per-sample pipeline has two halves with disjoint pipe profiles: the producer half
 // (ray refill, latent-grid gather + trilinear, Fourier features, head/TF/compositing/ET)
@@ -521,6 +528,8 @@ dvr_ws_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const floa
   }
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
+
+#endif  // FVSRN_AB_VARIANTS
 
 // ---------------------------------------------------------------- LPT schedule
 __global__ void tile_cost_kernel(CamDev cam, MarchDev md, ShardDev sh, long long n_slots,
@@ -736,6 +745,14 @@ __global__ void tiles_to_frame_kernel(const float4* __restrict__ gathered, int W
 }
 
 // ---------------------------------------------------------------- launch table
+#if FVSRN_AB_VARIANTS
+#define FVSRN_WS_CASE(H)                                                          \
+  if (kind == KernelKind::kDVRWS)                                                 \
+    return fast ? (const void*)dvr_ws_kernel<H, 4, (H - 4) / 2, fast_layers(H)>   \
+                : (const void*)dvr_ws_kernel<H, kActRuntime, 0, 0>;
+#else
+#define FVSRN_WS_CASE(H)
+#endif
 #define FVSRN_FOR_HIDDEN(X) X(16) X(32) X(48) X(64) X(96) X(128)
 
 // Default-config layer counts baked into the fast variants (fV-SRN 4x32 and 6x64).
@@ -744,6 +761,7 @@ constexpr int fast_layers(int hid) { return hid == 64 ? 6 : 4; }
 // fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode, layers =
 // fast_layers(HID)); else generic (runtime layer count and input layout)
 const void* kernel_for(KernelKind kind, int hid, bool fast) {
+#if FVSRN_AB_VARIANTS
   if (kind == KernelKind::kDVRDual) {
     if (!fast || hid != 32) return nullptr;
     return (const void*)dvr_dual_kernel<32, 14, 4>;
@@ -756,15 +774,16 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
       default: return nullptr;
     }
   }
+#else
+  if (kind == KernelKind::kDVRDual || kind == KernelKind::kDVRPipe || kind == KernelKind::kDVRWS) return nullptr;
+#endif
   switch (hid) {
 #define CASE(H)                                                                              \
   case H:                                                                                    \
     if (kind == KernelKind::kDVR)                                                            \
       return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H)>               \
                   : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
-    if (kind == KernelKind::kDVRWS)                                                          \
-      return fast ? (const void*)dvr_ws_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
-                  : (const void*)dvr_ws_kernel<H, kActRuntime, 0, 0>;                        \
+    FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
                   : (const void*)sample_kernel<H, kActRuntime, 0, 0>;                        \

@@ -14,6 +14,11 @@ namespace fvsrn {
 constexpr int kThreads = FVSRN_THREADS;  // 4 independent warps per CTA; weights shared in smem
 // CTAs per SM the register budget is sized for (A/B-measured on B200):
 // DVR 5 (<= 102 regs, 20 warps/SM), decode/eval 4 (<= 128 regs).
+// measured-slower DVR variants (warp-specialised, software-pipelined, two rays per lane,
+// two-tile tcgen05): compiled only for A/B builds (make variant VDEFS=-DFVSRN_AB_VARIANTS=1)
+#ifndef FVSRN_AB_VARIANTS
+#define FVSRN_AB_VARIANTS 0
+#endif
 #ifndef FVSRN_MIN_BLOCKS
 #define FVSRN_MIN_BLOCKS 5
 #endif

@@ -342,6 +342,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   if (warp == 0) tmem_dealloc(tmem, kAlloc);
 }
 
+#if FVSRN_AB_VARIANTS   // measured slower, off by default
 // Two-tile ping-pong variant: every thread owns two rays (tile 0 row t, tile 1 row t),
 // with one A tile, one TMEM accumulator region and one mbarrier per tile.  While the
 // tensor core runs layer l+1 of one tile, the CTA evaluates the activations (XU pipe)
@@ -500,10 +501,17 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
   if (warp == 0) tmem_dealloc(tmem, kAlloc);
 }
 
+#endif  // FVSRN_AB_VARIANTS
+
 const void* tc_kernel_for(int hid, bool two_tiles) {
   switch (hid) {
+#if FVSRN_AB_VARIANTS
     case 32: return two_tiles ? (const void*)dvr_tc2_kernel<32, 14, 4> : (const void*)dvr_tc_kernel<32, 14, 4>;
     case 64: return two_tiles ? (const void*)dvr_tc2_kernel<64, 30, 6> : (const void*)dvr_tc_kernel<64, 30, 6>;
+#else
+    case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;
+    case 64: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<64, 30, 6>;
+#endif
     default: return nullptr;
   }
 }

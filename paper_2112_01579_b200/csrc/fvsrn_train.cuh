@@ -35,7 +35,7 @@ struct AdamConsts {
 
 cudaError_t launch_mlp_grads(const TrainNetDev& net, const float* params, const float* x, const float* y_bar,
                              long long n, float* y_out, float* inputs, float* preacts, float* deltas,
-                             cudaStream_t s);
+                             float* x_bar, cudaStream_t s);
 cudaError_t launch_grid_scatter(int R, int F, const double* pos, const float* z_bar, long long n,
                                 float* grad, cudaStream_t s);
 cudaError_t launch_model_grads(const TrainNetDev& net, const float* params, const double* pos,
@@ -58,6 +58,10 @@ cudaError_t launch_screen_backward(const TrainNetDev& net, const float* params, 
 cudaError_t launch_f32_eval(const TrainNetDev& net, const float* params, const double* pos,
                             const double* dirs, const double* times, const float* xin, long long n,
                             int stage, float* out, cudaStream_t s);
+// dW_l / db_l of every layer from the caches (deterministic, tensor cores), written to
+// (or, with accumulate, added into) the flat gradient buffer at the w_off / b_off offsets
+cudaError_t launch_layer_grads(const TrainNetDev& net, const float* inputs, const float* deltas, long long n,
+                               float* grads, bool accumulate, cudaStream_t s);
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, const AdamConsts& k,
                         unsigned long long* bad, cudaStream_t s);
 

@@ -513,7 +513,8 @@ def set_dvr_kernel(name: str) -> str:
     selection.  A measurement switch: every choice renders the same image within fp16
     noise (tests/test_gpu_parity.py::test_dvr_kernel_variants)."""
     prev = L.lib().fvsrn_set_dvr_kernel(DVR_KERNELS[name])
-    L.check(0 if prev >= 0 else prev)
+    if prev < 0:
+        L.check(-prev)
     return {v: k for k, v in DVR_KERNELS.items()}[prev]
 
 
@@ -525,7 +526,8 @@ def set_grid_sampler(name: str) -> str:
     with 8-bit fractional weights), "ldg" (LDG.128 + HFMA2 trilinear) or "auto"; returns
     the previous selection."""
     prev = L.lib().fvsrn_set_grid_sampler(GRID_SAMPLERS[name])
-    L.check(0 if prev >= 0 else prev)
+    if prev < 0:
+        L.check(-prev)
     return {v: k for k, v in GRID_SAMPLERS.items()}[prev]
 
 

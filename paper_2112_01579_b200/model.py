@@ -409,8 +409,9 @@ def model_forward(model: FvsrnModel, p, d=None, t=None):
 def model_backward(model: FvsrnModel, ctx: ModelForwardContext, raw_bar, grads=None):
     """Accumulate the gradients of sum(raw_bar * raw) into a GradientBuffer
     (model.py:302-335): one CUDA kernel recomputes the forward with its caches, runs the
-    MLP backward and scatter-adds the latent-grid adjoint (both bracketing keyframe grids
-    for temporal models, weights 1-w / w); the weight and bias reductions are GEMMs."""
+    MLP backward and adds the latent-grid adjoint into the gradient grids with the
+    deterministic scatter (both bracketing keyframe grids for temporal models, weights
+    1-w / w); the weight and bias reductions run on the tensor cores (fvsrn_layer_grads)."""
     import ctypes as C
 
     import torch
@@ -441,15 +442,20 @@ def model_backward(model: FvsrnModel, ctx: ModelForwardContext, raw_bar, grads=N
     L.check(L.lib().fvsrn_model_grads(C.byref(nd.desc), ptr(nd.params), ptr(pd), ptr(dd), ptr(td),
                                       ptr(rbd), n, C.c_void_p(ggrad.data_ptr() if gsizes else None),
                                       ptr(inputs), ptr(preacts), ptr(deltas), C.c_void_p(stream)))
-    gw, gb = [], []
-    io = do = 0
-    for l in range(L_):
-        x = inputs[io:io + n * w_in[l]].view(n, w_in[l])
-        dl = deltas[do:do + n * w_out[l]].view(n, w_out[l])
-        gw.append((dl.t() @ x).cpu().numpy())                 # nn.py:252
-        gb.append(dl.sum(dim=0).cpu().numpy())                # nn.py:253
-        io += n * w_in[l]
-        do += n * w_out[l]
+    # nn.py:252-253 on the tensor cores (fvsrn_layer_grads), in the parameter layout
+    nw = sum(int(w.size) for w in model.params.weights)
+    flat = torch.zeros(nw + sum(int(b.size) for b in model.params.biases), dtype=torch.float32,
+                       device=dev)
+    L.check(L.lib().fvsrn_layer_grads(C.byref(nd.desc), ptr(inputs), ptr(deltas), n, n, ptr(flat), 0,
+                                      C.c_void_p(stream)))
+    host_wb = flat.cpu().numpy()
+    gw, gb, o = [], [], 0
+    for w in model.params.weights:
+        gw.append(host_wb[o:o + w.size].reshape(w.shape).copy())
+        o += w.size
+    for b in model.params.biases:
+        gb.append(host_wb[o:o + b.size].copy())
+        o += b.size
     gg, off = [], 0
     host = ggrad.cpu().numpy()
     for g, sz in zip(model.grids, gsizes):

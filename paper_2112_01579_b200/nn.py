@@ -206,9 +206,11 @@ def _mlp_run(params: MlpParams, x: np.ndarray, y_bar=None):
     yb = (None if y_bar is None else
           torch.as_tensor(np.ascontiguousarray(y_bar, dtype=np.float32), device=dev))
     ptr = lambda a: C.c_void_p(a.data_ptr() if a is not None else None)  # noqa: E731
+    xb = torch.empty((max(n, 1), d_in), dtype=torch.float32, device=dev) if y_bar is not None else None
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     L.check(L.lib().fvsrn_mlp_forward_backward(
         C.byref(nd.desc), ptr(nd.params), ptr(xd), ptr(yb), n, ptr(yd), ptr(inputs), ptr(preacts),
-        ptr(deltas), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        ptr(deltas), ptr(xb), stream))
     y = yd[:n].cpu().numpy()
     ins, pre = [], []
     io = 0
@@ -218,19 +220,21 @@ def _mlp_run(params: MlpParams, x: np.ndarray, y_bar=None):
         pre.append(preacts[l * n * H:(l + 1) * n * H].view(n, H).cpu().numpy() if l < Lc - 1 else y.copy())
     if y_bar is None:
         return y, MlpCache(inputs=ins, preacts=pre), None, None
-    gw, gb = [], []
-    io = do = 0
-    x_bar = None
-    for l in range(Lc):
-        xi = inputs[io:io + n * w_in[l]].view(n, w_in[l])
-        dl = deltas[do:do + n * w_out[l]].view(n, w_out[l])
-        gw.append((dl.t() @ xi).cpu().numpy())
-        gb.append(dl.sum(dim=0).cpu().numpy())
-        if l == 0:
-            x_bar = (dl @ torch.as_tensor(np.ascontiguousarray(params.weights[0], dtype=np.float32),
-                                          device=dev)).cpu().numpy()
-        io += n * w_in[l]
-        do += n * w_out[l]
+    # nn.py:252-254: weight / bias gradients on the tensor cores (fvsrn_layer_grads), the
+    # input adjoint delta_0 @ W_0 per row from the backward kernel
+    nw = sum(int(w.size) for w in params.weights)
+    flat = torch.zeros(nw + sum(int(b.size) for b in params.biases), dtype=torch.float32, device=dev)
+    L.check(L.lib().fvsrn_layer_grads(C.byref(nd.desc), ptr(inputs), ptr(deltas), n, n, ptr(flat), 0,
+                                      stream))
+    host = flat.cpu().numpy()
+    gw, gb, o = [], [], 0
+    for w in params.weights:
+        gw.append(host[o:o + w.size].reshape(w.shape).copy())
+        o += w.size
+    for b in params.biases:
+        gb.append(host[o:o + b.size].copy())
+        o += b.size
+    x_bar = xb[:n].cpu().numpy()
     return y, MlpCache(inputs=ins, preacts=pre), gw, (gb, x_bar)
 
 

