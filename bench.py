@@ -178,30 +178,39 @@ CPU_SINGLE_STRIDE = {"cfg1": 4, "cfg2": 64, "cfg3": 256, "cfg5": 512, "cfg4": 32
 CPU_DECODE_ARM_STRIDE = 16          # reference arm, cfg 4: x slabs [::16] per step
 
 
-def ref_threads(cores: int, kind: str = "dvr") -> tuple[int, int]:
-    """(render_image `threads`, NUMBA_NUM_THREADS) for the reference on `cores` cores.
-    Measured on 8 cores for the cfg-2 row sample (oracle/ref_runner.py): threads=8 with
-    single-threaded numba kernels 4.11 M evals/s, threads=8 x numba 8 2.78 M/s
-    (oversubscribed), threads=1 x numba 8 0.71 M/s (small wavefronts) -- so the
-    reference's best is one render thread per core over single-threaded numba kernels.
-    decode_volume has no thread pool (model.py:392-398): its parallelism is numba's, so
-    decode uses NUMBA_NUM_THREADS = cores.  FVSRN_REF_THREADS / FVSRN_REF_NUMBA override."""
-    if kind == "decode":
-        return 1, int(os.environ.get("FVSRN_REF_NUMBA", cores))
-    return (int(os.environ.get("FVSRN_REF_THREADS", cores)),
-            int(os.environ.get("FVSRN_REF_NUMBA", 1)))
+# (render_image threads, NUMBA_NUM_THREADS, BLAS threads) for the reference on this box's
+# cores, per config: the fastest of the candidates measured with oracle/ref_runner.py
+# (tools/ref_sweep.sh, profiles/r2/ref_sweep.txt).  The reference's numpy glue holds the
+# GIL and its naive 6x64 path calls threaded BLAS, so more threads is not always faster.
+REF_BEST = {"cfg1": ("cores", 1, 1), "cfg2": ("cores", 1, 1), "cfg3": (1, 1, "cores"),
+            "cfg5": ("cores", 1, 1), "cfg4": (1, "cores", "cores")}
 
 
-def cpu_leg(config: str, cores: int, row_stride: int, view: int = 0, single: bool = False,
+def ref_threads(cores: int, config: str = "cfg2") -> tuple[int, int, int]:
+    """(render_image `threads`, NUMBA_NUM_THREADS, BLAS threads) for the reference;
+    FVSRN_REF_THREADS / FVSRN_REF_NUMBA / FVSRN_REF_BLAS override."""
+    best = [cores if v == "cores" else v for v in REF_BEST.get(config, ("cores", 1, 1))]
+    return (int(os.environ.get("FVSRN_REF_THREADS", best[0])),
+            int(os.environ.get("FVSRN_REF_NUMBA", best[1])),
+            int(os.environ.get("FVSRN_REF_BLAS", best[2])))
+
+
+def _ref_env(threads_numba_blas) -> dict:
+    _, numba, blas = threads_numba_blas
+    return {"NUMBA_NUM_THREADS": str(numba), "OMP_NUM_THREADS": str(blas),
+            "OPENBLAS_NUM_THREADS": str(blas), "MKL_NUM_THREADS": str(blas)}
+
+
+def cpu_leg(config: str, cores: int, row_stride: int, step: int = 0, single: bool = False,
             timeout: float = 240.0):
-    """oracle/ref_runner.py in a subprocess (its own NUMBA_NUM_THREADS; `taskset -c 0`
-    for the single-core run); returns its JSON result or {"error": ...}."""
+    """oracle/ref_runner.py in a subprocess (its own thread settings; `taskset -c 0` for the
+    single-core run); returns its JSON result or {"error": ...}."""
     import subprocess
 
-    threads, numba = (1, 1) if single else ref_threads(cores, CONFIGS[config]["kind"])
-    env = dict(os.environ, NUMBA_NUM_THREADS=str(numba), PYTHONDONTWRITEBYTECODE="1")
+    tnb = (1, 1, 1) if single else ref_threads(cores, config)
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", **_ref_env(tnb))
     cmd = [sys.executable, "-m", "oracle.ref_runner", "--config", config,
-           "--threads", str(threads), "--view", str(view)]
+           "--threads", str(tnb[0]), "--step", str(step)]
     cmd += ["--full"] if row_stride == 1 else ["--row-stride", str(row_stride)]
     if single:
         cmd = ["taskset", "-c", "0"] + cmd
@@ -221,11 +230,10 @@ def cpu_baseline(config: str):
     if "error" in allc:
         return {"value": None, "unit": "evals/s", "cores": cores, "kind": "unavailable",
                 "sample": allc["error"]}
+    tnb = ref_threads(cores, config)
     out = {"value": allc["value"], "unit": "evals/s", "cores": cores, "kind": allc["kind"],
-           "sample": allc["sample"] + (f", render_image threads={allc['threads']}, "
-                                       f"NUMBA_NUM_THREADS={ref_threads(cores)[1]}"
-                                       if kind == "dvr" else
-                                       f", NUMBA_NUM_THREADS={ref_threads(cores, kind)[1]}"),
+           "sample": allc["sample"] + f", render_image threads={tnb[0]}, NUMBA_NUM_THREADS="
+                                      f"{tnb[1]}, BLAS threads={tnb[2]}",
            "seconds": allc["seconds"], "cpu_model": allc.get("cpu_model"),
            "single_core": ({"value": one["value"], "cores": 1, "sample": one["sample"] +
                             ", taskset -c 0, NUMBA_NUM_THREADS=1", "seconds": one["seconds"]}
@@ -243,29 +251,27 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    threads, numba = ref_threads(cores, CONFIGS[args.config]["kind"])
-    os.environ["NUMBA_NUM_THREADS"] = str(numba)       # before numba is imported
+    tnb = ref_threads(cores, args.config)
+    os.environ.update(_ref_env(tnb))                     # before numba / numpy's BLAS start
     from oracle.ref_runner import Runner, cpu_model
 
     cfg = CONFIGS[args.config]
-    runner = Runner(args.config, threads)
+    runner = Runner(args.config, tnb[0])
     runner.warm()
     if cfg["kind"] == "dvr":
         stride = CPU_ROW_STRIDE[args.config]
-        rows = np.arange(0, cfg["res"], stride)
-        step = lambda i: runner.render_rows(i % 8, rows)          # noqa: E731
-        sample = (f"{args.config}: every {stride}th row ({len(rows)} of {cfg['res']}) of view "
-                  f"(step mod 8), render_image threads={runner.threads}, NUMBA_NUM_THREADS={numba}")
+        step = lambda i: runner.render_step(i, stride)             # noqa: E731
+        sample = (f"{args.config}: " + (f"whole frame of view (step mod 8)" if stride == 1 else
+                  f"every {8 * stride}th row of all 8 views, offset by the step ({cfg['res'] // stride} "
+                  f"rows per step)") + f", render_image threads={tnb[0]}, NUMBA_NUM_THREADS={tnb[1]}, "
+                  f"BLAS threads={tnb[2]}")
     else:
         stride = CPU_DECODE_ARM_STRIDE
         step = lambda i: runner.decode(stride)                   # noqa: E731
         sample = (f"{args.config}: decode_volume's chunked eval_density over lattice x slabs "
-                  f"[::{stride}], NUMBA_NUM_THREADS={numba}")
+                  f"[::{stride}], NUMBA_NUM_THREADS={tnb[1]}")
     for i in range(args.warmup):
-        if cfg["kind"] == "dvr":
-            runner.render_rows(i % 8, rows[len(rows) // 2: len(rows) // 2 + 1])
-        else:
-            runner.decode(cfg["res"] // 2)
+        runner.warm()
     tot_n = tot_t = 0.0
     for i in range(args.steps):
         n, dt = step(i)
@@ -549,18 +555,21 @@ def main():
                 h2d = 4356 + 4 * 32
                 d2h = res * res * 16 if rank == 0 else 0
         else:
-            vol = P.decode_volume(model, res, t=t_frame)
+            # the stock call: a fresh ScalarVolume per call (page-locked, recycled by the
+            # library once the previous volume is dropped; two warm-up calls populate it)
+            vol = None
+            for i in range(2):
+                vol = P.decode_volume(model, res, t=t_frame)
             t0 = time.perf_counter()
-            for i in range(max(2, args.steps // 4)):
+            for i in range(args.steps):
                 vol = P.decode_volume(model, res, t=t_frame)
             dt = time.perf_counter() - t0
             del vol
-            n_e = max(2, args.steps // 4) * res ** 3
+            n_e = args.steps * res ** 3
             h2d, d2h = 4 * 32, res ** 3 * 4
         e2e = {"value": n_e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                **({"clocks": e2e_clocks.summary()} if cfg["kind"] == "dvr" and world == 1 else {}),
-               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * dt / args.steps
-               if cfg["kind"] == "dvr" else 1e3 * dt / max(2, args.steps // 4),
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * dt / args.steps,
                "api": ("render_image(ModelSource(model, tf), cam, settings) -> fvsrn_render: host "
                        "frame returned per call; the kernels store each pixel into it over PCIe "
                        "(page-locked, recycled)" if world == 1 else

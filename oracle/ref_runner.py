@@ -18,7 +18,7 @@ runs instead and the result says ``kind: "port"``.
 Only bench.py calls this module (in-process for the reference arm, as a subprocess
 under ``taskset`` for the single-core figure).  The product package never imports it.
 
-    python -m oracle.ref_runner --config cfg2 --threads 1 --row-stride 64 --view 0
+    python -m oracle.ref_runner --config cfg2 --threads 1 --row-stride 64 --step 0
 """
 
 from __future__ import annotations
@@ -174,6 +174,21 @@ class Runner:
             eval_density(self.model, pts[lo:lo + (1 << 16)])
         return len(pts), time.perf_counter() - t0
 
+    def render_step(self, step: int, stride: int):
+        """One bench step of a DVR config: every (8 * stride)-th row of ALL 8 views, the rows
+        offset by the step index (so consecutive steps cover different rows and every step
+        samples the same view mix); stride 1 = the whole frame of view (step mod 8)."""
+        res = self.cfg["res"]
+        if stride == 1:
+            return self.render_rows(step % 8, np.arange(res))
+        s = 8 * stride
+        n = t = 0.0
+        for v in range(8):
+            dn, dt = self.render_rows(v, np.arange(step % s, res, s))
+            n += dn
+            t += dt
+        return n, t
+
     def warm(self):
         """JIT / first-call warm-up on a tiny sample (untimed)."""
         if self.cfg["kind"] == "dvr":
@@ -187,16 +202,17 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--threads", type=int, default=1)
     ap.add_argument("--row-stride", type=int, default=8)
-    ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--full", action="store_true", help="the whole frame / lattice")
+    ap.add_argument("--step", type=int, default=0, help="bench step index (render_step)")
     args = ap.parse_args()
     r = Runner(args.config, args.threads)
     r.warm()
     if r.cfg["kind"] == "dvr":
         stride = 1 if args.full else args.row_stride
-        rows = np.arange(0, r.cfg["res"], stride)
-        n, dt = r.render_rows(args.view, rows)
-        sample = f"view {args.view}, every {stride}th row ({len(rows)} of {r.cfg['res']} rows)"
+        n, dt = r.render_step(args.step, stride)
+        sample = (f"whole frame of view {args.step % 8}" if stride == 1 else
+                  f"every {8 * stride}th row of all 8 views (offset {args.step % (8 * stride)}; "
+                  f"{r.cfg['res'] // stride} rows)")
     else:
         stride = 1 if args.full else args.row_stride
         n, dt = r.decode(stride)

@@ -1,17 +1,24 @@
 #!/bin/bash
-# One GPU-box pass: parity tests, bench lines for every config, the ncu launch list of
-# the default bench command, and full ncu captures of the dominant kernels.
+# One GPU-box pass: bench lines for every config (with CPU baselines of the reference,
+# benchmark.csv + manifest), the reference arm, a 2-rank one-GPU bench line (multi-rank
+# code path), the ncu launch list of the default bench command and full ncu captures of
+# the dominant kernels (raw + source pages).
 # usage: bash tools/gpu_round.sh <outdir>   (outdir under gpurun_out/)
 out=${1:-gpurun_out/round}
 mkdir -p $out
-timeout 600 python -m pytest tests -m gpu -q > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $out/pytest_gpu.log
-for c in cfg1 cfg2 cfg3 cfg4 cfg5; do
-  timeout 300 python bench.py --config $c --no-cpu-baseline --steps 16 2>&1 | tail -1 > $out/bench_$c.json
-  python -c "import json; d=json.load(open('$out/bench_$c.json')); print('$c', round(d['ms_per_step'],3), 'ms', round(d['value']/1e9,2), 'Gev/s', 'e2e', round(d.get('e2e',{}).get('value',0)/1e9,2), 'frac', round(d['roofline']['frac'],4), 'xu', round(d['roofline']['xu_pipe']['frac'],3), 'launches', d['gpu_launches'])" || cat $out/bench_$c.json
+for c in cfg1 cfg3 cfg4 cfg5 cfg2; do
+  timeout 900 python bench.py --config $c --steps 16 --csv $out/benchmark.csv 2> $out/bench_$c.err | tail -1 > $out/bench_$c.json
+  python -c "import json; d=json.load(open('$out/bench_$c.json')); print('$c', round(d['ms_per_step'],3), 'ms', round(d['value']/1e9,2), 'Gev/s', 'e2e', round(d.get('e2e',{}).get('value',0)/1e9,2), round(d.get('e2e',{}).get('ms_per_step',0),3), 'ms frac', round(d['roofline']['frac'],4), 'xu', round(d['roofline']['xu_pipe']['frac'],3), 'cpu', d.get('cpu_baseline',{}).get('value'), d.get('cpu_baseline',{}).get('kind'))" || tail -3 $out/bench_$c.err
 done
-timeout 600 python bench.py > $out/bench_default.json 2> $out/bench_default.err; tail -c 600 $out/bench_default.json
+timeout 600 python bench.py > $out/bench_default.json 2> $out/bench_default.err; tail -c 300 $out/bench_default.json; echo
+timeout 900 python bench.py --impl reference --steps 4 --warmup 3 > $out/bench_reference.json 2> $out/bench_reference.err; tail -c 400 $out/bench_reference.json; echo
+FVSRN_BENCH_ONE_GPU=1 timeout 600 python bench.py --gpus 2 --steps 8 --check-frame --no-cpu-baseline > $out/bench_2ranks_onegpu.json 2> $out/bench_2ranks.err; tail -c 300 $out/bench_2ranks_onegpu.json; echo
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 400 ncu --set full --import-source on --clock-control none -k regex:dvr_kernel -s 3 -c 1 --export $out/ncu_dvr_cfg2 -f python bench.py --config cfg2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:dvr_tc_kernel -s 3 -c 1 --export $out/ncu_tc_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:sample_kernel -s 3 -c 1 --export $out/ncu_decode_cfg4 -f python bench.py --config cfg4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+for r in ncu_tc_cfg3 ncu_decode_cfg4; do
+  ncu -i $out/$r.ncu-rep --page raw --csv > $out/${r}_raw.csv 2>/dev/null
+  ncu -i $out/$r.ncu-rep --page source --csv --print-source sass > $out/${r}_src.csv 2>/dev/null
+  rm -f $out/$r.ncu-rep
+done
 ls $out
