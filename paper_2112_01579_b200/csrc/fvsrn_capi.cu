@@ -646,6 +646,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
     case KernelKind::kDVRPipe: k = "dvr_pipe_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
+    case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + ",1> (mma.sync m16n8k16, static-texture features)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -697,7 +698,8 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
-  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRPipe || kind == KernelKind::kDVRTC ||
+  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPipe ||
+      kind == KernelKind::kDVRTC ||
       kind == KernelKind::kDVRDual) {
     // Small frames: the frame time is the longest rays' sequential march, and every
     // co-resident warp slows each step of it.  Keep ~1.75 work slots per lane (measured
@@ -765,7 +767,10 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
     return launch(m, KernelKind::kDVRDual, dual_smem_bytes(net, m->k0), args, s, n_slots / 64 + 1);
   if (dvr_mode() == DvrMode::kPipe && fast_path(m, KernelKind::kDVR))
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
-  return launch(m, KernelKind::kDVR, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
+  // static fp16 texture grid on the default shapes: the branch-free feature path
+  const KernelKind k = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kDVR) && fd.tex_on && !fd.tex_u8 &&
+                        fd.tex_w == 0.f) ? KernelKind::kDVRTex : KernelKind::kDVR;
+  return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
 }
 
 MarchDev march_for(const fvsrn_settings* st) {

@@ -665,6 +665,17 @@ struct FastRow {
     for (int j = 0; j < 4; ++j) v[j] = tex3D<float4>(fd.tex_lo[j], tx, ty, tz);
   }
 
+  // the whole row from a static fp16 texture grid (no u8 codes, no keyframe blend), with
+  // 16-byte stores: the branch-free feature path of the kDVRTex kernel
+  __device__ static void build_tex(const FeatDev& fd, float px, float py, float pz, __half* row) {
+    uint32_t z[8], w[kWords];
+    tex_words(fd, px, py, pz, z);
+    words_from_z(z, px, py, pz, w);
+    uint4* dst = reinterpret_cast<uint4*>(row);
+#pragma unroll
+    for (int j = 0; j < kWords / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+
   // the 16 latent channels of tex_fetch as 8 packed fp16 pairs
   __device__ static void tex_words(const FeatDev& fd, float px, float py, float pz, uint32_t (&z)[8]) {
     float4 v[4];

@@ -77,7 +77,7 @@ __host__ __device__ constexpr int fast_kt0() {
 // NM > 0 / NL > 0: specialised input row (FastRow<NM>) and compile-time layer count.
 // Persistent warps, 32 rays per warp; free lanes refill from a chunked global queue of
 // precomputed ray records (ray_setup_kernel), so the MMA tiles stay full.
-template <int HID, int ACT, int NM, int NL>
+template <int HID, int ACT, int NM, int NL, int TEX = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID>())
 dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
            MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
@@ -106,8 +106,12 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
     // ---- sample position p_k = pe + k * dd (render.py:224-225) and input row
     if (r.has) {
       const float kf = (float)r.k;
-      assemble_row_t<NM>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
-                         use_dir ? r.dx : 0.f, use_dir ? r.dy : 0.f, use_dir ? r.dz : 0.f, myrow);
+      if constexpr (TEX == 1 && NM > 0)
+        FastRow<NM>::build_tex(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
+                               myrow);
+      else
+        assemble_row_t<NM>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
+                           use_dir ? r.dx : 0.f, use_dir ? r.dy : 0.f, use_dir ? r.dz : 0.f, myrow);
     }
     __syncwarp();
     MLP::eval32(stage, rs, net, wf_s, b_s, ob, lane, hb);
@@ -783,6 +787,8 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
     if (kind == KernelKind::kDVR)                                                            \
       return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H)>               \
                   : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
+    if (kind == KernelKind::kDVRTex)                                                         \
+      return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1> : nullptr; \
     FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \

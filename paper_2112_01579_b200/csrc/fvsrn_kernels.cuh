@@ -16,6 +16,9 @@ constexpr int kThreads = FVSRN_THREADS;  // 4 independent warps per CTA; weights
 // DVR 5 (<= 102 regs, 20 warps/SM), decode/eval 4 (<= 128 regs).
 // measured-slower DVR variants (warp-specialised, software-pipelined, two rays per lane,
 // two-tile tcgen05): compiled only for A/B builds (make variant VDEFS=-DFVSRN_AB_VARIANTS=1)
+#ifndef FVSRN_TEX_SPECIAL
+#define FVSRN_TEX_SPECIAL 1
+#endif
 #ifndef FVSRN_AB_VARIANTS
 #define FVSRN_AB_VARIANTS 0
 #endif
@@ -93,7 +96,9 @@ struct RayRecs {
   float4* d;
 };
 
-enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused };
+// kDVRTex: dvr_kernel specialised for the default fast path with a static fp16 texture grid
+// (no u8 codes, no per-sample keyframe blend): the feature code has no runtime branches
+enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused, kDVRTex };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).
