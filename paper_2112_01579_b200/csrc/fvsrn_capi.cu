@@ -638,15 +638,17 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
   std::string k;
   switch (kind) {
     case KernelKind::kDVRTC:
+    case KernelKind::kDVRTCTex:
       k = std::string(g_tc_two_tiles ? "dvr_tc2_kernel<" : "dvr_tc_kernel<") + std::to_string(h) + "," +
           std::to_string((h - 4) / 2) + "," + std::to_string(m->layers) +
-          "> (tcgen05.mma kind::f16, TMEM accumulators)";
+          (kind == KernelKind::kDVRTCTex ? ",1" : "") + "> (tcgen05.mma kind::f16, TMEM accumulators)";
       break;
+    case KernelKind::kSampleTex: k = "sample_kernel<" + tmpl + ",1> (mma.sync m16n8k16, static-texture features)"; break;
     case KernelKind::kDVRWS: k = "dvr_ws_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRPipe: k = "dvr_pipe_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
-    case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + ",1> (mma.sync m16n8k16, static-texture features)"; break;
+    case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + ",1> (mma.sync m16n8k16, frame specialisation)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -658,10 +660,11 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps) {
+  const bool tc = kind == KernelKind::kDVRTC || kind == KernelKind::kDVRTCTex;
   const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
-                                               : kernel_for(kind, m->hid_pad, fast_path(m, kind));
-  const int threads = kind == KernelKind::kDVRWS ? kWsThreads
-                      : kind == KernelKind::kDVRTC ? kTcThreads : kThreads;
+                   : kind == KernelKind::kDVRTCTex ? tc_tex_kernel_for(m->hid_pad)
+                                                    : kernel_for(kind, m->hid_pad, fast_path(m, kind));
+  const int threads = kind == KernelKind::kDVRWS ? kWsThreads : tc ? kTcThreads : kThreads;
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
   int occ = 0;
   {
@@ -675,7 +678,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
         attr = smem;
       }
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
-      if (kind == KernelKind::kDVRTC) {
+      if (tc) {
         // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; the real
         // limits are registers (launch bounds), shared memory and TMEM columns (each
         // CTA allocates <= 64 of 512), so size the persistent grid from those.
@@ -699,7 +702,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
   if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPipe ||
-      kind == KernelKind::kDVRTC ||
+      tc ||
       kind == KernelKind::kDVRDual) {
     // Small frames: the frame time is the longest rays' sequential march, and every
     // co-resident warp slows each step of it.  Keep ~1.75 work slots per lane (measured
@@ -754,10 +757,12 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
                long long& n_slots, float*& d_out, unsigned long long*& queue,
                unsigned long long*& evc, unsigned long long*& nfc, cudaStream_t s) {
   if (n_slots <= 0) return FVSRN_OK;
+  const bool static_tex = FVSRN_TEX_SPECIAL && fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
     void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    return launch(m, KernelKind::kDVRTC, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
+    const KernelKind k = (static_tex && !g_tc_two_tiles) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
+    return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
                   g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1);
   }
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
@@ -768,8 +773,9 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   if (dvr_mode() == DvrMode::kPipe && fast_path(m, KernelKind::kDVR))
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   // static fp16 texture grid on the default shapes: the branch-free feature path
-  const KernelKind k = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kDVR) && fd.tex_on && !fd.tex_u8 &&
-                        fd.tex_w == 0.f) ? KernelKind::kDVRTex : KernelKind::kDVR;
+  // of a density-head model rendering a camera frame (no explicit rays)
+  const KernelKind k = (static_tex && fast_path(m, KernelKind::kDVR) && m->head == FVSRN_HEAD_DENSITY &&
+                        !explicit_rays) ? KernelKind::kDVRTex : KernelKind::kDVR;
   return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
 }
 
@@ -1810,9 +1816,12 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
   CUDA_TRY(cudaMallocAsync((void**)&coords, hc.size() * sizeof(float), s));
   CUDA_TRY(cudaMemcpyAsync(coords, hc.data(), hc.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   const size_t smem = stage_smem_bytes(net, false, m->k0);
+  // static fp16 texture grid on the default shapes: the branch-free feature path
+  const KernelKind sk = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kSample) && fd.tex_on && !fd.tex_u8 &&
+                         fd.tex_w == 0.f) ? KernelKind::kSampleTex : KernelKind::kSample;
   if (chunks <= 1 || !h_out) {
     void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad, &coords};
-    if ((rc = launch(m, KernelKind::kSample, smem, args, s, count / 32 + 1))) return rc;
+    if ((rc = launch(m, sk, smem, args, s, count / 32 + 1))) return rc;
   } else {
     // chunk c: decode [c0, c0 + n) into d_out + c0 on s, then copy it to h_out on copy_s
     const long long per = ((lattice_count + chunks - 1) / chunks + 31) / 32 * 32;
@@ -1820,7 +1829,7 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
       long long cb = lattice_begin + c0, cn = std::min(per, lattice_count - c0);
       float* dst = d_out + c0;
       void* args[] = {&net, &fd, &b0, &mode, &res, &step, &cb, &cn, &pp, &pd, &dst, &d_bad, &coords};
-      if ((rc = launch(m, KernelKind::kSample, smem, args, s, cn / 32 + 1))) return rc;
+      if ((rc = launch(m, sk, smem, args, s, cn / 32 + 1))) return rc;
       cudaEvent_t done;
       CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(done, s));

@@ -98,8 +98,17 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   typename MLP::HB hb;
   hb.load(wf_s, net, lane);
 
+  // TEX == 1: a camera frame (no explicit rays, no direction inputs) of a density-head
+  // model: those flags are compile-time, so the refill and compositing lose their branches
+  constexpr bool kFrame = TEX == 1;
   while (true) {
-    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
+    if constexpr (kFrame) {
+      RayRecs rr_pos = rr;
+      rr_pos.d = nullptr;
+      ws_refill(r, q, lane, cam, sh, false, rr_pos, n_slots, queue, md, out);
+    } else {
+      ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
+    }
     const unsigned act = __ballot_sync(0xffffffffu, r.has);
     if (act == 0) break;
     evals += __popc(act);
@@ -118,7 +127,8 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
     __syncwarp();
     // ---- head, TF, compositing, early termination (render.py:109-117, 226-232)
     if (r.has)
-      composite_step(r, *reinterpret_cast<const float4*>(ob + 4 * lane), density, *tf, md, out, nonfinite);
+      composite_step(r, *reinterpret_cast<const float4*>(ob + 4 * lane), kFrame || density, *tf, md, out,
+                     nonfinite);
   }
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
@@ -572,7 +582,7 @@ cudaError_t launch_tile_order(const CamDev& cam, const MarchDev& md, const Shard
 
 // ---------------------------------------------------------------- decode / eval
 // mode 0: lattice decode (model.py:385-398); mode 1: positions (+dirs) from memory
-template <int HID, int ACT, int NM, int NL>
+template <int HID, int ACT, int NM, int NL, int TEX = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID, false>())
 sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, int res, double step,
               long long begin, long long count, const double* __restrict__ pos,
@@ -609,7 +619,8 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
         px = (float)pos[3 * i]; py = (float)pos[3 * i + 1]; pz = (float)pos[3 * i + 2];
         if (dirs) { dx = (float)dirs[3 * i]; dy = (float)dirs[3 * i + 1]; dz = (float)dirs[3 * i + 2]; }
       }
-      assemble_row_t<NM>(fd, px, py, pz, dx, dy, dz, myrow);
+      if constexpr (TEX == 1 && NM > 0) FastRow<NM>::build_tex(fd, px, py, pz, myrow);
+      else assemble_row_t<NM>(fd, px, py, pz, dx, dy, dz, myrow);
     }
     __syncwarp();
     MLPDispatch<HID, ACT, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
@@ -793,6 +804,8 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
                   : (const void*)sample_kernel<H, kActRuntime, 0, 0>;                        \
+    if (kind == KernelKind::kSampleTex)                                                      \
+      return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1> : nullptr; \
     return fast ? (const void*)fused_eval_kernel<H, 4> : (const void*)fused_eval_kernel<H, kActRuntime>;
     FVSRN_FOR_HIDDEN(CASE)
 #undef CASE

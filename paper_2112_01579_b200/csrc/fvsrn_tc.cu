@@ -154,7 +154,7 @@ __device__ __forceinline__ void tmem_st_any(uint32_t taddr, const uint32_t (&r)[
 
 }  // namespace
 
-template <int HID, int NM, int NL>
+template <int HID, int NM, int NL, int TEX = 0>
 __global__ void __launch_bounds__(kTcThreads, tc_min_blocks<HID>())
 dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
               MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
@@ -224,8 +224,15 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       if (r.has) {
         const float kf = (float)r.k;
         const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
-        if (prefetch && pre_k == r.k) FastRow<NM>::words_from_z(pre, px, py, pz, w);
-        else FastRow<NM>::words(fd, px, py, pz, w);
+        if (prefetch && pre_k == r.k) {
+          FastRow<NM>::words_from_z(pre, px, py, pz, w);
+        } else if constexpr (TEX == 1) {   // static fp16 texture grid: no runtime branches
+          uint32_t z[8];
+          FastRow<NM>::tex_words(fd, px, py, pz, z);
+          FastRow<NM>::words_from_z(z, px, py, pz, w);
+        } else {
+          FastRow<NM>::words(fd, px, py, pz, w);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
@@ -512,6 +519,14 @@ const void* tc_kernel_for(int hid, bool two_tiles) {
     case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;
     case 64: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<64, 30, 6>;
 #endif
+    default: return nullptr;
+  }
+}
+
+const void* tc_tex_kernel_for(int hid) {
+  switch (hid) {
+    case 32: return (const void*)dvr_tc_kernel<32, 14, 4, 1>;
+    case 64: return (const void*)dvr_tc_kernel<64, 30, 6, 1>;
     default: return nullptr;
   }
 }

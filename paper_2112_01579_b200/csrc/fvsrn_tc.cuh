@@ -76,6 +76,8 @@ struct TcShape {
 // 6 layers, m=30), or nullptr.  Same argument list as dvr_kernel with TcNetDev first.
 // two_tiles: the ping-pong variant (256 rays per CTA).
 const void* tc_kernel_for(int hid, bool two_tiles);
+// the single-tile kernel specialised for a static fp16 texture grid (branch-free features)
+const void* tc_tex_kernel_for(int hid);
 size_t tc_smem_bytes(int hid, bool two_tiles);
 inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
 
