@@ -173,23 +173,36 @@ def ncu_traffic(config: str):
 # Bounded sample of one frame per config: every k-th row of a view (rays are independent,
 # so the rows cost what they cost inside the full frame); cfg 1 and the cfg 4 decode are
 # timed whole.  The reference arm and the all-core cpu_baseline use the same sample.
-CPU_ROW_STRIDE = {"cfg1": 1, "cfg2": 4, "cfg3": 64, "cfg5": 128}
-CPU_SINGLE_STRIDE = {"cfg1": 4, "cfg2": 64, "cfg3": 256, "cfg5": 512, "cfg4": 32}
+CPU_ROW_STRIDE = {"cfg1": 1, "cfg2": 2, "cfg3": 64, "cfg5": 64}
+CPU_SINGLE_STRIDE = {"cfg1": 4, "cfg2": 32, "cfg3": 256, "cfg5": 512, "cfg4": 32}
+
+
+def host_cores() -> int:
+    """Cores this process may run on (the affinity mask, not the machine's CPU count)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
 CPU_DECODE_ARM_STRIDE = 16          # reference arm, cfg 4: x slabs [::16] per step
 
 
 # (render_image threads, NUMBA_NUM_THREADS, BLAS threads) for the reference on this box's
-# cores, per config: the fastest of the candidates measured with oracle/ref_runner.py
-# (tools/ref_sweep.sh, profiles/r2/ref_sweep.txt).  The reference's numpy glue holds the
-# GIL and its naive 6x64 path calls threaded BLAS, so more threads is not always faster.
-REF_BEST = {"cfg1": ("cores", 1, 1), "cfg2": ("cores", 1, 1), "cfg3": (1, 1, "cores"),
-            "cfg5": ("cores", 1, 1), "cfg4": (1, "cores", "cores")}
+# c cores, per config: the fastest of the candidates measured on the bench's own samples
+# (tools/ref_sweep.sh, profiles/r2/ref_sweep.txt; 16 cores: cfg 2 at threads 8 x numba 2
+# 11.2 M evals/s vs 8.8 (16 x 1), 6.0 (4 x 4), 1.5 (1 x 16)).  The reference's numpy glue
+# holds the GIL and its naive 6x64 path calls threaded BLAS, so neither extreme wins.
+REF_BEST = {"cfg1": ("c/4", 4, 4), "cfg2": ("c/2", 2, 2), "cfg3": (1, 1, "c"),
+            "cfg5": ("c/2", 2, 2), "cfg4": (1, 1, "c")}
 
 
 def ref_threads(cores: int, config: str = "cfg2") -> tuple[int, int, int]:
     """(render_image `threads`, NUMBA_NUM_THREADS, BLAS threads) for the reference;
     FVSRN_REF_THREADS / FVSRN_REF_NUMBA / FVSRN_REF_BLAS override."""
-    best = [cores if v == "cores" else v for v in REF_BEST.get(config, ("cores", 1, 1))]
+    def val(v):
+        if isinstance(v, str):
+            return max(1, cores // int(v[2:]) if "/" in v else cores)
+        return v
+    best = [val(v) for v in REF_BEST.get(config, ("c/2", 2, 2))]
     return (int(os.environ.get("FVSRN_REF_THREADS", best[0])),
             int(os.environ.get("FVSRN_REF_NUMBA", best[1])),
             int(os.environ.get("FVSRN_REF_BLAS", best[2])))
@@ -222,7 +235,7 @@ def cpu_leg(config: str, cores: int, row_stride: int, step: int = 0, single: boo
 
 
 def cpu_baseline(config: str):
-    cores = os.cpu_count() or 1
+    cores = host_cores()
     kind = CONFIGS[config]["kind"]
     allc = cpu_leg(config, cores, 1 if kind == "decode" else CPU_ROW_STRIDE[config],
                    timeout=420.0)
@@ -250,7 +263,7 @@ def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path on the host cores, rank 0 only."""
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
+    cores = host_cores()
     tnb = ref_threads(cores, args.config)
     os.environ.update(_ref_env(tnb))                     # before numba / numpy's BLAS start
     from oracle.ref_runner import Runner, cpu_model
@@ -262,9 +275,8 @@ def run_reference(args, rank, world):
         stride = CPU_ROW_STRIDE[args.config]
         step = lambda i: runner.render_step(i, stride)             # noqa: E731
         sample = (f"{args.config}: " + (f"whole frame of view (step mod 8)" if stride == 1 else
-                  f"every {8 * stride}th row of all 8 views, offset by the step ({cfg['res'] // stride} "
-                  f"rows per step)") + f", render_image threads={tnb[0]}, NUMBA_NUM_THREADS={tnb[1]}, "
-                  f"BLAS threads={tnb[2]}")
+                  f"every {stride}th row of view (step mod 8) ({cfg['res'] // stride} rows per step)")
+                  + f", render_image threads={tnb[0]}, NUMBA_NUM_THREADS={tnb[1]}, BLAS threads={tnb[2]}")
     else:
         stride = CPU_DECODE_ARM_STRIDE
         step = lambda i: runner.decode(stride)                   # noqa: E731

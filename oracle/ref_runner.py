@@ -175,19 +175,11 @@ class Runner:
         return len(pts), time.perf_counter() - t0
 
     def render_step(self, step: int, stride: int):
-        """One bench step of a DVR config: every (8 * stride)-th row of ALL 8 views, the rows
-        offset by the step index (so consecutive steps cover different rows and every step
-        samples the same view mix); stride 1 = the whole frame of view (step mod 8)."""
+        """One bench step of a DVR config: every stride-th row of view (step mod 8), offset by
+        step // 8 (stride 1 = the whole frame).  One view per call keeps the batches the
+        reference's thread pool sees close to a full frame's (render.py:320-331)."""
         res = self.cfg["res"]
-        if stride == 1:
-            return self.render_rows(step % 8, np.arange(res))
-        s = 8 * stride
-        n = t = 0.0
-        for v in range(8):
-            dn, dt = self.render_rows(v, np.arange(step % s, res, s))
-            n += dn
-            t += dt
-        return n, t
+        return self.render_rows(step % 8, np.arange((step // 8) % stride, res, stride))
 
     def warm(self):
         """JIT / first-call warm-up on a tiny sample (untimed)."""
@@ -211,8 +203,8 @@ def main():
         stride = 1 if args.full else args.row_stride
         n, dt = r.render_step(args.step, stride)
         sample = (f"whole frame of view {args.step % 8}" if stride == 1 else
-                  f"every {8 * stride}th row of all 8 views (offset {args.step % (8 * stride)}; "
-                  f"{r.cfg['res'] // stride} rows)")
+                  f"every {stride}th row of view {args.step % 8} ({r.cfg['res'] // stride} of "
+                  f"{r.cfg['res']} rows)")
     else:
         stride = 1 if args.full else args.row_stride
         n, dt = r.decode(stride)
@@ -220,7 +212,7 @@ def main():
                   else f"x slabs [::{stride}] of the lattice")
     print(json.dumps({"evals": n, "seconds": dt, "value": n / dt, "kind": r.kind,
                       "threads": r.threads, "sample": f"{args.config}: {sample}",
-                      "cpu_model": cpu_model(), "affinity": sorted(os.sched_getaffinity(0))[:8]}))
+                      "cpu_model": cpu_model(), "cores": len(os.sched_getaffinity(0))}))
 
 
 if __name__ == "__main__":

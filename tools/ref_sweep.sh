@@ -1,21 +1,21 @@
 #!/bin/bash
 # Thread settings of the reference's CPU path on this box (bench.py REF_BEST): one bench
-# step of each config through oracle/ref_runner.py per candidate
-# (render_image threads, NUMBA_NUM_THREADS, BLAS threads).
-C=$(nproc)
+# step of each config (the same row sample the bench uses) through oracle/ref_runner.py per
+# candidate (render_image threads, NUMBA_NUM_THREADS, BLAS threads).
+C=$(python -c 'import os; print(len(os.sched_getaffinity(0)))')
+H=$((C / 2)); Q=$((C / 4)); [ $Q -lt 1 ] && Q=1
+echo "cores $C, $(grep -m1 'model name' /proc/cpuinfo)"
 run() {  # config threads numba blas stride
   r=$(env NUMBA_NUM_THREADS=$3 OMP_NUM_THREADS=$4 OPENBLAS_NUM_THREADS=$4 MKL_NUM_THREADS=$4 \
-      timeout 300 python -m oracle.ref_runner --config $1 --threads $2 --row-stride $5 2>/dev/null | tail -1)
-  echo "$1 threads=$2 numba=$3 blas=$4: $(echo $r | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]/1e6,3), "M evals/s", d["kind"], d["sample"])' 2>/dev/null || echo failed)"
+      timeout 400 python -m oracle.ref_runner --config $1 --threads $2 $5 2>/dev/null | tail -1)
+  echo "$1 threads=$2 numba=$3 blas=$4: $(echo $r | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]/1e6,3), "M evals/s", round(d["seconds"],1), "s", d["sample"])' 2>/dev/null || echo failed)"
 }
-echo "cores $C, $(grep -m1 'model name' /proc/cpuinfo)"
-for cfg in "cfg1 8" "cfg2 16" "cfg5 256" "cfg3 128"; do
+for cfg in "cfg1 --full" "cfg2 --row-stride=2" "cfg5 --row-stride=64" "cfg3 --row-stride=64"; do
   set -- $cfg
-  for cand in "$C 1 1" "$C 1 $C" "1 $C $C" "4 4 4" "8 2 2" "1 1 $C"; do
+  for cand in "$C 1 1" "1 $C $C" "$H 2 2" "$Q 4 4" "1 1 $C"; do
     run $1 $cand $2
   done
 done
-for cand in "1 $C $C" "1 $C 1" "1 1 $C"; do
-  r=$(env NUMBA_NUM_THREADS=$(echo $cand | cut -d' ' -f2) OMP_NUM_THREADS=$(echo $cand | cut -d' ' -f3) OPENBLAS_NUM_THREADS=$(echo $cand | cut -d' ' -f3) timeout 300 python -m oracle.ref_runner --config cfg4 --threads 1 --row-stride 16 | tail -1)
-  echo "cfg4 $cand: $r"
+for cand in "1 $C $C" "1 1 $C" "1 $C 1"; do
+  run cfg4 $cand --row-stride=16
 done
