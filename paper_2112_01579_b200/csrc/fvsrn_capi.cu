@@ -761,7 +761,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
     void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    const KernelKind k = (static_tex && !g_tc_two_tiles) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
+    const KernelKind k = (static_tex && !g_tc_two_tiles && m->head == FVSRN_HEAD_DENSITY && !explicit_rays)
+                             ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
     return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
                   g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1);
   }

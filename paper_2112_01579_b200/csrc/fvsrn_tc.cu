@@ -213,8 +213,17 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   uint32_t pre[8];
   int pre_k = -1;
 
+  // TEX == 1: a camera frame (no explicit rays, no direction inputs) of a density-head
+  // model with a static fp16 texture grid: those flags are compile-time
+  constexpr bool kFrame = TEX == 1;
   while (true) {
-    ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
+    if constexpr (kFrame) {
+      RayRecs rr_pos = rr;
+      rr_pos.d = nullptr;
+      ws_refill(r, q, lane, cam, sh, false, rr_pos, n_slots, queue, md, out);
+    } else {
+      ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
+    }
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
     tmem_bias<HID>(t_row, b_s + S::b_off(0));
@@ -339,7 +348,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         if (r.has)
           composite_step(r, make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
                                         __uint_as_float(o[2]), __uint_as_float(o[3])),
-                         density, *tf, md, out, nonfinite);
+                         kFrame || density, *tf, md, out, nonfinite);
       }
     }
   }
