@@ -104,3 +104,26 @@ def test_render_multi_contract_errors(model):
         D.render_multi([D.device_model(model, 0)] * 2, None, cam, st)   # density head needs a TF
     reps = (C.c_void_p * 1)()
     assert L.lib().fvsrn_render_multi(reps, 0, None, None, None, 0.0, None, None) == L.FVSRN_EINVAL
+
+
+@pytest.mark.parametrize("res,tf,et", [(256, "grayscale", 0.999), (97, "warm", 0.5), (180, "two_peaks", 1.0)])
+def test_small_frame_pair_kernel_bit_identical(model, res, tf, et):
+    """Small camera frames march two lanes per ray (dvr_pair_kernel); the same rays through
+    raymarch_forward take the one-lane kernel.  Pixels and evaluated-sample counts must be
+    identical (early termination on, loose and off)."""
+    src = P.ModelSource(model, P.TF_PRESETS[tf])
+    cam = P.fibonacci_cameras(8, res, res)[2]
+    st = P.RenderSettings(stepsize=1 / 128, early_term_alpha=et, background=(0.05, 0.1, 0.2))
+    from paper_2112_01579_b200 import device as D
+
+    D.kernel_timer(True)
+    img = P.render_image(src, cam, st).data.copy()
+    D.kernel_timer_read()
+    name = D.kernel_timer_info()
+    D.kernel_timer(False)
+    n_img = src.last_eval_count
+    o, d = P.camera_rays(cam)
+    px, _ = P.raymarch_forward(src, o, d, st)
+    assert "dvr_pair_kernel" in name, name
+    assert np.array_equal(px.reshape(res, res, 4), img)
+    assert src.last_eval_count == n_img

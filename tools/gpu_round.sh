@@ -11,7 +11,7 @@ for c in cfg1 cfg3 cfg4 cfg5 cfg2; do
   python -c "import json; d=json.load(open('$out/bench_$c.json')); print('$c', round(d['ms_per_step'],3), 'ms', round(d['value']/1e9,2), 'Gev/s', 'e2e', round(d.get('e2e',{}).get('value',0)/1e9,2), round(d.get('e2e',{}).get('ms_per_step',0),3), 'ms frac', round(d['roofline']['frac'],4), 'xu', round(d['roofline']['xu_pipe']['frac'],3), 'cpu', d.get('cpu_baseline',{}).get('value'), d.get('cpu_baseline',{}).get('kind'))" || tail -3 $out/bench_$c.err
 done
 timeout 600 python bench.py > $out/bench_default.json 2> $out/bench_default.err; tail -c 300 $out/bench_default.json; echo
-timeout 900 python bench.py --impl reference --steps 4 --warmup 3 > $out/bench_reference.json 2> $out/bench_reference.err; tail -c 400 $out/bench_reference.json; echo
+timeout 1500 python bench.py --impl reference --steps 20 --warmup 5 > $out/bench_reference.json 2> $out/bench_reference.err; tail -c 400 $out/bench_reference.json; echo
 FVSRN_BENCH_ONE_GPU=1 timeout 600 python bench.py --gpus 2 --steps 8 --check-frame --no-cpu-baseline > $out/bench_2ranks_onegpu.json 2> $out/bench_2ranks.err; tail -c 300 $out/bench_2ranks_onegpu.json; echo
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:dvr_tc_kernel -s 3 -c 1 --export $out/ncu_tc_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
