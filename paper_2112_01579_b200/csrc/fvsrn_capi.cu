@@ -649,6 +649,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + ",1> (mma.sync m16n8k16, frame specialisation)"; break;
+    case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "> (mma.sync m16n8k16, two lanes per ray)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -701,14 +702,19 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   }
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
-  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPipe ||
+  if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPair ||
+      kind == KernelKind::kDVRPipe ||
       tc ||
       kind == KernelKind::kDVRDual) {
     // Small frames: the frame time is the longest rays' sequential march, and every
     // co-resident warp slows each step of it.  Keep ~1.75 work slots per lane (measured
     // at 256^2: 0.456 ms at 5 CTAs/SM -> 0.318 ms at 2); large frames are unaffected.
+    // (two lanes per ray: 2.25 work slots per lane, measured at 256^2: 1.75 0.256 ms,
+    // 2.0-2.5 0.225-0.228, 3.0 0.240; FVSRN_SLOTS_PER_LANE overrides both)
+    static const char* spl_env = std::getenv("FVSRN_SLOTS_PER_LANE");
+    const double slots_per_lane = spl_env ? std::atof(spl_env) : (kind == KernelKind::kDVRPair ? 2.25 : 1.75);
     const double rays_per_sm_cta = (double)m->num_sms * threads;
-    const int occ_work = (int)std::lround((double)work_warps * 32.0 / (rays_per_sm_cta * 1.75));
+    const int occ_work = (int)std::lround((double)work_warps * 32.0 / (rays_per_sm_cta * slots_per_lane));
     occ = std::max(1, std::min(occ, occ_work));
   }
   long long blocks = (long long)m->num_sms * occ;
@@ -775,8 +781,17 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   // static fp16 texture grid on the default shapes: the branch-free feature path
   // of a density-head model rendering a camera frame (no explicit rays)
-  const KernelKind k = (static_tex && fast_path(m, KernelKind::kDVR) && m->head == FVSRN_HEAD_DENSITY &&
-                        !explicit_rays) ? KernelKind::kDVRTex : KernelKind::kDVR;
+  const bool frame = static_tex && fast_path(m, KernelKind::kDVR) && m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
+  // small frames (fewer rays than ~half the resident lanes of a full launch): two lanes per
+  // ray halve the longest rays' sequential march (cfg 1: see DESIGN.md section 4)
+  static const double pair_frac = [] {
+    const char* e = std::getenv("FVSRN_PAIR_FRAC");
+    return e ? std::atof(e) : 1.0;
+  }();
+  const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
+  if (frame && m->hid_pad == 32 && (double)n_slots <= pair_frac * (double)full_lanes)
+    return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1);
+  const KernelKind k = frame ? KernelKind::kDVRTex : KernelKind::kDVR;
   return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
 }
 

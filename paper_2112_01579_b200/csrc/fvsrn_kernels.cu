@@ -133,6 +133,64 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
+// ---------------------------------------------------------------- small frames: two lanes per ray
+// A frame with fewer rays than the GPU has lanes to spare is bound by its longest rays'
+// sequential march.  Here a ray occupies a lane pair: per warp step the even lane evaluates
+// sample k and the odd lane sample k+1 (one MLP pass over 16 rays x 2 samples), and the
+// even lane composites them in order -- sample k, its early-termination check, then sample
+// k+1 (render.py:226-232) -- so a ray advances two samples per step and every pixel is
+// bit-identical to the one-lane march.  A sample evaluated after its ray terminated is
+// discarded and not counted (the count stays the reference's: samples the march uses).
+// Frame specialisation only (static fp16 texture grid, density head, camera rays).
+template <int HID, int NM, int NL>
+__global__ void __launch_bounds__(kThreads, min_blocks<HID>())
+dvr_pair_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
+                MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
+                float* __restrict__ out, unsigned long long* __restrict__ queue,
+                unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  const int rs = fd.k0 + 8;
+  uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
+  stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
+  const int lane = threadIdx.x & 31;
+  const bool odd = (lane & 1) != 0;
+  __half* myrow = stage + lane * rs;
+  RayLane r;
+  r.has = false;
+  LaneQueue q{0, 0, false};
+  unsigned used = 0;
+  while (true) {
+    pair_refill(r, q, lane, cam, sh, rr, n_slots, queue, md, out);
+    if (__ballot_sync(0xffffffffu, r.has) == 0) break;
+    // even lane: sample k; hands sample k+1's position to its odd partner
+    const float kf = (float)r.k;
+    const float px0 = fmaf(kf, r.dd0, r.pe0), py0 = fmaf(kf, r.dd1, r.pe1), pz0 = fmaf(kf, r.dd2, r.pe2);
+    const float kf1 = (float)(r.k + 1);
+    const float px1 = fmaf(kf1, r.dd0, r.pe0), py1 = fmaf(kf1, r.dd1, r.pe1), pz1 = fmaf(kf1, r.dd2, r.pe2);
+    const bool next = r.has && r.k + 1 < r.n;
+    const float qx = __shfl_sync(0xffffffffu, px1, lane & ~1), qy = __shfl_sync(0xffffffffu, py1, lane & ~1),
+                qz = __shfl_sync(0xffffffffu, pz1, lane & ~1);
+    const bool partner_next = __shfl_sync(0xffffffffu, next, lane & ~1);   // every lane shuffles
+    const bool mine = odd ? partner_next : r.has;
+    if (mine) FastRow<NM>::build_tex(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
+    __syncwarp();
+    MLPDispatch<HID, 4, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
+    __syncwarp();
+    const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
+    const float4 o1 = make_float4(__shfl_down_sync(0xffffffffu, o.x, 1), __shfl_down_sync(0xffffffffu, o.y, 1),
+                                  __shfl_down_sync(0xffffffffu, o.z, 1), __shfl_down_sync(0xffffffffu, o.w, 1));
+    if (!odd && r.has) {
+      composite_step(r, o, true, *tf, md, out, nonfinite);
+      ++used;
+      if (r.has) {      // still marching: r.k is now k + 1 < n, the partner's sample
+        composite_step(r, o1, true, *tf, md, out, nonfinite);
+        ++used;
+      }
+    }
+  }
+  used = __reduce_add_sync(0xffffffffu, used);
+  if (lane == 0 && eval_count) atomicAdd(eval_count, (unsigned long long)used);
+}
+
 #if FVSRN_AB_VARIANTS   // measured-slower A/B variants, off by default
 // ---------------------------------------------------------------- software-pipelined DVR
 // dvr_kernel with the next step's input row built while the MLP of the current step
@@ -800,6 +858,8 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
                   : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
     if (kind == KernelKind::kDVRTex)                                                         \
       return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1> : nullptr; \
+    if (kind == KernelKind::kDVRPair)                                                        \
+      return fast ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H)> : nullptr;  \
     FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \

@@ -99,8 +99,9 @@ struct RayRecs {
 // kDVRTex: dvr_kernel specialised for the default fast path with a static fp16 texture grid
 // (no u8 codes, no per-sample keyframe blend): the feature code has no runtime branches
 // (kDVRTCTex, kSampleTex: the same for the tcgen05 march and the lattice decode)
+// (kDVRPair: the frame specialisation with two lanes per ray, for small frames)
 enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused, kDVRTex, kDVRTCTex,
-                        kSampleTex };
+                        kSampleTex, kDVRPair };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

@@ -83,6 +83,51 @@ __device__ __forceinline__ void ws_refill(RayLane& r, LaneQueue& q, int lane, co
   }
 }
 
+// ws_refill for the two-lanes-per-ray kernel: only even lanes own rays (the odd partner
+// evaluates the ray's next sample), so only they take slots from the queue.
+__device__ __forceinline__ void pair_refill(RayLane& r, LaneQueue& q, int lane, const CamDev& cam,
+                                            const ShardDev& sh, const RayRecs& rr, long long n_slots,
+                                            unsigned long long* __restrict__ queue, const MarchDev& md,
+                                            float* __restrict__ out) {
+  const bool even = (lane & 1) == 0;
+  while (true) {
+    const unsigned need = __ballot_sync(0xffffffffu, even && !r.has);
+    if (need == 0) break;
+    if (q.chunk_left == 0) {
+      if (q.qdone) break;
+      unsigned long long cb = 0;
+      if (lane == 0) cb = atomicAdd(queue, 16ull);
+      cb = __shfl_sync(0xffffffffu, cb, 0);
+      if ((long long)cb >= n_slots) { q.qdone = true; break; }
+      q.chunk_base = (long long)cb;
+      q.chunk_left = (int)min(16ll, n_slots - (long long)cb);
+    }
+    const int rank = __popc(need & lanemask_lt());
+    const int take = min(__popc(need), q.chunk_left);
+    if (even && !r.has && rank < take) {
+      const long long qs = q.chunk_base + rank;
+      const long long s = sh.order ? ((long long)sh.order[qs >> 6] << 6) | (qs & 63) : qs;
+      const float4 ra = __ldg(rr.a + s);
+      const int n = __float_as_int(ra.w);
+      if (n > 0) {
+        const float4 rb = __ldg(rr.b + s);
+        r.has = true;
+        r.k = 0; r.n = n;
+        r.oslot = sh.compact ? s : slot_pixel(cam, sh, s);
+        r.pe0 = ra.x; r.pe1 = ra.y; r.pe2 = ra.z;
+        r.dd0 = rb.x; r.dd1 = rb.y; r.dd2 = rb.z; r.dsf = rb.w;
+        r.dx = r.dy = r.dz = 0.f;
+        r.C0 = r.C1 = r.C2 = r.A = 0.f;
+      } else if (n < 0) {   // a miss: background pixel (ray_setup deferred it)
+        const long long o = sh.compact ? s : slot_pixel(cam, sh, s);
+        *reinterpret_cast<float4*>(out + 4 * o) = make_float4(md.bg[0], md.bg[1], md.bg[2], 0.f);
+      }
+    }
+    q.chunk_base += take;
+    q.chunk_left -= take;
+  }
+}
+
 // One compositing step of a ray with the head outputs o (density head: TF lookup;
 // colour head: sigmoid rgb + softplus sigma); retires the ray when it ends.
 __device__ __forceinline__ void composite_step(RayLane& r, float4 o, bool density, const TFDev& tf,
