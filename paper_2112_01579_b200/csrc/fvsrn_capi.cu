@@ -782,11 +782,12 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   // static fp16 texture grid on the default shapes: the branch-free feature path
   // of a density-head model rendering a camera frame (no explicit rays)
   const bool frame = static_tex && fast_path(m, KernelKind::kDVR) && m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
-  // small frames (fewer rays than ~half the resident lanes of a full launch): two lanes per
-  // ray halve the longest rays' sequential march (cfg 1: see DESIGN.md section 4)
+  // small and medium frames (up to ~5x the resident lanes of a full launch, ~690^2): two
+  // lanes per ray halve the longest rays' sequential march (tools/frame_sweep.py, cfg-2 model:
+  // 256^2 0.54 -> 0.40 ms, 512^2 1.13 -> 0.91, 640^2 1.39 -> 1.32, 768^2 equal)
   static const double pair_frac = [] {
     const char* e = std::getenv("FVSRN_PAIR_FRAC");
-    return e ? std::atof(e) : 1.0;
+    return e ? std::atof(e) : 5.0;
   }();
   const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
   if (frame && m->hid_pad == 32 && (double)n_slots <= pair_frac * (double)full_lanes)
