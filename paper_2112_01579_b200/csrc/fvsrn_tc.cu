@@ -67,6 +67,12 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_WAIT_BAR
 #define FVSRN_TC_WAIT_BAR 0
 #endif
+// FVSRN_TC_NSPLIT: the 64-wide layers' MMA is issued as two N=32 halves committing to two
+// mbarriers, so the activations of the first half overlap the second half's MMA (the packed
+// first half waits in registers: A is rewritten only after the whole MMA has read it)
+#ifndef FVSRN_TC_NSPLIT
+#define FVSRN_TC_NSPLIT 0
+#endif
 // hidden-layer A operands in TMEM (tcgen05.st of the packed activations, MMA reads A
 // from TMEM) instead of the shared-memory A tile: removes 2 x 128 B of shared-memory
 // traffic per sample and layer
@@ -168,6 +174,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   __half* a_s = reinterpret_cast<__half*>(smem + S::kAOff);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::kMbarOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kMbarOff + 8);
+  uint64_t* mbar1 = reinterpret_cast<uint64_t*>(smem + S::kMbarOff + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   {
@@ -191,13 +198,18 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   constexpr uint32_t kNeed = S::kTCols + kAcols;
   constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
-  if (tid == 0) mbar_init(smem_u32(mbar), 1);
+  if (tid == 0) {
+    mbar_init(smem_u32(mbar), 1);
+    mbar_init(smem_u32(mbar1), 1);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
-  const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar);
+  const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar), mb1 = smem_u32(mbar1);
+  uint32_t phase1 = 0;
+  constexpr bool kNSplit = FVSRN_TC_NSPLIT && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT;
   // row tid of the A tile: 8-row group stride SBO_A, row-in-group stride 16 B
   __half* myrow = a_s + (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
   const bool density = net.head == 0;
@@ -264,16 +276,30 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         const int N = l == NL - 1 ? S::kNLast : HID;
         const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
         const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
-        const uint32_t id = idesc_f16(128, N);
+        if (kNSplit && l < NL - 1 && ((FVSRN_TC_TMEM_A && l > 0) || kA0)) {
+          // two N=32 halves: rows 32..63 of the K-major weight tile start 4 core-matrix
+          // groups (4 * SBO) further on
+          const uint32_t id = idesc_f16(128, 32);
 #pragma unroll
-        for (int kk = 0; kk < K / 16; ++kk) {
-          if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
-            umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
-          else
-            umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
-                     smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk)
+              umma_f16_ts(tmem + 32u * h, tmem + S::kTCols + kk * 8u,
+                          smem_desc(wb + kk * 256u + 4u * h * sbo_b, 128u, sbo_b), id, 1u);
+            umma_commit(h == 0 ? mb : mb1);
+          }
+        } else {
+          const uint32_t id = idesc_f16(128, N);
+#pragma unroll
+          for (int kk = 0; kk < K / 16; ++kk) {
+            if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
+              umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+            else
+              umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
+                       smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+          }
+          umma_commit(mb);
         }
-        umma_commit(mb);
       }
       if (prefetch && l == NL - 1) {
         pre_k = -1;
@@ -297,7 +323,24 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
         // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
-        if constexpr (FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && HID == 64) {
+        if constexpr (kNSplit) {
+          // first half ready (the wait above was on its mbarrier); its activations overlap
+          // the second half's MMA and stay in registers until that MMA has read A
+          uint32_t acc[32], w0[16], w1[16];
+          tmem_ld<32>(t_row, acc);
+          tmem_wait_ld();
+          act_words<32>(acc, w0);
+          mbar_wait(mb1, phase1);
+          phase1 ^= 1u;
+          tc_fence_after();
+          tmem_ld<32>(t_row + 32, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_words<32>(acc, w1);
+          tmem_st<16>(t_row + S::kTCols, w0);
+          tmem_st<16>(t_row + S::kTCols + 16, w1);
+        } else if constexpr (FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && HID == 64) {
           // two 32-column halves: half the live accumulator registers
           uint32_t acc[32], w[16];
           tmem_ld<32>(t_row, acc);

@@ -68,7 +68,7 @@ struct TcShape {
   // with layer-0 rows in TMEM the one-tile kernel has no shared-memory A tile
   static constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
   static constexpr int kMbarOff = kA0 ? kAOff : kAOff + kATile;
-  static constexpr int kSmem = kMbarOff + 16;
+  static constexpr int kSmem = kMbarOff + 32;   // mbarrier, TMEM slot, second mbarrier
   static constexpr int kSmem2 = kAOff + 2 * kATile + 32;   // two-tile variant
 };
 
