@@ -340,6 +340,10 @@ def main():
                          "manifest.json beside it")
     ap.add_argument("--check-frame", action="store_true",
                     help="N>1: compare the assembled frame with a 1-GPU render on rank 0")
+    ap.add_argument("--checkpoint", default=None,
+                    help="render this .fvsrn checkpoint (same shape as the config) instead of the "
+                         "random-init model, e.g. tests/golden/trained_cfg2.fvsrn (trained weights: "
+                         "the upload-time probe may select the exact-weight grid sampler)")
     ap.add_argument("--grid-precision", default="f16", choices=["f16", "u8"],
                     help="u8: the latent grid round-trips through a u8 .fvsrn checkpoint "
                          "(grid_quantize, grid.py:157-166) and is sampled as 8-bit codes")
@@ -374,6 +378,13 @@ def main():
 
     cfg = CONFIGS[args.config]
     model = P.model_init(P.ModelConfig(**cfg["model"]))
+    if args.checkpoint:
+        model = P.checkpoint_load(args.checkpoint)
+        want = P.ModelConfig(**cfg["model"])
+        got = model.config
+        if (got.layers, got.hidden, got.grid_resolution, got.grid_channels, got.input_width) != \
+                (want.layers, want.hidden, want.grid_resolution, want.grid_channels, want.input_width):
+            sys.exit(f"--checkpoint {args.checkpoint} does not have the {args.config} shape")
     if args.grid_precision == "u8":
         import tempfile
 
@@ -635,7 +646,8 @@ def main():
                                       else "NCCL gather + reassembly") + ")")
                    if world > 1 else "1 GPU",
                    "tf": "grayscale", "t": t_cycle if t_frame is not None else None,
-                   "grid_precision": args.grid_precision},
+                   "grid_precision": args.grid_precision,
+                   "weights": args.checkpoint or "random init (ModelConfig seed 0)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "flops_per_eval": flops, "peak_source": peak_src,

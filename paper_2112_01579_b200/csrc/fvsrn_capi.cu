@@ -629,7 +629,7 @@ std::map<std::pair<const void*, int>, size_t> g_smem_attr;
 
 // What `launch` runs, for the measurement record (fvsrn_kernel_timer_info): the template
 // instantiation, the MMA path and the latent-grid sampler.
-std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
+std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
   const int h = m->hid_pad;
   const bool fast = fast_path(m, kind);
   const std::string tmpl = fast ? std::to_string(h) + ",4," + std::to_string((h - 4) / 2) + "," +
@@ -641,15 +641,16 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
     case KernelKind::kDVRTCTex:
       k = std::string(g_tc_two_tiles ? "dvr_tc2_kernel<" : "dvr_tc_kernel<") + std::to_string(h) + "," +
           std::to_string((h - 4) / 2) + "," + std::to_string(m->layers) +
-          (kind == KernelKind::kDVRTCTex ? ",1" : "") + "> (tcgen05.mma kind::f16, TMEM accumulators)";
+          (kind == KernelKind::kDVRTCTex ? "," + std::to_string(fmode) : "") +
+          "> (tcgen05.mma kind::f16, TMEM accumulators)";
       break;
-    case KernelKind::kSampleTex: k = "sample_kernel<" + tmpl + ",1> (mma.sync m16n8k16, static-texture features)"; break;
+    case KernelKind::kSampleTex: k = "sample_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, static-grid features)"; break;
     case KernelKind::kDVRWS: k = "dvr_ws_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRPipe: k = "dvr_pipe_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
-    case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + ",1> (mma.sync m16n8k16, frame specialisation)"; break;
-    case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "> (mma.sync m16n8k16, two lanes per ray)"; break;
+    case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, frame specialisation)"; break;
+    case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, two lanes per ray)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -660,11 +661,11 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind) {
 }
 
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
-           long long work_warps) {
+           long long work_warps, int fmode = 1) {
   const bool tc = kind == KernelKind::kDVRTC || kind == KernelKind::kDVRTCTex;
   const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
-                   : kind == KernelKind::kDVRTCTex ? tc_tex_kernel_for(m->hid_pad)
-                                                    : kernel_for(kind, m->hid_pad, fast_path(m, kind));
+                   : kind == KernelKind::kDVRTCTex ? tc_tex_kernel_for(m->hid_pad, fmode)
+                                                    : kernel_for(kind, m->hid_pad, fast_path(m, kind), fmode);
   const int threads = kind == KernelKind::kDVRWS ? kWsThreads : tc ? kTcThreads : kThreads;
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
   int occ = 0;
@@ -722,7 +723,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   if (need < blocks) blocks = std::max(1ll, need);
   std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
   if (g_kt.on && kind != KernelKind::kFused) {
-    g_kt.name = kernel_desc(m, kind);
+    g_kt.name = kernel_desc(m, kind, fmode);
     if (g_kt.used == g_kt.ev.size()) {
       std::pair<cudaEvent_t, cudaEvent_t> p;
       CUDA_TRY(cudaEventCreate(&p.first));
@@ -763,14 +764,17 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
                long long& n_slots, float*& d_out, unsigned long long*& queue,
                unsigned long long*& evc, unsigned long long*& nfc, cudaStream_t s) {
   if (n_slots <= 0) return FVSRN_OK;
+  // static fp16 grid in the march: texture units (fmode 1) or exact-weight loads (fmode 2)
   const bool static_tex = FVSRN_TEX_SPECIAL && fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
+  const bool static_ldg = FVSRN_TEX_SPECIAL && !fd.tex_on && fd.grid != nullptr && fd.f_pad == 16;
+  const int fmode = static_tex ? 1 : 2;
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
     void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    const KernelKind k = (static_tex && !g_tc_two_tiles && m->head == FVSRN_HEAD_DENSITY && !explicit_rays)
-                             ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
+    const KernelKind k = ((static_tex || static_ldg) && !g_tc_two_tiles && m->head == FVSRN_HEAD_DENSITY &&
+                          !explicit_rays) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
     return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
-                  g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1);
+                  g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1, fmode);
   }
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
   if (dvr_mode() == DvrMode::kWS)
@@ -781,7 +785,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   // static fp16 texture grid on the default shapes: the branch-free feature path
   // of a density-head model rendering a camera frame (no explicit rays)
-  const bool frame = static_tex && fast_path(m, KernelKind::kDVR) && m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
+  const bool frame = (static_tex || static_ldg) && fast_path(m, KernelKind::kDVR) &&
+                     m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
   // small and medium frames (up to ~5x the resident lanes of a full launch, ~690^2): two
   // lanes per ray halve the longest rays' sequential march (tools/frame_sweep.py, cfg-2 model:
   // 256^2 0.54 -> 0.40 ms, 512^2 1.13 -> 0.91, 640^2 1.39 -> 1.32, 768^2 equal)
@@ -791,9 +796,10 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   }();
   const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
   if (frame && m->hid_pad == 32 && (double)n_slots <= pair_frac * (double)full_lanes)
-    return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1);
+    return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1,
+                  fmode);
   const KernelKind k = frame ? KernelKind::kDVRTex : KernelKind::kDVR;
-  return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1);
+  return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1, fmode);
 }
 
 MarchDev march_for(const fvsrn_settings* st) {
@@ -1834,11 +1840,14 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
   CUDA_TRY(cudaMemcpyAsync(coords, hc.data(), hc.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   const size_t smem = stage_smem_bytes(net, false, m->k0);
   // static fp16 texture grid on the default shapes: the branch-free feature path
-  const KernelKind sk = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kSample) && fd.tex_on && !fd.tex_u8 &&
-                         fd.tex_w == 0.f) ? KernelKind::kSampleTex : KernelKind::kSample;
+  const bool s_tex = fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
+  const bool s_ldg = !fd.tex_on && fd.grid != nullptr && fd.f_pad == 16;
+  const KernelKind sk = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kSample) && (s_tex || s_ldg))
+                            ? KernelKind::kSampleTex : KernelKind::kSample;
+  const int sfm = s_tex ? 1 : 2;
   if (chunks <= 1 || !h_out) {
     void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad, &coords};
-    if ((rc = launch(m, sk, smem, args, s, count / 32 + 1))) return rc;
+    if ((rc = launch(m, sk, smem, args, s, count / 32 + 1, sfm))) return rc;
   } else {
     // chunk c: decode [c0, c0 + n) into d_out + c0 on s, then copy it to h_out on copy_s
     const long long per = ((lattice_count + chunks - 1) / chunks + 31) / 32 * 32;
@@ -1846,7 +1855,7 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
       long long cb = lattice_begin + c0, cn = std::min(per, lattice_count - c0);
       float* dst = d_out + c0;
       void* args[] = {&net, &fd, &b0, &mode, &res, &step, &cb, &cn, &pp, &pd, &dst, &d_bad, &coords};
-      if ((rc = launch(m, sk, smem, args, s, cn / 32 + 1))) return rc;
+      if ((rc = launch(m, sk, smem, args, s, cn / 32 + 1, sfm))) return rc;
       cudaEvent_t done;
       CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(done, s));

@@ -612,45 +612,65 @@ struct FastRow {
         w[2 * j + 1] = pack_half2(v.z, v.w);
       }
     } else {
-      const int R = fd.grid_res;
-      const float s = (float)(R - 1);
-      const float rm2 = (float)(R - 2);
-      float cx = fminf(fmaxf(px, 0.f), 1.f) * s;
-      float cy = fminf(fmaxf(py, 0.f), 1.f) * s;
-      float cz = fminf(fmaxf(pz, 0.f), 1.f) * s;
-      int x0, y0, z0;   // i0 = min(int c, R-2) (grid.py:47-53), c >= 0 so trunc == floor
-      float x0f = floor_pos(cx, x0), y0f = floor_pos(cy, y0), z0f = floor_pos(cz, z0);
-      if (x0 > R - 2) { x0 = R - 2; x0f = rm2; }
-      if (y0 > R - 2) { y0 = R - 2; y0f = rm2; }
-      if (z0 > R - 2) { z0 = R - 2; z0f = rm2; }
-      float fx = cx - x0f, fy = cy - y0f, fz = cz - z0f;
-      float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
-      const float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
-                           fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
-      __half2 wk[8];
+      uint32_t z[8];
+      ldg_words(fd, px, py, pz, z);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) wk[k] = __float2half2_rn(wf[k]);
-      const int sz = 16, sy = R * 16, sx = R * R * 16;
-      const uint4* base = reinterpret_cast<const uint4*>(fd.grid + ((size_t)(x0 * R + y0) * R + z0) * 16);
-      const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
-#pragma unroll
-      for (int c8 = 0; c8 < 2; ++c8) {
-        uint4 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(base + (off[k] >> 3) + c8);
-        // z = sum_k w_k g_k in packed half2 (HFMA2): 32 instructions per 8 channels
-        __half2 acc[4];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const __half2* g2 = reinterpret_cast<const __half2*>(&v[k]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] = k == 0 ? __hmul2(wk[k], g2[j]) : __hfma2(wk[k], g2[j], acc[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[4 * c8 + j] = *reinterpret_cast<uint32_t*>(&acc[j]);
-      }
+      for (int i = 0; i < 8; ++i) w[i] = z[i];
     }
     fourier_words(px, py, pz, w);
+  }
+
+  // exact-weight trilinear latent lookup (grid.py:47-84) of a 16-channel fp16 grid: 16
+  // LDG.128 + HFMA2 products, as 8 packed fp16 pairs
+  __device__ static void ldg_words(const FeatDev& fd, float px, float py, float pz, uint32_t (&z)[8]) {
+    const int R = fd.grid_res;
+    const float s = (float)(R - 1);
+    const float rm2 = (float)(R - 2);
+    float cx = fminf(fmaxf(px, 0.f), 1.f) * s;
+    float cy = fminf(fmaxf(py, 0.f), 1.f) * s;
+    float cz = fminf(fmaxf(pz, 0.f), 1.f) * s;
+    int x0, y0, z0;   // i0 = min(int c, R-2) (grid.py:47-53), c >= 0 so trunc == floor
+    float x0f = floor_pos(cx, x0), y0f = floor_pos(cy, y0), z0f = floor_pos(cz, z0);
+    if (x0 > R - 2) { x0 = R - 2; x0f = rm2; }
+    if (y0 > R - 2) { y0 = R - 2; y0f = rm2; }
+    if (z0 > R - 2) { z0 = R - 2; z0f = rm2; }
+    float fx = cx - x0f, fy = cy - y0f, fz = cz - z0f;
+    float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+    const float wf[8] = {gx * gy * gz, gx * gy * fz, gx * fy * gz, gx * fy * fz,
+                         fx * gy * gz, fx * gy * fz, fx * fy * gz, fx * fy * fz};
+    __half2 wk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wk[k] = __float2half2_rn(wf[k]);
+    const int sz = 16, sy = R * 16, sx = R * R * 16;
+    const uint4* base = reinterpret_cast<const uint4*>(fd.grid + ((size_t)(x0 * R + y0) * R + z0) * 16);
+    const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+#pragma unroll
+    for (int c8 = 0; c8 < 2; ++c8) {
+      uint4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(base + (off[k] >> 3) + c8);
+      // z = sum_k w_k g_k in packed half2 (HFMA2): 32 instructions per 8 channels
+      __half2 acc[4];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const __half2* g2 = reinterpret_cast<const __half2*>(&v[k]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = k == 0 ? __hmul2(wk[k], g2[j]) : __hfma2(wk[k], g2[j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) z[4 * c8 + j] = *reinterpret_cast<uint32_t*>(&acc[j]);
+    }
+  }
+
+  // the whole row from the static fp16 LDG grid (no u8 codes, no keyframe blend): the
+  // branch-free feature path of the frame kernels with the exact-weight sampler
+  __device__ static void build_ldg(const FeatDev& fd, float px, float py, float pz, __half* row) {
+    uint32_t z[8], w[kWords];
+    ldg_words(fd, px, py, pz, z);
+    words_from_z(z, px, py, pz, w);
+    uint4* dst = reinterpret_cast<uint4*>(row);
+#pragma unroll
+    for (int j = 0; j < kWords / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 
   // texture-unit latent lookup of a static fp16 grid (fd.tex_on, no u8 codes, no keyframe

@@ -98,9 +98,10 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   typename MLP::HB hb;
   hb.load(wf_s, net, lane);
 
-  // TEX == 1: a camera frame (no explicit rays, no direction inputs) of a density-head
-  // model: those flags are compile-time, so the refill and compositing lose their branches
-  constexpr bool kFrame = TEX == 1;
+  // TEX == 1 / 2 (static fp16 grid through the texture units / exact-weight loads): a camera
+  // frame (no explicit rays, no direction inputs) of a density-head model; those flags are
+  // compile-time, so the features, refill and compositing lose their branches
+  constexpr bool kFrame = TEX >= 1;
   while (true) {
     if constexpr (kFrame) {
       RayRecs rr_pos = rr;
@@ -117,6 +118,9 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
       const float kf = (float)r.k;
       if constexpr (TEX == 1 && NM > 0)
         FastRow<NM>::build_tex(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
+                               myrow);
+      else if constexpr (TEX == 2 && NM > 0)
+        FastRow<NM>::build_ldg(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
                                myrow);
       else
         assemble_row_t<NM>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2),
@@ -141,8 +145,9 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
 // k+1 (render.py:226-232) -- so a ray advances two samples per step and every pixel is
 // bit-identical to the one-lane march.  A sample evaluated after its ray terminated is
 // discarded and not counted (the count stays the reference's: samples the march uses).
-// Frame specialisation only (static fp16 texture grid, density head, camera rays).
-template <int HID, int NM, int NL>
+// Frame specialisation only (static fp16 grid through the texture units (TEX 1) or exact-
+// weight loads (TEX 2), density head, camera rays).
+template <int HID, int NM, int NL, int TEX>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID>())
 dvr_pair_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
                 MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
@@ -171,7 +176,10 @@ dvr_pair_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
                 qz = __shfl_sync(0xffffffffu, pz1, lane & ~1);
     const bool partner_next = __shfl_sync(0xffffffffu, next, lane & ~1);   // every lane shuffles
     const bool mine = odd ? partner_next : r.has;
-    if (mine) FastRow<NM>::build_tex(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
+    if (mine) {
+      if constexpr (TEX == 1) FastRow<NM>::build_tex(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
+      else FastRow<NM>::build_ldg(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
+    }
     __syncwarp();
     MLPDispatch<HID, 4, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
@@ -678,6 +686,7 @@ sample_kernel(NetDev net, FeatDev fd, const float* __restrict__ b0, int mode, in
         if (dirs) { dx = (float)dirs[3 * i]; dy = (float)dirs[3 * i + 1]; dz = (float)dirs[3 * i + 2]; }
       }
       if constexpr (TEX == 1 && NM > 0) FastRow<NM>::build_tex(fd, px, py, pz, myrow);
+      else if constexpr (TEX == 2 && NM > 0) FastRow<NM>::build_ldg(fd, px, py, pz, myrow);
       else assemble_row_t<NM>(fd, px, py, pz, dx, dy, dz, myrow);
     }
     __syncwarp();
@@ -833,7 +842,7 @@ constexpr int fast_layers(int hid) { return hid == 64 ? 6 : 4; }
 
 // fast: (snake_alt, NeRF m = (HID-4)/2 on 3 axes, F = 16, pos mode, layers =
 // fast_layers(HID)); else generic (runtime layer count and input layout)
-const void* kernel_for(KernelKind kind, int hid, bool fast) {
+const void* kernel_for(KernelKind kind, int hid, bool fast, int fmode) {
 #if FVSRN_AB_VARIANTS
   if (kind == KernelKind::kDVRDual) {
     if (!fast || hid != 32) return nullptr;
@@ -857,15 +866,21 @@ const void* kernel_for(KernelKind kind, int hid, bool fast) {
       return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H)>               \
                   : (const void*)dvr_kernel<H, kActRuntime, 0, 0>;                           \
     if (kind == KernelKind::kDVRTex)                                                         \
-      return fast ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1> : nullptr; \
+      return !fast ? nullptr : fmode == 2                                                    \
+          ? (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 2>                    \
+          : (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1>;                   \
     if (kind == KernelKind::kDVRPair)                                                        \
-      return fast ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H)> : nullptr;  \
+      return !fast ? nullptr : fmode == 2                                                    \
+          ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2>                  \
+          : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1>;                 \
     FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \
                   : (const void*)sample_kernel<H, kActRuntime, 0, 0>;                        \
     if (kind == KernelKind::kSampleTex)                                                      \
-      return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1> : nullptr; \
+      return !fast ? nullptr : fmode == 2                                                    \
+          ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H), 2>                 \
+          : (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1>;                \
     return fast ? (const void*)fused_eval_kernel<H, 4> : (const void*)fused_eval_kernel<H, kActRuntime>;
     FVSRN_FOR_HIDDEN(CASE)
 #undef CASE

@@ -105,7 +105,8 @@ enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFuse
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).
-const void* kernel_for(KernelKind kind, int hid_pad, bool fast);
+// fmode (frame kinds kDVRTex / kDVRPair / kSampleTex): 1 static texture grid, 2 static LDG grid
+const void* kernel_for(KernelKind kind, int hid_pad, bool fast, int fmode = 1);
 int fast_layer_count(int hid_pad);
 // LPT schedule: exact per-tile step counts (same f64 geometry as the renderer), then
 // local tiles sorted by descending cost.  `order` receives n_local tile indices.

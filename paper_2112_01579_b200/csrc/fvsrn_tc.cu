@@ -227,7 +227,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
 
   // TEX == 1: a camera frame (no explicit rays, no direction inputs) of a density-head
   // model with a static fp16 texture grid: those flags are compile-time
-  constexpr bool kFrame = TEX == 1;
+  constexpr bool kFrame = TEX >= 1;
   while (true) {
     if constexpr (kFrame) {
       RayRecs rr_pos = rr;
@@ -247,9 +247,10 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
         if (prefetch && pre_k == r.k) {
           FastRow<NM>::words_from_z(pre, px, py, pz, w);
-        } else if constexpr (TEX == 1) {   // static fp16 texture grid: no runtime branches
+        } else if constexpr (TEX >= 1) {   // static fp16 grid: no runtime branches
           uint32_t z[8];
-          FastRow<NM>::tex_words(fd, px, py, pz, z);
+          if constexpr (TEX == 1) FastRow<NM>::tex_words(fd, px, py, pz, z);
+          else FastRow<NM>::ldg_words(fd, px, py, pz, z);
           FastRow<NM>::words_from_z(z, px, py, pz, w);
         } else {
           FastRow<NM>::words(fd, px, py, pz, w);
@@ -575,10 +576,10 @@ const void* tc_kernel_for(int hid, bool two_tiles) {
   }
 }
 
-const void* tc_tex_kernel_for(int hid) {
+const void* tc_tex_kernel_for(int hid, int fmode) {
   switch (hid) {
-    case 32: return (const void*)dvr_tc_kernel<32, 14, 4, 1>;
-    case 64: return (const void*)dvr_tc_kernel<64, 30, 6, 1>;
+    case 32: return fmode == 2 ? (const void*)dvr_tc_kernel<32, 14, 4, 2> : (const void*)dvr_tc_kernel<32, 14, 4, 1>;
+    case 64: return fmode == 2 ? (const void*)dvr_tc_kernel<64, 30, 6, 2> : (const void*)dvr_tc_kernel<64, 30, 6, 1>;
     default: return nullptr;
   }
 }

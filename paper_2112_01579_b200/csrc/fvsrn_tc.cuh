@@ -77,7 +77,7 @@ struct TcShape {
 // two_tiles: the ping-pong variant (256 rays per CTA).
 const void* tc_kernel_for(int hid, bool two_tiles);
 // the single-tile kernel specialised for a static fp16 texture grid (branch-free features)
-const void* tc_tex_kernel_for(int hid);
+const void* tc_tex_kernel_for(int hid, int fmode = 1);   // fmode 1 texture, 2 LDG grid
 size_t tc_smem_bytes(int hid, bool two_tiles);
 inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
 
