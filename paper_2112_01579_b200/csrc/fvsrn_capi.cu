@@ -739,10 +739,17 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   return FVSRN_OK;
 }
 
+// auto: tcgen05 at 64-wide (measured 27.0 vs 34.2 ms) and, since the biases ride in the
+// MMA (tc_bias_mma), at 32-wide too (cfg 2 3.02 vs 3.11 ms for mma.sync); FVSRN_TC32=0
+// keeps mma.sync at 32-wide.  Small frames take the two-lanes-per-ray mma.sync kernel.
+const bool g_tc32_auto = [] {
+  const char* e = std::getenv("FVSRN_TC32");
+  return !(e && e[0] == '0');
+}();
 bool use_tc(const fvsrn_model* m) {
   if (!m->tc_ok || !fast_path(m, KernelKind::kDVR)) return false;
   if (dvr_mode() == DvrMode::kTC) return true;
-  return dvr_mode() == DvrMode::kAuto && m->hid_pad == 64;
+  return dvr_mode() == DvrMode::kAuto && (m->hid_pad == 64 || (m->hid_pad == 32 && g_tc32_auto));
 }
 
 // Stream-ordered per-frame ray records: a, b (+ d for direction-input models).
@@ -768,36 +775,39 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   const bool static_tex = FVSRN_TEX_SPECIAL && fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
   const bool static_ldg = FVSRN_TEX_SPECIAL && !fd.tex_on && fd.grid != nullptr && fd.f_pad == 16;
   const int fmode = static_tex ? 1 : 2;
+  // a camera frame of a density-head model with a static fp16 grid: the branch-free
+  // frame-specialised kernels
+  const bool frame = (static_tex || static_ldg) && fast_path(m, KernelKind::kDVR) &&
+                     m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
+  // small and medium frames (up to ~5x the resident lanes of a full launch, ~690^2): two
+  // lanes per ray halve the longest rays' sequential march (tools/frame_sweep.py, cfg-2 model:
+  // 256^2 0.54 -> 0.40 ms, 512^2 1.13 -> 0.91, 640^2 1.39 -> 1.32, 768^2 equal).  Decided on
+  // the whole frame (W x H), not this rank's share, so every shard of a multi-GPU frame runs
+  // the same kernel as the 1-GPU frame (bit-identical assembly).
+  static const double pair_frac = [] {
+    const char* e = std::getenv("FVSRN_PAIR_FRAC");
+    return e ? std::atof(e) : 5.0;
+  }();
+  const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
+  const bool small = frame && m->hid_pad == 32 && dvr_mode() != DvrMode::kTC &&
+                     (double)cam.W * (double)cam.H <= pair_frac * (double)full_lanes;
+  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+  if (small)
+    return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1,
+                  fmode);
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
-    void* args[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    const KernelKind k = ((static_tex || static_ldg) && !g_tc_two_tiles && m->head == FVSRN_HEAD_DENSITY &&
-                          !explicit_rays) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
-    return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), args, s,
+    void* targs[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+    const KernelKind k = (frame && !g_tc_two_tiles) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
+    return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), targs, s,
                   g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1, fmode);
   }
-  void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
   if (dvr_mode() == DvrMode::kWS)
     return launch(m, KernelKind::kDVRWS, ws_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
   if (dvr_mode() == DvrMode::kDual && fast_path(m, KernelKind::kDVR) && m->hid_pad == 32)
     return launch(m, KernelKind::kDVRDual, dual_smem_bytes(net, m->k0), args, s, n_slots / 64 + 1);
   if (dvr_mode() == DvrMode::kPipe && fast_path(m, KernelKind::kDVR))
     return launch(m, KernelKind::kDVRPipe, pipe_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
-  // static fp16 texture grid on the default shapes: the branch-free feature path
-  // of a density-head model rendering a camera frame (no explicit rays)
-  const bool frame = (static_tex || static_ldg) && fast_path(m, KernelKind::kDVR) &&
-                     m->head == FVSRN_HEAD_DENSITY && !explicit_rays;
-  // small and medium frames (up to ~5x the resident lanes of a full launch, ~690^2): two
-  // lanes per ray halve the longest rays' sequential march (tools/frame_sweep.py, cfg-2 model:
-  // 256^2 0.54 -> 0.40 ms, 512^2 1.13 -> 0.91, 640^2 1.39 -> 1.32, 768^2 equal)
-  static const double pair_frac = [] {
-    const char* e = std::getenv("FVSRN_PAIR_FRAC");
-    return e ? std::atof(e) : 5.0;
-  }();
-  const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
-  if (frame && m->hid_pad == 32 && (double)n_slots <= pair_frac * (double)full_lanes)
-    return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1,
-                  fmode);
   const KernelKind k = frame ? KernelKind::kDVRTex : KernelKind::kDVR;
   return launch(m, k, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 32 + 1, fmode);
 }
@@ -1442,12 +1452,23 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
     std::vector<__half> wt;
     std::vector<float> bt;
     for (int l = 0; l < L; ++l) {
-      const int Nt = (l == L - 1) ? 16 : H, K = Ks[l];
+      const int Nt = (l == L - 1) ? 16 : H, Kw = Ks[l];
+      // bias in the MMA (tc_bias_mma): layers >= 1 get an extra k16 tile carrying the bias as fp16
+      // hi + lo (column Kw: hi, Kw + 1: lo; the A side holds 1, 1 there)
+      const bool bias_mma = tc_bias_mma(H);
+      const int K = (bias_mma && l > 0) ? Kw + 16 : Kw;
       std::vector<__half> tile((size_t)Nt * K, __float2half_rn(0.f));
-      for (int n = 0; n < Nt && n < N[l]; ++n)
-        for (int k = 0; k < K; ++k)
-          tile[(size_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] =
-              __float2half_rn(ws[l][(size_t)n * K + k]);
+      auto at = [&](int n, int k) -> __half& {
+        return tile[(size_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)];
+      };
+      for (int n = 0; n < Nt && n < N[l]; ++n) {
+        for (int k = 0; k < Kw; ++k) at(n, k) = __float2half_rn(ws[l][(size_t)n * Kw + k]);
+        if (bias_mma && l > 0) {
+          const __half hi = __float2half_rn(bs[l][n]);
+          at(n, Kw) = hi;
+          at(n, Kw + 1) = __float2half_rn(bs[l][n] - __half2float(hi));
+        }
+      }
       wt.insert(wt.end(), tile.begin(), tile.end());
       for (int n = 0; n < Nt; ++n) bt.push_back(n < N[l] ? bs[l][n] : 0.f);
     }

@@ -205,6 +205,15 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (S::kBiasMma) {
+    static_assert(S::kA0, "bias-in-MMA needs the layer-0 rows in TMEM");
+    // W0's pad column (K0 - 1; the row's pad is 1.0) := this frame's layer-0 bias
+    constexpr int K = S::kK0, k = S::kK0 - 1;
+    for (int n = tid; n < HID; n += kTcThreads)
+      w_s[(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] = __float2half_rn(b_s[n]);
+    fence_proxy_async_smem();
+    __syncthreads();
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
   const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar), mb1 = smem_u32(mbar1);
@@ -238,7 +247,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     }
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
-    tmem_bias<HID>(t_row, b_s + S::b_off(0));
+    if constexpr (!S::kBiasMma) tmem_bias<HID>(t_row, b_s + S::b_off(0));
     if constexpr (kA0) {
       // tcgen05.st is .sync.aligned: every lane stores (rays-less lanes a zero row)
       uint32_t w[FastRow<NM>::kWords];
@@ -259,6 +268,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
 #pragma unroll
         for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
       }
+      if constexpr (S::kBiasMma) w[FastRow<NM>::kWords - 1] |= 0x3C000000u;   // pad column = 1.0
       tmem_st_any<FastRow<NM>::kWords>(t_row + S::kTCols, w);
     } else if (r.has) {
       const float kf = (float)r.k;
@@ -273,7 +283,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     for (int l = 0; l < NL; ++l) {
       if (tid == 0) {
         tc_fence_after();
-        const int K = l == 0 ? S::kK0 : HID;
+        const int K = l == 0 ? S::kK0 : S::kKh;
         const int N = l == NL - 1 ? S::kNLast : HID;
         const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
         const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
@@ -293,11 +303,13 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           const uint32_t id = idesc_f16(128, N);
 #pragma unroll
           for (int kk = 0; kk < K / 16; ++kk) {
+            // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
+            const uint32_t acc = (S::kBiasMma && kk == 0) ? 0u : 1u;
             if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
-              umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+              umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
             else
               umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
-                       smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
+                       smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
           }
           umma_commit(mb);
         }
@@ -336,8 +348,10 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           tc_fence_after();
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          }
           act_words<32>(acc, w1);
           tmem_st<16>(t_row + S::kTCols, w0);
           tmem_st<16>(t_row + S::kTCols + 16, w1);
@@ -350,16 +364,20 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           tmem_st<16>(t_row + S::kTCols, w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          }
           act_words<32>(acc, w);
           tmem_st<16>(t_row + S::kTCols + 16, w);
         } else if constexpr (FVSRN_TC_TMEM_A) {
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
           tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          }
           uint32_t w[HID / 2];
           act_words<HID>(acc, w);
           tmem_st<HID / 2>(t_row + S::kTCols, w);
@@ -370,16 +388,26 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           act_row<32>(acc, myrow);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          }
           act_row<32>(acc, myrow + 4 * 64);
         } else {
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
           tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          }
           act_row<HID>(acc, myrow);
+        }
+        if constexpr (S::kBiasMma) {
+          if (l == 0) {   // the bias tile of layers >= 1: A columns HID/2.. = [1, 1, 0, ...]
+            uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            tmem_st_x8(t_row + S::kTCols + HID / 2, c);
+          }
         }
         tmem_wait_st();
         fence_proxy_async_smem();

@@ -48,15 +48,30 @@ __host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / 
 #ifndef FVSRN_TC_TMEM_A0
 #define FVSRN_TC_TMEM_A0 1
 #endif
+// FVSRN_TC_BIAS_MMA: the biases ride in the MMA instead of a per-layer tcgen05.st of the
+// bias row into the accumulators: layer 0 through the input row's pad column (1.0) and a
+// bias column of W0 patched in per frame; hidden / last layers through one extra k16 tile
+// (A: constant [1, 1, 0...], B: the bias split into fp16 hi + lo columns)
+// (measured: 4x32 cfg 2 3.22 -> 3.02 ms, 86 instead of 96 registers; 6x64 cfg 3 25.4 -> 26.2
+// ms, the k16 bias tile lengthens the per-layer MMA the CTA waits on)
+#ifndef FVSRN_TC_BIAS_MMA32
+#define FVSRN_TC_BIAS_MMA32 1
+#endif
+#ifndef FVSRN_TC_BIAS_MMA64
+#define FVSRN_TC_BIAS_MMA64 0
+#endif
+constexpr bool tc_bias_mma(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0; }
 template <int HID, int NM, int NL>
 struct TcShape {
   static constexpr int kK0 = tc_round(16 + 2 * NM + 3, 16);   // FastRow<NM>::kK0
-  static constexpr int kKA = kK0 > HID ? kK0 : HID;          // A tile width (halfs)
+  static constexpr bool kBiasMma = tc_bias_mma(HID);
+  static constexpr int kKh = HID + (kBiasMma ? 16 : 0);   // K of layers 1..NL-1
+  static constexpr int kKA = kK0 > kKh ? kK0 : kKh;          // A tile width (halfs)
   static constexpr int kNLast = 16;
   static constexpr int kTCols = HID <= 32 ? 32 : (HID <= 64 ? 64 : 128);
   static constexpr uint32_t kSboA = (uint32_t)(kKA / 8) * 128u;
-  static constexpr int w_off(int l) { return l == 0 ? 0 : HID * kK0 + (l - 1) * HID * HID; }
-  static constexpr int kWTotal = HID * kK0 + (NL - 2) * HID * HID + kNLast * HID;   // halfs
+  static constexpr int w_off(int l) { return l == 0 ? 0 : HID * kK0 + (l - 1) * HID * kKh; }
+  static constexpr int kWTotal = HID * kK0 + (NL - 2) * HID * kKh + kNLast * kKh;   // halfs
   static constexpr int b_off(int l) { return l * HID; }
   static constexpr int kBTotal = (NL - 1) * HID + kNLast;
   // shared memory map (bytes)
