@@ -27,7 +27,13 @@ $(LIB): $(OBJS)
 variant: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) $(VDEFS) -shared -o build/libfvsrn_$(VNAME).so $(SRCS) $(LDLIBS) 2> build/ptxas_$(VNAME).log || (cat build/ptxas_$(VNAME).log; false)
 
+# A/B of a tcgen05-kernel-only switch: recompiles fvsrn_tc.cu alone and links it with the
+# default objects: make tcvariant VDEFS="-DFVSRN_TC_POLY=8" VNAME=tp8
+tcvariant: $(OBJS)
+	$(NVCC) $(NVFLAGS) $(VDEFS) -c -o build/tc_$(VNAME).o $(CSRC)/fvsrn_tc.cu 2> build/ptxas_$(VNAME).log || (cat build/ptxas_$(VNAME).log; false)
+	$(NVCC) $(ARCH) -shared -o build/libfvsrn_$(VNAME).so $(filter-out build/fvsrn_tc.o,$(OBJS)) build/tc_$(VNAME).o $(LDLIBS)
+
 clean:
 	rm -f $(LIB) $(OBJS)
 
-.PHONY: all clean variant
+.PHONY: all clean variant tcvariant

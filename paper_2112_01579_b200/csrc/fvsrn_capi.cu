@@ -1461,8 +1461,10 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       auto at = [&](int n, int k) -> __half& {
         return tile[(size_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)];
       };
+      // skip path (tc_skip): the fp16 tiles of layers >= 1 multiply cos(a), with weight -2 W
+      const float wscale = (tc_skip(H) && l > 0) ? -2.f : 1.f;
       for (int n = 0; n < Nt && n < N[l]; ++n) {
-        for (int k = 0; k < Kw; ++k) at(n, k) = __float2half_rn(ws[l][(size_t)n * Kw + k]);
+        for (int k = 0; k < Kw; ++k) at(n, k) = __float2half_rn(wscale * ws[l][(size_t)n * Kw + k]);
         if (bias_mma && l > 0) {
           const __half hi = __float2half_rn(bs[l][n]);
           at(n, Kw) = hi;
@@ -1471,6 +1473,26 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       }
       wt.insert(wt.end(), tile.begin(), tile.end());
       for (int n = 0; n < Nt; ++n) bt.push_back(n < N[l] ? bs[l][n] : 0.f);
+    }
+    if (tc_skip(H)) {
+      // tf32 tiles (f32 storage, rounded to nearest tf32) of layers >= 1 multiplying a itself:
+      // element (n, k) at float (n/8)*(H/4)*32 + (k/4)*32 + (n%8)*4 + (k%4)
+      for (int l = 1; l < L; ++l) {
+        const int Nt = (l == L - 1) ? 16 : H, Kw = Ks[l];
+        std::vector<float> tile((size_t)Nt * H, 0.f);
+        for (int n = 0; n < Nt && n < N[l]; ++n)
+          for (int k = 0; k < Kw && k < H; ++k) {
+            uint32_t u;
+            const float w = ws[l][(size_t)n * Kw + k];
+            std::memcpy(&u, &w, 4);
+            if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+            float q;
+            std::memcpy(&q, &u, 4);
+            tile[(size_t)(n / 8) * (H / 4) * 32 + (k / 4) * 32 + (n % 8) * 4 + (k % 4)] = q;
+          }
+        const __half* hp = reinterpret_cast<const __half*>(tile.data());
+        wt.insert(wt.end(), hp, hp + 2 * tile.size());
+      }
     }
     int rc = upload(wt.data(), wt.size() * sizeof(__half), (void**)&m->d_wtc);
     if (rc) return rc;

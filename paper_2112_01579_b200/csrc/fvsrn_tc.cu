@@ -16,6 +16,12 @@
 // The MLP never touches global memory; the HMMA issue slots and the B-fragment LDS of
 // the mma.sync kernel disappear from the SM sub-partitions' instruction streams.
 // Used for the default fV-SRN configurations (FastRow inputs, snake_alt, 32/64 wide).
+// The tcgen05 kernels are issue-bound with XU headroom (cfg 2: issue 74%, XU 63%), the
+// mma.sync ones XU-bound: here the NeRF base angles go to MUFU.SIN/COS (3 issue slots per
+// axis instead of 15 FMA-pipe operations): cfg 2 2.86 -> 2.82 ms, cfg 5 42.6 -> 41.6 ms
+#ifndef FVSRN_FOURIER_POLY
+#define FVSRN_FOURIER_POLY 0
+#endif
 #include "fvsrn_march.cuh"
 #include "fvsrn_tc.cuh"
 #include "fvsrn_tmem.cuh"
@@ -121,6 +127,42 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[HID], uint32_t (
   }
 }
 
+// cos(a) on the FMA pipe (range reduction by the 1.5*2^23 trick, degree-4 minimax in r^2
+// of cos(2 pi r), |err| < 4.3e-5): 8 FP32 operations, no MUFU
+__device__ __forceinline__ float cos_fma(float x) {
+  const float kb = fmaf(x, 0.15915494309189535f, 12582912.f);
+  const float k = kb - 12582912.f;
+  const float r = fmaf(x, 0.15915494309189535f, -k);
+  const float u = r * r;
+  float p = fmaf(45.62269592285156f, u, -82.3971176147461f);
+  p = fmaf(p, u, 64.67363739013672f);
+  p = fmaf(p, u, -19.731164932250977f);
+  return fmaf(p, u, 0.9999644756317139f);
+}
+
+// skip path: cos(a) of one accumulator row -> fp16 chunks of the shared-memory A tile row
+// (every FVSRN_TC_POLY-th element on the FMA pipe, as act_row)
+template <int HID>
+__device__ __forceinline__ void cos_row(const uint32_t (&acc)[HID], __half* row) {
+  constexpr int P = FVSRN_TC_POLY;
+#pragma unroll
+  for (int c = 0; c < HID / 8; ++c) {
+    uint32_t w4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float h[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int e = 8 * c + 2 * j + i;
+        const float x = __uint_as_float(acc[e]);
+        h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? cos_fma(x) : __cosf(x);
+      }
+      w4[j] = pack_half2(h[0], h[1]);
+    }
+    *reinterpret_cast<uint4*>(row + c * 64) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[N]) {
   if constexpr (N == 16) tmem_st_x16(taddr, r);
@@ -180,21 +222,27 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   {
     const uint4* src = net.w;
     uint4* dst = reinterpret_cast<uint4*>(w_s);
-    for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
+    for (int i = tid; i < S::kWBytes / 16; i += kTcThreads) dst[i] = src[i];
     for (int i = tid; i < S::kBTotal; i += kTcThreads)
       b_s[i] = (b0 && i < HID) ? b0[i] : net.b[i];
     const int words = sizeof(TFDev) / 4;
     const int* ts = reinterpret_cast<const int*>(tf_g);
     int* td = reinterpret_cast<int*>(tf);
     for (int i = tid; i < words; i += kTcThreads) td[i] = ts[i];
-    if constexpr (!S::kA0) {
-      uint4* az = reinterpret_cast<uint4*>(a_s);   // pad columns must stay finite
-      for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
+    if constexpr (!S::kA0 || S::kSkip) {
+      // pad columns must stay finite; skip path: columns HID, HID+1 = 1.0 (the bias tile)
+      uint4* az = reinterpret_cast<uint4*>(a_s);
+      for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) {
+        const bool ones = S::kSkip && (i / 8) % (S::kKA / 8) == HID / 8;   // chunk of columns HID..HID+7
+        az[i] = make_uint4(ones ? 0x3C003C00u : 0u, 0u, 0u, 0u);
+      }
     }
   }
   constexpr bool kA0 = S::kA0;
   // TMEM columns: D [0, kTCols), A [kTCols, kTCols + max(K0, HID)/2)
-  constexpr uint32_t kAcols = kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
+  // skip path: the A columns are the second accumulator region (layer-0 rows, then the
+  // odd layers' accumulators)
+  constexpr uint32_t kAcols = S::kSkip ? S::kTCols : kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
   constexpr uint32_t kNeed = S::kTCols + kAcols;
   constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
@@ -287,7 +335,17 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         const int N = l == NL - 1 ? S::kNLast : HID;
         const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
         const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
-        if (kNSplit && l < NL - 1 && ((FVSRN_TC_TMEM_A && l > 0) || kA0)) {
+        if (S::kSkip && l > 0) {
+          // D_l = a_{l-1} x W_l (tf32, issued when layer l-1 completed, below)
+          //     + cos(a_{l-1}) (fp16 smem tile) x (-2 W_l) + [1, 1] x [b_hi, b_lo]
+          const uint32_t d = tmem + (uint32_t)((l & 1) * S::kTCols);
+          const uint32_t id16 = idesc_f16(128, N);
+#pragma unroll
+          for (int kk = 0; kk < S::kKh / 16; ++kk)
+            umma_f16(d, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
+                     smem_desc(wb + kk * 256u, 128u, sbo_b), id16, 1u);
+          umma_commit(mb);
+        } else if (kNSplit && l < NL - 1 && ((FVSRN_TC_TMEM_A && l > 0) || kA0)) {
           // two N=32 halves: rows 32..63 of the K-major weight tile start 4 core-matrix
           // groups (4 * SBO) further on
           const uint32_t id = idesc_f16(128, 32);
@@ -333,7 +391,28 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       }
       phase ^= 1u;
       tc_fence_after();
-      if (l < NL - 1) {
+      if (S::kSkip && l < NL - 1) {
+        if (tid == 0) {
+          // the a x W part of the next layer only needs this layer's accumulators: issue it
+          // now, so the tensor core works under the cos evaluation below
+          const int N1 = l + 1 == NL - 1 ? S::kNLast : HID;
+          const uint32_t d = tmem + (uint32_t)(((l + 1) & 1) * S::kTCols);
+          const uint32_t ax = tmem + (uint32_t)((l & 1) * S::kTCols);
+          const uint32_t xb = w_base + (uint32_t)S::x_off(l + 1);
+          const uint32_t id32 = idesc_tf32(128, N1);
+#pragma unroll
+          for (int kk = 0; kk < HID / 8; ++kk)
+            umma_tf32_ts(d, ax + kk * 8u, smem_desc(xb + kk * 256u, 128u, S::kSboX), id32, kk > 0 ? 1u : 0u);
+        }
+        // cos(a) of this layer's accumulator region -> the shared-memory A tile
+        uint32_t acc[HID];
+        tmem_ld<HID>(t_row + (uint32_t)((l & 1) * S::kTCols), acc);
+        tmem_wait_ld();
+        cos_row<HID>(acc, myrow);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+      } else if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
         // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
         if constexpr (kNSplit) {
@@ -410,12 +489,13 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           }
         }
         tmem_wait_st();
-        fence_proxy_async_smem();
+        // the next A operand went to TMEM (tcgen05.st): no generic-proxy smem writes
+        if constexpr (!FVSRN_TC_TMEM_A) fence_proxy_async_smem();
         tc_fence_before();
         __syncthreads();
       } else {
         uint32_t o[4];
-        tmem_ld_x4(t_row, o);
+        tmem_ld_x4(t_row + (uint32_t)(S::kSkip ? ((NL - 1) & 1) * S::kTCols : 0), o);
         tmem_wait_ld();
         if (r.has)
           composite_step(r, make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
