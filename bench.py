@@ -144,10 +144,12 @@ def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
     hidden activation except the ones evaluated on the FMA pipe (tcgen05 kernel: every 6th
     element of a row, FVSRN_TC_POLY; mma.sync kernels: none, FVSRN_POLY_EVERY=0), plus
     MUFU.TANH for the sigmoid head and MUFU.EX2 for alpha.  The NeRF base sin/cos run on
-    the FMA pipe (FVSRN_FOURIER_POLY=1)."""
+    the FMA pipe in the mma.sync kernels (FVSRN_FOURIER_POLY=1) and on MUFU.SIN/COS in the
+    tcgen05 kernels (3 axes x 2)."""
     layers, hid = model_cfg["layers"], model_cfg["hidden"]
-    per_row = hid - hid // 6 if kernel.startswith("dvr_tc") else hid
-    return (layers - 1) * per_row + 2
+    tc = kernel.startswith("dvr_tc")
+    per_row = hid - hid // 6 if tc else hid
+    return (layers - 1) * per_row + 2 + (6 if tc else 0)
 
 
 def measured_peaks():
@@ -159,13 +161,25 @@ def measured_peaks():
     return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
 
 
-def ncu_traffic(config: str):
+def _kernel_key(name: str) -> str:
+    """'void fvsrn::dvr_tc_kernel<(int)32, (int)14, ...>(...)' / 'dvr_tc_kernel<32,14,...> (...)'
+    -> 'dvr_tc_kernel<32,14,...>'"""
+    n = name.replace("void ", "").replace("fvsrn::", "").replace("(int)", "").replace("(bool)", "")
+    n = n.split("(")[0] if "<" not in n.split("(")[0] else n[: n.index(">") + 1]
+    return n.replace(" ", "")
+
+
+def ncu_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/ncu_summary.json), used only when that capture is of the kernel this run
+    launched; otherwise null."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         with open(p) as f:
             d = json.load(f)
         e = d.get(config, {})
-        return e.get("dram_bytes_per_launch"), e
+        if e and _kernel_key(e.get("kernel", "")) == _kernel_key(kernel):
+            return e.get("dram_bytes_per_launch"), e
     return None, {}
 
 
@@ -625,7 +639,7 @@ def main():
     # stream); its algorithmic FLOPs are rank 0's share of the evaluations
     rank0_evals = total_evals / world
     achieved = rank0_evals * flops / (dom_ms / 1e3) / 1e12
-    traffic, ncu = ncu_traffic(args.config)
+    traffic, ncu = ncu_traffic(args.config, kernel_desc)
     mufu_per_eval = mufu_per_eval_of(cfg["model"], kernel_desc)
     sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
     xu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
