@@ -650,7 +650,8 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kSample: k = "sample_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, frame specialisation)"; break;
-    case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, two lanes per ray)"; break;
+    case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + ",2> (mma.sync m16n8k16, two lanes per ray)"; break;
+    case KernelKind::kDVRQuad: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + ",4> (mma.sync m16n8k16, four lanes per ray)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -704,6 +705,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
   if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPair ||
+      kind == KernelKind::kDVRQuad ||
       kind == KernelKind::kDVRPipe ||
       tc ||
       kind == KernelKind::kDVRDual) {
@@ -713,7 +715,9 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
     // (two lanes per ray: 2.25 work slots per lane, measured at 256^2: 1.75 0.256 ms,
     // 2.0-2.5 0.225-0.228, 3.0 0.240; FVSRN_SLOTS_PER_LANE overrides both)
     static const char* spl_env = std::getenv("FVSRN_SLOTS_PER_LANE");
-    const double slots_per_lane = spl_env ? std::atof(spl_env) : (kind == KernelKind::kDVRPair ? 2.25 : 1.75);
+    static const char* spl4_env = std::getenv("FVSRN_SLOTS_PER_LANE4");
+    const double slots_per_lane = kind == KernelKind::kDVRQuad ? (spl4_env ? std::atof(spl4_env) : 2.25)
+                                  : spl_env ? std::atof(spl_env) : (kind == KernelKind::kDVRPair ? 2.25 : 1.75);
     const double rays_per_sm_cta = (double)m->num_sms * threads;
     const int occ_work = (int)std::lround((double)work_warps * 32.0 / (rays_per_sm_cta * slots_per_lane));
     occ = std::max(1, std::min(occ, occ_work));
@@ -789,9 +793,20 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
     return e ? std::atof(e) : 5.0;
   }();
   const long long full_lanes = (long long)m->num_sms * kThreads * kMinBlocks;
+  // four lanes per ray up to 2x the resident lanes (~435^2; tools/frame_sweep.py, cfg-2
+  // model at stepsize 1/256: 128^2 0.32 -> 0.21 ms, 256^2 0.44 -> 0.38, 320^2 0.61 -> 0.52,
+  // 384^2 0.69 -> 0.65, 512^2 equal); FVSRN_QUAD_FRAC overrides (0 = off)
+  static const double quad_frac = [] {
+    const char* e = std::getenv("FVSRN_QUAD_FRAC");
+    return e ? std::atof(e) : 2.0;
+  }();
+  const double frame_px = (double)cam.W * (double)cam.H;
   const bool small = frame && m->hid_pad == 32 && dvr_mode() != DvrMode::kTC &&
-                     (double)cam.W * (double)cam.H <= pair_frac * (double)full_lanes;
+                     frame_px <= pair_frac * (double)full_lanes;
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+  if (small && frame_px <= quad_frac * (double)full_lanes)
+    return launch(m, KernelKind::kDVRQuad, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 8 + 1,
+                  fmode);
   if (small)
     return launch(m, KernelKind::kDVRPair, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 16 + 1,
                   fmode);

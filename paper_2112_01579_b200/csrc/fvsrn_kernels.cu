@@ -137,60 +137,82 @@ dvr_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* 
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
 }
 
-// ---------------------------------------------------------------- small frames: two lanes per ray
+// ---------------------------------------------------------------- small frames: Q lanes per ray
 // A frame with fewer rays than the GPU has lanes to spare is bound by its longest rays'
-// sequential march.  Here a ray occupies a lane pair: per warp step the even lane evaluates
-// sample k and the odd lane sample k+1 (one MLP pass over 16 rays x 2 samples), and the
-// even lane composites them in order -- sample k, its early-termination check, then sample
-// k+1 (render.py:226-232) -- so a ray advances two samples per step and every pixel is
-// bit-identical to the one-lane march.  A sample evaluated after its ray terminated is
-// discarded and not counted (the count stays the reference's: samples the march uses).
-// Frame specialisation only (static fp16 grid through the texture units (TEX 1) or exact-
-// weight loads (TEX 2), density head, camera rays).
-template <int HID, int NM, int NL, int TEX>
+// sequential march.  Here a ray occupies a group of Q lanes (Q = 2 or 4): per warp step
+// lane q of the group evaluates sample k+q (one MLP pass over 32/Q rays x Q samples), and
+// the group leader composites them in order -- sample k, its early-termination check,
+// then k+1, ... (render.py:226-232) -- so a ray advances Q samples per step and every
+// pixel is bit-identical to the one-lane march.  A sample evaluated after its ray
+// terminated is discarded and not counted (the count stays the reference's: samples the
+// march uses).  Frame specialisation only (static fp16 grid through the texture units
+// (TEX 1) or exact-weight loads (TEX 2), density head, camera rays).
+template <int HID, int NM, int NL, int TEX, int Q>
 __global__ void __launch_bounds__(kThreads, min_blocks<HID>())
 dvr_pair_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
                 MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
                 float* __restrict__ out, unsigned long long* __restrict__ queue,
                 unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
+  static_assert(Q == 2 || Q == 4, "lanes per ray");
   const int rs = fd.k0 + 8;
   uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
   stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
   const int lane = threadIdx.x & 31;
-  const bool odd = (lane & 1) != 0;
+  const int qi = lane & (Q - 1), lead = lane & ~(Q - 1);
   __half* myrow = stage + lane * rs;
   RayLane r;
   r.has = false;
   LaneQueue q{0, 0, false};
   unsigned used = 0;
   while (true) {
-    pair_refill(r, q, lane, cam, sh, rr, n_slots, queue, md, out);
+    pair_refill<Q>(r, q, lane, cam, sh, rr, n_slots, queue, md, out);
     if (__ballot_sync(0xffffffffu, r.has) == 0) break;
-    // even lane: sample k; hands sample k+1's position to its odd partner
-    const float kf = (float)r.k;
-    const float px0 = fmaf(kf, r.dd0, r.pe0), py0 = fmaf(kf, r.dd1, r.pe1), pz0 = fmaf(kf, r.dd2, r.pe2);
-    const float kf1 = (float)(r.k + 1);
-    const float px1 = fmaf(kf1, r.dd0, r.pe0), py1 = fmaf(kf1, r.dd1, r.pe1), pz1 = fmaf(kf1, r.dd2, r.pe2);
-    const bool next = r.has && r.k + 1 < r.n;
-    const float qx = __shfl_sync(0xffffffffu, px1, lane & ~1), qy = __shfl_sync(0xffffffffu, py1, lane & ~1),
-                qz = __shfl_sync(0xffffffffu, pz1, lane & ~1);
-    const bool partner_next = __shfl_sync(0xffffffffu, next, lane & ~1);   // every lane shuffles
-    const bool mine = odd ? partner_next : r.has;
+    float px, py, pz;
+    bool mine;
+    if constexpr (Q == 2) {
+      // even lane: sample k; it hands sample k+1's position to its odd partner
+      const float kf = (float)r.k, kf1 = (float)(r.k + 1);
+      const float px1 = fmaf(kf1, r.dd0, r.pe0), py1 = fmaf(kf1, r.dd1, r.pe1), pz1 = fmaf(kf1, r.dd2, r.pe2);
+      const bool next = r.has && r.k + 1 < r.n;
+      const float qx = __shfl_sync(0xffffffffu, px1, lead), qy = __shfl_sync(0xffffffffu, py1, lead),
+                  qz = __shfl_sync(0xffffffffu, pz1, lead);
+      const bool partner_next = __shfl_sync(0xffffffffu, next, lead);   // every lane shuffles
+      const bool odd = qi != 0;
+      mine = odd ? partner_next : r.has;
+      px = odd ? qx : fmaf(kf, r.dd0, r.pe0);
+      py = odd ? qy : fmaf(kf, r.dd1, r.pe1);
+      pz = odd ? qz : fmaf(kf, r.dd2, r.pe2);
+    } else {
+      // lane qi of the group: sample k + qi of the leader's ray (the same FMAs the leader
+      // would do, on the leader's values); every lane shuffles
+      const float pe0 = __shfl_sync(0xffffffffu, r.pe0, lead), pe1 = __shfl_sync(0xffffffffu, r.pe1, lead),
+                  pe2 = __shfl_sync(0xffffffffu, r.pe2, lead);
+      const float dd0 = __shfl_sync(0xffffffffu, r.dd0, lead), dd1 = __shfl_sync(0xffffffffu, r.dd1, lead),
+                  dd2 = __shfl_sync(0xffffffffu, r.dd2, lead);
+      const int k = __shfl_sync(0xffffffffu, r.k, lead), n = __shfl_sync(0xffffffffu, r.n, lead);
+      const bool has = __shfl_sync(0xffffffffu, r.has, lead);
+      mine = has && k + qi < n;
+      const float kf = (float)(k + qi);
+      px = fmaf(kf, dd0, pe0); py = fmaf(kf, dd1, pe1); pz = fmaf(kf, dd2, pe2);
+    }
     if (mine) {
-      if constexpr (TEX == 1) FastRow<NM>::build_tex(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
-      else FastRow<NM>::build_ldg(fd, odd ? qx : px0, odd ? qy : py0, odd ? qz : pz0, myrow);
+      if constexpr (TEX == 1) FastRow<NM>::build_tex(fd, px, py, pz, myrow);
+      else FastRow<NM>::build_ldg(fd, px, py, pz, myrow);
     }
     __syncwarp();
     MLPDispatch<HID, 4, NL, fast_kt0<NM>()>::eval32(stage, rs, net, wf_s, b_s, ob, lane);
     __syncwarp();
-    const float4 o = *reinterpret_cast<const float4*>(ob + 4 * lane);
-    const float4 o1 = make_float4(__shfl_down_sync(0xffffffffu, o.x, 1), __shfl_down_sync(0xffffffffu, o.y, 1),
-                                  __shfl_down_sync(0xffffffffu, o.z, 1), __shfl_down_sync(0xffffffffu, o.w, 1));
-    if (!odd && r.has) {
-      composite_step(r, o, true, *tf, md, out, nonfinite);
-      ++used;
-      if (r.has) {      // still marching: r.k is now k + 1 < n, the partner's sample
-        composite_step(r, o1, true, *tf, md, out, nonfinite);
+    float4 o[Q];
+    o[0] = *reinterpret_cast<const float4*>(ob + 4 * lane);
+#pragma unroll
+    for (int j = 1; j < Q; ++j)
+      o[j] = make_float4(__shfl_down_sync(0xffffffffu, o[0].x, j), __shfl_down_sync(0xffffffffu, o[0].y, j),
+                         __shfl_down_sync(0xffffffffu, o[0].z, j), __shfl_down_sync(0xffffffffu, o[0].w, j));
+    if (qi == 0) {
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        if (!r.has) break;      // ended (end of ray or early termination) before sample k + j
+        composite_step(r, o[j], true, *tf, md, out, nonfinite);
         ++used;
       }
     }
@@ -871,8 +893,12 @@ const void* kernel_for(KernelKind kind, int hid, bool fast, int fmode) {
           : (const void*)dvr_kernel<H, 4, (H - 4) / 2, fast_layers(H), 1>;                   \
     if (kind == KernelKind::kDVRPair)                                                        \
       return !fast ? nullptr : fmode == 2                                                    \
-          ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2>                  \
-          : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1>;                 \
+          ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2, 2>               \
+          : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1, 2>;              \
+    if (kind == KernelKind::kDVRQuad)                                                        \
+      return !fast ? nullptr : fmode == 2                                                    \
+          ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2, 4>               \
+          : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1, 4>;              \
     FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \

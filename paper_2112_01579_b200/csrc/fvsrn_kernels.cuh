@@ -101,7 +101,7 @@ struct RayRecs {
 // (kDVRTCTex, kSampleTex: the same for the tcgen05 march and the lattice decode)
 // (kDVRPair: the frame specialisation with two lanes per ray, for small frames)
 enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused, kDVRTex, kDVRTCTex,
-                        kSampleTex, kDVRPair };
+                        kSampleTex, kDVRPair, kDVRQuad };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

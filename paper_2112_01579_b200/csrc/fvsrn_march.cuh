@@ -85,22 +85,25 @@ __device__ __forceinline__ void ws_refill(RayLane& r, LaneQueue& q, int lane, co
 
 // ws_refill for the two-lanes-per-ray kernel: only even lanes own rays (the odd partner
 // evaluates the ray's next sample), so only they take slots from the queue.
+template <int Q = 2>
 __device__ __forceinline__ void pair_refill(RayLane& r, LaneQueue& q, int lane, const CamDev& cam,
                                             const ShardDev& sh, const RayRecs& rr, long long n_slots,
                                             unsigned long long* __restrict__ queue, const MarchDev& md,
                                             float* __restrict__ out) {
-  const bool even = (lane & 1) == 0;
+  // Q lanes per ray: the group leaders (lane % Q == 0) hold the rays; chunks of 32/Q slots
+  constexpr int kChunk = 32 / Q;
+  const bool even = (lane & (Q - 1)) == 0;
   while (true) {
     const unsigned need = __ballot_sync(0xffffffffu, even && !r.has);
     if (need == 0) break;
     if (q.chunk_left == 0) {
       if (q.qdone) break;
       unsigned long long cb = 0;
-      if (lane == 0) cb = atomicAdd(queue, 16ull);
+      if (lane == 0) cb = atomicAdd(queue, (unsigned long long)kChunk);
       cb = __shfl_sync(0xffffffffu, cb, 0);
       if ((long long)cb >= n_slots) { q.qdone = true; break; }
       q.chunk_base = (long long)cb;
-      q.chunk_left = (int)min(16ll, n_slots - (long long)cb);
+      q.chunk_left = (int)min((long long)kChunk, n_slots - (long long)cb);
     }
     const int rank = __popc(need & lanemask_lt());
     const int take = min(__popc(need), q.chunk_left);

@@ -262,6 +262,15 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     fence_proxy_async_smem();
     __syncthreads();
   }
+  if constexpr (S::kBiasCp) {
+    // bias broadcast tiles from b_s (b0 of this frame for layer 0)
+    for (int i = tid; i < S::kBTotal * 8; i += kTcThreads) {
+      const int c = i >> 3, r = i & 7;
+      *reinterpret_cast<float*>(smem + S::kBcOff + (c / 8) * 256 + ((c % 8) / 4) * 128 + r * 16 + (c % 4) * 4) = b_s[c];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
   const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar), mb1 = smem_u32(mbar1);
@@ -295,7 +304,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     }
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
-    if constexpr (!S::kBiasMma) tmem_bias<HID>(t_row, b_s + S::b_off(0));
+    if constexpr (!S::kBiasMma && !S::kBiasCp) tmem_bias<HID>(t_row, b_s + S::b_off(0));
     if constexpr (kA0) {
       // tcgen05.st is .sync.aligned: every lane stores (rays-less lanes a zero row)
       uint32_t w[FastRow<NM>::kWords];
@@ -335,6 +344,13 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
         const int N = l == NL - 1 ? S::kNLast : HID;
         const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
         const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
+        if constexpr (S::kBiasCp) {
+          // D := this layer's bias (zero 8-row-group stride: the tile's row on every lane)
+          const uint32_t bt = smem_u32(smem) + (uint32_t)(S::kBcOff + S::b_off(l) * 32);
+#pragma unroll
+          for (int g = 0; g < (l == NL - 1 ? S::kNLast : HID) / 8; ++g)
+            tmem_cp_128x256b(tmem + 8u * g, smem_desc(bt + 256u * g, 128u, 0u));
+        }
         if (S::kSkip && l > 0) {
           // D_l = a_{l-1} x W_l (tf32, issued when layer l-1 completed, below)
           //     + cos(a_{l-1}) (fp16 smem tile) x (-2 W_l) + [1, 1] x [b_hi, b_lo]
@@ -427,7 +443,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           tc_fence_after();
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if constexpr (!S::kBiasMma) {
+          if constexpr (!S::kBiasMma && !S::kBiasCp) {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }
@@ -443,7 +459,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           tmem_st<16>(t_row + S::kTCols, w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if constexpr (!S::kBiasMma) {
+          if constexpr (!S::kBiasMma && !S::kBiasCp) {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }
@@ -453,7 +469,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
           tmem_wait_ld();
-          if constexpr (!S::kBiasMma) {
+          if constexpr (!S::kBiasMma && !S::kBiasCp) {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }
@@ -467,7 +483,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           act_row<32>(acc, myrow);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
-          if constexpr (!S::kBiasMma) {
+          if constexpr (!S::kBiasMma && !S::kBiasCp) {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }
@@ -476,7 +492,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
           tmem_wait_ld();
-          if constexpr (!S::kBiasMma) {
+          if constexpr (!S::kBiasMma && !S::kBiasCp) {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }

@@ -60,7 +60,20 @@ __host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / 
 #ifndef FVSRN_TC_BIAS_MMA64
 #define FVSRN_TC_BIAS_MMA64 0
 #endif
-constexpr bool tc_bias_mma(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0; }
+// FVSRN_TC_BIAS_CP: the biases are copied into the accumulators by the tensor core itself
+// (tcgen05.cp.128x256b from an 8-row shared-memory tile read with a zero 8-row-group
+// stride, i.e. one row broadcast to all 128 lanes), issued by the elected thread right
+// before the layer's MMAs: no per-thread LDS + tcgen05.st and no k16 bias tile
+#ifndef FVSRN_TC_BIAS_CP32
+#define FVSRN_TC_BIAS_CP32 0
+#endif
+#ifndef FVSRN_TC_BIAS_CP64
+#define FVSRN_TC_BIAS_CP64 0
+#endif
+constexpr bool tc_bias_cp(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_CP32 != 0 : FVSRN_TC_BIAS_CP64 != 0; }
+constexpr bool tc_bias_mma(int hid) {
+  return !tc_bias_cp(hid) && (hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0);
+}
 // FVSRN_TC_SKIP32: the 32-wide hidden layers take snake_alt apart inside the MMA,
 //   W h = W a - 2 W cos(a):
 // the pre-activation a is read straight from the previous layer's f32 accumulator in TMEM
@@ -96,7 +109,12 @@ struct TcShape {
   static constexpr int kWOff = 0;
   static constexpr int kBOff = tc_round(kWOff + kWBytes, 16);
   static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
-  static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
+  // bias broadcast tiles (tc_bias_cp): column c of the layer-major bias vector at byte
+  // (c/8)*256 + ((c%8)/4)*128 + r*16 + (c%4)*4 for the 8 identical rows r
+  static constexpr bool kBiasCp = tc_bias_cp(HID);
+  static constexpr int kBcOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
+  static constexpr int kBcBytes = kBiasCp ? kBTotal * 32 : 0;
+  static constexpr int kAOff = tc_round(kBcOff + kBcBytes, 128);
   static constexpr int kATile = kTcThreads * kKA * 2;
   // with layer-0 rows in TMEM the one-tile kernel has no shared-memory A tile
   static constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);

@@ -108,8 +108,8 @@ def test_render_multi_contract_errors(model):
 
 @pytest.mark.parametrize("res,tf,et", [(256, "grayscale", 0.999), (97, "warm", 0.5), (180, "two_peaks", 1.0)])
 def test_small_frame_pair_kernel_bit_identical(model, res, tf, et):
-    """Small camera frames march two lanes per ray (dvr_pair_kernel); the same rays through
-    raymarch_forward take the one-lane kernel.  Pixels and evaluated-sample counts must be
+    """Small camera frames march two or four lanes per ray (dvr_pair_kernel); the same rays
+    through raymarch_forward take the one-lane kernel.  Pixels and evaluated-sample counts must be
     identical (early termination on, loose and off)."""
     src = P.ModelSource(model, P.TF_PRESETS[tf])
     cam = P.fibonacci_cameras(8, res, res)[2]
@@ -129,3 +129,50 @@ def test_small_frame_pair_kernel_bit_identical(model, res, tf, et):
     assert "dvr_pair_kernel" in name, name
     assert np.array_equal(px.reshape(res, res, 4), img)
     assert src.last_eval_count == n_img
+
+
+_QUAD_SCRIPT = r"""
+import json, sys
+import numpy as np
+import paper_2112_01579_b200 as P
+from paper_2112_01579_b200 import device as D
+m = P.model_init(P.ModelConfig(layers=4, hidden=32, grid_resolution=32, grid_channels=16, seed=0))
+out = []
+for res, tf, et in ((256, "grayscale", 0.999), (97, "warm", 0.5), (180, "two_peaks", 1.0), (8, "grayscale", 0.999)):
+    src = P.ModelSource(m, P.TF_PRESETS[tf])
+    cam = P.fibonacci_cameras(8, res, res)[2]
+    st = P.RenderSettings(stepsize=1 / 128, early_term_alpha=et, background=(0.05, 0.1, 0.2))
+    prev = D.set_dvr_kernel("warp")
+    try:
+        D.kernel_timer(True)
+        img = P.render_image(src, cam, st).data.copy()
+        D.kernel_timer_read()
+        name = D.kernel_timer_info()
+        D.kernel_timer(False)
+        n_img = src.last_eval_count
+        o, d = P.camera_rays(cam)
+        px, _ = P.raymarch_forward(src, o, d, st)
+    finally:
+        D.set_dvr_kernel(prev)
+    out.append({"res": res, "kernel": name, "equal": bool(np.array_equal(px.reshape(res, res, 4), img)),
+                "count_equal": src.last_eval_count == n_img})
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("quad_frac,lanes", [("100", "four lanes per ray"), ("0", "two lanes per ray")])
+def test_small_frame_lane_group_kernels_bit_identical(quad_frac, lanes):
+    """Four lanes per ray (FVSRN_QUAD_FRAC admits the frame) and two lanes per ray
+    (FVSRN_QUAD_FRAC=0): pixels and counts identical to the one-lane march, ET on / loose /
+    off, and a frame smaller than one warp's rays."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, FVSRN_QUAD_FRAC=quad_frac)
+    r = subprocess.run([sys.executable, "-c", _QUAD_SCRIPT], env=env, capture_output=True, text=True,
+                       timeout=300, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    for case in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert lanes in case["kernel"], case
+        assert case["equal"] and case["count_equal"], case

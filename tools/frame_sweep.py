@@ -1,6 +1,8 @@
 """Device ms/frame of the config-2 model across frame sizes (CUDA events around
 render_device, L2 flushed between frames), for tuning the small-frame paths:
-    FVSRN_PAIR_FRAC=0 python tools/frame_sweep.py ; python tools/frame_sweep.py"""
+    FVSRN_PAIR_FRAC=0 python tools/frame_sweep.py ; python tools/frame_sweep.py
+    FVSRN_QUAD_FRAC=5 python tools/frame_sweep.py   (four lanes per ray)
+    python tools/frame_sweep.py 128 256 384        (sizes)"""
 import os
 import sys
 
@@ -14,7 +16,7 @@ src = P.ModelSource(m, P.TF_PRESETS["grayscale"])
 st = P.RenderSettings(stepsize=1 / 256)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream()
-for res in (128, 192, 256, 320, 384, 448, 512, 640, 768):
+for res in ([int(a) for a in sys.argv[1:]] or (128, 192, 256, 320, 384, 448, 512, 640, 768)):
     cams = P.fibonacci_cameras(8, res, res)
     frame = torch.empty((res, res, 4), dtype=torch.float32, device="cuda")
     for i in range(3):
