@@ -558,6 +558,16 @@ __device__ __forceinline__ void assemble_row(const FeatDev& fd, float px, float 
 // Fast path for the default fV-SRN input (pos mode, NeRF m = NM on 3 axes, F = 16):
 // the whole row [z16 | (sin,cos) x NM | p | 0] is built in registers and written
 // with 16-byte stores (conflict-free at the odd 16-byte row stride).
+#ifndef FVSRN_LDG256
+#define FVSRN_LDG256 1
+#endif
+// 32 bytes (32-byte aligned) through the read-only path in one LDG.256 (sm_100)
+__device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+}
+
 template <int NM>
 struct FastRow {
   static constexpr int kWidth = 16 + 2 * NM + 3;
@@ -644,11 +654,21 @@ struct FastRow {
     const int sz = 16, sy = R * 16, sx = R * R * 16;
     const uint4* base = reinterpret_cast<const uint4*>(fd.grid + ((size_t)(x0 * R + y0) * R + z0) * 16);
     const int off[8] = {0, sz, sy, sy + sz, sx, sx + sz, sx + sy, sx + sy + sz};
+    // one 256-bit load per corner (LDG.256: the voxel's 16 fp16 channels), FVSRN_LDG256=0:
+    // two 128-bit loads
+    uint4 vv[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#if FVSRN_LDG256
+      ldg256(base + (off[k] >> 3), vv[0][k], vv[1][k]);
+#else
+      vv[0][k] = __ldg(base + (off[k] >> 3));
+      vv[1][k] = __ldg(base + (off[k] >> 3) + 1);
+#endif
+    }
 #pragma unroll
     for (int c8 = 0; c8 < 2; ++c8) {
-      uint4 v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldg(base + (off[k] >> 3) + c8);
+      const uint4 (&v)[8] = vv[c8];
       // z = sum_k w_k g_k in packed half2 (HFMA2): 32 instructions per 8 channels
       __half2 acc[4];
 #pragma unroll

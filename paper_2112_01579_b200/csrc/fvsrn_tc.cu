@@ -242,7 +242,15 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   // TMEM columns: D [0, kTCols), A [kTCols, kTCols + max(K0, HID)/2)
   // skip path: the A columns are the second accumulator region (layer-0 rows, then the
   // odd layers' accumulators)
-  constexpr uint32_t kAcols = S::kSkip ? S::kTCols : kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
+  constexpr bool kNSplit = FVSRN_TC_NSPLIT == 1 && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT;
+  // FVSRN_TC_NSPLIT == 2: the hidden layers' MMA in two N=32 halves, the activations of the
+  // first half overlapping the second half's MMA, with the hidden A operand double-buffered
+  // in TMEM (layer l reads buffer l & 1, writes l + 1's) so nothing waits in registers
+  constexpr bool kDbl = FVSRN_TC_NSPLIT == 2 && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && S::kA0 &&
+                        !S::kBiasMma && !S::kBiasCp;
+  // TMEM column offset (from kTCols) of layer l's A operand
+  auto a_col = [](int l) -> uint32_t { return (kDbl && l > 0 && (l & 1)) ? 32u : 0u; };
+  constexpr uint32_t kAcols = S::kSkip ? S::kTCols : kDbl ? 64u : kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
   constexpr uint32_t kNeed = S::kTCols + kAcols;
   constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
@@ -275,7 +283,6 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
   const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar), mb1 = smem_u32(mbar1);
   uint32_t phase1 = 0;
-  constexpr bool kNSplit = FVSRN_TC_NSPLIT && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT;
   // row tid of the A tile: 8-row group stride SBO_A, row-in-group stride 16 B
   __half* myrow = a_s + (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
   const bool density = net.head == 0;
@@ -361,6 +368,16 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
             umma_f16(d, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
                      smem_desc(wb + kk * 256u, 128u, sbo_b), id16, 1u);
           umma_commit(mb);
+        } else if (kDbl && l > 0 && l < NL - 1) {
+          const uint32_t id = idesc_f16(128, 32);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int kk = 0; kk < K / 16; ++kk)
+              umma_f16_ts(tmem + 32u * h, tmem + S::kTCols + a_col(l) + kk * 8u,
+                          smem_desc(wb + kk * 256u + 4u * h * sbo_b, 128u, sbo_b), id, 1u);
+            umma_commit(h == 0 ? mb : mb1);
+          }
         } else if (kNSplit && l < NL - 1 && ((FVSRN_TC_TMEM_A && l > 0) || kA0)) {
           // two N=32 halves: rows 32..63 of the K-major weight tile start 4 core-matrix
           // groups (4 * SBO) further on
@@ -380,7 +397,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
             // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
             const uint32_t acc = (S::kBiasMma && kk == 0) ? 0u : 1u;
             if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
-              umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
+              umma_f16_ts(tmem, tmem + S::kTCols + a_col(l) + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
             else
               umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
                        smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
@@ -431,7 +448,26 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       } else if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
         // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
-        if constexpr (kNSplit) {
+        if (kDbl && l > 0) {
+          // first half ready (the wait above was on its mbarrier): bias + activations of
+          // columns 0..31 while the tensor core computes columns 32..63
+          const uint32_t an = t_row + S::kTCols + a_col(l + 1);
+          uint32_t acc[32], w[16];
+          tmem_ld<32>(t_row, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<32>(t_row, b_s + S::b_off(l + 1));
+          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
+          act_words<32>(acc, w);
+          tmem_st<16>(an, w);
+          mbar_wait(mb1, phase1);
+          phase1 ^= 1u;
+          tc_fence_after();
+          tmem_ld<32>(t_row + 32, acc);
+          tmem_wait_ld();
+          if (l + 1 < NL - 1) tmem_bias<32>(t_row + 32, b_s + S::b_off(l + 1) + 32);
+          act_words<32>(acc, w);
+          tmem_st<16>(an + 16, w);
+        } else if constexpr (kNSplit) {
           // first half ready (the wait above was on its mbarrier); its activations overlap
           // the second half's MMA and stay in registers until that MMA has read A
           uint32_t acc[32], w0[16], w1[16];
@@ -456,7 +492,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
           tmem_ld<32>(t_row, acc);
           tmem_wait_ld();
           act_words<32>(acc, w);
-          tmem_st<16>(t_row + S::kTCols, w);
+          tmem_st<16>(t_row + S::kTCols + a_col(l + 1), w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
           if constexpr (!S::kBiasMma && !S::kBiasCp) {
@@ -464,7 +500,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
             else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
           }
           act_words<32>(acc, w);
-          tmem_st<16>(t_row + S::kTCols + 16, w);
+          tmem_st<16>(t_row + S::kTCols + a_col(l + 1) + 16, w);
         } else if constexpr (FVSRN_TC_TMEM_A) {
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);
