@@ -645,6 +645,10 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
           "> (tcgen05.mma kind::f16, TMEM accumulators)";
       break;
     case KernelKind::kSampleTex: k = "sample_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, static-grid features)"; break;
+    case KernelKind::kSampleTC:
+      k = "decode_tc_kernel<" + std::to_string(h) + "," + std::to_string((h - 4) / 2) + "," +
+          std::to_string(m->layers) + "," + std::to_string(fmode) + "> (tcgen05.mma kind::f16, TMEM accumulators)";
+      break;
     case KernelKind::kDVRWS: k = "dvr_ws_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRPipe: k = "dvr_pipe_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
     case KernelKind::kDVRDual: k = "dvr_dual_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
@@ -657,7 +661,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
   const char* grid = m->R <= 0 ? "no latent grid"
                      : use_tex(m) ? (m->tex_u8 ? "texture units, RGBA8 u8 codes, hardware trilinear (8-bit weights)"
                                                : "texture units, RGBA16F, hardware trilinear (8-bit weights)")
-                                  : "LDG.128 fp16 + HFMA2 trilinear";
+                                  : "LDG.256 fp16 + HFMA2 trilinear";
   return k + "; grid: " + grid;
 }
 
@@ -666,8 +670,10 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   const bool tc = kind == KernelKind::kDVRTC || kind == KernelKind::kDVRTCTex;
   const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
                    : kind == KernelKind::kDVRTCTex ? tc_tex_kernel_for(m->hid_pad, fmode)
+                   : kind == KernelKind::kSampleTC ? tc_decode_kernel_for(m->hid_pad, fmode)
                                                     : kernel_for(kind, m->hid_pad, fast_path(m, kind), fmode);
-  const int threads = kind == KernelKind::kDVRWS ? kWsThreads : tc ? kTcThreads : kThreads;
+  const bool tmem_k = tc || kind == KernelKind::kSampleTC;   // tcgen05 kernels (TMEM, 128 threads)
+  const int threads = kind == KernelKind::kDVRWS ? kWsThreads : tmem_k ? kTcThreads : kThreads;
   if (!fn) return fail(FVSRN_ECAPACITY, "no kernel for this hidden width");
   int occ = 0;
   {
@@ -681,7 +687,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
         attr = smem;
       }
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
-      if (tc) {
+      if (tmem_k) {
         // The occupancy API reports 1 CTA/SM for kernels that allocate TMEM; the real
         // limits are registers (launch bounds), shared memory and TMEM columns (each
         // CTA allocates <= 64 of 512), so size the persistent grid from those.
@@ -1476,10 +1482,8 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       auto at = [&](int n, int k) -> __half& {
         return tile[(size_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)];
       };
-      // skip path (tc_skip): the fp16 tiles of layers >= 1 multiply cos(a), with weight -2 W
-      const float wscale = (tc_skip(H) && l > 0) ? -2.f : 1.f;
       for (int n = 0; n < Nt && n < N[l]; ++n) {
-        for (int k = 0; k < Kw; ++k) at(n, k) = __float2half_rn(wscale * ws[l][(size_t)n * Kw + k]);
+        for (int k = 0; k < Kw; ++k) at(n, k) = __float2half_rn(ws[l][(size_t)n * Kw + k]);
         if (bias_mma && l > 0) {
           const __half hi = __float2half_rn(bs[l][n]);
           at(n, Kw) = hi;
@@ -1488,26 +1492,6 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       }
       wt.insert(wt.end(), tile.begin(), tile.end());
       for (int n = 0; n < Nt; ++n) bt.push_back(n < N[l] ? bs[l][n] : 0.f);
-    }
-    if (tc_skip(H)) {
-      // tf32 tiles (f32 storage, rounded to nearest tf32) of layers >= 1 multiplying a itself:
-      // element (n, k) at float (n/8)*(H/4)*32 + (k/4)*32 + (n%8)*4 + (k%4)
-      for (int l = 1; l < L; ++l) {
-        const int Nt = (l == L - 1) ? 16 : H, Kw = Ks[l];
-        std::vector<float> tile((size_t)Nt * H, 0.f);
-        for (int n = 0; n < Nt && n < N[l]; ++n)
-          for (int k = 0; k < Kw && k < H; ++k) {
-            uint32_t u;
-            const float w = ws[l][(size_t)n * Kw + k];
-            std::memcpy(&u, &w, 4);
-            if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
-            float q;
-            std::memcpy(&q, &u, 4);
-            tile[(size_t)(n / 8) * (H / 4) * 32 + (k / 4) * 32 + (n % 8) * 4 + (k % 4)] = q;
-          }
-        const __half* hp = reinterpret_cast<const __half*>(tile.data());
-        wt.insert(wt.end(), hp, hp + 2 * tile.size());
-      }
     }
     int rc = upload(wt.data(), wt.size() * sizeof(__half), (void**)&m->d_wtc);
     if (rc) return rc;
@@ -1900,12 +1884,21 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
   // static fp16 texture grid on the default shapes: the branch-free feature path
   const bool s_tex = fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
   const bool s_ldg = !fd.tex_on && fd.grid != nullptr && fd.f_pad == 16;
-  const KernelKind sk = (FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kSample) && (s_tex || s_ldg))
-                            ? KernelKind::kSampleTex : KernelKind::kSample;
+  const bool s_static = FVSRN_TEX_SPECIAL && fast_path(m, KernelKind::kSample) && (s_tex || s_ldg);
+  // the tcgen05 decode wherever the march uses tcgen05 (FVSRN_DECODE_TC=0: mma.sync)
+  static const bool decode_tc = [] {
+    const char* e = std::getenv("FVSRN_DECODE_TC");
+    return !(e && e[0] == '0');
+  }();
+  const bool tcd = s_static && decode_tc && use_tc(m);
+  const KernelKind sk = tcd ? KernelKind::kSampleTC : s_static ? KernelKind::kSampleTex : KernelKind::kSample;
   const int sfm = s_tex ? 1 : 2;
+  TcNetDev tn{m->d_wtc, m->d_btc, m->head};
+  const size_t tsmem = tcd ? tc_smem_bytes(m->hid_pad, false) : 0;
   if (chunks <= 1 || !h_out) {
     void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad, &coords};
-    if ((rc = launch(m, sk, smem, args, s, count / 32 + 1, sfm))) return rc;
+    void* targs[] = {&tn, &fd, &b0, &res, &begin, &count, &coords, &d_out, &d_bad};
+    if ((rc = launch(m, sk, tcd ? tsmem : smem, tcd ? targs : args, s, count / 32 + 1, sfm))) return rc;
   } else {
     // chunk c: decode [c0, c0 + n) into d_out + c0 on s, then copy it to h_out on copy_s
     const long long per = ((lattice_count + chunks - 1) / chunks + 31) / 32 * 32;
@@ -1913,7 +1906,8 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
       long long cb = lattice_begin + c0, cn = std::min(per, lattice_count - c0);
       float* dst = d_out + c0;
       void* args[] = {&net, &fd, &b0, &mode, &res, &step, &cb, &cn, &pp, &pd, &dst, &d_bad, &coords};
-      if ((rc = launch(m, sk, smem, args, s, cn / 32 + 1, sfm))) return rc;
+      void* targs[] = {&tn, &fd, &b0, &res, &cb, &cn, &coords, &dst, &d_bad};
+      if ((rc = launch(m, sk, tcd ? tsmem : smem, tcd ? targs : args, s, cn / 32 + 1, sfm))) return rc;
       cudaEvent_t done;
       CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(done, s));

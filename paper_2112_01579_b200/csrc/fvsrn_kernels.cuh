@@ -99,9 +99,10 @@ struct RayRecs {
 // kDVRTex: dvr_kernel specialised for the default fast path with a static fp16 texture grid
 // (no u8 codes, no per-sample keyframe blend): the feature code has no runtime branches
 // (kDVRTCTex, kSampleTex: the same for the tcgen05 march and the lattice decode)
-// (kDVRPair: the frame specialisation with two lanes per ray, for small frames)
+// (kDVRPair / kDVRQuad: the frame specialisation with two / four lanes per ray, for small
+// frames; kSampleTC: the tcgen05 lattice decode, fvsrn_tc.cu)
 enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused, kDVRTex, kDVRTCTex,
-                        kSampleTex, kDVRPair, kDVRQuad };
+                        kSampleTex, kDVRPair, kDVRQuad, kSampleTC };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

@@ -1,18 +1,22 @@
-// fvsrn_tc.cu -- tcgen05 / TMEM variant of the fused fV-SRN DVR kernel (sm_100a).
+// fvsrn_tc.cu -- tcgen05 / TMEM kernels of the fused fV-SRN evaluation (sm_100a): the DVR
+// march (dvr_tc_kernel) and the lattice decode (decode_tc_kernel).
 //
-// One CTA = 4 warps = 128 rays = one M=128 UMMA tile.  Thread t owns ray t and TMEM
-// lane t, so the row-per-thread accumulator layout of tcgen05.ld is also the
-// ray-per-thread layout of the marcher: no fragment shuffles, no output staging.
-// Per ray-march step (render.py:219-232):
-//   1. every thread refills its ray if needed (chunked global queue, f64 geometry)
-//      and writes its input row [z | sin/cos pairs | p] (FastRow) into the A tile in
-//      shared memory, in the UMMA K-major canonical layout (8x16 B core matrices);
-//   2. per layer: one elected thread issues K/16 tcgen05.mma (A = rows in smem,
-//      B = weights in smem, D = f32 accumulators in TMEM, pre-loaded with the layer
-//      bias by tcgen05.st so the bias stays f32-exact) and commits to an mbarrier;
-//      every thread tcgen05.ld's its row, evaluates the snake activation in registers
-//      (one MUFU.COS per element) and writes the fp16 row back into the A tile;
-//   3. the last layer's 4 outputs go straight to head/TF/compositing/ET in registers.
+// One CTA = 4 warps = 128 rows = one M=128 UMMA tile.  Thread t owns row t (a ray, or a
+// lattice point) and TMEM lane t, so the row-per-thread accumulator layout of tcgen05.ld
+// is also the ray-per-thread layout of the marcher: no fragment shuffles, no output
+// staging.  Per step (render.py:219-232 for the march):
+//   1. every thread refills its ray / takes its lattice point and writes its input row
+//      [z | sin/cos pairs | p | 1] (FastRow) into TMEM with tcgen05.st;
+//   2. per layer (TcMlp::run): one elected thread issues K/16 tcgen05.mma (A = the row or
+//      the hidden activations in TMEM, B = weights in shared memory, D = f32 accumulators
+//      in TMEM) and commits to an mbarrier; every thread tcgen05.ld's its row, evaluates
+//      the snake activation in registers (one MUFU.COS per element, every 6th on the FMA
+//      pipe) and tcgen05.st's the packed fp16 row back as the next A operand.  Biases:
+//      at 32-wide inside the MMA (layer 0 through the row's 1.0 pad column and a W0 bias
+//      column patched per frame, later layers through one extra k16 tile of [1, 1] x
+//      [b_hi, b_lo]); at 64-wide preloaded into D with tcgen05.st;
+//   3. the last layer's 4 outputs go straight to head/TF/compositing/ET (march) or to the
+//      density store (decode) in registers.
 // The MLP never touches global memory; the HMMA issue slots and the B-fragment LDS of
 // the mma.sync kernel disappear from the SM sub-partitions' instruction streams.
 // Used for the default fV-SRN configurations (FastRow inputs, snake_alt, 32/64 wide).
@@ -57,58 +61,12 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 }
 
 // Activation of element e of a row: every FVSRN_TC_POLY-th element evaluates its cosine
-// on the FMA pipe instead of the XU (MUFU) pipe.  The tcgen05 kernels are XU-bound in
-// their activation phases with issue slots to spare (6x64 at 4 CTAs/SM: issue 46%,
-// XU 67%), so moving every 6th cosine balances the two (cfg 3: 28.2 -> 26.9 ms;
-// every 3rd 28.9, 4th 27.8, 8th 27.1, 12th 27.2, 16th 27.3).  0 disables.
+// on the FMA pipe instead of the XU (MUFU) pipe (cfg 3: 28.2 -> 26.9 ms when introduced;
+// round 2, cfg 2 / cfg 3 ms: every 4th 3.02 / 25.98, 5th 2.86 / 25.08, 6th 2.82 / 25.19,
+// 7th 2.83, 8th - / 25.41, 12th 2.88).  0 disables.
 #ifndef FVSRN_TC_POLY
 #define FVSRN_TC_POLY 6
 #endif
-#ifndef FVSRN_TC_SPLIT
-#define FVSRN_TC_SPLIT 1
-#endif
-#ifndef FVSRN_TC_PREFETCH
-#define FVSRN_TC_PREFETCH 0
-#endif
-#ifndef FVSRN_TC_WAIT_BAR
-#define FVSRN_TC_WAIT_BAR 0
-#endif
-// FVSRN_TC_NSPLIT: the 64-wide layers' MMA is issued as two N=32 halves committing to two
-// mbarriers, so the activations of the first half overlap the second half's MMA (the packed
-// first half waits in registers: A is rewritten only after the whole MMA has read it)
-#ifndef FVSRN_TC_NSPLIT
-#define FVSRN_TC_NSPLIT 0
-#endif
-// hidden-layer A operands in TMEM (tcgen05.st of the packed activations, MMA reads A
-// from TMEM) instead of the shared-memory A tile: removes 2 x 128 B of shared-memory
-// traffic per sample and layer
-#ifndef FVSRN_TC_TMEM_A
-#define FVSRN_TC_TMEM_A 1
-#endif
-// FVSRN_TC_TMEM_A0 (fvsrn_tc.cuh): layer-0 input rows in TMEM too (measured at 3
-// CTAs/SM: faster at 32-wide, slower at 64-wide)
-// snake_alt activations of one accumulator row -> fp16 chunks of the A tile row
-// (chunk c = columns 8c..8c+7 at +128 B per chunk in the canonical layout)
-template <int HID>
-__device__ __forceinline__ void act_row(const uint32_t (&acc)[HID], __half* row) {
-  constexpr int P = FVSRN_TC_POLY;
-#pragma unroll
-  for (int c = 0; c < HID / 8; ++c) {
-    uint32_t w4[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float h[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int e = 8 * c + 2 * j + i;       // compile-time after unrolling
-        const float x = __uint_as_float(acc[e]);
-        h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
-      }
-      w4[j] = pack_half2(h[0], h[1]);
-    }
-    *reinterpret_cast<uint4*>(row + c * 64) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-  }
-}
 
 // snake_alt activations of one accumulator row -> packed fp16 pairs (TMEM A operand)
 template <int HID>
@@ -124,42 +82,6 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[HID], uint32_t (
       h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
     }
     w[j] = pack_half2(h[0], h[1]);
-  }
-}
-
-// cos(a) on the FMA pipe (range reduction by the 1.5*2^23 trick, degree-4 minimax in r^2
-// of cos(2 pi r), |err| < 4.3e-5): 8 FP32 operations, no MUFU
-__device__ __forceinline__ float cos_fma(float x) {
-  const float kb = fmaf(x, 0.15915494309189535f, 12582912.f);
-  const float k = kb - 12582912.f;
-  const float r = fmaf(x, 0.15915494309189535f, -k);
-  const float u = r * r;
-  float p = fmaf(45.62269592285156f, u, -82.3971176147461f);
-  p = fmaf(p, u, 64.67363739013672f);
-  p = fmaf(p, u, -19.731164932250977f);
-  return fmaf(p, u, 0.9999644756317139f);
-}
-
-// skip path: cos(a) of one accumulator row -> fp16 chunks of the shared-memory A tile row
-// (every FVSRN_TC_POLY-th element on the FMA pipe, as act_row)
-template <int HID>
-__device__ __forceinline__ void cos_row(const uint32_t (&acc)[HID], __half* row) {
-  constexpr int P = FVSRN_TC_POLY;
-#pragma unroll
-  for (int c = 0; c < HID / 8; ++c) {
-    uint32_t w4[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float h[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int e = 8 * c + 2 * j + i;
-        const float x = __uint_as_float(acc[e]);
-        h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? cos_fma(x) : __cosf(x);
-      }
-      w4[j] = pack_half2(h[0], h[1]);
-    }
-    *reinterpret_cast<uint4*>(row + c * 64) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
   }
 }
 
@@ -200,8 +122,154 @@ __device__ __forceinline__ void tmem_st_any(uint32_t taddr, const uint32_t (&r)[
   }
 }
 
+// Dynamic shared memory of the one-tile kernels (TcShape map); addressed through the
+// symbol so shared-window offsets fold into immediates instead of live pointer registers
+extern __shared__ __align__(128) unsigned char tc_smem[];
+
+// The per-CTA tcgen05 MLP shared by the march and the decode kernels.  TMEM columns:
+// D [0, kTCols), A [kTCols, kTCols + kKA/2) (the layer-0 row, then the hidden
+// activations).  Shared memory (TcShape): weights, f32 biases, TF, mbarrier, TMEM slot.
+template <int HID, int NM, int NL>
+struct TcMlp {
+  using S = TcShape<HID, NM, NL>;
+  static_assert(S::kA0, "the one-tile kernels keep the layer-0 rows in TMEM");
+  static constexpr int kWords = FastRow<NM>::kWords;
+  static constexpr uint32_t kNeed = S::kTCols + S::kKA / 2;
+  static constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
+
+  uint32_t tmem, t_row, phase;
+  int tid;
+
+  __device__ static const float* b_s() { return reinterpret_cast<const float*>(tc_smem + S::kBOff); }
+  __device__ static uint32_t mb() { return smem_u32(tc_smem + S::kMbarOff); }
+
+  // Weights and biases (b0: this frame's layer-0 bias, or null) into shared memory, TMEM
+  // allocation, mbarrier; ends with a CTA barrier (so caller-side shared-memory writes
+  // issued before it are visible after it).
+  __device__ void init(const TcNetDev& net, const float* __restrict__ b0) {
+    tid = threadIdx.x;
+    const int warp = tid >> 5;
+    __half* w_s = reinterpret_cast<__half*>(tc_smem + S::kWOff);
+    float* bs = reinterpret_cast<float*>(tc_smem + S::kBOff);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_smem + S::kMbarOff + 8);
+    {
+      const uint4* src = net.w;
+      uint4* dst = reinterpret_cast<uint4*>(w_s);
+      for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
+      for (int i = tid; i < S::kBTotal; i += kTcThreads) bs[i] = (b0 && i < HID) ? b0[i] : net.b[i];
+    }
+    if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
+    if (tid == 0) mbar_init(mb(), 1);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if constexpr (S::kBiasMma) {
+      // W0's pad column (K0 - 1; the row's pad is 1.0) := this frame's layer-0 bias
+      constexpr int K = S::kK0, k = S::kK0 - 1;
+      for (int n = tid; n < HID; n += kTcThreads)
+        w_s[(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] = __float2half_rn(bs[n]);
+      fence_proxy_async_smem();
+      __syncthreads();
+    }
+    tmem = *tmem_slot;
+    t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
+    phase = 0;
+  }
+
+  __device__ void finish() {
+    tc_fence_before();
+    __syncthreads();
+    if ((tid >> 5) == 0) tmem_dealloc(tmem, kAlloc);
+  }
+
+  // Start of a step, before the row is built: the layer-0 bias into D (64-wide; its 64
+  // registers are dead again before the row's are live)
+  __device__ void begin_row() {
+    if constexpr (!S::kBiasMma) tmem_bias<HID>(t_row, b_s() + S::b_off(0));
+  }
+
+  // This thread's layer-0 row (zeros for a thread without work) -> TMEM A; every thread
+  // calls it (tcgen05.st is .sync.aligned).  Ends with the CTA barrier the MMA issue needs.
+  __device__ void put_row(uint32_t (&w)[kWords]) {
+    if constexpr (S::kBiasMma) w[kWords - 1] |= 0x3C000000u;   // pad column = 1.0
+    tmem_st_any<kWords>(t_row + S::kTCols, w);
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+  }
+
+  // All layers of this step; o = the last layer's first 4 accumulators of this row.
+  __device__ void run(uint32_t (&o)[4]) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      if (tid == 0) {
+        tc_fence_after();
+        const int K = l == 0 ? S::kK0 : S::kKh;
+        const int N = l == NL - 1 ? S::kNLast : HID;
+        const uint32_t wb = smem_u32(tc_smem + S::kWOff) + 2u * (uint32_t)S::w_off(l);
+        const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
+        const uint32_t id = idesc_f16(128, N);
+#pragma unroll
+        for (int kk = 0; kk < K / 16; ++kk) {
+          // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
+          const uint32_t acc = (S::kBiasMma && kk == 0) ? 0u : 1u;
+          umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
+        }
+        umma_commit(mb());
+      }
+      mbar_wait(mb(), phase);
+      phase ^= 1u;
+      tc_fence_after();
+      if (l < NL - 1) {
+        // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> the next A operand
+        if constexpr (HID == 64) {
+          // two 32-column halves: half the live accumulator registers
+          uint32_t acc[32], w[16];
+          tmem_ld<32>(t_row, acc);
+          tmem_wait_ld();
+          act_words<32>(acc, w);
+          tmem_st<16>(t_row + S::kTCols, w);
+          tmem_ld<32>(t_row + 32, acc);
+          tmem_wait_ld();
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s() + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
+          }
+          act_words<32>(acc, w);
+          tmem_st<16>(t_row + S::kTCols + 16, w);
+        } else {
+          uint32_t acc[HID];
+          tmem_ld<HID>(t_row, acc);
+          tmem_wait_ld();
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s() + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
+          }
+          uint32_t w[HID / 2];
+          act_words<HID>(acc, w);
+          tmem_st<HID / 2>(t_row + S::kTCols, w);
+        }
+        if constexpr (S::kBiasMma) {
+          if (l == 0) {   // the bias tile of layers >= 1: A columns HID/2.. = [1, 1, 0, ...]
+            uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            tmem_st_x8(t_row + S::kTCols + HID / 2, c);
+          }
+        }
+        tmem_wait_st();   // the next A operand went to TMEM: no shared-memory proxy fence
+        tc_fence_before();
+        __syncthreads();
+      } else {
+        tmem_ld_x4(t_row, o);
+        tmem_wait_ld();
+      }
+    }
+  }
+};
+
 }  // namespace
 
+// TEX == 0: any frame or explicit rays; TEX == 1 / 2: a camera frame of a density-head
+// model with a static fp16 texture grid / exact-weight LDG grid (compile-time flags)
 template <int HID, int NM, int NL, int TEX = 0>
 __global__ void __launch_bounds__(kTcThreads, tc_min_blocks<HID>())
 dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
@@ -209,98 +277,23 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
               float* __restrict__ out, unsigned long long* __restrict__ queue,
               unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
   using S = TcShape<HID, NM, NL>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __half* w_s = reinterpret_cast<__half*>(smem + S::kWOff);
-  float* b_s = reinterpret_cast<float*>(smem + S::kBOff);
-  TFDev* tf = reinterpret_cast<TFDev*>(smem + S::kTFOff);
-  __half* a_s = reinterpret_cast<__half*>(smem + S::kAOff);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::kMbarOff);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kMbarOff + 8);
-  uint64_t* mbar1 = reinterpret_cast<uint64_t*>(smem + S::kMbarOff + 16);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  TFDev* tf = reinterpret_cast<TFDev*>(tc_smem + S::kTFOff);
   {
-    const uint4* src = net.w;
-    uint4* dst = reinterpret_cast<uint4*>(w_s);
-    for (int i = tid; i < S::kWBytes / 16; i += kTcThreads) dst[i] = src[i];
-    for (int i = tid; i < S::kBTotal; i += kTcThreads)
-      b_s[i] = (b0 && i < HID) ? b0[i] : net.b[i];
     const int words = sizeof(TFDev) / 4;
     const int* ts = reinterpret_cast<const int*>(tf_g);
     int* td = reinterpret_cast<int*>(tf);
-    for (int i = tid; i < words; i += kTcThreads) td[i] = ts[i];
-    if constexpr (!S::kA0 || S::kSkip) {
-      // pad columns must stay finite; skip path: columns HID, HID+1 = 1.0 (the bias tile)
-      uint4* az = reinterpret_cast<uint4*>(a_s);
-      for (int i = tid; i < kTcThreads * S::kKA / 8; i += kTcThreads) {
-        const bool ones = S::kSkip && (i / 8) % (S::kKA / 8) == HID / 8;   // chunk of columns HID..HID+7
-        az[i] = make_uint4(ones ? 0x3C003C00u : 0u, 0u, 0u, 0u);
-      }
-    }
+    for (int i = threadIdx.x; i < words; i += kTcThreads) td[i] = ts[i];
   }
-  constexpr bool kA0 = S::kA0;
-  // TMEM columns: D [0, kTCols), A [kTCols, kTCols + max(K0, HID)/2)
-  // skip path: the A columns are the second accumulator region (layer-0 rows, then the
-  // odd layers' accumulators)
-  constexpr bool kNSplit = FVSRN_TC_NSPLIT == 1 && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT;
-  // FVSRN_TC_NSPLIT == 2: the hidden layers' MMA in two N=32 halves, the activations of the
-  // first half overlapping the second half's MMA, with the hidden A operand double-buffered
-  // in TMEM (layer l reads buffer l & 1, writes l + 1's) so nothing waits in registers
-  constexpr bool kDbl = FVSRN_TC_NSPLIT == 2 && HID == 64 && FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && S::kA0 &&
-                        !S::kBiasMma && !S::kBiasCp;
-  // TMEM column offset (from kTCols) of layer l's A operand
-  auto a_col = [](int l) -> uint32_t { return (kDbl && l > 0 && (l & 1)) ? 32u : 0u; };
-  constexpr uint32_t kAcols = S::kSkip ? S::kTCols : kDbl ? 64u : kA0 ? S::kKA / 2 : (FVSRN_TC_TMEM_A ? HID / 2 : 0);
-  constexpr uint32_t kNeed = S::kTCols + kAcols;
-  constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
-  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
-  if (tid == 0) {
-    mbar_init(smem_u32(mbar), 1);
-    mbar_init(smem_u32(mbar1), 1);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if constexpr (S::kBiasMma) {
-    static_assert(S::kA0, "bias-in-MMA needs the layer-0 rows in TMEM");
-    // W0's pad column (K0 - 1; the row's pad is 1.0) := this frame's layer-0 bias
-    constexpr int K = S::kK0, k = S::kK0 - 1;
-    for (int n = tid; n < HID; n += kTcThreads)
-      w_s[(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] = __float2half_rn(b_s[n]);
-    fence_proxy_async_smem();
-    __syncthreads();
-  }
-  if constexpr (S::kBiasCp) {
-    // bias broadcast tiles from b_s (b0 of this frame for layer 0)
-    for (int i = tid; i < S::kBTotal * 8; i += kTcThreads) {
-      const int c = i >> 3, r = i & 7;
-      *reinterpret_cast<float*>(smem + S::kBcOff + (c / 8) * 256 + ((c % 8) / 4) * 128 + r * 16 + (c % 4) * 4) = b_s[c];
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-  }
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
-  const uint32_t a_base = smem_u32(a_s), w_base = smem_u32(w_s), mb = smem_u32(mbar), mb1 = smem_u32(mbar1);
-  uint32_t phase1 = 0;
-  // row tid of the A tile: 8-row group stride SBO_A, row-in-group stride 16 B
-  __half* myrow = a_s + (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
+  TcMlp<HID, NM, NL> mlp;
+  mlp.init(net, b0);
+  const int lane = threadIdx.x & 31;
   const bool density = net.head == 0;
+  constexpr bool kFrame = TEX >= 1;
 
   RayLane r;
   r.has = false;
   LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
-  uint32_t phase = 0;
-  // FVSRN_TC_PREFETCH: the next sample's latent-grid texture fetches are issued before the
-  // last layer's MMA wait, so their latency hides under it (static fp16 texture grids)
-  const bool prefetch = FVSRN_TC_PREFETCH && kA0 && fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f;
-  uint32_t pre[8];
-  int pre_k = -1;
-
-  // TEX == 1: a camera frame (no explicit rays, no direction inputs) of a density-head
-  // model with a static fp16 texture grid: those flags are compile-time
-  constexpr bool kFrame = TEX >= 1;
   while (true) {
     if constexpr (kFrame) {
       RayRecs rr_pos = rr;
@@ -311,255 +304,87 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     }
     if (!__syncthreads_or(r.has)) break;
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
-    if constexpr (!S::kBiasMma && !S::kBiasCp) tmem_bias<HID>(t_row, b_s + S::b_off(0));
-    if constexpr (kA0) {
-      // tcgen05.st is .sync.aligned: every lane stores (rays-less lanes a zero row)
-      uint32_t w[FastRow<NM>::kWords];
-      if (r.has) {
-        const float kf = (float)r.k;
-        const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
-        if (prefetch && pre_k == r.k) {
-          FastRow<NM>::words_from_z(pre, px, py, pz, w);
-        } else if constexpr (TEX >= 1) {   // static fp16 grid: no runtime branches
-          uint32_t z[8];
-          if constexpr (TEX == 1) FastRow<NM>::tex_words(fd, px, py, pz, z);
-          else FastRow<NM>::ldg_words(fd, px, py, pz, z);
-          FastRow<NM>::words_from_z(z, px, py, pz, w);
-        } else {
-          FastRow<NM>::words(fd, px, py, pz, w);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
-      }
-      if constexpr (S::kBiasMma) w[FastRow<NM>::kWords - 1] |= 0x3C000000u;   // pad column = 1.0
-      tmem_st_any<FastRow<NM>::kWords>(t_row + S::kTCols, w);
-    } else if (r.has) {
+    mlp.begin_row();
+    uint32_t w[FastRow<NM>::kWords];
+    if (r.has) {
       const float kf = (float)r.k;
-      FastRow<NM>::template build<8>(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1),
-                                     fmaf(kf, r.dd2, r.pe2), myrow);
-    }
-    tmem_wait_st();
-    if constexpr (!kA0) fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      if (tid == 0) {
-        tc_fence_after();
-        const int K = l == 0 ? S::kK0 : S::kKh;
-        const int N = l == NL - 1 ? S::kNLast : HID;
-        const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
-        const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
-        if constexpr (S::kBiasCp) {
-          // D := this layer's bias (zero 8-row-group stride: the tile's row on every lane)
-          const uint32_t bt = smem_u32(smem) + (uint32_t)(S::kBcOff + S::b_off(l) * 32);
-#pragma unroll
-          for (int g = 0; g < (l == NL - 1 ? S::kNLast : HID) / 8; ++g)
-            tmem_cp_128x256b(tmem + 8u * g, smem_desc(bt + 256u * g, 128u, 0u));
-        }
-        if (S::kSkip && l > 0) {
-          // D_l = a_{l-1} x W_l (tf32, issued when layer l-1 completed, below)
-          //     + cos(a_{l-1}) (fp16 smem tile) x (-2 W_l) + [1, 1] x [b_hi, b_lo]
-          const uint32_t d = tmem + (uint32_t)((l & 1) * S::kTCols);
-          const uint32_t id16 = idesc_f16(128, N);
-#pragma unroll
-          for (int kk = 0; kk < S::kKh / 16; ++kk)
-            umma_f16(d, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
-                     smem_desc(wb + kk * 256u, 128u, sbo_b), id16, 1u);
-          umma_commit(mb);
-        } else if (kDbl && l > 0 && l < NL - 1) {
-          const uint32_t id = idesc_f16(128, 32);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk)
-              umma_f16_ts(tmem + 32u * h, tmem + S::kTCols + a_col(l) + kk * 8u,
-                          smem_desc(wb + kk * 256u + 4u * h * sbo_b, 128u, sbo_b), id, 1u);
-            umma_commit(h == 0 ? mb : mb1);
-          }
-        } else if (kNSplit && l < NL - 1 && ((FVSRN_TC_TMEM_A && l > 0) || kA0)) {
-          // two N=32 halves: rows 32..63 of the K-major weight tile start 4 core-matrix
-          // groups (4 * SBO) further on
-          const uint32_t id = idesc_f16(128, 32);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int kk = 0; kk < K / 16; ++kk)
-              umma_f16_ts(tmem + 32u * h, tmem + S::kTCols + kk * 8u,
-                          smem_desc(wb + kk * 256u + 4u * h * sbo_b, 128u, sbo_b), id, 1u);
-            umma_commit(h == 0 ? mb : mb1);
-          }
-        } else {
-          const uint32_t id = idesc_f16(128, N);
-#pragma unroll
-          for (int kk = 0; kk < K / 16; ++kk) {
-            // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
-            const uint32_t acc = (S::kBiasMma && kk == 0) ? 0u : 1u;
-            if ((FVSRN_TC_TMEM_A && l > 0) || kA0)
-              umma_f16_ts(tmem, tmem + S::kTCols + a_col(l) + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
-            else
-              umma_f16(tmem, smem_desc(a_base + kk * 256u, 128u, S::kSboA),
-                       smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
-          }
-          umma_commit(mb);
-        }
-      }
-      if (prefetch && l == NL - 1) {
-        pre_k = -1;
-        if (r.has && r.k + 1 < r.n) {
-          const float kf = (float)(r.k + 1);
-          FastRow<NM>::tex_words(fd, fmaf(kf, r.dd0, r.pe0), fmaf(kf, r.dd1, r.pe1), fmaf(kf, r.dd2, r.pe2), pre);
-          pre_k = r.k + 1;
-        }
-      }
-      if constexpr (FVSRN_TC_WAIT_BAR) {
-        // one thread polls the MMA-completion barrier; the others wait in the hardware
-        // CTA barrier instead of spinning on try_wait (issue slots stay with other CTAs)
-        if (tid == 0) mbar_wait(mb, phase);
-        tc_fence_before();
-        __syncthreads();
+      const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
+      if constexpr (TEX >= 1) {   // static fp16 grid: no runtime branches
+        uint32_t z[8];
+        if constexpr (TEX == 1) FastRow<NM>::tex_words(fd, px, py, pz, z);
+        else FastRow<NM>::ldg_words(fd, px, py, pz, z);
+        FastRow<NM>::words_from_z(z, px, py, pz, w);
       } else {
-        mbar_wait(mb, phase);
+        FastRow<NM>::words(fd, px, py, pz, w);
       }
-      phase ^= 1u;
-      tc_fence_after();
-      if (S::kSkip && l < NL - 1) {
-        if (tid == 0) {
-          // the a x W part of the next layer only needs this layer's accumulators: issue it
-          // now, so the tensor core works under the cos evaluation below
-          const int N1 = l + 1 == NL - 1 ? S::kNLast : HID;
-          const uint32_t d = tmem + (uint32_t)(((l + 1) & 1) * S::kTCols);
-          const uint32_t ax = tmem + (uint32_t)((l & 1) * S::kTCols);
-          const uint32_t xb = w_base + (uint32_t)S::x_off(l + 1);
-          const uint32_t id32 = idesc_tf32(128, N1);
+    } else {
 #pragma unroll
-          for (int kk = 0; kk < HID / 8; ++kk)
-            umma_tf32_ts(d, ax + kk * 8u, smem_desc(xb + kk * 256u, 128u, S::kSboX), id32, kk > 0 ? 1u : 0u);
-        }
-        // cos(a) of this layer's accumulator region -> the shared-memory A tile
-        uint32_t acc[HID];
-        tmem_ld<HID>(t_row + (uint32_t)((l & 1) * S::kTCols), acc);
-        tmem_wait_ld();
-        cos_row<HID>(acc, myrow);
-        fence_proxy_async_smem();
-        tc_fence_before();
-        __syncthreads();
-      } else if (l < NL - 1) {
-        // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> A tile columns;
-        // FVSRN_TC_SPLIT: read the row in 32-column halves (fewer live registers)
-        if (kDbl && l > 0) {
-          // first half ready (the wait above was on its mbarrier): bias + activations of
-          // columns 0..31 while the tensor core computes columns 32..63
-          const uint32_t an = t_row + S::kTCols + a_col(l + 1);
-          uint32_t acc[32], w[16];
-          tmem_ld<32>(t_row, acc);
-          tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<32>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          act_words<32>(acc, w);
-          tmem_st<16>(an, w);
-          mbar_wait(mb1, phase1);
-          phase1 ^= 1u;
-          tc_fence_after();
-          tmem_ld<32>(t_row + 32, acc);
-          tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<32>(t_row + 32, b_s + S::b_off(l + 1) + 32);
-          act_words<32>(acc, w);
-          tmem_st<16>(an + 16, w);
-        } else if constexpr (kNSplit) {
-          // first half ready (the wait above was on its mbarrier); its activations overlap
-          // the second half's MMA and stay in registers until that MMA has read A
-          uint32_t acc[32], w0[16], w1[16];
-          tmem_ld<32>(t_row, acc);
-          tmem_wait_ld();
-          act_words<32>(acc, w0);
-          mbar_wait(mb1, phase1);
-          phase1 ^= 1u;
-          tc_fence_after();
-          tmem_ld<32>(t_row + 32, acc);
-          tmem_wait_ld();
-          if constexpr (!S::kBiasMma && !S::kBiasCp) {
-            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          }
-          act_words<32>(acc, w1);
-          tmem_st<16>(t_row + S::kTCols, w0);
-          tmem_st<16>(t_row + S::kTCols + 16, w1);
-        } else if constexpr (FVSRN_TC_TMEM_A && FVSRN_TC_SPLIT && HID == 64) {
-          // two 32-column halves: half the live accumulator registers
-          uint32_t acc[32], w[16];
-          tmem_ld<32>(t_row, acc);
-          tmem_wait_ld();
-          act_words<32>(acc, w);
-          tmem_st<16>(t_row + S::kTCols + a_col(l + 1), w);
-          tmem_ld<32>(t_row + 32, acc);
-          tmem_wait_ld();
-          if constexpr (!S::kBiasMma && !S::kBiasCp) {
-            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          }
-          act_words<32>(acc, w);
-          tmem_st<16>(t_row + S::kTCols + a_col(l + 1) + 16, w);
-        } else if constexpr (FVSRN_TC_TMEM_A) {
-          uint32_t acc[HID];
-          tmem_ld<HID>(t_row, acc);
-          tmem_wait_ld();
-          if constexpr (!S::kBiasMma && !S::kBiasCp) {
-            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          }
-          uint32_t w[HID / 2];
-          act_words<HID>(acc, w);
-          tmem_st<HID / 2>(t_row + S::kTCols, w);
-        } else if constexpr (FVSRN_TC_SPLIT && HID == 64) {
-          uint32_t acc[32];
-          tmem_ld<32>(t_row, acc);
-          tmem_wait_ld();
-          act_row<32>(acc, myrow);
-          tmem_ld<32>(t_row + 32, acc);
-          tmem_wait_ld();
-          if constexpr (!S::kBiasMma && !S::kBiasCp) {
-            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          }
-          act_row<32>(acc, myrow + 4 * 64);
-        } else {
-          uint32_t acc[HID];
-          tmem_ld<HID>(t_row, acc);
-          tmem_wait_ld();
-          if constexpr (!S::kBiasMma && !S::kBiasCp) {
-            if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-            else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          }
-          act_row<HID>(acc, myrow);
-        }
-        if constexpr (S::kBiasMma) {
-          if (l == 0) {   // the bias tile of layers >= 1: A columns HID/2.. = [1, 1, 0, ...]
-            uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            tmem_st_x8(t_row + S::kTCols + HID / 2, c);
-          }
-        }
-        tmem_wait_st();
-        // the next A operand went to TMEM (tcgen05.st): no generic-proxy smem writes
-        if constexpr (!FVSRN_TC_TMEM_A) fence_proxy_async_smem();
-        tc_fence_before();
-        __syncthreads();
-      } else {
-        uint32_t o[4];
-        tmem_ld_x4(t_row + (uint32_t)(S::kSkip ? ((NL - 1) & 1) * S::kTCols : 0), o);
-        tmem_wait_ld();
-        if (r.has)
-          composite_step(r, make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
-                                        __uint_as_float(o[2]), __uint_as_float(o[3])),
-                         kFrame || density, *tf, md, out, nonfinite);
-      }
+      for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
     }
+    mlp.put_row(w);
+    uint32_t o[4];
+    mlp.run(o);
+    if (r.has)
+      composite_step(r, make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
+                                    __uint_as_float(o[2]), __uint_as_float(o[3])),
+                     kFrame || density, *tf, md, out, nonfinite);
   }
   if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kAlloc);
+  mlp.finish();
+}
+
+// Density at the res^3 lattice (model.py:385-398, decode_volume; sample_kernel mode 0
+// with the same linspace coordinate table), indices [begin, begin + count) in x-major
+// order, for a static fp16 grid (TEX 1 texture units, 2 exact-weight LDG).  Persistent
+// CTAs stride over 128-point tiles; the lattice coordinates advance with carries (no
+// per-step 64-bit division).  ScalarVolume invariant checked on the device (bad).
+template <int HID, int NM, int NL, int TEX>
+__global__ void __launch_bounds__(kTcThreads, tc_min_blocks<HID>())
+decode_tc_kernel(TcNetDev net, FeatDev fd, const float* __restrict__ b0, int res, long long begin,
+                 long long count, const float* __restrict__ coords, float* __restrict__ out,
+                 unsigned long long* __restrict__ bad) {
+  TcMlp<HID, NM, NL> mlp;
+  mlp.init(net, b0);
+  const int tid = threadIdx.x;
+  const long long r2 = (long long)res * res;
+  const long long S = (long long)gridDim.x * kTcThreads;
+  const long long g0 = begin + (long long)blockIdx.x * kTcThreads + tid;
+  int ix = (int)(g0 / r2), iy = (int)((g0 / res) % res), iz = (int)(g0 % res);
+  const int sx = (int)(S / r2), sy = (int)((S / res) % res), sz = (int)(S % res);
+  for (long long base = (long long)blockIdx.x * kTcThreads; base < count; base += S) {   // CTA-uniform
+    const long long i = base + tid;
+    const bool valid = i < count;
+    mlp.begin_row();
+    uint32_t w[FastRow<NM>::kWords];
+    if (valid) {
+      const float px = __ldg(coords + ix), py = __ldg(coords + iy), pz = __ldg(coords + iz);
+      uint32_t z[8];
+      if constexpr (TEX == 1) FastRow<NM>::tex_words(fd, px, py, pz, z);
+      else FastRow<NM>::ldg_words(fd, px, py, pz, z);
+      FastRow<NM>::words_from_z(z, px, py, pz, w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < FastRow<NM>::kWords; ++j) w[j] = 0u;
+    }
+    // idx += S
+    iz += sz;
+    int carry = iz >= res;
+    iz -= carry ? res : 0;
+    iy += sy + carry;
+    carry = iy >= res;
+    iy -= carry ? res : 0;
+    ix += sx + carry;
+    mlp.put_row(w);
+    uint32_t o[4];
+    mlp.run(o);
+    if (valid) {
+      const float v = sigmoidf_(__uint_as_float(o[0]));
+      out[i] = v;
+      // ScalarVolume invariant (volume.py:41-49) checked on the device: finite, in [0,1]
+      if (bad && !(v >= 0.f && v <= 1.f)) atomicAdd(bad, 1ull);
+    }
+  }
+  mlp.finish();
 }
 
 #if FVSRN_AB_VARIANTS   // measured slower, off by default
@@ -726,7 +551,7 @@ dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const f
 const void* tc_kernel_for(int hid, bool two_tiles) {
   switch (hid) {
 #if FVSRN_AB_VARIANTS
-    case 32: return two_tiles ? (const void*)dvr_tc2_kernel<32, 14, 4> : (const void*)dvr_tc_kernel<32, 14, 4>;
+    case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;   // tc2: no bias-in-MMA
     case 64: return two_tiles ? (const void*)dvr_tc2_kernel<64, 30, 6> : (const void*)dvr_tc_kernel<64, 30, 6>;
 #else
     case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;
@@ -740,6 +565,14 @@ const void* tc_tex_kernel_for(int hid, int fmode) {
   switch (hid) {
     case 32: return fmode == 2 ? (const void*)dvr_tc_kernel<32, 14, 4, 2> : (const void*)dvr_tc_kernel<32, 14, 4, 1>;
     case 64: return fmode == 2 ? (const void*)dvr_tc_kernel<64, 30, 6, 2> : (const void*)dvr_tc_kernel<64, 30, 6, 1>;
+    default: return nullptr;
+  }
+}
+
+const void* tc_decode_kernel_for(int hid, int fmode) {
+  switch (hid) {
+    case 32: return fmode == 2 ? (const void*)decode_tc_kernel<32, 14, 4, 2> : (const void*)decode_tc_kernel<32, 14, 4, 1>;
+    case 64: return fmode == 2 ? (const void*)decode_tc_kernel<64, 30, 6, 2> : (const void*)decode_tc_kernel<64, 30, 6, 1>;
     default: return nullptr;
   }
 }

@@ -60,31 +60,7 @@ __host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / 
 #ifndef FVSRN_TC_BIAS_MMA64
 #define FVSRN_TC_BIAS_MMA64 0
 #endif
-// FVSRN_TC_BIAS_CP: the biases are copied into the accumulators by the tensor core itself
-// (tcgen05.cp.128x256b from an 8-row shared-memory tile read with a zero 8-row-group
-// stride, i.e. one row broadcast to all 128 lanes), issued by the elected thread right
-// before the layer's MMAs: no per-thread LDS + tcgen05.st and no k16 bias tile
-#ifndef FVSRN_TC_BIAS_CP32
-#define FVSRN_TC_BIAS_CP32 0
-#endif
-#ifndef FVSRN_TC_BIAS_CP64
-#define FVSRN_TC_BIAS_CP64 0
-#endif
-constexpr bool tc_bias_cp(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_CP32 != 0 : FVSRN_TC_BIAS_CP64 != 0; }
-constexpr bool tc_bias_mma(int hid) {
-  return !tc_bias_cp(hid) && (hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0);
-}
-// FVSRN_TC_SKIP32: the 32-wide hidden layers take snake_alt apart inside the MMA,
-//   W h = W a - 2 W cos(a):
-// the pre-activation a is read straight from the previous layer's f32 accumulator in TMEM
-// as a kind::tf32 A operand (two accumulator regions, ping-pong), and only cos(a) is
-// computed, packed to fp16 and written as a shared-memory A tile for kind::f16 MMAs with
-// B = -2 W (plus the k16 bias tile).  Per activation: FMUL.RZ + MUFU.COS + half an F2FP,
-// no FFMA and no fp16 copy of a.
-#ifndef FVSRN_TC_SKIP32
-#define FVSRN_TC_SKIP32 0
-#endif
-constexpr bool tc_skip(int hid) { return hid == 32 && FVSRN_TC_SKIP32 != 0 && tc_bias_mma(hid); }
+constexpr bool tc_bias_mma(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0; }
 template <int HID, int NM, int NL>
 struct TcShape {
   static constexpr int kK0 = tc_round(16 + 2 * NM + 3, 16);   // FastRow<NM>::kK0
@@ -96,32 +72,18 @@ struct TcShape {
   static constexpr uint32_t kSboA = (uint32_t)(kKA / 8) * 128u;
   static constexpr int w_off(int l) { return l == 0 ? 0 : HID * kK0 + (l - 1) * HID * kKh; }
   static constexpr int kWTotal = HID * kK0 + (NL - 2) * HID * kKh + kNLast * kKh;   // halfs
-  // skip path: tf32 (f32-stored) weights of layers 1..NL-1 after the fp16 tiles, each an
-  // (N x HID) K-major canonical tile (core matrix 8 rows x 4 tf32, row = HID * 4 bytes)
-  static constexpr bool kSkip = tc_skip(HID);
-  static constexpr int kXOff = kWTotal * 2;   // bytes
-  static constexpr int x_off(int l) { return kXOff + (l - 1) * HID * HID * 4; }
-  static constexpr uint32_t kSboX = (uint32_t)HID * 32u;   // (HID * 4 / 16) * 128
-  static constexpr int kWBytes = kWTotal * 2 + (kSkip ? ((NL - 2) * HID + kNLast) * HID * 4 : 0);
   static constexpr int b_off(int l) { return l * HID; }
   static constexpr int kBTotal = (NL - 1) * HID + kNLast;
   // shared memory map (bytes)
   static constexpr int kWOff = 0;
-  static constexpr int kBOff = tc_round(kWOff + kWBytes, 16);
+  static constexpr int kBOff = tc_round(kWOff + kWTotal * 2, 16);
   static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
-  // bias broadcast tiles (tc_bias_cp): column c of the layer-major bias vector at byte
-  // (c/8)*256 + ((c%8)/4)*128 + r*16 + (c%4)*4 for the 8 identical rows r
-  static constexpr bool kBiasCp = tc_bias_cp(HID);
-  static constexpr int kBcOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
-  static constexpr int kBcBytes = kBiasCp ? kBTotal * 32 : 0;
-  static constexpr int kAOff = tc_round(kBcOff + kBcBytes, 128);
+  static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
   static constexpr int kATile = kTcThreads * kKA * 2;
   // with layer-0 rows in TMEM the one-tile kernel has no shared-memory A tile
   static constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
-  // (the skip path keeps a shared-memory A tile for the cos rows: columns 0..HID-1 cos(a),
-  // HID, HID+1 the constant 1.0 of the bias tile)
-  static constexpr int kMbarOff = (kA0 && !kSkip) ? kAOff : kAOff + kATile;
-  static constexpr int kSmem = kMbarOff + 32;   // mbarrier, TMEM slot, second mbarrier
+  static constexpr int kMbarOff = kA0 ? kAOff : kAOff + kATile;
+  static constexpr int kSmem = kMbarOff + 16;   // mbarrier, TMEM slot
   static constexpr int kSmem2 = kAOff + 2 * kATile + 32;   // two-tile variant
 };
 
@@ -131,6 +93,8 @@ struct TcShape {
 const void* tc_kernel_for(int hid, bool two_tiles);
 // the single-tile kernel specialised for a static fp16 texture grid (branch-free features)
 const void* tc_tex_kernel_for(int hid, int fmode = 1);   // fmode 1 texture, 2 LDG grid
+// the lattice decode (decode_tc_kernel) for a static fp16 grid: fmode 1 texture, 2 LDG
+const void* tc_decode_kernel_for(int hid, int fmode);
 size_t tc_smem_bytes(int hid, bool two_tiles);
 inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
 

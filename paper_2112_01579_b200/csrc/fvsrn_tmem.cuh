@@ -92,11 +92,6 @@ __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
 #ifndef FVSRN_MBAR_SUSPEND_NS
 #define FVSRN_MBAR_SUSPEND_NS 0   // try_wait suspend-time hint (0: hardware default)
 #endif
-// FVSRN_MBAR_TRIES: try_wait attempts per watchdog count, branched inside one PTX block
-// (2 instructions per attempt instead of 5 with the counter update and its test)
-#ifndef FVSRN_MBAR_TRIES
-#define FVSRN_MBAR_TRIES 1
-#endif
 __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   uint32_t done = 0, polls = 0;
   while (true) {
@@ -105,33 +100,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity), "n"(FVSRN_MBAR_SUSPEND_NS) : "memory");
-#elif FVSRN_MBAR_TRIES > 1
-    static_assert(FVSRN_MBAR_TRIES <= 8, "FVSRN_MBAR_TRIES");
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-#if FVSRN_MBAR_TRIES > 2
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-#endif
-#if FVSRN_MBAR_TRIES > 3
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-#endif
-#if FVSRN_MBAR_TRIES > 4
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "@p bra.uni MBW_DONE;\n\t"
-#endif
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "MBW_DONE:\n\t"
-        "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
 #else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -139,7 +107,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
 #endif
     if (done) break;
-    if (++polls > (1u << 26) / FVSRN_MBAR_TRIES) __trap();
+    if (++polls > (1u << 26)) __trap();
 #if FVSRN_MBAR_BACKOFF_NS > 0
     __nanosleep(FVSRN_MBAR_BACKOFF_NS);   // give the issue slots to other warps
 #endif
@@ -165,21 +133,6 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}"
       :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
-// D[tmem] (+)= A[tmem] * B[smem]^T, kind::tf32 (f32-stored A/B, 10-bit mantissa -> f32), A from
-// TMEM (lane = row, one 32-bit column per K element: an f32 accumulator region is a valid A)
-__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}"
-      :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
-}
-// shared memory -> TMEM, 128 lanes x 256 bits (8 columns), executed in issue order with
-// this thread's tcgen05.mma
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
-}
 // all previously issued MMAs of this thread arrive on the mbarrier when complete
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
@@ -195,10 +148,6 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 // Instruction descriptor: kind::f16, A/B fp16 K-major, D f32, M x N.
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-// Instruction descriptor: kind::tf32, A/B tf32 (format 2) K-major, D f32, M x N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 }  // namespace fvsrn
