@@ -656,6 +656,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
     case KernelKind::kDVRTex: k = "dvr_kernel<" + tmpl + "," + std::to_string(fmode) + "> (mma.sync m16n8k16, frame specialisation)"; break;
     case KernelKind::kDVRPair: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + ",2> (mma.sync m16n8k16, two lanes per ray)"; break;
     case KernelKind::kDVRQuad: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + ",4> (mma.sync m16n8k16, four lanes per ray)"; break;
+    case KernelKind::kDVROcto: k = "dvr_pair_kernel<" + tmpl + "," + std::to_string(fmode) + ",8> (mma.sync m16n8k16, eight lanes per ray)"; break;
     default: k = "dvr_kernel<" + tmpl + "> (mma.sync m16n8k16)"; break;
   }
   const char* grid = m->R <= 0 ? "no latent grid"
@@ -711,7 +712,7 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
   if (occ < 1) return fail(FVSRN_ECAPACITY, "kernel does not fit on an SM (shared memory)");
   if (g_occ_cap > 0) occ = std::min(occ, g_occ_cap);
   if (kind == KernelKind::kDVR || kind == KernelKind::kDVRTex || kind == KernelKind::kDVRPair ||
-      kind == KernelKind::kDVRQuad ||
+      kind == KernelKind::kDVRQuad || kind == KernelKind::kDVROcto ||
       kind == KernelKind::kDVRPipe ||
       tc ||
       kind == KernelKind::kDVRDual) {
@@ -722,7 +723,8 @@ int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cuda
     // 2.0-2.5 0.225-0.228, 3.0 0.240; FVSRN_SLOTS_PER_LANE overrides both)
     static const char* spl_env = std::getenv("FVSRN_SLOTS_PER_LANE");
     static const char* spl4_env = std::getenv("FVSRN_SLOTS_PER_LANE4");
-    const double slots_per_lane = kind == KernelKind::kDVRQuad ? (spl4_env ? std::atof(spl4_env) : 2.25)
+    const double slots_per_lane = (kind == KernelKind::kDVRQuad || kind == KernelKind::kDVROcto)
+                                      ? (spl4_env ? std::atof(spl4_env) : 2.25)
                                   : spl_env ? std::atof(spl_env) : (kind == KernelKind::kDVRPair ? 2.25 : 1.75);
     const double rays_per_sm_cta = (double)m->num_sms * threads;
     const int occ_work = (int)std::lround((double)work_warps * 32.0 / (rays_per_sm_cta * slots_per_lane));
@@ -810,6 +812,15 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   const bool small = frame && m->hid_pad == 32 && dvr_mode() != DvrMode::kTC &&
                      frame_px <= pair_frac * (double)full_lanes;
   void* args[] = {&net, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
+  // eight lanes per ray up to 1.25x (~345^2; stepsize 1/256: 128^2 0.218 -> 0.178 ms, 192^2
+  // 0.298 -> 0.252, 320^2 0.524 -> 0.508; 384^2 is better with four); FVSRN_OCTO_FRAC overrides
+  static const double octo_frac = [] {
+    const char* e = std::getenv("FVSRN_OCTO_FRAC");
+    return e ? std::atof(e) : 1.25;
+  }();
+  if (small && frame_px <= octo_frac * (double)full_lanes)
+    return launch(m, KernelKind::kDVROcto, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 4 + 1,
+                  fmode);
   if (small && frame_px <= quad_frac * (double)full_lanes)
     return launch(m, KernelKind::kDVRQuad, stage_smem_bytes(net, true, m->k0), args, s, n_slots / 8 + 1,
                   fmode);

@@ -153,7 +153,7 @@ dvr_pair_kernel(NetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
                 MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
                 float* __restrict__ out, unsigned long long* __restrict__ queue,
                 unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
-  static_assert(Q == 2 || Q == 4, "lanes per ray");
+  static_assert(Q == 2 || Q == 4 || Q == 8, "lanes per ray");
   const int rs = fd.k0 + 8;
   uint2* wf_s; float* b_s; TFDev* tf; __half* stage; float* ob;
   stage_setup(net, b0, tf_g, rs, wf_s, b_s, tf, stage, ob);
@@ -899,6 +899,10 @@ const void* kernel_for(KernelKind kind, int hid, bool fast, int fmode) {
       return !fast ? nullptr : fmode == 2                                                    \
           ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2, 4>               \
           : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1, 4>;              \
+    if (kind == KernelKind::kDVROcto)                                                        \
+      return !fast ? nullptr : fmode == 2                                                    \
+          ? (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 2, 8>               \
+          : (const void*)dvr_pair_kernel<H, (H - 4) / 2, fast_layers(H), 1, 8>;              \
     FVSRN_WS_CASE(H)                                                                         \
     if (kind == KernelKind::kSample)                                                         \
       return fast ? (const void*)sample_kernel<H, 4, (H - 4) / 2, fast_layers(H)>            \

@@ -102,7 +102,7 @@ struct RayRecs {
 // (kDVRPair / kDVRQuad: the frame specialisation with two / four lanes per ray, for small
 // frames; kSampleTC: the tcgen05 lattice decode, fvsrn_tc.cu)
 enum class KernelKind { kDVR, kDVRWS, kDVRTC, kDVRPipe, kDVRDual, kSample, kFused, kDVRTex, kDVRTCTex,
-                        kSampleTex, kDVRPair, kDVRQuad, kSampleTC };
+                        kSampleTex, kDVRPair, kDVRQuad, kSampleTC, kDVROcto };
 
 // Returns the kernel instantiation for a padded hidden width (16..128), or nullptr.
 // fast: specialised default-input / snake_alt variant (see FastRow).

@@ -92,6 +92,29 @@ def test_decode_vs_reference():
     assert np.abs(v - a["decode_temporal_12_t16.25"]).max() <= DENS_TOL
 
 
+@pytest.mark.parametrize("kernel", ["tc", "warp"])
+def test_decode_kernels_vs_oracle(kernel):
+    """The tcgen05 lattice decode (default for the default shapes) and the mma.sync one,
+    each against the oracle on a whole 48^3 lattice, and launched as named."""
+    from paper_2112_01579_b200 import device as D
+
+    m, om = _model("cfg2"), _omodel("cfg2")
+    prev = D.set_dvr_kernel(kernel)
+    try:
+        D.kernel_timer(True)
+        vol = P.decode_volume(m, 48).values
+        D.kernel_timer_read()
+        name = D.kernel_timer_info()
+        D.kernel_timer(False)
+    finally:
+        D.set_dvr_kernel(prev)
+    assert ("decode_tc_kernel" in name) == (kernel == "tc"), name
+    axis = np.linspace(0.0, 1.0, 48)
+    gx, gy, gz = np.meshgrid(axis, axis, axis, indexing="ij")
+    want = O.eval_density(om, np.stack([gx.ravel(), gy.ravel(), gz.ravel()], -1)).reshape(48, 48, 48)
+    assert np.abs(vol - want).max() <= DENS_TOL
+
+
 def test_decode_full_256_vs_oracle_slices():
     # config 4: full 256^3 decode on the GPU; oracle on two lattice slabs
     m, om = _model("cfg2"), _omodel("cfg2")

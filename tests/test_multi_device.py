@@ -160,16 +160,18 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("quad_frac,lanes", [("100", "four lanes per ray"), ("0", "two lanes per ray")])
-def test_small_frame_lane_group_kernels_bit_identical(quad_frac, lanes):
-    """Four lanes per ray (FVSRN_QUAD_FRAC admits the frame) and two lanes per ray
-    (FVSRN_QUAD_FRAC=0): pixels and counts identical to the one-lane march, ET on / loose /
-    off, and a frame smaller than one warp's rays."""
+@pytest.mark.parametrize("octo_frac,quad_frac,lanes", [("100", "0", "eight lanes per ray"),
+                                                        ("0", "100", "four lanes per ray"),
+                                                        ("0", "0", "two lanes per ray")])
+def test_small_frame_lane_group_kernels_bit_identical(octo_frac, quad_frac, lanes):
+    """Eight / four / two lanes per ray (FVSRN_OCTO_FRAC / FVSRN_QUAD_FRAC admit the frame):
+    pixels and counts identical to the one-lane march, ET on / loose / off, and a frame
+    smaller than one warp's rays."""
     import json
     import os
     import subprocess
     import sys
-    env = dict(os.environ, FVSRN_QUAD_FRAC=quad_frac)
+    env = dict(os.environ, FVSRN_OCTO_FRAC=octo_frac, FVSRN_QUAD_FRAC=quad_frac)
     r = subprocess.run([sys.executable, "-c", _QUAD_SCRIPT], env=env, capture_output=True, text=True,
                        timeout=300, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]
