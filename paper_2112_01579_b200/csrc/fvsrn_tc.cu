@@ -67,6 +67,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_POLY
 #define FVSRN_TC_POLY 6
 #endif
+#ifndef FVSRN_TC_DEADROW
+#define FVSRN_TC_DEADROW 1
+#endif
 
 // snake_alt activations of one accumulator row -> packed fp16 pairs (TMEM A operand)
 template <int HID>
@@ -290,7 +293,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   const bool density = net.head == 0;
   constexpr bool kFrame = TEX >= 1;
 
-  RayLane r;
+  RayLane r{};   // zero state: a lane without a ray builds a finite dummy row
   r.has = false;
   LaneQueue q{0, 0, false};
   unsigned long long evals = 0;
@@ -306,7 +309,10 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     evals += __popc(__ballot_sync(0xffffffffu, r.has));
     mlp.begin_row();
     uint32_t w[FastRow<NM>::kWords];
-    if (r.has) {
+    // FVSRN_TC_DEADROW: lanes without a ray build a row from their stale (finite) ray
+    // state instead of branching around the feature code and zeroing the row; the row is
+    // independent of the others in the MMA and its result is dropped
+    if ((FVSRN_TC_DEADROW && HID <= 32) || r.has) {   // (64-wide: spills)
       const float kf = (float)r.k;
       const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
       if constexpr (TEX >= 1) {   // static fp16 grid: no runtime branches
