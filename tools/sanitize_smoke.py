@@ -1,5 +1,7 @@
 """Small invocations of every kernel family, for compute-sanitizer runs:
-    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py"""
+    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+(the small frame takes the eight-lanes-per-ray kernel; FVSRN_OCTO_FRAC=0 the four-lane one,
+FVSRN_OCTO_FRAC=0 FVSRN_QUAD_FRAC=0 the two-lane one)"""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np
@@ -15,13 +17,16 @@ for kw in (dict(layers=4, hidden=32, grid_resolution=8, seed=0),
     m = P.model_init(P.ModelConfig(**kw))
     t = 3.0 if m.is_temporal else None
     src = P.ModelSource(m, P.TF_PRESETS["warm"], t=t)
-    for k in ("auto", "warp", "tc"):
-        D.set_dvr_kernel(k)
-        P.render_image(src, cam, s)
-    D.set_dvr_kernel("auto")
+    for sampler in ("auto", "ldg"):    # texture units / exact-weight LDG.256 sampler
+        D.set_grid_sampler(sampler)
+        for k in ("auto", "warp", "tc"):   # auto on this small frame: the lane-group kernels
+            D.set_dvr_kernel(k)
+            P.render_image(src, cam, s)
+            P.decode_volume(m, 12, t=t)    # tcgen05 decode (tc / auto) or mma.sync (warp)
+        D.set_dvr_kernel("auto")
+    D.set_grid_sampler("auto")
     p = np.random.default_rng(0).uniform(0, 1, (100, 3))
     P.eval_density(m, p, t=t)
-    P.decode_volume(m, 12, t=t)
 vol = P.ScalarVolume(np.random.default_rng(1).uniform(0, 1, (9, 7, 5)).astype(np.float32))
 P.render_image(P.VolumeSource(vol, P.TF_PRESETS["grayscale"]), cam, s)
 m = P.model_init(P.ModelConfig(layers=3, hidden=32, grid_resolution=8, seed=0))
