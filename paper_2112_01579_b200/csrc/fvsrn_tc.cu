@@ -161,6 +161,9 @@ struct TcMlp {
       for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
       for (int i = tid; i < S::kBTotal; i += kTcThreads) bs[i] = (b0 && i < HID) ? b0[i] : net.b[i];
     }
+    // the weight tiles were written through the generic proxy and are read by the tensor
+    // core (async proxy)
+    fence_proxy_async_smem();
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
     if (tid == 0) mbar_init(mb(), 1);
     tc_fence_before();
