@@ -15,7 +15,7 @@ timeout 1500 python bench.py --impl reference --steps 20 --warmup 5 > $out/bench
 FVSRN_BENCH_ONE_GPU=1 timeout 600 python bench.py --gpus 2 --steps 8 --check-frame --no-cpu-baseline > $out/bench_2ranks_onegpu.json 2> $out/bench_2ranks.err; tail -c 300 $out/bench_2ranks_onegpu.json; echo
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 # full captures of each config's dominant kernel (the one bench.py reports in roofline.kernel)
-for spec in "cfg2:dvr_tc_kernel" "cfg3:dvr_tc_kernel" "cfg5:dvr_tc_kernel" "cfg1:dvr_pair_kernel" "cfg4:sample_kernel"; do
+for spec in "cfg2:dvr_tc_kernel" "cfg3:dvr_tc_kernel" "cfg5:dvr_tc_kernel" "cfg1:dvr_pair_kernel" "cfg4:decode_tc_kernel"; do
   c=${spec%%:*}; k=${spec#*:}
   timeout 400 ncu --set full --import-source on --clock-control none -k regex:$k -s 3 -c 1 --export $out/ncu_$c -f python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
   ncu -i $out/ncu_$c.ncu-rep --page raw --csv > $out/ncu_${c}_raw.csv 2>/dev/null

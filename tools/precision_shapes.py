@@ -61,6 +61,20 @@ def main():
             print(f"  {name:9s} {sampler}: max {e.max():.3e} mean {e.mean():.3e} p99.99 "
                   f"{np.quantile(e, 0.9999):.3e} at p={np.round(p[k], 4).tolist()} "
                   f"(ref {want[k]:.4f})", flush=True)
+    print("decode_volume (64^3 lattice) vs pinned oracle (tolerance 1e-2)")
+    axis = np.linspace(0.0, 1.0, 64)
+    gx, gy, gz = np.meshgrid(axis, axis, axis, indexing="ij")
+    lat = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], -1)
+    for name, (m, om) in ms.items():
+        t = 6.5 if name == "cfg5" else None
+        want = O.eval_density(om, lat, t=t).reshape(64, 64, 64)
+        P.device.kernel_timer(True)
+        got = P.decode_volume(m, 64, t=t).values
+        P.device.kernel_timer_read()
+        kname = P.device.kernel_timer_info().split(" ")[0]
+        P.device.kernel_timer(False)
+        e = np.abs(got - want)
+        print(f"  {name:9s} {kname}: max {e.max():.3e} mean {e.mean():.3e}", flush=True)
     if not args.renders:
         return
     a = np.load(G / "golden_shapes.npz")
