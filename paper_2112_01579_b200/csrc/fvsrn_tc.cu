@@ -65,18 +65,23 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 // round 2, cfg 2 / cfg 3 ms: every 4th 3.02 / 25.98, 5th 2.86 / 25.08, 6th 2.82 / 25.19,
 // 7th 2.83, 8th - / 25.41, 12th 2.88).  0 disables.
 #ifndef FVSRN_TC_POLY
-#define FVSRN_TC_POLY 6
+#define FVSRN_TC_POLY 6     // 32-wide
 #endif
+#ifndef FVSRN_TC_POLY64
+#define FVSRN_TC_POLY64 5   // 64-wide (per 32-column half)
+#endif
+template <int HID>
+constexpr int tc_poly() { return HID <= 32 ? FVSRN_TC_POLY : FVSRN_TC_POLY64; }
 #ifndef FVSRN_TC_DEADROW
 #define FVSRN_TC_DEADROW 1
 #endif
 
-// snake_alt activations of one accumulator row -> packed fp16 pairs (TMEM A operand)
-template <int HID>
-__device__ __forceinline__ void act_words(const uint32_t (&acc)[HID], uint32_t (&w)[HID / 2]) {
-  constexpr int P = FVSRN_TC_POLY;
+// snake_alt activations of N accumulator columns -> packed fp16 pairs (TMEM A operand);
+// every P-th column's cosine on the FMA pipe
+template <int N, int P = FVSRN_TC_POLY>
+__device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w)[N / 2]) {
 #pragma unroll
-  for (int j = 0; j < HID / 2; ++j) {
+  for (int j = 0; j < N / 2; ++j) {
     float h[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -169,7 +174,7 @@ struct TcMlp {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if constexpr (S::kBiasMma) {
+    if constexpr (S::kBias0) {
       // W0's pad column (K0 - 1; the row's pad is 1.0) := this frame's layer-0 bias
       constexpr int K = S::kK0, k = S::kK0 - 1;
       for (int n = tid; n < HID; n += kTcThreads)
@@ -191,13 +196,13 @@ struct TcMlp {
   // Start of a step, before the row is built: the layer-0 bias into D (64-wide; its 64
   // registers are dead again before the row's are live)
   __device__ void begin_row() {
-    if constexpr (!S::kBiasMma) tmem_bias<HID>(t_row, b_s() + S::b_off(0));
+    if constexpr (!S::kBias0) tmem_bias<HID>(t_row, b_s() + S::b_off(0));
   }
 
   // This thread's layer-0 row (zeros for a thread without work) -> TMEM A; every thread
   // calls it (tcgen05.st is .sync.aligned).  Ends with the CTA barrier the MMA issue needs.
   __device__ void put_row(uint32_t (&w)[kWords]) {
-    if constexpr (S::kBiasMma) w[kWords - 1] |= 0x3C000000u;   // pad column = 1.0
+    if constexpr (S::kBias0) w[kWords - 1] |= 0x3C000000u;   // pad column = 1.0
     tmem_st_any<kWords>(t_row + S::kTCols, w);
     tmem_wait_st();
     tc_fence_before();
@@ -218,7 +223,7 @@ struct TcMlp {
 #pragma unroll
         for (int kk = 0; kk < K / 16; ++kk) {
           // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
-          const uint32_t acc = (S::kBiasMma && kk == 0) ? 0u : 1u;
+          const uint32_t acc = (kk == 0 && (S::kBiasMma || (l == 0 && S::kBias0))) ? 0u : 1u;
           umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
         }
         umma_commit(mb());
@@ -233,7 +238,7 @@ struct TcMlp {
           uint32_t acc[32], w[16];
           tmem_ld<32>(t_row, acc);
           tmem_wait_ld();
-          act_words<32>(acc, w);
+          act_words<32, tc_poly<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols, w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
@@ -241,7 +246,7 @@ struct TcMlp {
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s() + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
           }
-          act_words<32>(acc, w);
+          act_words<32, tc_poly<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols + 16, w);
         } else {
           uint32_t acc[HID];
@@ -252,7 +257,7 @@ struct TcMlp {
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
           }
           uint32_t w[HID / 2];
-          act_words<HID>(acc, w);
+          act_words<HID, tc_poly<HID>()>(acc, w);
           tmem_st<HID / 2>(t_row + S::kTCols, w);
         }
         if constexpr (S::kBiasMma) {

@@ -60,11 +60,17 @@ __host__ __device__ constexpr int tc_round(int x, int m) { return (x + m - 1) / 
 #ifndef FVSRN_TC_BIAS_MMA64
 #define FVSRN_TC_BIAS_MMA64 0
 #endif
+#ifndef FVSRN_TC_BIAS0_PAD
+#define FVSRN_TC_BIAS0_PAD 1
+#endif
 constexpr bool tc_bias_mma(int hid) { return hid <= 32 ? FVSRN_TC_BIAS_MMA32 != 0 : FVSRN_TC_BIAS_MMA64 != 0; }
 template <int HID, int NM, int NL>
 struct TcShape {
   static constexpr int kK0 = tc_round(16 + 2 * NM + 3, 16);   // FastRow<NM>::kK0
   static constexpr bool kBiasMma = tc_bias_mma(HID);
+  // layer-0 bias through the input row's pad column (1.0) and W0's pad column (this frame's
+  // b0, fp16), whenever K0 has a pad column: no per-step bias store into D for layer 0
+  static constexpr bool kBias0 = kBiasMma || (FVSRN_TC_BIAS0_PAD != 0 && tc_round(16 + 2 * NM + 3, 16) > 16 + 2 * NM + 3);
   static constexpr int kKh = HID + (kBiasMma ? 16 : 0);   // K of layers 1..NL-1
   static constexpr int kKA = kK0 > kKh ? kK0 : kKh;          // A tile width (halfs)
   static constexpr int kNLast = 16;
