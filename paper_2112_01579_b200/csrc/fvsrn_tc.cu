@@ -70,6 +70,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_POLY64
 #define FVSRN_TC_POLY64 5   // 64-wide (per 32-column half)
 #endif
+#ifndef FVSRN_TC_BIAS_HALVES
+#define FVSRN_TC_BIAS_HALVES 1
+#endif
 template <int HID>
 constexpr int tc_poly() { return HID <= 32 ? FVSRN_TC_POLY : FVSRN_TC_POLY64; }
 #ifndef FVSRN_TC_DEADROW
@@ -238,13 +241,25 @@ struct TcMlp {
           uint32_t acc[32], w[16];
           tmem_ld<32>(t_row, acc);
           tmem_wait_ld();
+#if FVSRN_TC_BIAS_HALVES
+          // the next layer's bias, one half at a time right after that half was read (32
+          // bias registers live instead of 64)
+          if constexpr (!S::kBiasMma) {
+            if (l + 1 < NL - 1) tmem_bias<32>(t_row, b_s() + S::b_off(l + 1));
+            else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
+          }
+#endif
           act_words<32, tc_poly<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols, w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
           if constexpr (!S::kBiasMma) {
+#if FVSRN_TC_BIAS_HALVES
+            if (l + 1 < NL - 1) tmem_bias<32>(t_row + 32, b_s() + S::b_off(l + 1) + 32);
+#else
             if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s() + S::b_off(l + 1));
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
+#endif
           }
           act_words<32, tc_poly<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols + 16, w);
