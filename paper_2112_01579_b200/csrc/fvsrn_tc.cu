@@ -78,6 +78,9 @@ constexpr int tc_poly() { return HID <= 32 ? FVSRN_TC_POLY : FVSRN_TC_POLY64; }
 #ifndef FVSRN_TC_DEADROW
 #define FVSRN_TC_DEADROW 1
 #endif
+#ifndef FVSRN_TC_DEADROW_MAXW
+#define FVSRN_TC_DEADROW_MAXW 64   // widest layer that builds dummy rows (64: 24.69 -> 24.58 ms at cfg 3)
+#endif
 
 // snake_alt activations of N accumulator columns -> packed fp16 pairs (TMEM A operand);
 // every P-th column's cosine on the FMA pipe
@@ -335,7 +338,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     // FVSRN_TC_DEADROW: lanes without a ray build a row from their stale (finite) ray
     // state instead of branching around the feature code and zeroing the row; the row is
     // independent of the others in the MMA and its result is dropped
-    if ((FVSRN_TC_DEADROW && HID <= 32) || r.has) {   // (64-wide: spills)
+    if ((FVSRN_TC_DEADROW && HID <= FVSRN_TC_DEADROW_MAXW) || r.has) {
       const float kf = (float)r.k;
       const float px = fmaf(kf, r.dd0, r.pe0), py = fmaf(kf, r.dd1, r.pe1), pz = fmaf(kf, r.dd2, r.pe2);
       if constexpr (TEX >= 1) {   // static fp16 grid: no runtime branches
