@@ -68,7 +68,7 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #define FVSRN_TC_POLY 6     // 32-wide
 #endif
 #ifndef FVSRN_TC_POLY64
-#define FVSRN_TC_POLY64 5   // 64-wide (per 32-column half)
+#define FVSRN_TC_POLY64 6   // 64-wide, per 32-column half (4/5/6/7/8: 24.44/24.55/24.35/25.13/24.83 ms at cfg 3)
 #endif
 #ifndef FVSRN_TC_BIAS_HALVES
 #define FVSRN_TC_BIAS_HALVES 1
