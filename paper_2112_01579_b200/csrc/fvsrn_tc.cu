@@ -70,6 +70,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_POLY64
 #define FVSRN_TC_POLY64 6   // 64-wide, per 32-column half (4/5/6/7/8: 24.44/24.55/24.35/25.13/24.83 ms at cfg 3)
 #endif
+#ifndef FVSRN_TC_SPLIT32
+#define FVSRN_TC_SPLIT32 1   // 32-wide epilogue in two 16-column halves (64 registers: 8 CTAs/SM)
+#endif
 #ifndef FVSRN_TC_BIAS_HALVES
 #define FVSRN_TC_BIAS_HALVES 1
 #endif
@@ -93,6 +96,22 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w
     for (int i = 0; i < 2; ++i) {
       const int e = 2 * j + i;
       const float x = __uint_as_float(acc[e]);
+      h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
+    }
+    w[j] = pack_half2(h[0], h[1]);
+  }
+}
+
+// columns 16..31 of a 32-wide row (the FMA-pipe pattern continues from column 16)
+template <int P>
+__device__ __forceinline__ void act_words16_hi(const uint32_t (&acc)[16], uint32_t (&w)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float h[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = 16 + 2 * j + i;
+      const float x = __uint_as_float(acc[e - 16]);
       h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
     }
     w[j] = pack_half2(h[0], h[1]);
@@ -266,6 +285,17 @@ struct TcMlp {
           }
           act_words<32, tc_poly<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols + 16, w);
+        } else if constexpr (FVSRN_TC_SPLIT32 && HID == 32 && S::kBiasMma) {
+          // two 16-column halves (fewer live accumulator registers)
+          uint32_t acc[16], w[8];
+          tmem_ld<16>(t_row, acc);
+          tmem_wait_ld();
+          act_words<16, tc_poly<HID>()>(acc, w);
+          tmem_st_x8(t_row + S::kTCols, w);
+          tmem_ld<16>(t_row + 16, acc);
+          tmem_wait_ld();
+          act_words16_hi<tc_poly<HID>()>(acc, w);
+          tmem_st_x8(t_row + S::kTCols + 8, w);
         } else {
           uint32_t acc[HID];
           tmem_ld<HID>(t_row, acc);

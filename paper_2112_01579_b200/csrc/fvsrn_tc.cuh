@@ -8,7 +8,7 @@ constexpr int kTcThreads = 128;   // 4 warps = 128 rays = one M=128 UMMA tile
 
 // CTAs per SM the register budget is sized for (96 regs for 32-wide, 168 for 64-wide)
 #ifndef FVSRN_TC_MIN_BLOCKS
-#define FVSRN_TC_MIN_BLOCKS 6   // 4x32 (bias in the MMA, 80 registers): 5 3.01, 6 2.88, 7 2.89, 8 3.00 ms at cfg 2
+#define FVSRN_TC_MIN_BLOCKS 8   // 4x32, 16-column split epilogue (64 registers): 6 2.744, 7 2.783, 8 2.729 ms at cfg 2 (full-row epilogue at 80 registers: 5 3.01, 6 2.88, 7 2.89, 8 3.00)
 #endif
 #ifndef FVSRN_TC_MIN_BLOCKS_WIDE
 #define FVSRN_TC_MIN_BLOCKS_WIDE 4
