@@ -70,6 +70,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_POLY64
 #define FVSRN_TC_POLY64 6   // 64-wide, per 32-column half (4/5/6/7/8: 24.44/24.55/24.35/25.13/24.83 ms at cfg 3)
 #endif
+#ifndef FVSRN_TC_CHUNK64
+#define FVSRN_TC_CHUNK64 16   // 64-wide epilogue chunk, 32 or 16 columns (16: 84 registers, cfg 3 24.34 -> 23.95 ms)
+#endif
 #ifndef FVSRN_TC_SPLIT32
 #define FVSRN_TC_SPLIT32 1   // 32-wide epilogue in two 16-column halves (64 registers: 8 CTAs/SM)
 #endif
@@ -102,16 +105,16 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w
   }
 }
 
-// columns 16..31 of a 32-wide row (the FMA-pipe pattern continues from column 16)
-template <int P>
-__device__ __forceinline__ void act_words16_hi(const uint32_t (&acc)[16], uint32_t (&w)[8]) {
+// N accumulator columns that sit at column OFF of the FMA-pipe pattern (e % P == P - 1)
+template <int N, int OFF, int P>
+__device__ __forceinline__ void act_words_at(const uint32_t (&acc)[N], uint32_t (&w)[N / 2]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < N / 2; ++j) {
     float h[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const int e = 16 + 2 * j + i;
-      const float x = __uint_as_float(acc[e - 16]);
+      const int e = OFF + 2 * j + i;
+      const float x = __uint_as_float(acc[2 * j + i]);
       h[i] = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
     }
     w[j] = pack_half2(h[0], h[1]);
@@ -258,7 +261,21 @@ struct TcMlp {
       tc_fence_after();
       if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> the next A operand
-        if constexpr (HID == 64) {
+        if constexpr (HID == 64 && FVSRN_TC_CHUNK64 == 16 && !S::kBiasMma) {
+          // four 16-column quarters; the next layer's bias stored per quarter right after
+          // that quarter was read; the FMA-pipe pattern restarts every 32 columns
+          uint32_t acc[16], w[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            tmem_ld<16>(t_row + 16u * q, acc);
+            tmem_wait_ld();
+            if (l + 1 < NL - 1) tmem_bias<16>(t_row + 16u * q, b_s() + S::b_off(l + 1) + 16 * q);
+            else if (q == 0) tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
+            if (q & 1) act_words_at<16, 16, tc_poly<HID>()>(acc, w);
+            else act_words_at<16, 0, tc_poly<HID>()>(acc, w);
+            tmem_st_x8(t_row + S::kTCols + 8u * q, w);
+          }
+        } else if constexpr (HID == 64) {
           // two 32-column halves: half the live accumulator registers
           uint32_t acc[32], w[16];
           tmem_ld<32>(t_row, acc);
@@ -294,7 +311,7 @@ struct TcMlp {
           tmem_st_x8(t_row + S::kTCols, w);
           tmem_ld<16>(t_row + 16, acc);
           tmem_wait_ld();
-          act_words16_hi<tc_poly<HID>()>(acc, w);
+          act_words_at<16, 16, tc_poly<HID>()>(acc, w);
           tmem_st_x8(t_row + S::kTCols + 8, w);
         } else {
           uint32_t acc[HID];
