@@ -141,15 +141,21 @@ class ClockSampler:
 
 def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
     """MUFU (XU-pipe) instructions per evaluation in the launched kernel: one MUFU.COS per
-    hidden activation except the ones evaluated on the FMA pipe (tcgen05 kernel: every 6th
-    element of a row, FVSRN_TC_POLY; mma.sync kernels: none, FVSRN_POLY_EVERY=0), plus
-    MUFU.TANH for the sigmoid head and MUFU.EX2 for alpha.  The NeRF base sin/cos run on
+    hidden activation except the ones evaluated on the FMA pipe (tcgen05 kernels; mma.sync
+    kernels: none, FVSRN_POLY_EVERY=0), plus MUFU.TANH for the sigmoid head and, in the
+    march, MUFU.EX2 for alpha.  The NeRF base sin/cos run on
     the FMA pipe in the mma.sync kernels (FVSRN_FOURIER_POLY=1) and on MUFU.SIN/COS in the
     tcgen05 kernels (3 axes x 2)."""
     layers, hid = model_cfg["layers"], model_cfg["hidden"]
-    tc = kernel.startswith("dvr_tc")
-    per_row = hid - hid // 6 if tc else hid
-    return (layers - 1) * per_row + 2 + (6 if tc else 0)
+    tc = kernel.startswith(("dvr_tc", "decode_tc"))
+    if tc:
+        # fvsrn_tc.cu: every 5th column at 32-wide (FVSRN_TC_POLY), every 6th column of each
+        # 32-column half at 64-wide (FVSRN_TC_POLY64) evaluates its cosine on the FMA pipe
+        on_fma = (hid + 1) // 5 if hid <= 32 else (hid // 32) * (33 // 6)
+        per_row = hid - on_fma
+    else:
+        per_row = hid
+    return (layers - 1) * per_row + (1 if kernel.startswith("decode") else 2) + (6 if tc else 0)
 
 
 def measured_peaks():

@@ -65,7 +65,7 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 // round 2, cfg 2 / cfg 3 ms: every 4th 3.02 / 25.98, 5th 2.86 / 25.08, 6th 2.82 / 25.19,
 // 7th 2.83, 8th - / 25.41, 12th 2.88).  0 disables.
 #ifndef FVSRN_TC_POLY
-#define FVSRN_TC_POLY 6     // 32-wide
+#define FVSRN_TC_POLY 5     // 32-wide (at 8 CTAs/SM, cfg 2: every 4th/5th/6th/7th/8th 2.83/2.72/2.75/2.76/2.76 ms)
 #endif
 #ifndef FVSRN_TC_POLY64
 #define FVSRN_TC_POLY64 6   // 64-wide, per 32-column half (4/5/6/7/8: 24.44/24.55/24.35/25.13/24.83 ms at cfg 3)
