@@ -58,12 +58,6 @@ std::atomic<int> g_dvr_mode_i{[] {
   if (FVSRN_AB_VARIANTS && e && std::string(e) == "dual") return (int)DvrMode::kDual;
   return (int)DvrMode::kAuto;
 }()};
-// tcgen05 kernel: one 128-ray tile per CTA (default, measured faster), or two tiles in
-// ping-pong (FVSRN_TC_TILES=2)
-const bool g_tc_two_tiles = [] {
-  const char* e = std::getenv("FVSRN_TC_TILES");
-  return FVSRN_AB_VARIANTS && e && e[0] == '2';
-}();
 // latent-grid sampler for F = 16 grids: 0 auto, 1 texture units, 2 LDG + HFMA2
 std::atomic<int> g_grid_mode{[] {
   const char* e = std::getenv("FVSRN_GRID");
@@ -639,7 +633,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
   switch (kind) {
     case KernelKind::kDVRTC:
     case KernelKind::kDVRTCTex:
-      k = std::string(g_tc_two_tiles ? "dvr_tc2_kernel<" : "dvr_tc_kernel<") + std::to_string(h) + "," +
+      k = std::string("dvr_tc_kernel<") + std::to_string(h) + "," +
           std::to_string((h - 4) / 2) + "," + std::to_string(m->layers) +
           (kind == KernelKind::kDVRTCTex ? "," + std::to_string(fmode) : "") +
           "> (tcgen05.mma kind::f16, TMEM accumulators)";
@@ -669,7 +663,7 @@ std::string kernel_desc(const fvsrn_model* m, KernelKind kind, int fmode = 1) {
 int launch(const fvsrn_model* m, KernelKind kind, size_t smem, void** args, cudaStream_t s,
            long long work_warps, int fmode = 1) {
   const bool tc = kind == KernelKind::kDVRTC || kind == KernelKind::kDVRTCTex;
-  const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad, g_tc_two_tiles)
+  const void* fn = kind == KernelKind::kDVRTC ? tc_kernel_for(m->hid_pad)
                    : kind == KernelKind::kDVRTCTex ? tc_tex_kernel_for(m->hid_pad, fmode)
                    : kind == KernelKind::kSampleTC ? tc_decode_kernel_for(m->hid_pad, fmode)
                                                     : kernel_for(kind, m->hid_pad, fast_path(m, kind), fmode);
@@ -830,9 +824,8 @@ int launch_dvr(const fvsrn_model* m, NetDev& net, FeatDev& fd, const TFDev*& tfp
   if (use_tc(m)) {
     TcNetDev tn{m->d_wtc, m->d_btc, m->head};
     void* targs[] = {&tn, &fd, &tfp, &b0, &md, &cam, &sh, &explicit_rays, &rr, &n_slots, &d_out, &queue, &evc, &nfc};
-    const KernelKind k = (frame && !g_tc_two_tiles) ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
-    return launch(m, k, tc_smem_bytes(m->hid_pad, g_tc_two_tiles), targs, s,
-                  g_tc_two_tiles ? n_slots / 64 + 1 : n_slots / 32 + 1, fmode);
+    const KernelKind k = frame ? KernelKind::kDVRTCTex : KernelKind::kDVRTC;
+    return launch(m, k, tc_smem_bytes(m->hid_pad), targs, s, n_slots / 32 + 1, fmode);
   }
   if (dvr_mode() == DvrMode::kWS)
     return launch(m, KernelKind::kDVRWS, ws_smem_bytes(net, m->k0), args, s, n_slots / 32 + 1);
@@ -1905,7 +1898,7 @@ static int decode_impl(fvsrn_model_t m, int32_t res, double t, int64_t lattice_b
   const KernelKind sk = tcd ? KernelKind::kSampleTC : s_static ? KernelKind::kSampleTex : KernelKind::kSample;
   const int sfm = s_tex ? 1 : 2;
   TcNetDev tn{m->d_wtc, m->d_btc, m->head};
-  const size_t tsmem = tcd ? tc_smem_bytes(m->hid_pad, false) : 0;
+  const size_t tsmem = tcd ? tc_smem_bytes(m->hid_pad) : 0;
   if (chunks <= 1 || !h_out) {
     void* args[] = {&net, &fd, &b0, &mode, &res, &step, &begin, &count, &pp, &pd, &d_out, &d_bad, &coords};
     void* targs[] = {&tn, &fd, &b0, &res, &begin, &count, &coords, &d_out, &d_bad};

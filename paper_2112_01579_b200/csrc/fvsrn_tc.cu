@@ -466,176 +466,13 @@ decode_tc_kernel(TcNetDev net, FeatDev fd, const float* __restrict__ b0, int res
   mlp.finish();
 }
 
-#if FVSRN_AB_VARIANTS   // measured slower, off by default
-// Two-tile ping-pong variant: every thread owns two rays (tile 0 row t, tile 1 row t),
-// with one A tile, one TMEM accumulator region and one mbarrier per tile.  While the
-// tensor core runs layer l+1 of one tile, the CTA evaluates the activations (XU pipe)
-// or composites / refills / builds the next rows (FMA/LSU pipes) of the other tile, so
-// the MMA round trip and the CTA barriers overlap useful work.
-template <int HID, int NM, int NL>
-__global__ void __launch_bounds__(kTcThreads, tc2_min_blocks<HID>())
-dvr_tc2_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const float* __restrict__ b0,
-               MarchDev md, CamDev cam, ShardDev sh, int explicit_rays, RayRecs rr, long long n_slots,
-               float* __restrict__ out, unsigned long long* __restrict__ queue,
-               unsigned long long* __restrict__ eval_count, unsigned long long* __restrict__ nonfinite) {
-  using S = TcShape<HID, NM, NL>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __half* w_s = reinterpret_cast<__half*>(smem + S::kWOff);
-  float* b_s = reinterpret_cast<float*>(smem + S::kBOff);
-  TFDev* tf = reinterpret_cast<TFDev*>(smem + S::kTFOff);
-  __half* a_s0 = reinterpret_cast<__half*>(smem + S::kAOff);
-  __half* a_s1 = reinterpret_cast<__half*>(smem + S::kAOff + S::kATile);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + S::kAOff + 2 * S::kATile);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kAOff + 2 * S::kATile + 16);
+// (The two-tile ping-pong variant, dvr_tc2_kernel, was measured slower at both widths and
+// removed once the kernels moved to the shared TcMlp engine.)
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  {
-    const uint4* src = net.w;
-    uint4* dst = reinterpret_cast<uint4*>(w_s);
-    for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
-    for (int i = tid; i < S::kBTotal; i += kTcThreads)
-      b_s[i] = (b0 && i < HID) ? b0[i] : net.b[i];
-    const int words = sizeof(TFDev) / 4;
-    const int* ts = reinterpret_cast<const int*>(tf_g);
-    int* td = reinterpret_cast<int*>(tf);
-    for (int i = tid; i < words; i += kTcThreads) td[i] = ts[i];
-    uint4* az = reinterpret_cast<uint4*>(a_s0);   // pad columns must stay finite
-    for (int i = tid; i < 2 * kTcThreads * S::kKA / 8; i += kTcThreads) az[i] = make_uint4(0, 0, 0, 0);
-  }
-  constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
-  // per tile: D [0, kTCols) then A (hidden activations, and layer-0 rows when kA0)
-  constexpr uint32_t kTile = S::kTCols + (kA0 ? S::kKA / 2 : HID / 2);
-  constexpr uint32_t kAlloc = 2 * kTile <= 64 ? 64 : 2 * kTile <= 128 ? 128 : 2 * kTile <= 256 ? 256 : 512;
-  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), kAlloc);
-  if (tid == 0) { mbar_init(smem_u32(mbar), 1); mbar_init(smem_u32(mbar + 1), 1); }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t w_base = smem_u32(w_s);
-  const uint32_t a_base[2] = {smem_u32(a_s0), smem_u32(a_s1)};
-  const uint32_t mb[2] = {smem_u32(mbar), smem_u32(mbar + 1)};
-  const uint32_t t_d[2] = {tmem, tmem + kTile};                             // accumulator columns
-  const uint32_t t_a[2] = {tmem + S::kTCols, tmem + kTile + S::kTCols};     // A operand columns
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;                     // this warp's lanes
-  const int row_off = (tid >> 3) * (S::kSboA / 2) + (tid & 7) * 8;
-  __half* myrow[2] = {a_s0 + row_off, a_s1 + row_off};
-  const bool density = net.head == 0;
-
-  RayLane r[2];
-  r[0].has = false;
-  r[1].has = false;
-  LaneQueue q{0, 0, false};
-  unsigned long long evals = 0;
-  uint32_t phase[2] = {0u, 0u};
-  bool live[2];
-
-  auto issue = [&](int l, int t) {
-    if (tid == 0) {
-      tc_fence_after();
-      const int K = l == 0 ? S::kK0 : HID;
-      const int N = l == NL - 1 ? S::kNLast : HID;
-      const uint32_t wb = w_base + 2u * (uint32_t)S::w_off(l);
-      const uint32_t sbo_b = (uint32_t)(K / 8) * 128u;
-      const uint32_t id = idesc_f16(128, N);
-#pragma unroll
-      for (int kk = 0; kk < K / 16; ++kk) {
-        if (l > 0 || kA0)
-          umma_f16_ts(t_d[t], t_a[t] + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
-        else
-          umma_f16(t_d[t], smem_desc(a_base[t] + kk * 256u, 128u, S::kSboA),
-                   smem_desc(wb + kk * 256u, 128u, sbo_b), id, 1u);
-      }
-      umma_commit(mb[t]);
-    }
-  };
-  // refill tile t, pre-load its layer-0 bias, write its rows; returns (CTA-wide) whether
-  // the tile has any ray, after the fences + barrier that make the rows MMA-visible
-  auto start = [&](int t) -> bool {
-    ws_refill(r[t], q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
-    evals += __popc(__ballot_sync(0xffffffffu, r[t].has));
-    tmem_bias<HID>(t_d[t] + lane_off, b_s + S::b_off(0));
-    if constexpr (kA0) {          // tcgen05.st is .sync.aligned: every lane stores
-      uint32_t w[FastRow<NM>::kWords];
-      if (r[t].has) {
-        const float kf = (float)r[t].k;
-        FastRow<NM>::words(fd, fmaf(kf, r[t].dd0, r[t].pe0), fmaf(kf, r[t].dd1, r[t].pe1),
-                           fmaf(kf, r[t].dd2, r[t].pe2), w);
-      } else {
-#pragma unroll
-        for (int i = 0; i < FastRow<NM>::kWords; ++i) w[i] = 0u;
-      }
-      tmem_st_any<FastRow<NM>::kWords>(t_a[t] + lane_off, w);
-    } else if (r[t].has) {
-      const float kf = (float)r[t].k;
-      FastRow<NM>::template build<8>(fd, fmaf(kf, r[t].dd0, r[t].pe0), fmaf(kf, r[t].dd1, r[t].pe1),
-                                     fmaf(kf, r[t].dd2, r[t].pe2), myrow[t]);
-    }
-    tmem_wait_st();
-    if constexpr (!kA0) fence_proxy_async_smem();
-    tc_fence_before();
-    return __syncthreads_or(r[t].has) != 0;
-  };
-
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    live[t] = start(t);
-    if (live[t]) issue(0, t);
-  }
-  while (live[0] || live[1]) {
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (!live[t]) continue;
-        mbar_wait(mb[t], phase[t]);
-        phase[t] ^= 1u;
-        tc_fence_after();
-        const uint32_t t_row = t_d[t] + lane_off;
-        if (l < NL - 1) {
-          uint32_t acc[HID];
-          tmem_ld<HID>(t_row, acc);
-          tmem_wait_ld();
-          if (l + 1 < NL - 1) tmem_bias<HID>(t_row, b_s + S::b_off(l + 1));
-          else tmem_bias<S::kNLast>(t_row, b_s + S::b_off(l + 1));
-          uint32_t w[HID / 2];
-          act_words<HID>(acc, w);
-          tmem_st<HID / 2>(t_a[t] + lane_off, w);
-          tmem_wait_st();
-          tc_fence_before();
-          __syncthreads();
-          issue(l + 1, t);
-        } else {
-          uint32_t o[4];
-          tmem_ld_x4(t_row, o);
-          tmem_wait_ld();
-          if (r[t].has)
-            composite_step(r[t], make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
-                                             __uint_as_float(o[2]), __uint_as_float(o[3])),
-                           density, *tf, md, out, nonfinite);
-          live[t] = start(t);
-          if (live[t]) issue(0, t);
-        }
-      }
-    }
-  }
-  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kAlloc);
-}
-
-#endif  // FVSRN_AB_VARIANTS
-
-const void* tc_kernel_for(int hid, bool two_tiles) {
+const void* tc_kernel_for(int hid) {
   switch (hid) {
-#if FVSRN_AB_VARIANTS
-    case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;   // tc2: no bias-in-MMA
-    case 64: return two_tiles ? (const void*)dvr_tc2_kernel<64, 30, 6> : (const void*)dvr_tc_kernel<64, 30, 6>;
-#else
-    case 32: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<32, 14, 4>;
-    case 64: return two_tiles ? nullptr : (const void*)dvr_tc_kernel<64, 30, 6>;
-#endif
+    case 32: return (const void*)dvr_tc_kernel<32, 14, 4>;
+    case 64: return (const void*)dvr_tc_kernel<64, 30, 6>;
     default: return nullptr;
   }
 }
@@ -656,10 +493,10 @@ const void* tc_decode_kernel_for(int hid, int fmode) {
   }
 }
 
-size_t tc_smem_bytes(int hid, bool two_tiles) {
+size_t tc_smem_bytes(int hid) {
   switch (hid) {
-    case 32: return two_tiles ? TcShape<32, 14, 4>::kSmem2 : TcShape<32, 14, 4>::kSmem;
-    case 64: return two_tiles ? TcShape<64, 30, 6>::kSmem2 : TcShape<64, 30, 6>::kSmem;
+    case 32: return TcShape<32, 14, 4>::kSmem;
+    case 64: return TcShape<64, 30, 6>::kSmem;
     default: return 0;
   }
 }

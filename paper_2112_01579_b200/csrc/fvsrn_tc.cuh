@@ -17,17 +17,6 @@ template <int HID>
 constexpr int tc_min_blocks() {
   return HID <= 32 ? FVSRN_TC_MIN_BLOCKS : FVSRN_TC_MIN_BLOCKS_WIDE;
 }
-// two-tile variant (two rays per thread)
-#ifndef FVSRN_TC2_MIN_BLOCKS
-#define FVSRN_TC2_MIN_BLOCKS 3
-#endif
-#ifndef FVSRN_TC2_MIN_BLOCKS_WIDE
-#define FVSRN_TC2_MIN_BLOCKS_WIDE 2
-#endif
-template <int HID>
-constexpr int tc2_min_blocks() {
-  return HID <= 32 ? FVSRN_TC2_MIN_BLOCKS : FVSRN_TC2_MIN_BLOCKS_WIDE;
-}
 
 // Weights of all layers, fp16, each layer an (N x K) K-major tile in the UMMA canonical
 // no-swizzle layout: element (n, k) at half index
@@ -90,18 +79,16 @@ struct TcShape {
   static constexpr bool kA0 = FVSRN_TC_TMEM_A0 == 1 || (FVSRN_TC_TMEM_A0 == 2 && HID <= 32);
   static constexpr int kMbarOff = kA0 ? kAOff : kAOff + kATile;
   static constexpr int kSmem = kMbarOff + 16;   // mbarrier, TMEM slot
-  static constexpr int kSmem2 = kAOff + 2 * kATile + 32;   // two-tile variant
 };
 
 // tcgen05 DVR kernel for the default fV-SRN shapes (hid 32: 4 layers, m=14; hid 64:
 // 6 layers, m=30), or nullptr.  Same argument list as dvr_kernel with TcNetDev first.
-// two_tiles: the ping-pong variant (256 rays per CTA).
-const void* tc_kernel_for(int hid, bool two_tiles);
+const void* tc_kernel_for(int hid);
 // the single-tile kernel specialised for a static fp16 texture grid (branch-free features)
 const void* tc_tex_kernel_for(int hid, int fmode = 1);   // fmode 1 texture, 2 LDG grid
 // the lattice decode (decode_tc_kernel) for a static fp16 grid: fmode 1 texture, 2 LDG
 const void* tc_decode_kernel_for(int hid, int fmode);
-size_t tc_smem_bytes(int hid, bool two_tiles);
+size_t tc_smem_bytes(int hid);
 inline int tc_layers(int hid) { return hid == 64 ? 6 : 4; }
 
 }  // namespace fvsrn
