@@ -170,7 +170,10 @@ struct TcMlp {
   using S = TcShape<HID, NM, NL>;
   static_assert(S::kA0, "the one-tile kernels keep the layer-0 rows in TMEM");
   static constexpr int kWords = FastRow<NM>::kWords;
-  static constexpr uint32_t kNeed = S::kTCols + S::kKA / 2;
+  // bias-in-MMA: the bias tile's constant A side [1, 1, 0, ...] (8 columns) sits after the
+  // layer-0 row, written once; the bias k-step of every hidden layer reads it there
+  static constexpr uint32_t kOnesCol = S::kKA / 2;
+  static constexpr uint32_t kNeed = S::kTCols + S::kKA / 2 + (S::kBiasMma ? 8 : 0);
   static constexpr uint32_t kAlloc = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : 256;
 
   uint32_t tmem, t_row, phase;
@@ -213,6 +216,11 @@ struct TcMlp {
     tmem = *tmem_slot;
     t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
     phase = 0;
+    if constexpr (S::kBiasMma) {
+      uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      tmem_st_x8(t_row + S::kTCols + kOnesCol, c);
+      tmem_wait_st();   // ordered before the first MMA by put_row's barrier
+    }
   }
 
   __device__ void finish() {
@@ -252,7 +260,9 @@ struct TcMlp {
         for (int kk = 0; kk < K / 16; ++kk) {
           // D preloaded with the bias accumulates from the first k step; bias-in-MMA starts D
           const uint32_t acc = (kk == 0 && (S::kBiasMma || (l == 0 && S::kBias0))) ? 0u : 1u;
-          umma_f16_ts(tmem, tmem + S::kTCols + kk * 8u, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
+          // the bias k-step of a hidden layer reads the constant ones columns
+          const uint32_t a_col = (S::kBiasMma && l > 0 && kk == K / 16 - 1) ? kOnesCol : 8u * kk;
+          umma_f16_ts(tmem, tmem + S::kTCols + a_col, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
         }
         umma_commit(mb());
       }
@@ -325,12 +335,6 @@ struct TcMlp {
           act_words<HID, tc_poly<HID>()>(acc, w);
           tmem_st<HID / 2>(t_row + S::kTCols, w);
         }
-        if constexpr (S::kBiasMma) {
-          if (l == 0) {   // the bias tile of layers >= 1: A columns HID/2.. = [1, 1, 0, ...]
-            uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            tmem_st_x8(t_row + S::kTCols + HID / 2, c);
-          }
-        }
         tmem_wait_st();   // the next A operand went to TMEM: no shared-memory proxy fence
         tc_fence_before();
         __syncthreads();
@@ -369,7 +373,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
   RayLane r{};   // zero state: a lane without a ray builds a finite dummy row
   r.has = false;
   LaneQueue q{0, 0, false};
-  unsigned long long evals = 0;
+  unsigned evals = 0;   // this thread's evaluations (reduced over the warp at the end)
   while (true) {
     if constexpr (kFrame) {
       RayRecs rr_pos = rr;
@@ -379,7 +383,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
       ws_refill(r, q, lane, cam, sh, explicit_rays != 0, rr, n_slots, queue, md, out);
     }
     if (!__syncthreads_or(r.has)) break;
-    evals += __popc(__ballot_sync(0xffffffffu, r.has));
+    evals += r.has ? 1u : 0u;
     mlp.begin_row();
     uint32_t w[FastRow<NM>::kWords];
     // FVSRN_TC_DEADROW: lanes without a ray build a row from their stale (finite) ray
@@ -408,7 +412,8 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
                                     __uint_as_float(o[2]), __uint_as_float(o[3])),
                      kFrame || density, *tf, md, out, nonfinite);
   }
-  if (lane == 0 && eval_count) atomicAdd(eval_count, evals);
+  evals = __reduce_add_sync(0xffffffffu, evals);
+  if (lane == 0 && eval_count) atomicAdd(eval_count, (unsigned long long)evals);
   mlp.finish();
 }
 
