@@ -1497,6 +1497,9 @@ int32_t fvsrn_model_create(const fvsrn_model_desc* d, int32_t device, fvsrn_mode
       wt.insert(wt.end(), tile.begin(), tile.end());
       for (int n = 0; n < Nt; ++n) bt.push_back(n < N[l] ? bs[l][n] : 0.f);
     }
+    // the last layer's first weight row in f32 (TcShape::kWLast: the density head's last
+    // layer evaluated on the FMA pipe)
+    for (int k = 0; k < H; ++k) bt.push_back(k < Ks[L - 1] ? ws[L - 1][(size_t)k] : 0.f);
     int rc = upload(wt.data(), wt.size() * sizeof(__half), (void**)&m->d_wtc);
     if (rc) return rc;
     rc = upload(bt.data(), bt.size() * sizeof(float), (void**)&m->d_btc);

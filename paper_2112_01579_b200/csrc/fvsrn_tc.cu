@@ -70,6 +70,14 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_POLY64
 #define FVSRN_TC_POLY64 6   // 64-wide, per 32-column half (4/5/6/7/8: 24.44/24.55/24.35/25.13/24.83 ms at cfg 3)
 #endif
+// narrowest width whose density head evaluates the last layer on the FMA pipe (64: cfg 3
+// 24.04 -> 23.80 ms; at 32-wide it spills at 64 registers, 2.70 -> 2.77 ms)
+#ifndef FVSRN_TC_LAST_LDS_PIN
+#define FVSRN_TC_LAST_LDS_PIN 1   // cfg 3 23.80 -> 23.73 ms
+#endif
+#ifndef FVSRN_TC_LAST_FMA_MINW
+#define FVSRN_TC_LAST_FMA_MINW 64
+#endif
 #ifndef FVSRN_TC_CHUNK64
 #define FVSRN_TC_CHUNK64 16   // 64-wide epilogue chunk, 32 or 16 columns (16: 84 registers, cfg 3 24.34 -> 23.95 ms)
 #endif
@@ -119,6 +127,34 @@ __device__ __forceinline__ void act_words_at(const uint32_t (&acc)[N], uint32_t 
     }
     w[j] = pack_half2(h[0], h[1]);
   }
+}
+
+// dot += sum over N accumulator columns (at column OFF of the FMA-pipe pattern) of
+// snake_alt(a) x wl[OFF + e], f32 (the density head's last layer on the FMA pipe)
+template <int N, int OFF, int P>
+__device__ __forceinline__ float act_dot_at(const uint32_t (&acc)[N], const float* wl, float dot) {
+#pragma unroll
+  for (int j = 0; j < N; j += 4) {
+    float wq[4];
+#if FVSRN_TC_LAST_LDS_PIN
+    // loaded where used (volatile: not hoisted above the TMEM loads, fewer live registers)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(wq[0]), "=f"(wq[1]), "=f"(wq[2]), "=f"(wq[3]) : "r"(smem_u32(wl + OFF + j)));
+#else
+    {
+      const float4 wv = *reinterpret_cast<const float4*>(wl + OFF + j);
+      wq[0] = wv.x; wq[1] = wv.y; wq[2] = wv.z; wq[3] = wv.w;
+    }
+#endif
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = OFF + j + i;
+      const float x = __uint_as_float(acc[j + i]);
+      const float h = (P > 0 && e % (P > 0 ? P : 1) == P - 1) ? snake_alt_h_fma(x) : act_h<4>(x);
+      dot = fmaf(wq[i], h, dot);
+    }
+  }
+  return dot;
 }
 
 template <int N>
@@ -195,7 +231,7 @@ struct TcMlp {
       const uint4* src = net.w;
       uint4* dst = reinterpret_cast<uint4*>(w_s);
       for (int i = tid; i < S::kWTotal / 8; i += kTcThreads) dst[i] = src[i];
-      for (int i = tid; i < S::kBTotal; i += kTcThreads) bs[i] = (b0 && i < HID) ? b0[i] : net.b[i];
+      for (int i = tid; i < S::kBAll; i += kTcThreads) bs[i] = (b0 && i < HID) ? b0[i] : net.b[i];
     }
     // the weight tiles were written through the generic proxy and are read by the tensor
     // core (async proxy)
@@ -246,9 +282,14 @@ struct TcMlp {
   }
 
   // All layers of this step; o = the last layer's first 4 accumulators of this row.
-  __device__ void run(uint32_t (&o)[4]) {
+  // fma_last (a density head, CTA-uniform): the last layer's single used output is a dot
+  // product of the f32 activations with its weight row on the FMA pipe (o[0]), instead of
+  // an fp16 tcgen05 round trip (FVSRN_TC_LAST_FMA_MINW)
+  __device__ void run(uint32_t (&o)[4], bool fma_last = false) {
+    fma_last = fma_last && HID >= FVSRN_TC_LAST_FMA_MINW;
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
+      if (fma_last && l == NL - 1) break;
       if (tid == 0) {
         tc_fence_after();
         const int K = l == 0 ? S::kK0 : S::kKh;
@@ -269,7 +310,24 @@ struct TcMlp {
       mbar_wait(mb(), phase);
       phase ^= 1u;
       tc_fence_after();
-      if (l < NL - 1) {
+      if (fma_last && l == NL - 2) {
+        const float* wl = b_s() + S::kWLast;
+        float dot[HID / 16];
+#pragma unroll
+        for (int q = 0; q < HID / 16; ++q) {
+          uint32_t acc[16];
+          tmem_ld<16>(t_row + 16u * q, acc);
+          tmem_wait_ld();
+          // pattern column within the tc_poly period (restarting every 32 columns at 64-wide)
+          if (HID == 64 ? (q & 1) : q == 1) dot[q] = act_dot_at<16, 16, tc_poly<HID>()>(acc, wl + 16 * (q & ~1), 0.f);
+          else dot[q] = act_dot_at<16, 0, tc_poly<HID>()>(acc, wl + 16 * q, 0.f);
+        }
+        float d = b_s()[S::b_off(NL - 1)];
+#pragma unroll
+        for (int q = 0; q < HID / 16; ++q) d += dot[q];
+        o[0] = __float_as_uint(d);
+        o[1] = o[2] = o[3] = 0u;
+      } else if (l < NL - 1) {
         // snake_alt in the 2x-prescaled basis (act_h<4>), fp16 pairs -> the next A operand
         if constexpr (HID == 64 && FVSRN_TC_CHUNK64 == 16 && !S::kBiasMma) {
           // four 16-column quarters; the next layer's bias stored per quarter right after
@@ -406,7 +464,7 @@ dvr_tc_kernel(TcNetDev net, FeatDev fd, const TFDev* __restrict__ tf_g, const fl
     }
     mlp.put_row(w);
     uint32_t o[4];
-    mlp.run(o);
+    mlp.run(o, kFrame || density);
     if (r.has)
       composite_step(r, make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]),
                                     __uint_as_float(o[2]), __uint_as_float(o[3])),
@@ -460,7 +518,7 @@ decode_tc_kernel(TcNetDev net, FeatDev fd, const float* __restrict__ b0, int res
     ix += sx + carry;
     mlp.put_row(w);
     uint32_t o[4];
-    mlp.run(o);
+    mlp.run(o, true);
     if (valid) {
       const float v = sigmoidf_(__uint_as_float(o[0]));
       out[i] = v;

@@ -69,10 +69,14 @@ struct TcShape {
   static constexpr int kWTotal = HID * kK0 + (NL - 2) * HID * kKh + kNLast * kKh;   // halfs
   static constexpr int b_off(int l) { return l * HID; }
   static constexpr int kBTotal = (NL - 1) * HID + kNLast;
+  // after the biases: the density output's row of the last layer's weights, f32 (the
+  // density head's last layer runs on the FMA pipe, FVSRN_TC_LAST_FMA_MINW)
+  static constexpr int kWLast = kBTotal;
+  static constexpr int kBAll = kBTotal + HID;
   // shared memory map (bytes)
   static constexpr int kWOff = 0;
   static constexpr int kBOff = tc_round(kWOff + kWTotal * 2, 16);
-  static constexpr int kTFOff = tc_round(kBOff + kBTotal * 4, 16);
+  static constexpr int kTFOff = tc_round(kBOff + kBAll * 4, 16);
   static constexpr int kAOff = tc_round(kTFOff + (int)sizeof(TFDev), 128);
   static constexpr int kATile = kTcThreads * kKA * 2;
   // with layer-0 rows in TMEM the one-tile kernel has no shared-memory A tile
