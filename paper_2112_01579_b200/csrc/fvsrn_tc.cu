@@ -75,6 +75,9 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_LAST_LDS_PIN
 #define FVSRN_TC_LAST_LDS_PIN 1   // cfg 3 23.80 -> 23.73 ms
 #endif
+#ifndef FVSRN_TC_DECODE_LAST_FMA_MINW
+#define FVSRN_TC_DECODE_LAST_FMA_MINW 32   // the decode has registers to spare at 32-wide: cfg 4 0.546 -> 0.535 ms
+#endif
 #ifndef FVSRN_TC_LAST_FMA_MINW
 #define FVSRN_TC_LAST_FMA_MINW 64
 #endif
@@ -285,8 +288,9 @@ struct TcMlp {
   // fma_last (a density head, CTA-uniform): the last layer's single used output is a dot
   // product of the f32 activations with its weight row on the FMA pipe (o[0]), instead of
   // an fp16 tcgen05 round trip (FVSRN_TC_LAST_FMA_MINW)
+  template <int MINW = FVSRN_TC_LAST_FMA_MINW>
   __device__ void run(uint32_t (&o)[4], bool fma_last = false) {
-    fma_last = fma_last && HID >= FVSRN_TC_LAST_FMA_MINW;
+    fma_last = fma_last && HID >= MINW;
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       if (fma_last && l == NL - 1) break;
@@ -518,7 +522,7 @@ decode_tc_kernel(TcNetDev net, FeatDev fd, const float* __restrict__ b0, int res
     ix += sx + carry;
     mlp.put_row(w);
     uint32_t o[4];
-    mlp.run(o, true);
+    mlp.template run<FVSRN_TC_DECODE_LAST_FMA_MINW>(o, true);
     if (valid) {
       const float v = sigmoidf_(__uint_as_float(o[0]));
       out[i] = v;
