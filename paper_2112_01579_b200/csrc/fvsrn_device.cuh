@@ -568,6 +568,10 @@ __device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
       : "l"(p));
 }
 
+#ifndef FVSRN_TEX_F16X2
+#define FVSRN_TEX_F16X2 1
+#endif
+
 template <int NM>
 struct FastRow {
   static constexpr int kWidth = 16 + 2 * NM + 3;
@@ -590,7 +594,13 @@ struct FastRow {
 #pragma unroll
     for (int i = 0; i < kWords; ++i) w[i] = 0u;
     // latent grid (grid.py:47-84), 16 channels
-    if (fd.tex_on) {
+    if (fd.tex_on && !fd.tex_u8 && fd.tex_w == 0.f) {
+      // static fp16 texture grid: the same fetch as the specialised frame kernels
+      uint32_t z[8];
+      tex_words(fd, px, py, pz, z);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = z[i];
+    } else if (fd.tex_on) {
       // texture units: unnormalised coordinates, texel centres at i + 1/2, clamp
       // addressing (== the reference's clamp of p and of i0 <= R-2); array width is the
       // grid's z axis (fastest in memory), depth its x axis
@@ -716,8 +726,21 @@ struct FastRow {
     for (int j = 0; j < kWords / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 
-  // the 16 latent channels of tex_fetch as 8 packed fp16 pairs
+  // the 16 latent channels of a static fp16 texture grid as 8 packed fp16 pairs
+  // (FVSRN_TEX_F16X2: the texture unit returns them packed -- tex.3d.v2.f16x2 -- instead
+  // of 16 f32 values the SM converts; every static-texture path fetches through here)
   __device__ static void tex_words(const FeatDev& fd, float px, float py, float pz, uint32_t (&z)[8]) {
+#if FVSRN_TEX_F16X2
+    const float s = (float)(fd.grid_res - 1);
+    const float tz = fmaf(fminf(fmaxf(px, 0.f), 1.f), s, 0.5f);
+    const float ty = fmaf(fminf(fmaxf(py, 0.f), 1.f), s, 0.5f);
+    const float tx = fmaf(fminf(fmaxf(pz, 0.f), 1.f), s, 0.5f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("tex.3d.v2.f16x2.f32 {%0, %1}, [%2, {%3, %4, %5, %6}];"
+                   : "=r"(z[2 * j]), "=r"(z[2 * j + 1])
+                   : "l"(fd.tex_lo[j]), "f"(tx), "f"(ty), "f"(tz), "f"(0.f));
+#else
     float4 v[4];
     tex_fetch(fd, px, py, pz, v);
 #pragma unroll
@@ -725,6 +748,7 @@ struct FastRow {
       z[2 * j] = pack_half2(v[j].x, v[j].y);
       z[2 * j + 1] = pack_half2(v[j].z, v[j].w);
     }
+#endif
   }
 
   __device__ static void words_from_z(const uint32_t (&z)[8], float px, float py, float pz,
