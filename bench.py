@@ -148,14 +148,23 @@ def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
     tcgen05 kernels (3 axes x 2)."""
     layers, hid = model_cfg["layers"], model_cfg["hidden"]
     tc = kernel.startswith(("dvr_tc", "decode_tc"))
-    if tc:
-        # fvsrn_tc.cu: every 5th column at 32-wide (FVSRN_TC_POLY), every 6th column of each
-        # 32-column half at 64-wide (FVSRN_TC_POLY64) evaluates its cosine on the FMA pipe
-        on_fma = (hid + 1) // 5 if hid <= 32 else (hid // 32) * (33 // 6)
-        per_row = hid - on_fma
-    else:
-        per_row = hid
-    return (layers - 1) * per_row + (1 if kernel.startswith("decode") else 2) + (6 if tc else 0)
+    decode = kernel.startswith("decode")
+    if not tc:
+        return (layers - 1) * hid + (1 if decode else 2)
+    # fvsrn_tc.cu, per 32-column segment of a hidden row: every 3rd packed fp16 word
+    # (FVSRN_TC_H2 / FVSRN_TC_H2_64) evaluates both cosines in HFMA2 arithmetic; the
+    # density head's last hidden row, when it is an f32 dot product on the FMA pipe
+    # (64-wide march, 32/64-wide decode), keeps the per-element pattern (every 5th column
+    # at 32-wide, every 6th column of each 32-column half at 64-wide)
+    seg = max(hid // 32, 1)
+    h2_words = sum(1 for g in range(16) if g % 3 == 2)
+    row_h2 = hid - seg * 2 * h2_words
+    row_dot = hid - ((hid + 1) // 5 if hid <= 32 else seg * (33 // 6))
+    dot_last = hid >= (32 if decode else 64)
+    rows = [row_h2] * (layers - 1)
+    if dot_last:
+        rows[-1] = row_dot
+    return sum(rows) + (1 if decode else 2) + 6
 
 
 def measured_peaks():

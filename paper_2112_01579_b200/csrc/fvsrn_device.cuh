@@ -182,6 +182,50 @@ __device__ __forceinline__ float snake_alt_h_fma(float x) {
   return x + p;
 }
 
+// snake_alt h = x - 2 cos x for TWO accumulator columns as one packed fp16 pair, on the
+// FMA pipe in HFMA2 arithmetic (11 instructions per pair, no MUFU; the f32 version above
+// costs 9 per element + half a pack).  x is rounded to fp16 first (the result is an fp16
+// A operand anyway); k = rint(x/pi) by the 1.5*2^10 trick (|x| < 1600), r = x/pi - k in
+// [-1/2, 1/2] half turns, -2 cos(pi r) as a degree-3 minimax polynomial in r^2
+// (|err| < 1.4e-5 before fp16 rounding), the sign (-1)^k taken from the integer's low
+// bit in the rounded t's mantissa and XORed into both halves' sign bits.
+// FULL: whole turns instead, r = x/2pi - rint(x/2pi) in [-1/2, 1/2], -2 cos(2 pi r) of
+// degree 4 in r^2 (|err| < 8.1e-5), no sign fix-up: 10 instructions per pair, slightly
+// larger fp16 rounding error (mean |h err| 1.72e-3 vs 1.58e-3 over |x| < 8; MUFU + f32:
+// 0.79e-3).  Measured (per word period 3): cfg 2 2.495 (half) / 2.50 (full) ms, cfg 3
+// 22.63 (half) / 22.31 (full) ms.
+template <bool FULL>
+__device__ __forceinline__ uint32_t snake_alt_h2_fma(float x0, float x1) {
+  const __half2 x = __floats2half2_rn(x0, x1);
+  const __half2 magic = __float2half2_rn(1536.f);
+  if constexpr (FULL) {
+    const __half2 inv_2pi = __float2half2_rn(0.15915494309189535f);
+    const __half2 k = __hsub2(__hfma2(x, inv_2pi, magic), magic);
+    const __half2 r = __hfma2(x, inv_2pi, __hneg2(k));
+    const __half2 v = __hmul2(r, r);
+    __half2 p = __hfma2(__float2half2_rn(-91.29309655f), v, __float2half2_rn(164.80709908f));
+    p = __hfma2(p, v, __float2half2_rn(-129.34686346f));
+    p = __hfma2(p, v, __float2half2_rn(39.46208358f));
+    p = __hfma2(p, v, __float2half2_rn(-1.9999196f));
+    const __half2 h = __hadd2(x, p);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __half2 inv_pi = __float2half2_rn(0.3183098861837907f);
+    const __half2 t = __hfma2(x, inv_pi, magic);
+    const __half2 k = __hsub2(t, magic);
+    const __half2 r = __hfma2(x, inv_pi, __hneg2(k));
+    const __half2 v = __hmul2(r, r);
+    __half2 p = __hfma2(__float2half2_rn(2.4442540271609667f), v, __float2half2_rn(-8.082567766703097f));
+    p = __hfma2(p, v, __float2half2_rn(9.867876064596281f));
+    p = __hfma2(p, v, __float2half2_rn(-1.9999865922852822f));
+    const uint32_t tb = *reinterpret_cast<const uint32_t*>(&t);
+    uint32_t pb = *reinterpret_cast<const uint32_t*>(&p);
+    pb ^= (tb << 15) & 0x80008000u;
+    const __half2 h = __hadd2(x, *reinterpret_cast<const __half2*>(&pb));
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+
 // sin(2 pi r), cos(2 pi r) for r in [-1/2, 1/2] on the FMA pipe: degree-5 least-
 // squares-minimax polynomials in u = r^2 (|err| < 1.3e-6, MUFU.SIN/COS-class accuracy).
 // 12 FP32 ops instead of FMUL.RZ + MUFU.SIN + MUFU.COS: the DVR path is XU-bound, so

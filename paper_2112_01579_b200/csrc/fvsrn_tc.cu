@@ -10,8 +10,9 @@
 //   2. per layer (TcMlp::run): one elected thread issues K/16 tcgen05.mma (A = the row or
 //      the hidden activations in TMEM, B = weights in shared memory, D = f32 accumulators
 //      in TMEM) and commits to an mbarrier; every thread tcgen05.ld's its row, evaluates
-//      the snake activation in registers (one MUFU.COS per element, every 6th on the FMA
-//      pipe) and tcgen05.st's the packed fp16 row back as the next A operand.  Biases:
+//      the snake activation in registers (one MUFU.COS per element; every 3rd packed
+//      fp16 pair on the FMA pipe in HFMA2 arithmetic) and tcgen05.st's the packed fp16
+//      row back as the next A operand.  Biases:
 //      at 32-wide inside the MMA (layer 0 through the row's 1.0 pad column and a W0 bias
 //      column patched per frame, later layers through one extra k16 tile of [1, 1] x
 //      [b_hi, b_lo]); at 64-wide preloaded into D with tcgen05.st;
@@ -90,8 +91,33 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_BIAS_HALVES
 #define FVSRN_TC_BIAS_HALVES 1
 #endif
+// Word-level replacement of FVSRN_TC_POLY (round 2, late): every FVSRN_TC_H2-th packed
+// fp16 word (a pair of columns) of a hidden row evaluates both cosines on the FMA pipe in
+// packed HFMA2 arithmetic (snake_alt_h2_fma: 10-11 instructions per PAIR, against 9 per
+// element + a pack for the f32 polynomial); the other words use MUFU.  The kernels are
+// issue-bound, so the cheaper FMA-pipe cosine lets a larger share leave the XU pipe.
+// cfg 2 ms, word period 2/3/4/5: 2.644/2.497/2.54/2.603 (per-element f32 every 5th:
+// 2.70); cfg 3 (64-wide, whole turns) period 3: 22.31 (half turns 2/3/4/5: 22.77/22.63/
+// 22.59/23.23; f32 every 6th: 23.71); cfg 4 0.538 -> 0.505, cfg 5 38.65 -> 35.75.
+// 0 = the per-element FVSRN_TC_POLY pattern.
+#ifndef FVSRN_TC_H2
+#define FVSRN_TC_H2 3
+#endif
+#ifndef FVSRN_TC_H2_64
+#define FVSRN_TC_H2_64 3
+#endif
+#ifndef FVSRN_TC_H2_FULL32
+#define FVSRN_TC_H2_FULL32 0   // half turns + sign fix-up (smaller error, same speed)
+#endif
+#ifndef FVSRN_TC_H2_FULL64
+#define FVSRN_TC_H2_FULL64 1   // whole turns (one instruction less per pair: 22.63 -> 22.31 ms)
+#endif
 template <int HID>
 constexpr int tc_poly() { return HID <= 32 ? FVSRN_TC_POLY : FVSRN_TC_POLY64; }
+template <int HID>
+constexpr int tc_h2() { return HID <= 32 ? FVSRN_TC_H2 : FVSRN_TC_H2_64; }
+template <int HID>
+constexpr bool tc_h2_full() { return (HID <= 32 ? FVSRN_TC_H2_FULL32 : FVSRN_TC_H2_FULL64) != 0; }
 #ifndef FVSRN_TC_DEADROW
 #define FVSRN_TC_DEADROW 1
 #endif
@@ -101,10 +127,15 @@ constexpr int tc_poly() { return HID <= 32 ? FVSRN_TC_POLY : FVSRN_TC_POLY64; }
 
 // snake_alt activations of N accumulator columns -> packed fp16 pairs (TMEM A operand);
 // every P-th column's cosine on the FMA pipe
-template <int N, int P = FVSRN_TC_POLY>
+template <int N, int P = FVSRN_TC_POLY, int Q = 0, bool FULL = false>
 __device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w)[N / 2]) {
 #pragma unroll
   for (int j = 0; j < N / 2; ++j) {
+    if constexpr (Q > 0) {
+      const float x0 = __uint_as_float(acc[2 * j]), x1 = __uint_as_float(acc[2 * j + 1]);
+      w[j] = j % Q == Q - 1 ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
+      continue;
+    }
     float h[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -117,10 +148,16 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w
 }
 
 // N accumulator columns that sit at column OFF of the FMA-pipe pattern (e % P == P - 1)
-template <int N, int OFF, int P>
+template <int N, int OFF, int P, int Q = 0, bool FULL = false>
 __device__ __forceinline__ void act_words_at(const uint32_t (&acc)[N], uint32_t (&w)[N / 2]) {
 #pragma unroll
   for (int j = 0; j < N / 2; ++j) {
+    if constexpr (Q > 0) {
+      const float x0 = __uint_as_float(acc[2 * j]), x1 = __uint_as_float(acc[2 * j + 1]);
+      const int g = OFF / 2 + j;
+      w[j] = g % Q == Q - 1 ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
+      continue;
+    }
     float h[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -343,8 +380,8 @@ struct TcMlp {
             tmem_wait_ld();
             if (l + 1 < NL - 1) tmem_bias<16>(t_row + 16u * q, b_s() + S::b_off(l + 1) + 16 * q);
             else if (q == 0) tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
-            if (q & 1) act_words_at<16, 16, tc_poly<HID>()>(acc, w);
-            else act_words_at<16, 0, tc_poly<HID>()>(acc, w);
+            if (q & 1) act_words_at<16, 16, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
+            else act_words_at<16, 0, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
             tmem_st_x8(t_row + S::kTCols + 8u * q, w);
           }
         } else if constexpr (HID == 64) {
@@ -360,7 +397,7 @@ struct TcMlp {
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
           }
 #endif
-          act_words<32, tc_poly<HID>()>(acc, w);
+          act_words<32, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols, w);
           tmem_ld<32>(t_row + 32, acc);
           tmem_wait_ld();
@@ -372,18 +409,18 @@ struct TcMlp {
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
 #endif
           }
-          act_words<32, tc_poly<HID>()>(acc, w);
+          act_words<32, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
           tmem_st<16>(t_row + S::kTCols + 16, w);
         } else if constexpr (FVSRN_TC_SPLIT32 && HID == 32 && S::kBiasMma) {
           // two 16-column halves (fewer live accumulator registers)
           uint32_t acc[16], w[8];
           tmem_ld<16>(t_row, acc);
           tmem_wait_ld();
-          act_words<16, tc_poly<HID>()>(acc, w);
+          act_words<16, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
           tmem_st_x8(t_row + S::kTCols, w);
           tmem_ld<16>(t_row + 16, acc);
           tmem_wait_ld();
-          act_words_at<16, 16, tc_poly<HID>()>(acc, w);
+          act_words_at<16, 16, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
           tmem_st_x8(t_row + S::kTCols + 8, w);
         } else {
           uint32_t acc[HID];
@@ -394,7 +431,7 @@ struct TcMlp {
             else tmem_bias<S::kNLast>(t_row, b_s() + S::b_off(l + 1));
           }
           uint32_t w[HID / 2];
-          act_words<HID, tc_poly<HID>()>(acc, w);
+          act_words<HID, tc_poly<HID>(), tc_h2<HID>(), tc_h2_full<HID>()>(acc, w);
           tmem_st<HID / 2>(t_row + S::kTCols, w);
         }
         tmem_wait_st();   // the next A operand went to TMEM: no shared-memory proxy fence

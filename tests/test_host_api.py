@@ -336,11 +336,12 @@ def test_bench_kernel_key_and_mufu_counts():
     assert bench._kernel_key(ncu_name) == bench._kernel_key(lib_name) == "dvr_tc_kernel<32,14,4,1>"
     assert bench._kernel_key("void dvr_tc_kernel<64, 30, 6, 1>(TcNetDev)") != bench._kernel_key(lib_name)
     m32, m64 = {"layers": 4, "hidden": 32}, {"layers": 6, "hidden": 64}
-    # 32-wide tcgen05: 6 of 32 cosines per row on the FMA pipe (every 5th), + 6 NeRF sin/cos + tanh + ex2
-    assert bench.mufu_per_eval_of(m32, lib_name) == 3 * 26 + 2 + 6
-    # 64-wide: 5 per 32-column half (every 6th)
-    assert bench.mufu_per_eval_of(m64, "dvr_tc_kernel<64,30,6,1>") == 5 * 54 + 2 + 6
+    # 32-wide tcgen05: 10 of 32 cosines per row on the FMA pipe (every 3rd packed word, HFMA2),
+    # + 6 NeRF sin/cos + tanh + ex2
+    assert bench.mufu_per_eval_of(m32, lib_name) == 3 * 22 + 2 + 6
+    # 64-wide: 10 per 32-column half (every 3rd word); the f32 dot-product row: 5 per half (every 6th)
+    assert bench.mufu_per_eval_of(m64, "dvr_tc_kernel<64,30,6,1>") == 4 * 44 + 54 + 2 + 6
     # mma.sync kernels: every cosine on MUFU, NeRF base angles on the FMA pipe
     assert bench.mufu_per_eval_of(m32, "dvr_pair_kernel<32,4,14,4,1,8>") == 3 * 32 + 2
-    # the decode has no alpha ex2
-    assert bench.mufu_per_eval_of(m32, "decode_tc_kernel<32,14,4,1>") == 3 * 26 + 1 + 6
+    # the decode: last hidden row is the f32 dot product (every 5th column), no alpha ex2
+    assert bench.mufu_per_eval_of(m32, "decode_tc_kernel<32,14,4,1>") == 2 * 22 + 26 + 1 + 6
