@@ -150,7 +150,9 @@ def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
     tc = kernel.startswith(("dvr_tc", "decode_tc"))
     decode = kernel.startswith("decode")
     if not tc:
-        return (layers - 1) * hid + (1 if decode else 2)
+        # mma.sync kernels (fvsrn_device.cuh, FVSRN_MMA_H2): every 4th n8 column tile of a
+        # snake_alt row evaluates its cosines in HFMA2 arithmetic
+        return (layers - 1) * (hid - hid // 4) + (1 if decode else 2)
     # fvsrn_tc.cu, per 32-column segment of a hidden row: every 3rd packed fp16 word
     # (FVSRN_TC_H2 / FVSRN_TC_H2_64) evaluates both cosines in HFMA2 arithmetic; the
     # density head's last hidden row, when it is an f32 dot product on the FMA pipe

@@ -156,6 +156,13 @@ constexpr int kActRuntime = -1;
 #ifndef FVSRN_POLY_EVERY
 #define FVSRN_POLY_EVERY 0
 #endif
+// mma.sync kernels: every FVSRN_MMA_H2-th n8 column tile of the activations evaluates its
+// snake_alt cosines in HFMA2 arithmetic (snake_alt_h2_fma below); 0 = all MUFU
+// (cfg 1, dvr_pair_kernel: 0.210 -> 0.198 ms with every 4th tile (2nd: 0.204); cfg 2 on
+// the mma.sync kernel 3.118 -> 3.094 ms (2nd: 3.208))
+#ifndef FVSRN_MMA_H2
+#define FVSRN_MMA_H2 4
+#endif
 __device__ __forceinline__ float cos_poly(float a) {
   const float t = a * 0.15915494309189535f;
   const float k = (t + 12582912.f) - 12582912.f;     // round to nearest (|t| < 2^22)
@@ -319,6 +326,19 @@ struct WarpMLP {
         const int e = (mt * KT + kt) * 8;   // element index within this thread's tile set
 #define FVSRN_ACT(i, x) (P > 0 && ((e + (i)) % (P > 0 ? P : 1)) == (P > 0 ? P - 1 : 0) \
                              ? act_h2<A, true>(x) : act_h2<A, false>(x))
+        if constexpr (A == 4 && FVSRN_MMA_H2 > 0) {
+          // every FVSRN_MMA_H2-th n8 column tile: both cosines of each packed word in HFMA2
+          // arithmetic.  Chosen by column only (the same for every row, lane and m16 tile),
+          // so a ray's result does not depend on the row / warp it was scheduled to.
+          constexpr int Q = FVSRN_MMA_H2 > 0 ? FVSRN_MMA_H2 : 1;
+          const float* src[4] = {a0, a0 + 2, a1, a1 + 2};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            h[mt][kt][i] = (2 * kt + (i >> 1)) % Q == Q - 1
+                               ? snake_alt_h2_fma<false>(src[i][0], src[i][1])
+                               : pack_half2(act_h<4>(src[i][0]), act_h<4>(src[i][1]));
+          continue;
+        }
         h[mt][kt][0] = pack_half2(FVSRN_ACT(0, a0[0]), FVSRN_ACT(1, a0[1]));
         h[mt][kt][1] = pack_half2(FVSRN_ACT(2, a0[2]), FVSRN_ACT(3, a0[3]));
         h[mt][kt][2] = pack_half2(FVSRN_ACT(4, a1[0]), FVSRN_ACT(5, a1[1]));

@@ -341,7 +341,7 @@ def test_bench_kernel_key_and_mufu_counts():
     assert bench.mufu_per_eval_of(m32, lib_name) == 3 * 22 + 2 + 6
     # 64-wide: 10 per 32-column half (every 3rd word); the f32 dot-product row: 5 per half (every 6th)
     assert bench.mufu_per_eval_of(m64, "dvr_tc_kernel<64,30,6,1>") == 4 * 44 + 54 + 2 + 6
-    # mma.sync kernels: every cosine on MUFU, NeRF base angles on the FMA pipe
-    assert bench.mufu_per_eval_of(m32, "dvr_pair_kernel<32,4,14,4,1,8>") == 3 * 32 + 2
+    # mma.sync kernels: 3 of 4 n8 column tiles' cosines on MUFU, NeRF base angles on the FMA pipe
+    assert bench.mufu_per_eval_of(m32, "dvr_pair_kernel<32,4,14,4,1,8>") == 3 * 24 + 2
     # the decode: last hidden row is the f32 dot product (every 5th column), no alpha ex2
     assert bench.mufu_per_eval_of(m32, "decode_tc_kernel<32,14,4,1>") == 2 * 22 + 26 + 1 + 6
