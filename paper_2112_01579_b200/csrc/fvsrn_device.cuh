@@ -240,6 +240,11 @@ __device__ __forceinline__ uint32_t snake_alt_h2_fma(float x0, float x1) {
 #ifndef FVSRN_FOURIER_POLY
 #define FVSRN_FOURIER_POLY 1
 #endif
+#ifndef FVSRN_FOURIER_H2
+#define FVSRN_FOURIER_H2 2   // FastRow: how many of the last doubling levels run in packed fp16
+                             // (cfg 2 2.497 -> 2.473 ms with 2 or 4; 2 keeps the trained renders
+                             // within 0.1 dB, 4 costs ~0.6 dB: profiles/r2/h2/precision_f*.txt)
+#endif
 __device__ __forceinline__ void sincos_turns(float r, float& s, float& c) {
   const float u = r * r;
   float pc = fmaf(-21.0767765045166f, u, 58.794036865234375f);
@@ -834,18 +839,34 @@ struct FastRow {
         if (FVSRN_FOURIER_POLY) sincos_turns(r, sn[a], cs[a]);
         else __sincosf(r * 6.28318548202514648f, &sn[a], &cs[a]);
       }
+      // the last FVSRN_FOURIER_H2 doublings in packed fp16 on the (sin, cos) words:
+      // (s, c) -> (2s c, 1 - 2 s^2) = HFMA2((2s, -2s), (c, s), (0, 1)): 3 instructions per
+      // axis instead of 4 FP32 operations + a pack
+      constexpr int kLevels = (NM - 1) / 3;
+      constexpr int kH2From = kLevels - FVSRN_FOURIER_H2 + 1;   // first packed level
+      uint32_t pw[3];
 #pragma unroll
       for (int i = 0; i < NM; ++i) {
         const int a = i % 3;
+        const int lev = i / 3;
         if (i > 0 && a == 0) {
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
-            float s2 = 2.f * sn[b] * cs[b];
-            float c2 = fmaf(cs[b], cs[b], -sn[b] * sn[b]);
-            sn[b] = s2; cs[b] = c2;
+            if (FVSRN_FOURIER_H2 > 0 && lev >= kH2From) {
+              if (lev == kH2From) pw[b] = pack_half2(sn[b], cs[b]);
+              const __half2 x = *reinterpret_cast<const __half2*>(&pw[b]);
+              const __half2 u = __hmul2(__low2half2(x), __floats2half2_rn(2.f, -2.f));
+              const __half2 sw = __lowhigh2highlow(x);
+              const __half2 y = __hfma2(u, sw, __floats2half2_rn(0.f, 1.f));
+              pw[b] = *reinterpret_cast<const uint32_t*>(&y);
+            } else {
+              float s2 = 2.f * sn[b] * cs[b];
+              float c2 = fmaf(cs[b], cs[b], -sn[b] * sn[b]);
+              sn[b] = s2; cs[b] = c2;
+            }
           }
         }
-        w[8 + i] = pack_half2(sn[a], cs[a]);
+        w[8 + i] = (FVSRN_FOURIER_H2 > 0 && lev >= kH2From && lev > 0) ? pw[a] : pack_half2(sn[a], cs[a]);
       }
     }
     w[8 + NM] = pack_half2(px, py);
