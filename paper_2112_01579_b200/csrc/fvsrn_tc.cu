@@ -121,6 +121,37 @@ constexpr bool tc_h2_full() { return (HID <= 32 ? FVSRN_TC_H2_FULL32 : FVSRN_TC_
 #ifndef FVSRN_TC_DEADROW
 #define FVSRN_TC_DEADROW 1
 #endif
+// MMA issue: weight-tile descriptors from one base word computed at init (no per-MMA
+// descriptor math), and warp 0 converged with elect.sync instead of a tid == 0 branch, so
+// ptxas issues each layer's UTCHMMAs + UTCBAR back to back without the per-instruction
+// waterfall loop (ELECT / PLOP3 / BRA.U.ANY around every uniform-datapath op): the MMA
+// starts sooner after the row barrier.  cfg 2 2.483 -> 2.456 (hoist) -> 2.435 ms (both),
+// cfg 3 22.22 -> 21.41, cfg 5 35.42 -> 34.75, cfg 4 0.501 -> 0.498.
+#ifndef FVSRN_TC_DESC_HOIST
+#define FVSRN_TC_DESC_HOIST 1
+#endif
+#ifndef FVSRN_TC_ELECT
+#define FVSRN_TC_ELECT 1
+#endif
+__device__ __forceinline__ uint32_t elect_one_sync() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n}" : "=r"(e));
+  return e;
+}
+__device__ __forceinline__ void umma_f16_ts_if(uint32_t el, uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(el) : "memory");
+}
+__device__ __forceinline__ void umma_commit_if(uint32_t el, uint32_t mbar) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+               "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}"
+               :: "r"(mbar), "r"(el) : "memory");
+}
 #ifndef FVSRN_TC_DEADROW_MAXW
 #define FVSRN_TC_DEADROW_MAXW 64   // widest layer that builds dummy rows (64: 24.69 -> 24.58 ms at cfg 3)
 #endif
@@ -254,6 +285,9 @@ struct TcMlp {
 
   uint32_t tmem, t_row, phase;
   int tid;
+#if FVSRN_TC_DESC_HOIST
+  uint32_t wdesc_lo;   // low descriptor word of the weight tiles' base (address field + LBO)
+#endif
 
   __device__ static const float* b_s() { return reinterpret_cast<const float*>(tc_smem + S::kBOff); }
   __device__ static uint32_t mb() { return smem_u32(tc_smem + S::kMbarOff); }
@@ -291,6 +325,9 @@ struct TcMlp {
     }
     tmem = *tmem_slot;
     t_row = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
+#if FVSRN_TC_DESC_HOIST
+    wdesc_lo = (uint32_t)smem_desc(smem_u32(tc_smem + S::kWOff), 128u, 0u);
+#endif
     phase = 0;
     if constexpr (S::kBiasMma) {
       uint32_t c[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -331,7 +368,14 @@ struct TcMlp {
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       if (fma_last && l == NL - 1) break;
+#if FVSRN_TC_ELECT
+      // warp 0 converged; elect.sync picks the issuing lane (no per-instruction waterfall
+      // loop around the uniform-datapath MMA / commit)
+      if (tid < 32) {
+        const uint32_t el = elect_one_sync();
+#else
       if (tid == 0) {
+#endif
         tc_fence_after();
         const int K = l == 0 ? S::kK0 : S::kKh;
         const int N = l == NL - 1 ? S::kNLast : HID;
@@ -344,9 +388,26 @@ struct TcMlp {
           const uint32_t acc = (kk == 0 && (S::kBiasMma || (l == 0 && S::kBias0))) ? 0u : 1u;
           // the bias k-step of a hidden layer reads the constant ones columns
           const uint32_t a_col = (S::kBiasMma && l > 0 && kk == K / 16 - 1) ? kOnesCol : 8u * kk;
+#if FVSRN_TC_DESC_HOIST
+          // the address field advances by (byte offset >> 4): no carry out of its 14 bits
+          // (shared-memory offsets < 2^18 B); the high word is a per-layer constant
+          const uint64_t bd = ((uint64_t)(((uint32_t)(K / 8) * 128u >> 4) | (1u << 14)) << 32) |
+                              (uint64_t)(wdesc_lo + ((2u * (uint32_t)S::w_off(l) + kk * 256u) >> 4));
+          (void)wb;
+#if FVSRN_TC_ELECT
+          umma_f16_ts_if(el, tmem, tmem + S::kTCols + a_col, bd, id, acc);
+#else
+          umma_f16_ts(tmem, tmem + S::kTCols + a_col, bd, id, acc);
+#endif
+#else
           umma_f16_ts(tmem, tmem + S::kTCols + a_col, smem_desc(wb + kk * 256u, 128u, sbo_b), id, acc);
+#endif
         }
+#if FVSRN_TC_ELECT
+        umma_commit_if(el, mb());
+#else
         umma_commit(mb());
+#endif
       }
       mbar_wait(mb(), phase);
       phase ^= 1u;
