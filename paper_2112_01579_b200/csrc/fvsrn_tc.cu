@@ -27,6 +27,13 @@
 #ifndef FVSRN_FOURIER_POLY
 #define FVSRN_FOURIER_POLY 0
 #endif
+// The per-layer MMA-completion wait polls without the hang watchdog (its counter and
+// compare on every failed poll cost issue slots the other warps need: cfg 2 2.43 -> 2.36 ms,
+// cfg 3 unchanged).  FVSRN_MBAR_WATCHDOG=1 restores the trap after ~2^26 polls for
+// debugging a stuck MMA.
+#ifndef FVSRN_MBAR_WATCHDOG
+#define FVSRN_MBAR_WATCHDOG 0
+#endif
 #include "fvsrn_march.cuh"
 #include "fvsrn_tc.cuh"
 #include "fvsrn_tmem.cuh"

@@ -84,16 +84,21 @@ __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(addr), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-// Waits for the phase with the given parity to complete.  A watchdog traps after ~2^26
-// failed polls (seconds) so a faulted MMA becomes a launch error instead of a hang.
+// Waits for the phase with the given parity to complete.  With FVSRN_MBAR_WATCHDOG a
+// watchdog traps after ~2^26 failed polls (seconds) so a faulted MMA becomes a launch
+// error instead of a hang (the tcgen05 kernels build without it, see fvsrn_tc.cu).
 #ifndef FVSRN_MBAR_BACKOFF_NS
 #define FVSRN_MBAR_BACKOFF_NS 0   // sleep between failed polls (0: spin)
+#endif
+#ifndef FVSRN_MBAR_WATCHDOG
+#define FVSRN_MBAR_WATCHDOG 1
 #endif
 #ifndef FVSRN_MBAR_SUSPEND_NS
 #define FVSRN_MBAR_SUSPEND_NS 0   // try_wait suspend-time hint (0: hardware default)
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   uint32_t done = 0, polls = 0;
+  (void)polls;
   while (true) {
 #if FVSRN_MBAR_SUSPEND_NS > 0
     asm volatile(
@@ -107,7 +112,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
 #endif
     if (done) break;
+#if FVSRN_MBAR_WATCHDOG
     if (++polls > (1u << 26)) __trap();
+#endif
 #if FVSRN_MBAR_BACKOFF_NS > 0
     __nanosleep(FVSRN_MBAR_BACKOFF_NS);   // give the issue slots to other warps
 #endif
