@@ -687,8 +687,10 @@ def main():
                      "xu_pipe": {"mufu_per_eval": mufu_per_eval, "achieved_Gops": xu_achieved / 1e9,
                                  "peak_Gops": xu_peak / 1e9, "frac": xu_achieved / xu_peak,
                                  "note": "MUFU (16/clk/SM): one cos per hidden activation not "
-                                         "moved to the FMA pipe, one tanh (sigmoid head), one "
-                                         "ex2 (alpha); see DESIGN.md section 4"},
+                                         "evaluated as a packed HFMA2 pair or f32 polynomial on "
+                                         "the FMA pipe, 6 NeRF base sin/cos (tcgen05 kernels), one "
+                                         "tanh (sigmoid head), one ex2 (alpha); see DESIGN.md "
+                                         "sections 3-4"},
                      **({"ncu": ncu} if ncu else {})},
         "gpu_launches": lib_launches,
         "clocks": clocks.summary(),
