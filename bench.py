@@ -141,8 +141,9 @@ class ClockSampler:
 
 def mufu_per_eval_of(model_cfg: dict, kernel: str) -> int:
     """MUFU (XU-pipe) instructions per evaluation in the launched kernel: one MUFU.COS per
-    hidden activation except the ones evaluated on the FMA pipe (tcgen05 kernels; mma.sync
-    kernels: none, FVSRN_POLY_EVERY=0), plus MUFU.TANH for the sigmoid head and, in the
+    hidden activation except the ones evaluated on the FMA pipe (packed HFMA2 pairs in both
+    kernel families, the f32 polynomial in the tcgen05 dot-product rows), plus MUFU.TANH for
+    the sigmoid head and, in the
     march, MUFU.EX2 for alpha.  The NeRF base sin/cos run on
     the FMA pipe in the mma.sync kernels (FVSRN_FOURIER_POLY=1) and on MUFU.SIN/COS in the
     tcgen05 kernels (3 axes x 2)."""
