@@ -113,6 +113,11 @@ __device__ __forceinline__ void tmem_bias(uint32_t taddr, const float* b) {
 #ifndef FVSRN_TC_H2_64
 #define FVSRN_TC_H2_64 3
 #endif
+// which word of each period (2: words 2, 5, 8, 11, 14 of a 16-word segment; phase 0, six
+// words: cfg 2 2.383 vs 2.368 ms, cfg 3 21.35 vs 21.42 -- kept at 2)
+#ifndef FVSRN_TC_H2_PHASE
+#define FVSRN_TC_H2_PHASE 2
+#endif
 #ifndef FVSRN_TC_H2_FULL32
 #define FVSRN_TC_H2_FULL32 0   // half turns + sign fix-up (smaller error, same speed)
 #endif
@@ -171,7 +176,7 @@ __device__ __forceinline__ void act_words(const uint32_t (&acc)[N], uint32_t (&w
   for (int j = 0; j < N / 2; ++j) {
     if constexpr (Q > 0) {
       const float x0 = __uint_as_float(acc[2 * j]), x1 = __uint_as_float(acc[2 * j + 1]);
-      w[j] = j % Q == Q - 1 ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
+      w[j] = j % Q == FVSRN_TC_H2_PHASE % Q ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
       continue;
     }
     float h[2];
@@ -193,7 +198,7 @@ __device__ __forceinline__ void act_words_at(const uint32_t (&acc)[N], uint32_t 
     if constexpr (Q > 0) {
       const float x0 = __uint_as_float(acc[2 * j]), x1 = __uint_as_float(acc[2 * j + 1]);
       const int g = OFF / 2 + j;
-      w[j] = g % Q == Q - 1 ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
+      w[j] = g % Q == FVSRN_TC_H2_PHASE % Q ? snake_alt_h2_fma<FULL>(x0, x1) : pack_half2(act_h<4>(x0), act_h<4>(x1));
       continue;
     }
     float h[2];
