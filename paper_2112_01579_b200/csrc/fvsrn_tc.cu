@@ -34,6 +34,12 @@
 #ifndef FVSRN_MBAR_WATCHDOG
 #define FVSRN_MBAR_WATCHDOG 0
 #endif
+// a 64 ns nanosleep between failed polls hands the issue slots to the epilogue warps
+// (cfg 2 2.364 -> 2.347 ms over two A/B runs; 20/128/256 ns 2.356/2.348/2.353; cfg 3 and
+// cfg 4 unchanged)
+#ifndef FVSRN_MBAR_BACKOFF_NS
+#define FVSRN_MBAR_BACKOFF_NS 64
+#endif
 #include "fvsrn_march.cuh"
 #include "fvsrn_tc.cuh"
 #include "fvsrn_tmem.cuh"
